@@ -1,0 +1,159 @@
+"""ctypes bindings for the step-loop C-ABI.
+
+Three libraries export the same surface with different prefixes:
+
+  plbm_gpu_*     libplbm_gpu.so   — the product (B200 engine, include/plbm_gpu.h)
+  plbm_oracle_*  oracle/_build/libplbm_oracle.so — C restatement (tests only)
+  plbm_ref_*     oracle/_ref/libplbm_ref.so      — the reference itself (tests only)
+
+This module only binds symbols; it never falls back from one library to
+another.  A missing product library raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Dict, List, Tuple
+
+import numpy as np
+
+from .scenario import (Counters, CreationEvent, EngineError, Error, FACE_NAMES,
+                       FIELD_F, Scenario)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(_HERE)
+GPU_LIB = os.path.join(_HERE, "libplbm_gpu.so")
+ORACLE_LIB = os.path.join(REPO, "oracle", "_build", "libplbm_oracle.so")
+REF_LIB = os.path.join(REPO, "oracle", "_ref", "libplbm_ref.so")
+
+_libs: Dict[str, C.CDLL] = {}
+
+
+def _bind(lib: C.CDLL, prefix: str) -> None:
+    P = C.c_void_p
+    i32p = C.POINTER(C.c_int32)
+    f = lambda n: getattr(lib, f"{prefix}_{n}")  # noqa: E731
+    f("create").restype = P
+    f("create").argtypes = [P, C.c_int, C.POINTER(Error)]
+    f("step").restype = C.c_int
+    f("step").argtypes = [P, C.c_int, C.POINTER(Error)]
+    f("counters").restype = None
+    f("counters").argtypes = [P, C.POINTER(Counters)]
+    f("tiles").restype = C.c_int
+    f("tiles").argtypes = [P, i32p, i32p, C.POINTER(C.c_int64), C.c_int]
+    f("read_tile").restype = C.c_int
+    f("read_tile").argtypes = [P, i32p, C.c_int, C.c_int, C.POINTER(C.c_double)]
+    f("creation_log").restype = C.c_int
+    f("creation_log").argtypes = [P, C.POINTER(CreationEvent), C.c_int]
+    f("poke_f").restype = C.c_int
+    f("poke_f").argtypes = [P, i32p, C.c_int, C.c_int, i32p, C.c_double]
+    f("destroy").restype = None
+    f("destroy").argtypes = [P]
+
+
+def load(path: str, prefix: str) -> C.CDLL:
+    key = f"{path}:{prefix}"
+    if key not in _libs:
+        if not os.path.exists(path):
+            raise FileNotFoundError(
+                f"{path} is not built — run `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = C.CDLL(path)
+        _bind(lib, prefix)
+        _libs[key] = lib
+    return _libs[key]
+
+
+class StepEngine:
+    """One engine instance behind the C-ABI (Engine's shape:
+    proj/include/plbm/engine.hpp:98-116)."""
+
+    def __init__(self, scenario: Scenario, lib_path: str, prefix: str, workers: int = 0):
+        self.scenario = scenario
+        self.prefix = prefix
+        self.lib = load(lib_path, prefix)
+        self._c = scenario.to_c()
+        err = Error()
+        self._h = self._fn("create")(C.cast(self._c.ptr(), C.c_void_p), workers, C.byref(err))
+        if not self._h:
+            raise ValueError(f"{prefix}_create failed: {err.message.decode()}")
+        E = scenario.tile_extent
+        self.ncell = E ** 3
+
+    def _fn(self, name):
+        return getattr(self.lib, f"{self.prefix}_{name}")
+
+    def step(self, n: int = 1) -> None:
+        err = Error()
+        rc = self._fn("step")(self._h, n, C.byref(err))
+        if rc != 0:
+            raise EngineError(err)
+
+    def counters(self) -> dict:
+        c = Counters()
+        self._fn("counters")(self._h, C.byref(c))
+        return c.as_dict()
+
+    def tiles(self) -> List[Tuple[Tuple[int, int, int], int, int]]:
+        n = self._fn("tiles")(self._h, None, None, None, 0)
+        coords = (C.c_int32 * (3 * max(n, 1)))()
+        owners = (C.c_int32 * max(n, 1))()
+        births = (C.c_int64 * max(n, 1))()
+        self._fn("tiles")(self._h, coords, owners, births, n)
+        return [((coords[3 * k], coords[3 * k + 1], coords[3 * k + 2]), owners[k], births[k])
+                for k in range(n)]
+
+    def read_tile(self, coords, comp: int, fld: int) -> np.ndarray:
+        E = self.scenario.tile_extent
+        n = self.ncell * (19 if fld == FIELD_F else 1)
+        out = np.empty(n, dtype=np.float64)
+        cc = (C.c_int32 * 3)(*coords)
+        rc = self._fn("read_tile")(self._h, cc, comp, fld,
+                                   out.ctypes.data_as(C.POINTER(C.c_double)))
+        if rc != 0:
+            raise KeyError(f"read_tile{tuple(coords)} comp {comp} field {fld}: rc={rc}")
+        if fld == FIELD_F:
+            return out.reshape(19, E, E, E)
+        return out.reshape(E, E, E)
+
+    def creation_log(self) -> List[Tuple[int, Tuple[int, int, int], str, int]]:
+        n = self._fn("creation_log")(self._h, None, 0)
+        buf = (CreationEvent * max(n, 1))()
+        self._fn("creation_log")(self._h, buf, n)
+        return [(buf[k].iteration, tuple(buf[k].coords),
+                 "init" if buf[k].trigger < 0 else FACE_NAMES[buf[k].trigger], buf[k].owner)
+                for k in range(n)]
+
+    def poke_f(self, coords, comp: int, i: int, local, value: float) -> None:
+        cc = (C.c_int32 * 3)(*coords)
+        ll = (C.c_int32 * 3)(*local)
+        if self._fn("poke_f")(self._h, cc, comp, i, ll, value) != 0:
+            raise KeyError("poke_f: no such tile")
+
+    def close(self) -> None:
+        if self._h:
+            self._fn("destroy")(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def ref_engine(sc: Scenario, workers: int = 1) -> StepEngine:
+    return StepEngine(sc, REF_LIB, "plbm_ref", workers)
+
+
+def oracle_engine(sc: Scenario) -> StepEngine:
+    return StepEngine(sc, ORACLE_LIB, "plbm_oracle", 1)
+
+
+def gpu_engine(sc: Scenario, device: int = 0) -> StepEngine:
+    return StepEngine(sc, GPU_LIB, "plbm_gpu", device)
