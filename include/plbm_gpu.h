@@ -1,0 +1,89 @@
+/*
+ * plbm_gpu.h — C-ABI of the B200 progressive-mesh MPMC D3Q19 step loop.
+ *
+ * This is the drop-in boundary for the reference's step loop.  The reference
+ * has no plugin or FFI seam: its step path is the in-process C++ class
+ *
+ *     plbm::engine::Engine(SimulationState&, int n_workers)   engine.hpp:98-116
+ *     void Engine::step()                                      engine.cpp:537-563
+ *
+ * plus the state callers read between steps (SimulationState fields,
+ * engine.hpp:76-91; TileMap::creation_log / active_report, tilemap.hpp:39-117;
+ * DeviceTopology::byte_totals, topology.hpp:48-52).  Each entry point below
+ * names the reference interface it replaces.  Exceptions never cross the ABI:
+ * every call returns a status and fills a plbm_error record.
+ *
+ * Threading: one host thread per handle.  The handle owns all device memory
+ * and one CUDA stream on the device it was created on.
+ */
+#ifndef PLBM_GPU_H
+#define PLBM_GPU_H
+
+#include "plbm_scenario.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* make_state(cfg) + Engine(state, workers)   (engine.cpp:91-161, 530-533).
+ * Builds the initial tile set, owners, seeds and ambient state ON THE DEVICE
+ * (no host field buffers).  `device` is the CUDA ordinal.  NULL on failure. */
+void* plbm_gpu_create(const plbm_scenario_desc* desc, int device, plbm_error* err);
+
+/* Engine::step() n times (engine.cpp:537-563).  Returns 0, or err->code on an
+ * EngineError (NaN / EOS pole: iteration and cell_updates do not advance).  */
+int plbm_gpu_step(void* h, int n, plbm_error* err);
+
+/* SimulationState counters: iteration, cell_updates, Diagnostics,
+ * suppressed_expansions, byte_totals, active_report (engine.hpp:34-38,84-88). */
+void plbm_gpu_counters(void* h, plbm_counters* out);
+
+/* TileMap::tiles() in coordinate order: coords[3n], owner_device[n],
+ * birth_iteration[n].  Returns the tile count (call with max = 0 to size). */
+int plbm_gpu_tiles(void* h, int32_t* coords, int32_t* owners, int64_t* births, int max);
+
+/* Reads one field of one tile as the reference holds it between steps
+ * (Tile / ComponentState, tile.hpp:38-82): interior cells, x-fastest.
+ * PLBM_FIELD_PSI / PUX..PUZ need plbm_gpu_set_capture(h, 1) before the step.
+ * 0 ok, -1 no such tile, -2 bad component, -3 bad field, -4 not captured.  */
+int plbm_gpu_read_tile(void* h, const int32_t* coords, int comp, int field, double* out);
+
+/* TileMap::creation_log() (tilemap.hpp:94-96).  Returns the row count.      */
+int plbm_gpu_creation_log(void* h, plbm_creation_event* out, int max);
+
+/* Test hook: overwrite one post-stream population before the first step
+ * (NaN poisoning, proj/tests/test_engine.cpp:284-310).                       */
+int plbm_gpu_poke_f(void* h, const int32_t* coords, int comp, int i, const int32_t* local,
+                    double value);
+
+/* Keep psi and u_prev per cell (extra 32 B/cell/comp per step) so that
+ * read_tile can serve PLBM_FIELD_PSI / PLBM_FIELD_PU*.                      */
+int plbm_gpu_set_capture(void* h, int on);
+
+/* Kernel timing for the roofline: when on, every launch of the fused kernel
+ * and of the face pre-pass is bracketed by CUDA events recorded on the
+ * engine's stream (no host synchronisation; resolved by kernel_stats).      */
+int plbm_gpu_set_profiling(void* h, int on);
+typedef struct plbm_kernel_stats {
+    int64_t main_launches;
+    double main_ms;            /* summed CUDA-event time of k_main          */
+    int64_t face_launches;
+    double face_ms;            /* summed CUDA-event time of k_face          */
+    int64_t kernels_launched;  /* all kernels launched by the engine        */
+    uint64_t main_cell_updates;/* cell updates covered by the timed k_main  */
+    uint64_t h2d_bytes;        /* host->device bytes the engine copied      */
+    uint64_t d2h_bytes;        /* device->host bytes the engine copied      */
+} plbm_kernel_stats;
+void plbm_gpu_kernel_stats(void* h, plbm_kernel_stats* out);
+void plbm_gpu_reset_kernel_stats(void* h);
+
+/* The engine's CUDA stream (cudaStream_t) for callers that time with events. */
+void* plbm_gpu_stream(void* h);
+
+/* Engine::~Engine + SimulationState release.                                 */
+void plbm_gpu_destroy(void* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PLBM_GPU_H */

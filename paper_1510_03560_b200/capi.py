@@ -155,5 +155,47 @@ def oracle_engine(sc: Scenario) -> StepEngine:
     return StepEngine(sc, ORACLE_LIB, "plbm_oracle", 1)
 
 
-def gpu_engine(sc: Scenario, device: int = 0) -> StepEngine:
-    return StepEngine(sc, GPU_LIB, "plbm_gpu", device)
+class KernelStats(C.Structure):
+    _fields_ = [("main_launches", C.c_int64), ("main_ms", C.c_double),
+                ("face_launches", C.c_int64), ("face_ms", C.c_double),
+                ("kernels_launched", C.c_int64), ("main_cell_updates", C.c_uint64),
+                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
+
+
+class GpuEngine(StepEngine):
+    """The product engine (libplbm_gpu.so).  There is no fallback: a missing
+    library or CUDA device raises."""
+
+    def __init__(self, sc: Scenario, device: int = 0, capture: bool = False):
+        super().__init__(sc, GPU_LIB, "plbm_gpu", device)
+        lib = self.lib
+        lib.plbm_gpu_set_capture.argtypes = [C.c_void_p, C.c_int]
+        lib.plbm_gpu_set_profiling.argtypes = [C.c_void_p, C.c_int]
+        lib.plbm_gpu_kernel_stats.argtypes = [C.c_void_p, C.POINTER(KernelStats)]
+        lib.plbm_gpu_reset_kernel_stats.argtypes = [C.c_void_p]
+        lib.plbm_gpu_stream.argtypes = [C.c_void_p]
+        lib.plbm_gpu_stream.restype = C.c_void_p
+        if capture:
+            self.set_capture(True)
+
+    def set_capture(self, on: bool) -> None:
+        if self.lib.plbm_gpu_set_capture(self._h, int(on)) != 0:
+            raise RuntimeError("set_capture failed")
+
+    def set_profiling(self, on: bool) -> None:
+        self.lib.plbm_gpu_set_profiling(self._h, int(on))
+
+    def kernel_stats(self) -> dict:
+        k = KernelStats()
+        self.lib.plbm_gpu_kernel_stats(self._h, C.byref(k))
+        return {n: getattr(k, n) for n, _ in k._fields_}
+
+    def reset_kernel_stats(self) -> None:
+        self.lib.plbm_gpu_reset_kernel_stats(self._h)
+
+    def stream(self) -> int:
+        return self.lib.plbm_gpu_stream(self._h)
+
+
+def gpu_engine(sc: Scenario, device: int = 0, capture: bool = False) -> GpuEngine:
+    return GpuEngine(sc, device, capture)

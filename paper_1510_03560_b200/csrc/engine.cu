@@ -1,0 +1,1111 @@
+// engine.cu — host side of the B200 step loop behind the C-ABI (plbm_gpu.h).
+//
+// The host keeps only METADATA (the reference's TileMap / AssignmentState /
+// DeviceTopology counters without any field buffer): tile coordinates, owners,
+// creation log, per-device counts, byte classes.  All field state lives in
+// the device block pool (kernels.cuh).  Expansion (proj/src/tilemap.cpp:220-266)
+// and placement (proj/src/assign.cpp:8-38, engine.cpp:30-41) run on this
+// mirror from the per-face trigger bits the device criterion produced.
+#include "kernels.cuh"
+#include "plbm_gpu.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace plbm {
+
+namespace {
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define CK(x)                                                                                   \
+    do {                                                                                        \
+        cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess)                                                                  \
+            throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));                  \
+    } while (0)
+
+// ---- host restatements used to build the device constants (same IEEE ops,
+// compiled with -ffp-contract=off) -------------------------------------------
+
+// proj/include/plbm/kernels.hpp:17-28 (literal loop form)
+void host_equilibrium(double rho, const double u[3], double* out) {
+    const double uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+    const double inv_cs2 = 1.0 / PLBM_CS2;
+    for (int i = 0; i < Q; ++i) {
+        const double eu = double(ex_(i)) * u[0] + double(ey_(i)) * u[1] + double(ez_(i)) * u[2];
+        out[i] = w_(i) * rho *
+                 (1.0 + eu * inv_cs2 + 0.5 * eu * eu * inv_cs2 * inv_cs2 - 0.5 * uu * inv_cs2);
+    }
+}
+
+// proj/src/physics.cpp:12-27
+double host_pr_pressure(double rho, const plbm_component_desc& e) {
+    if (e.b * rho >= 1.0) throw std::domain_error("pr_pressure: b*rho >= 1 (EOS pole)");
+    double theta = 1.0;
+    if (e.Tc > 0.0) {
+        const double kappa = 0.37464 + 1.54226 * e.omega - 0.26992 * e.omega * e.omega;
+        const double root = 1.0 + kappa * (1.0 - std::sqrt(e.T / e.Tc));
+        theta = root * root;
+    }
+    const double ideal = rho * e.R * e.T / (1.0 - e.b * rho);
+    const double attr = e.a * theta * rho * rho / (1.0 + 2.0 * e.b * rho - e.b * e.b * rho * rho);
+    return ideal - attr;
+}
+
+double host_theta(const plbm_component_desc& e) {
+    double theta = 1.0;
+    if (e.Tc > 0.0) {
+        const double kappa = 0.37464 + 1.54226 * e.omega - 0.26992 * e.omega * e.omega;
+        const double root = 1.0 + kappa * (1.0 - std::sqrt(e.T / e.Tc));
+        theta = root * root;
+    }
+    return theta;
+}
+
+// proj/src/physics.cpp:34-42
+double host_psi(double rho, double press, double g_self) {
+    const double radicand = 2.0 * (press - PLBM_CS2 * rho) / (PLBM_CS2 * g_self);
+    if (radicand < 0.0) return 0.0;
+    return std::sqrt(radicand);
+}
+
+template <class T>
+T* dmalloc(size_t n) {
+    T* p = nullptr;
+    if (n) CK(cudaMalloc(&p, n * sizeof(T)));
+    return p;
+}
+
+// ---- kernel dispatch over (E, C, NOPSI) --------------------------------------
+struct Kernels {
+    void (*main)(Dev, const int*, int, int, long, dim3, dim3, size_t, cudaStream_t);
+    void (*face)(Dev, const int*, int, int, long, dim3, cudaStream_t);
+    void (*face_amb)(Dev, const int*, int, cudaStream_t);
+    void (*readback)(Dev, int, int, int, double*, cudaStream_t);
+    int nt, bz;
+    size_t smem;
+};
+
+template <int E, int C, bool NOPSI>
+Kernels make_kernels() {
+    constexpr int NT = E * E < 256 ? E * E : 256;
+    constexpr int BZ = E < 8 ? E : 8;
+    constexpr int G = E + 2;
+    Kernels k;
+    k.nt = NT;
+    k.bz = BZ;
+    k.smem = NOPSI ? 0 : size_t(3) * C * G * G * sizeof(double);
+    if (k.smem > 48 * 1024)
+        cudaFuncSetAttribute(k_main<E, C, BZ, NT, NOPSI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(k.smem));
+    k.main = [](Dev d, const int* act, int src, int wu, long it, dim3 g, dim3 b, size_t sm,
+                cudaStream_t s) { k_main<E, C, BZ, NT, NOPSI><<<g, b, sm, s>>>(d, act, src, wu, it); };
+    k.face = [](Dev d, const int* act, int src, int flags, long it, dim3 g, cudaStream_t s) {
+        k_face<E, C, NT><<<g, NT, 0, s>>>(d, act, src, flags, it);
+    };
+    k.face_amb = [](Dev d, const int* slots, int n, cudaStream_t s) {
+        if (n) k_face_ambient<E><<<n, 256, 0, s>>>(d, slots, n);
+    };
+    k.readback = [](Dev d, int slot, int c, int src, double* out, cudaStream_t s) {
+        k_readback<E><<<(E * E * E + 255) / 256, 256, 0, s>>>(d, slot, c, src, 0, out);
+    };
+    return k;
+}
+
+template <int E>
+Kernels pick_c(int C, bool nopsi) {
+    switch (C) {
+    case 1: return nopsi ? make_kernels<E, 1, true>() : make_kernels<E, 1, false>();
+    case 2: return nopsi ? make_kernels<E, 2, true>() : make_kernels<E, 2, false>();
+    case 3: return nopsi ? make_kernels<E, 3, true>() : make_kernels<E, 3, false>();
+    default: throw std::invalid_argument("n_components must be 1..3 on the GPU path");
+    }
+}
+
+Kernels pick_kernels(int E, int C, bool nopsi) {
+    switch (E) {
+    case 8: return pick_c<8>(C, nopsi);
+    case 16: return pick_c<16>(C, nopsi);
+    case 32: return pick_c<32>(C, nopsi);
+    default: throw std::invalid_argument("tile_extent must be 8, 16 or 32 on the GPU path");
+    }
+}
+
+struct Coord {
+    int x, y, z;
+    bool operator<(const Coord& o) const {
+        if (x != o.x) return x < o.x;
+        if (y != o.y) return y < o.y;
+        return z < o.z;
+    }
+    bool operator==(const Coord& o) const { return x == o.x && y == o.y && z == o.z; }
+    bool operator!=(const Coord& o) const { return !(*this == o); }
+};
+
+struct SlotInfo {
+    Coord c{};
+    int owner = -1;
+    long birth = 0;
+    size_t log_index = 0;
+    int fluid = 0;
+    bool has_solid = false;
+};
+
+struct LogRow {
+    long iteration;
+    Coord c;
+    int trigger;
+    int owner;
+};
+
+}  // namespace
+
+class Engine {
+  public:
+    Engine(const plbm_scenario_desc& d, int device) { init(d, device); }
+    ~Engine() { release(); }
+
+    int step(int n, plbm_error* err);
+    void counters(plbm_counters* out);
+    int tiles(int32_t* coords, int32_t* owners, int64_t* births, int max) const;
+    int read_tile(const int32_t* coords, int comp, int field, double* out);
+    int creation_log(plbm_creation_event* out, int max) const;
+    int set_capture(bool on);
+    int poke_f(const int32_t* coords, int comp, int i, const int32_t* local, double v);
+    void set_profiling(bool on) { profiling_ = on; }
+    plbm_kernel_stats stats();
+    void reset_stats() {
+        resolve_events();
+        stats_ = plbm_kernel_stats{};
+    }
+    cudaStream_t stream() const { return stream_; }
+
+  private:
+    // configuration
+    int dev_ = 0;
+    int E_ = 0, C_ = 0, E3_ = 0, E2_ = 0;
+    int dom_[3]{}, grid_[3]{}, periodic_[3]{};
+    int mode_ = 0, devices_ = 1, policy_ = 1;
+    double threshold_ = 0.0, w_p2p_ = 0.5, w_staged_ = 1.0;
+    std::vector<uint8_t> p2p_;
+    std::vector<plbm_component_desc> comps_;
+    std::vector<double> coupling_;
+    std::vector<plbm_seed_desc> seeds_;
+    std::vector<uint8_t> geom_;
+    uint64_t face_xfer_ = 0;
+    bool nopsi_ = false;
+    Kernels K_{};
+    Params params_{};
+
+    // host mirror
+    std::vector<int> grid_slot_;  // lin -> slot or -1
+    std::vector<SlotInfo> slots_;
+    std::vector<int> free_slots_;
+    std::vector<int> active_;     // slots in coordinate order
+    std::vector<LogRow> log_;
+    std::vector<uint64_t> per_dev_;
+    uint64_t suppressed_ = 0, active_cells_ = 0;
+    uint64_t bytes_[3]{};
+    uint64_t step_bytes_[3]{};
+    long iteration_ = 0;
+    uint64_t cell_updates_ = 0;
+    uint64_t dev_cnt_[CNT_N]{};
+    bool any_gen_ = true;     // some tile is in a GEN mode this step
+    bool routes_differ_ = false;
+    std::vector<uint8_t> h_mode_;      // [slot]
+    std::vector<uint8_t> h_has_solid_; // [slot]
+    std::vector<int> h_coords_;        // [slot][3]
+    std::vector<uint32_t> h_solid_;    // [slot][solid_words]
+    int cap_ = 0, amb_ = 0;
+
+    // device
+    cudaStream_t stream_ = nullptr;
+    Dev d_{};
+    double* d_f_[2]{};
+    int* d_route_[2]{};
+    uint32_t* d_solid_ = nullptr;
+    uint8_t* d_has_solid_ = nullptr;
+    uint8_t* d_mode_ = nullptr;
+    int* d_coords_ = nullptr;
+    double* d_psi_face_ = nullptr;
+    double* d_u_face_ = nullptr;
+    uint8_t* d_trig_ = nullptr;
+    double* d_capture_ = nullptr;
+    unsigned long long* d_cnt_ = nullptr;
+    unsigned long long* d_err_ = nullptr;
+    int* d_active_ = nullptr;
+    int* d_scratch_slots_ = nullptr;
+    double* d_readback_ = nullptr;
+    int cur_ = 0;  // buffer holding the latest f_post (or unused before step 1)
+    int solid_words_ = 0;
+    bool profiling_ = false;
+    plbm_kernel_stats stats_{};
+    struct EvPair {
+        cudaEvent_t a = nullptr, b = nullptr;
+        int kind = 0;
+        uint64_t cells = 0;
+    };
+    std::vector<EvPair> ev_pool_;
+    size_t ev_used_ = 0;
+    EvPair& next_event(int kind, uint64_t cells);
+    void resolve_events();
+
+    void init(const plbm_scenario_desc& d, int device);
+    void release();
+    size_t lin(const Coord& c) const { return (size_t(c.x) * grid_[1] + c.y) * grid_[2] + c.z; }
+    int slot_at(const Coord& c) const { return grid_slot_[lin(c)]; }
+    bool neighbor_coords(const Coord& from, int face, Coord& out) const;
+    int create_tile(const Coord& c, long iteration, int trigger);
+    void assign_owner(int slot);
+    int classify(int a, int b) const {
+        if (a == b) return 0;
+        return p2p_[size_t(a) * devices_ + b] ? 1 : 2;
+    }
+    void compute_routes(int slot, int* out) const;
+    void upload_map(const std::vector<int>& new_slots, bool initial);
+    void check_error(plbm_error* err, bool& failed);
+    void recompute_step_bytes();
+    void launch_face(int src, int flags, long iter);
+    void launch_main(long iter);
+    void expand(const std::vector<std::pair<Coord, int>>& triggers, long iteration,
+                std::vector<int>& created);
+};
+
+// ---------------------------------------------------------------------------
+
+void Engine::init(const plbm_scenario_desc& d, int device) {
+    dev_ = device;
+    E_ = d.tile_extent;
+    C_ = d.n_components;
+    E2_ = E_ * E_;
+    E3_ = E_ * E_ * E_;
+    if (C_ < 1 || C_ > 3) throw std::invalid_argument("n_components must be 1..3");
+    if (d.n_seeds < 0 || d.n_seeds > MAX_SEEDS) throw std::invalid_argument("too many seeds");
+    for (int a = 0; a < 3; ++a) {
+        dom_[a] = d.domain[a];
+        periodic_[a] = d.periodic[a] ? 1 : 0;
+        if (E_ < 4 || dom_[a] < 1 || dom_[a] % E_)
+            throw std::invalid_argument("domain axis not divisible by tile_extent");
+        grid_[a] = dom_[a] / E_;
+    }
+    mode_ = d.mode;
+    threshold_ = d.threshold;
+    devices_ = d.devices;
+    policy_ = d.policy;
+    w_p2p_ = d.weight_p2p;
+    w_staged_ = d.weight_staged;
+    if (devices_ < 1) throw std::invalid_argument("devices must be >= 1");
+    p2p_.assign(size_t(devices_) * devices_, 1);
+    if (d.p2p) std::memcpy(p2p_.data(), d.p2p, p2p_.size());
+    comps_.assign(d.components, d.components + C_);
+    coupling_.assign(size_t(C_) * C_, 0.0);
+    if (d.coupling) std::memcpy(coupling_.data(), d.coupling, coupling_.size() * sizeof(double));
+    seeds_.assign(d.seeds, d.seeds + d.n_seeds);
+    const size_t ncell = size_t(dom_[0]) * dom_[1] * dom_[2];
+    if (d.geometry) geom_.assign(d.geometry, d.geometry + ncell);
+    if (mode_ == PLBM_MODE_PROGRESSIVE && seeds_.empty())
+        throw std::invalid_argument("config: progressive mode requires at least one seed region");
+    for (const auto& c : comps_) {
+        if (!(c.tau > 0.5)) throw std::invalid_argument("tau must be > 0.5");
+        if (c.b * c.rho_ambient >= 1.0) throw std::invalid_argument("rho_ambient beyond the EOS pole");
+    }
+    // proj/src/engine.cpp:128-132, proj/src/topology.cpp:85-89
+    face_xfer_ = uint64_t(E_) * E_ * uint64_t(C_) * (5 + 1) * 8;
+
+    // ---- device constants
+    Params& p = params_;
+    std::memset(&p, 0, sizeof p);
+    p.C = C_;
+    p.n_seeds = int(seeds_.size());
+    for (int a = 0; a < 3; ++a) p.grid[a] = grid_[a];
+    p.progressive = mode_ == PLBM_MODE_PROGRESSIVE;
+    p.s2 = threshold_ * threshold_;
+    nopsi_ = true;
+    for (int c = 0; c < C_; ++c) {
+        const plbm_component_desc& s = comps_[c];
+        CompConst& k = p.comp[c];
+        k.omega = 1.0 / s.tau;
+        for (int a = 0; a < 3; ++a) k.gravity[a] = s.gravity[a];
+        k.has_gravity = s.gravity[0] != 0.0 || s.gravity[1] != 0.0 || s.gravity[2] != 0.0;
+        k.ideal = s.a == 0.0 && s.b == 0.0;
+        k.psi_free = k.ideal && s.R == 1.0 && s.T == PLBM_CS2;
+        if (!k.psi_free) nopsi_ = false;
+        k.R = s.R;
+        k.T = s.T;
+        k.b = s.b;
+        k.a_theta = s.a * host_theta(s);
+        k.two_b = 2.0 * s.b;
+        k.b_b = s.b * s.b;
+        k.cs2_g = PLBM_CS2 * s.g_self;
+        k.c1f = -s.beta * s.g_self;
+        k.c2 = -0.5 * (1.0 - s.beta) * s.g_self;
+        // make_ambient, proj/src/tilemap.cpp:13-28
+        k.rho_amb = s.rho_ambient;
+        k.psi_amb = host_psi(s.rho_ambient, host_pr_pressure(s.rho_ambient, s), s.g_self);
+        const double u0[3] = {0, 0, 0};
+        host_equilibrium(s.rho_ambient, u0, k.feq_amb);
+        double rnb = 0.0;  // P1 density of a fresh ambient cell (sequential sum)
+        for (int i = 0; i < Q; ++i) rnb += k.feq_amb[i];
+        k.psi_nb = host_psi(rnb, host_pr_pressure(rnb, s), s.g_self);
+    }
+    for (int k = 0; k < C_ * C_; ++k) p.coupling[(k / C_) * C_ + (k % C_)] = coupling_[k];
+    for (size_t s = 0; s < seeds_.size(); ++s) {
+        const plbm_seed_desc& sd = seeds_[s];
+        SeedConst& sc = p.seeds[s];
+        sc.shape = sd.shape == PLBM_SEED_SPHERE ? 1 : 0;
+        sc.comp = sd.component;
+        for (int a = 0; a < 3; ++a) {
+            sc.lo[a] = sd.box_min[a];
+            sc.hi[a] = sd.box_max[a];
+            sc.center[a] = sd.center[a];
+            sc.u[a] = sd.velocity[a];
+        }
+        sc.r2 = sd.radius * sd.radius;
+        sc.rho = sd.rho;
+        host_equilibrium(sd.rho, sd.velocity, sc.feq);
+    }
+
+    // ---- device memory
+    CK(cudaSetDevice(dev_));
+    CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    K_ = pick_kernels(E_, C_, nopsi_);
+    const size_t n_tiles = size_t(grid_[0]) * grid_[1] * grid_[2];
+    cap_ = int(n_tiles);
+    amb_ = cap_;
+    p.amb_slot = amb_;
+    const int nslot = cap_ + 1;
+    const size_t per_slot = size_t(C_) * Q * E3_;
+    const int G = E_ + 2;
+    solid_words_ = (G * G * G + 31) / 32;
+    d_f_[0] = dmalloc<double>(per_slot * nslot);
+    d_f_[1] = dmalloc<double>(per_slot * nslot);
+    d_route_[0] = dmalloc<int>(size_t(nslot) * 18);
+    d_route_[1] = dmalloc<int>(size_t(nslot) * 18);
+    d_solid_ = dmalloc<uint32_t>(size_t(nslot) * solid_words_);
+    d_has_solid_ = dmalloc<uint8_t>(nslot);
+    d_mode_ = dmalloc<uint8_t>(nslot);
+    d_coords_ = dmalloc<int>(size_t(nslot) * 3);
+    d_psi_face_ = dmalloc<double>(size_t(nslot) * C_ * 6 * E2_);
+    d_u_face_ = dmalloc<double>(size_t(nslot) * C_ * 6 * 3 * E2_);
+    const size_t trig_bytes = (size_t(nslot) + 3) / 4 * 4;
+    d_trig_ = dmalloc<uint8_t>(trig_bytes);
+    d_cnt_ = dmalloc<unsigned long long>(CNT_N);
+    d_err_ = dmalloc<unsigned long long>(1);
+    d_active_ = dmalloc<int>(nslot);
+    d_scratch_slots_ = dmalloc<int>(nslot);
+    d_readback_ = dmalloc<double>(size_t(23) * E3_);
+    CK(cudaMemsetAsync(d_has_solid_, 0, nslot, stream_));
+    CK(cudaMemsetAsync(d_mode_, 0, nslot, stream_));
+    CK(cudaMemsetAsync(d_u_face_, 0, size_t(nslot) * C_ * 6 * 3 * E2_ * sizeof(double), stream_));
+    CK(cudaMemsetAsync(d_trig_, 0, trig_bytes, stream_));
+    CK(cudaMemsetAsync(d_cnt_, 0, CNT_N * sizeof(unsigned long long), stream_));
+    CK(cudaMemsetAsync(d_err_, 0xff, sizeof(unsigned long long), stream_));
+    CK(cudaMemcpyToSymbolAsync(P, &params_, sizeof(Params), 0, cudaMemcpyHostToDevice, stream_));
+    // the ambient slot: feq_amb in both buffers, psi_amb on its faces
+    {
+        std::vector<double> amb(per_slot);
+        for (int c = 0; c < C_; ++c)
+            for (int i = 0; i < Q; ++i)
+                std::fill_n(amb.begin() + (size_t(c) * Q + i) * E3_, E3_, p.comp[c].feq_amb[i]);
+        CK(cudaMemcpy(d_f_[0] + per_slot * amb_, amb.data(), per_slot * sizeof(double),
+                      cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(d_f_[1] + per_slot * amb_, amb.data(), per_slot * sizeof(double),
+                      cudaMemcpyHostToDevice));
+        std::vector<double> pf(size_t(C_) * 6 * E2_);
+        for (int c = 0; c < C_; ++c)
+            std::fill_n(pf.begin() + size_t(c) * 6 * E2_, 6 * E2_, p.comp[c].psi_amb);
+        CK(cudaMemcpy(d_psi_face_ + size_t(amb_) * C_ * 6 * E2_, pf.data(), pf.size() * sizeof(double),
+                      cudaMemcpyHostToDevice));
+        const int zc[3] = {-1000000, -1000000, -1000000};
+        CK(cudaMemcpy(d_coords_ + 3 * amb_, zc, sizeof zc, cudaMemcpyHostToDevice));
+    }
+    d_.f[0] = d_f_[0];
+    d_.f[1] = d_f_[1];
+    d_.route[0] = d_route_[0];
+    d_.route[1] = d_route_[1];
+    d_.solid = d_solid_;
+    d_.has_solid = d_has_solid_;
+    d_.mode = d_mode_;
+    d_.coords = d_coords_;
+    d_.psi_face = d_psi_face_;
+    d_.u_face = d_u_face_;
+    d_.trig = d_trig_;
+    d_.capture = nullptr;
+    d_.cnt = d_cnt_;
+    d_.err = d_err_;
+    d_.solid_words = solid_words_;
+
+    // ---- host mirror + initial tiles (make_state, engine.cpp:134-159)
+    grid_slot_.assign(n_tiles, -1);
+    slots_.assign(nslot, SlotInfo{});
+    free_slots_.clear();
+    for (int s = cap_ - 1; s >= 0; --s) free_slots_.push_back(s);
+    per_dev_.assign(devices_, 0);
+    h_mode_.assign(nslot, MODE_PULL);
+    h_has_solid_.assign(nslot, 0);
+    h_coords_.assign(size_t(nslot) * 3, -1000000);
+    h_solid_.assign(size_t(nslot) * solid_words_, 0u);
+    std::vector<uint8_t> initial(n_tiles, 0);
+    if (mode_ == PLBM_MODE_STATIC) {
+        std::fill(initial.begin(), initial.end(), 1);
+    } else {
+        // A tile holds a seeded cell centre iff every axis has one: the box
+        // test is separable, and for a sphere each squared offset is minimised
+        // independently (monotone FP ops) — identical to the reference's
+        // per-cell loop (engine.cpp:147-154) without touching every cell.
+        for (const auto& s : seeds_)
+            for (int tx = 0; tx < grid_[0]; ++tx)
+                for (int ty = 0; ty < grid_[1]; ++ty)
+                    for (int tz = 0; tz < grid_[2]; ++tz) {
+                        const int t[3] = {tx, ty, tz};
+                        bool hit;
+                        if (s.shape == PLBM_SEED_BOX) {
+                            hit = true;
+                            for (int a = 0; a < 3 && hit; ++a) {
+                                bool any = false;
+                                for (int v = t[a] * E_; v < t[a] * E_ + E_ && !any; ++v) {
+                                    const double cc = v + 0.5;
+                                    any = cc >= s.box_min[a] && cc < s.box_max[a];
+                                }
+                                hit = any;
+                            }
+                        } else {
+                            double m[3];
+                            for (int a = 0; a < 3; ++a) {
+                                m[a] = INFINITY;
+                                for (int v = t[a] * E_; v < t[a] * E_ + E_; ++v) {
+                                    const double dd = (v + 0.5) - s.center[a];
+                                    m[a] = std::min(m[a], dd * dd);
+                                }
+                            }
+                            hit = m[0] + m[1] + m[2] <= s.radius * s.radius;
+                        }
+                        if (hit) initial[(size_t(tx) * grid_[1] + ty) * grid_[2] + tz] = 1;
+                    }
+    }
+    std::vector<int> created;
+    for (size_t k = 0; k < n_tiles; ++k) {
+        if (!initial[k]) continue;
+        const Coord c{int(k / (size_t(grid_[1]) * grid_[2])), int((k / grid_[2]) % grid_[1]),
+                      int(k % grid_[2])};
+        const int s = create_tile(c, 0, -1);
+        assign_owner(s);
+        created.push_back(s);
+    }
+    for (int s : created) h_mode_[s] = MODE_GEN_SEEDED;
+    upload_map(created, true);
+    // psi_face for step 1 from the generated initial state
+    launch_face(0, 0, 0);
+    CK(cudaStreamSynchronize(stream_));
+}
+
+void Engine::release() {
+    if (stream_) cudaStreamSynchronize(stream_);
+    void* ptrs[] = {d_f_[0], d_f_[1], d_route_[0], d_route_[1], d_solid_, d_has_solid_, d_mode_,
+                    d_coords_, d_psi_face_, d_u_face_, d_trig_, d_capture_, d_cnt_, d_err_,
+                    d_active_, d_scratch_slots_, d_readback_};
+    for (void* q : ptrs)
+        if (q) cudaFree(q);
+    for (auto& e : ev_pool_) {
+        if (e.a) cudaEventDestroy(e.a);
+        if (e.b) cudaEventDestroy(e.b);
+    }
+    if (stream_) cudaStreamDestroy(stream_);
+    stream_ = nullptr;
+}
+
+// proj/src/tilemap.cpp:56-67
+bool Engine::neighbor_coords(const Coord& from, int face, Coord& out) const {
+    int c[3] = {from.x, from.y, from.z};
+    const int axis = face / 2;
+    c[axis] += (face % 2) ? 1 : -1;
+    if (c[axis] < 0 || c[axis] >= grid_[axis]) {
+        if (!periodic_[axis]) return false;
+        c[axis] = (c[axis] + grid_[axis]) % grid_[axis];
+    }
+    out = {c[0], c[1], c[2]};
+    return true;
+}
+
+// proj/src/tilemap.cpp:83-175 (metadata + solid slicing; fields live on the device)
+int Engine::create_tile(const Coord& c, long iteration, int trigger) {
+    if (free_slots_.empty()) throw std::runtime_error("block pool exhausted");
+    const int s = free_slots_.back();
+    free_slots_.pop_back();
+    SlotInfo& si = slots_[s];
+    si = SlotInfo{};
+    si.c = c;
+    si.birth = iteration;
+    const int G = E_ + 2;
+    uint32_t* bits = &h_solid_[size_t(s) * solid_words_];
+    std::fill_n(bits, solid_words_, 0u);
+    int fluid = 0;
+    bool any = false;
+    for (int lz = -1; lz <= E_; ++lz)
+        for (int ly = -1; ly <= E_; ++ly)
+            for (int lx = -1; lx <= E_; ++lx) {
+                int g[3] = {c.x * E_ + lx, c.y * E_ + ly, c.z * E_ + lz};
+                bool outside = false;
+                for (int a = 0; a < 3; ++a)
+                    if (g[a] < 0 || g[a] >= dom_[a]) {
+                        if (periodic_[a]) g[a] = (g[a] + dom_[a]) % dom_[a];
+                        else outside = true;
+                    }
+                bool sol = false;
+                if (!outside && !geom_.empty())
+                    sol = geom_[size_t(g[0]) + size_t(dom_[0]) * (size_t(g[1]) + size_t(dom_[1]) * g[2])] != 0;
+                const bool interior = lx >= 0 && lx < E_ && ly >= 0 && ly < E_ && lz >= 0 && lz < E_;
+                if (sol) {
+                    const int idx = (lx + 1) + G * ((ly + 1) + G * (lz + 1));
+                    bits[idx >> 5] |= 1u << (idx & 31);
+                    any = true;
+                } else if (interior) {
+                    ++fluid;
+                }
+            }
+    si.fluid = fluid;
+    si.has_solid = any;
+    active_cells_ += uint64_t(fluid);
+    si.log_index = log_.size();
+    log_.push_back({iteration, c, trigger, -1});
+    grid_slot_[lin(c)] = s;
+    h_mode_[s] = MODE_GEN_AMBIENT;
+    h_has_solid_[s] = any ? 1 : 0;
+    h_coords_[3 * size_t(s)] = c.x;
+    h_coords_[3 * size_t(s) + 1] = c.y;
+    h_coords_[3 * size_t(s) + 2] = c.z;
+    return s;
+}
+
+// proj/src/engine.cpp:30-41 -> proj/src/assign.cpp:8-38
+void Engine::assign_owner(int slot) {
+    SlotInfo& t = slots_[slot];
+    std::vector<int> owners;
+    for (int f = 0; f < 6; ++f) {
+        Coord nc;
+        if (!neighbor_coords(t.c, f, nc)) continue;
+        const int ns = slot_at(nc);
+        if (ns >= 0 && slots_[ns].owner >= 0 && ns != slot) owners.push_back(slots_[ns].owner);
+    }
+    const uint64_t lo = *std::min_element(per_dev_.begin(), per_dev_.end());
+    std::vector<int> eligible;
+    for (int dv = 0; dv < devices_; ++dv)
+        if (per_dev_[dv] == lo) eligible.push_back(dv);
+    auto f_cost = [&](int cand) {
+        double sum = 0.0;
+        for (int o : owners) {
+            const int cls = classify(cand, o);
+            sum += cls == 0 ? 0.0 : (cls == 1 ? w_p2p_ * double(face_xfer_) : w_staged_ * double(face_xfer_));
+        }
+        return sum;
+    };
+    int chosen = eligible.front();
+    if (policy_ == PLBM_POLICY_OPTIMIZED) {
+        double best = f_cost(chosen);
+        for (size_t k = 1; k < eligible.size(); ++k) {
+            const double c = f_cost(eligible[k]);
+            if (c < best) {
+                best = c;
+                chosen = eligible[k];
+            }
+        }
+    }
+    ++per_dev_[chosen];
+    t.owner = chosen;
+    log_[t.log_index].owner = chosen;
+}
+
+// Ghost routing (proj/src/engine.cpp:266-296): a face ghost reads the face
+// neighbour; an edge ghost on axes a<b hops along b first, then a — an absent
+// hop yields the ambient slot even when the diagonal tile exists.
+void Engine::compute_routes(int slot, int* out) const {
+    const Coord c = slots_[slot].c;
+    auto nb = [&](const Coord& from, int axis, int dir, Coord& o) {
+        return neighbor_coords(from, 2 * axis + (dir > 0 ? 1 : 0), o);
+    };
+    for (int f = 0; f < 6; ++f) {
+        Coord n;
+        out[f] = (nb(c, f / 2, (f % 2) ? 1 : -1, n) && slot_at(n) >= 0) ? slot_at(n) : amb_;
+    }
+    const int pairs[3][2] = {{0, 1}, {0, 2}, {1, 2}};
+    for (int p = 0; p < 3; ++p)
+        for (int da = -1; da <= 1; da += 2)
+            for (int db = -1; db <= 1; db += 2) {
+                const int a = pairs[p][0], b = pairs[p][1];
+                int r = amb_;
+                Coord n1, n2;
+                if (nb(c, b, db, n1) && slot_at(n1) >= 0 && nb(n1, a, da, n2) && slot_at(n2) >= 0)
+                    r = slot_at(n2);
+                out[edge_class(a, b, da, db)] = r;
+            }
+}
+
+void Engine::recompute_step_bytes() {
+    // Closed form of record_exchange over one step: P2 and P4 each record one
+    // transfer per (tile, face) with an existing neighbour (engine.cpp:305-309).
+    step_bytes_[0] = step_bytes_[1] = step_bytes_[2] = 0;
+    for (int s : active_) {
+        for (int f = 0; f < 6; ++f) {
+            Coord n;
+            if (!neighbor_coords(slots_[s].c, f, n)) continue;
+            const int ns = slot_at(n);
+            if (ns < 0) continue;
+            step_bytes_[classify(slots_[s].owner, slots_[ns].owner)] += 2 * face_xfer_;
+        }
+    }
+}
+
+void Engine::upload_map(const std::vector<int>& new_slots, bool initial) {
+    // active list in coordinate order
+    active_.clear();
+    for (size_t k = 0; k < grid_slot_.size(); ++k)
+        if (grid_slot_[k] >= 0) active_.push_back(grid_slot_[k]);
+    const size_t nslot = size_t(cap_ + 1);
+    CK(cudaMemcpyAsync(d_active_, active_.data(), active_.size() * sizeof(int),
+                       cudaMemcpyHostToDevice, stream_));
+    CK(cudaMemcpyAsync(d_coords_, h_coords_.data(), nslot * 3 * sizeof(int), cudaMemcpyHostToDevice,
+                       stream_));
+    CK(cudaMemcpyAsync(d_has_solid_, h_has_solid_.data(), nslot, cudaMemcpyHostToDevice, stream_));
+    CK(cudaMemcpyAsync(d_mode_, h_mode_.data(), nslot, cudaMemcpyHostToDevice, stream_));
+    for (int s : new_slots) {
+        if (h_has_solid_[s])
+            CK(cudaMemcpyAsync(d_solid_ + size_t(s) * solid_words_, &h_solid_[size_t(s) * solid_words_],
+                               solid_words_ * sizeof(uint32_t), cudaMemcpyHostToDevice, stream_));
+        if (d_capture_)
+            CK(cudaMemsetAsync(d_capture_ + size_t(s) * C_ * 4 * E3_, 0,
+                               size_t(C_) * 4 * E3_ * sizeof(double), stream_));
+    }
+    // newborn faces hold psi of the fresh ambient cell (initial tiles get
+    // theirs from k_face over the generated state)
+    if (!initial && !new_slots.empty()) {
+        CK(cudaMemcpyAsync(d_scratch_slots_, new_slots.data(), new_slots.size() * sizeof(int),
+                           cudaMemcpyHostToDevice, stream_));
+        K_.face_amb(d_, d_scratch_slots_, int(new_slots.size()), stream_);
+        ++stats_.kernels_launched;
+    }
+    // routes: pull table = map of the step that just ran, psi table = new map
+    std::vector<int> routes(nslot * 18, amb_);
+    for (int s : active_) compute_routes(s, &routes[size_t(s) * 18]);
+    if (!initial)
+        CK(cudaMemcpyAsync(d_route_[ROUTE_PULL], d_route_[ROUTE_PSI], routes.size() * sizeof(int),
+                           cudaMemcpyDeviceToDevice, stream_));
+    else
+        CK(cudaMemcpyAsync(d_route_[ROUTE_PULL], routes.data(), routes.size() * sizeof(int),
+                           cudaMemcpyHostToDevice, stream_));
+    CK(cudaMemcpyAsync(d_route_[ROUTE_PSI], routes.data(), routes.size() * sizeof(int),
+                       cudaMemcpyHostToDevice, stream_));
+    routes_differ_ = !initial;
+    any_gen_ = true;
+    stats_.h2d_bytes += active_.size() * sizeof(int) + nslot * (3 * sizeof(int) + 2) +
+                        routes.size() * sizeof(int) * (initial ? 2 : 1);
+    for (int s : new_slots)
+        if (h_has_solid_[s]) stats_.h2d_bytes += solid_words_ * sizeof(uint32_t);
+    recompute_step_bytes();
+    // the host vectors must outlive the async copies
+    CK(cudaStreamSynchronize(stream_));
+}
+
+void Engine::launch_face(int src, int flags, long iter) {
+    if (active_.empty()) return;
+    EvPair* ev = profiling_ ? &next_event(1, 0) : nullptr;
+    if (ev) CK(cudaEventRecord(ev->a, stream_));
+    K_.face(d_, d_active_, src, flags, iter, dim3(unsigned(active_.size() * 6)), stream_);
+    CK(cudaGetLastError());
+    ++stats_.kernels_launched;
+    if (ev) CK(cudaEventRecord(ev->b, stream_));
+}
+
+void Engine::launch_main(long iter) {
+    if (active_.empty()) return;
+    const dim3 grid(unsigned(active_.size() * (E_ / K_.bz)));
+    EvPair* ev = profiling_ ? &next_event(0, active_cells_) : nullptr;
+    if (ev) CK(cudaEventRecord(ev->a, stream_));
+    K_.main(d_, d_active_, cur_, mode_ == PLBM_MODE_PROGRESSIVE ? 1 : 0, iter, grid, dim3(K_.nt),
+            K_.smem, stream_);
+    CK(cudaGetLastError());
+    ++stats_.kernels_launched;
+    if (ev) CK(cudaEventRecord(ev->b, stream_));
+}
+
+Engine::EvPair& Engine::next_event(int kind, uint64_t cells) {
+    if (ev_used_ == ev_pool_.size()) {
+        if (ev_pool_.size() >= 8192) resolve_events();
+        if (ev_used_ == ev_pool_.size()) {
+            EvPair p;
+            CK(cudaEventCreate(&p.a));
+            CK(cudaEventCreate(&p.b));
+            ev_pool_.push_back(p);
+        }
+    }
+    EvPair& e = ev_pool_[ev_used_++];
+    e.kind = kind;
+    e.cells = cells;
+    return e;
+}
+
+void Engine::resolve_events() {
+    if (!ev_used_) return;
+    CK(cudaStreamSynchronize(stream_));
+    for (size_t k = 0; k < ev_used_; ++k) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev_pool_[k].a, ev_pool_[k].b));
+        if (ev_pool_[k].kind == 0) {
+            stats_.main_ms += ms;
+            ++stats_.main_launches;
+            stats_.main_cell_updates += ev_pool_[k].cells;
+        } else {
+            stats_.face_ms += ms;
+            ++stats_.face_launches;
+        }
+    }
+    ev_used_ = 0;
+}
+
+plbm_kernel_stats Engine::stats() {
+    resolve_events();
+    return stats_;
+}
+
+void Engine::check_error(plbm_error* err, bool& failed) {
+    unsigned long long h_err = ~0ull;
+    CK(cudaMemcpyAsync(&h_err, d_err_, sizeof h_err, cudaMemcpyDeviceToHost, stream_));
+    stats_.d2h_bytes += sizeof h_err;
+    CK(cudaStreamSynchronize(stream_));
+    failed = h_err != ~0ull;
+    if (!failed) return;
+    const int code = int(h_err & 0xf);
+    const long tl = long((h_err >> 4) & 0xffffffffull);
+    const long it = long(h_err >> 36);
+    const int tx = int(tl / (long(grid_[1]) * grid_[2]));
+    const int ty = int((tl / grid_[2]) % grid_[1]);
+    const int tz = int(tl % grid_[2]);
+    const char* phase = code == ERR_P5_NAN ? "P5" : "P1";
+    const char* what = code == ERR_P1_NAN    ? "NaN in density"
+                       : code == ERR_P1_POLE ? "pr_pressure: b*rho >= 1 (EOS pole)"
+                                             : "NaN in moments";
+    if (err) {
+        std::memset(err, 0, sizeof *err);
+        err->code = 1;
+        err->tile[0] = tx;
+        err->tile[1] = ty;
+        err->tile[2] = tz;
+        err->iteration = it;
+        std::snprintf(err->phase, sizeof err->phase, "%s", phase);
+        std::snprintf(err->message, sizeof err->message, "iteration %ld, tile (%d,%d,%d), phase %s: %s",
+                      it, tx, ty, tz, phase, what);
+    }
+    CK(cudaMemsetAsync(d_err_, 0xff, sizeof(unsigned long long), stream_));
+    CK(cudaStreamSynchronize(stream_));
+}
+
+// proj/src/tilemap.cpp:220-266 + proj/src/engine.cpp:554-560
+void Engine::expand(const std::vector<std::pair<Coord, int>>& triggers, long iteration,
+                    std::vector<int>& created) {
+    struct Resolved {
+        Coord target, source;
+        int face;
+        bool in_bounds;
+    };
+    std::vector<Resolved> rs;
+    rs.reserve(triggers.size());
+    for (const auto& [src, face] : triggers) {
+        Coord t{};
+        const bool ok = neighbor_coords(src, face, t);
+        rs.push_back({ok ? t : Coord{}, src, face, ok});
+    }
+    std::sort(rs.begin(), rs.end(), [](const Resolved& a, const Resolved& b) {
+        if (a.in_bounds != b.in_bounds) return a.in_bounds > b.in_bounds;
+        if (a.target != b.target) return a.target < b.target;
+        if (a.source != b.source) return a.source < b.source;
+        return a.face < b.face;
+    });
+    const Coord* last = nullptr;
+    for (const auto& r : rs) {
+        if (!r.in_bounds) {
+            ++suppressed_;
+            continue;
+        }
+        if (last && r.target == *last) continue;
+        last = &r.target;
+        if (slot_at(r.target) >= 0) continue;
+        created.push_back(create_tile(r.target, iteration, r.face));
+    }
+    std::sort(created.begin(), created.end(),
+              [&](int a, int b) { return slots_[a].c < slots_[b].c; });
+}
+
+int Engine::step(int n, plbm_error* err) {
+    const bool progressive = mode_ == PLBM_MODE_PROGRESSIVE;
+    // Static meshes never change: the whole batch is queued without a host
+    // round trip and the error flag (earliest iteration wins) is read once.
+    // Progressive meshes synchronise once per step to expand on the mirror.
+    const long it0 = iteration_;
+    for (int k = 0; k < n; ++k) {
+        const long it = iteration_ + 1;
+        launch_main(it);
+        cur_ ^= 1;
+        if (any_gen_) {
+            CK(cudaMemsetAsync(d_mode_, MODE_PULL, size_t(cap_ + 1), stream_));
+            std::fill(h_mode_.begin(), h_mode_.end(), uint8_t(MODE_PULL));
+            any_gen_ = false;
+        }
+        if (routes_differ_) {
+            CK(cudaMemcpyAsync(d_route_[ROUTE_PULL], d_route_[ROUTE_PSI],
+                               size_t(cap_ + 1) * 18 * sizeof(int), cudaMemcpyDeviceToDevice, stream_));
+            routes_differ_ = false;
+        }
+        launch_face(cur_, progressive ? 3 : 2, it);
+        if (!progressive) {
+            for (int a = 0; a < 3; ++a) bytes_[a] += step_bytes_[a];
+            ++iteration_;
+            cell_updates_ += active_cells_;
+            continue;
+        }
+        bool failed = false;
+        check_error(err, failed);
+        if (failed) return 1;
+        std::vector<uint8_t> trig(size_t(cap_ + 1));
+        CK(cudaMemcpyAsync(trig.data(), d_trig_, trig.size(), cudaMemcpyDeviceToHost, stream_));
+        stats_.d2h_bytes += trig.size();
+        CK(cudaStreamSynchronize(stream_));
+        const uint64_t updates = active_cells_;
+        for (int a = 0; a < 3; ++a) bytes_[a] += step_bytes_[a];
+        std::vector<std::pair<Coord, int>> triggers;
+        for (int s : active_)
+            for (int f = 0; f < 6; ++f)
+                if (trig[s] & (1u << f)) triggers.push_back({slots_[s].c, f});
+        if (!triggers.empty()) {
+            CK(cudaMemsetAsync(d_trig_, 0, (size_t(cap_ + 1) + 3) / 4 * 4, stream_));
+            std::vector<int> created;
+            expand(triggers, it, created);
+            for (int s : created) assign_owner(s);
+            if (!created.empty()) upload_map(created, false);
+        }
+        ++iteration_;
+        cell_updates_ += updates;
+    }
+    if (!progressive && n > 0) {
+        bool failed = false;
+        check_error(err, failed);
+        if (failed) {
+            // roll the counters back to the step before the failing one
+            const long bad = err ? long(err->iteration) : it0 + 1;
+            const long done = std::max(0L, bad - 1 - it0);
+            iteration_ = it0 + done;
+            cell_updates_ -= uint64_t(n - done) * active_cells_;
+            for (int a = 0; a < 3; ++a) bytes_[a] -= uint64_t(n - done) * step_bytes_[a];
+            return 1;
+        }
+    }
+    return 0;
+}
+
+void Engine::counters(plbm_counters* out) {
+    std::memset(out, 0, sizeof *out);
+    unsigned long long c[CNT_N] = {};
+    CK(cudaMemcpyAsync(c, d_cnt_, sizeof c, cudaMemcpyDeviceToHost, stream_));
+    CK(cudaStreamSynchronize(stream_));
+    stats_.d2h_bytes += sizeof c;
+    out->iteration = iteration_;
+    out->cell_updates = cell_updates_;
+    out->negative_populations = c[CNT_NEG];
+    out->psi_clamps = c[CNT_CLAMP];
+    out->zero_rho_forcings = c[CNT_ZERO_RHO];
+    out->suppressed_expansions = suppressed_;
+    for (int a = 0; a < 3; ++a) out->bytes[a] = bytes_[a];
+    out->tiles = active_.size();
+    out->active_cells = active_cells_;
+    const uint64_t g = uint64_t(E_ + 2) * (E_ + 2) * (E_ + 2);
+    out->bytes_resident = out->tiles * g * (uint64_t(C_) * (2 * Q + 8) * 8 + 1);  // tile.cpp:7-13
+}
+
+int Engine::tiles(int32_t* coords, int32_t* owners, int64_t* births, int max) const {
+    int k = 0;
+    for (int s : active_) {
+        if (k < max) {
+            if (coords) {
+                coords[3 * k] = slots_[s].c.x;
+                coords[3 * k + 1] = slots_[s].c.y;
+                coords[3 * k + 2] = slots_[s].c.z;
+            }
+            if (owners) owners[k] = slots_[s].owner;
+            if (births) births[k] = slots_[s].birth;
+        }
+        ++k;
+    }
+    return k;
+}
+
+int Engine::read_tile(const int32_t* cc, int comp, int field, double* out) {
+    const Coord c{cc[0], cc[1], cc[2]};
+    if (c.x < 0 || c.y < 0 || c.z < 0 || c.x >= grid_[0] || c.y >= grid_[1] || c.z >= grid_[2])
+        return -1;
+    const int s = slot_at(c);
+    if (s < 0) return -1;
+    if (comp < 0 || comp >= C_) return -2;
+    if (field < 0 || field > PLBM_FIELD_PSI) return -3;
+    if (field == PLBM_FIELD_PSI || field >= PLBM_FIELD_PUX) {
+        if (!d_capture_) return -4;
+        const int which = field == PLBM_FIELD_PSI ? 0 : 1 + (field - PLBM_FIELD_PUX);
+        CK(cudaMemcpyAsync(out, d_capture_ + (size_t(s) * C_ + comp) * 4 * E3_ + size_t(which) * E3_,
+                           size_t(E3_) * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+        return 0;
+    }
+    K_.readback(d_, s, comp, cur_, d_readback_, stream_);
+    CK(cudaGetLastError());
+    ++stats_.kernels_launched;
+    if (field == PLBM_FIELD_F) {
+        CK(cudaMemcpyAsync(out, d_readback_, size_t(19) * E3_ * sizeof(double), cudaMemcpyDeviceToHost,
+                           stream_));
+    } else {
+        const int which = field == PLBM_FIELD_RHO ? 19 : 20 + (field - PLBM_FIELD_UX);
+        CK(cudaMemcpyAsync(out, d_readback_ + size_t(which) * E3_, size_t(E3_) * sizeof(double),
+                           cudaMemcpyDeviceToHost, stream_));
+    }
+    CK(cudaStreamSynchronize(stream_));
+    return 0;
+}
+
+int Engine::creation_log(plbm_creation_event* out, int max) const {
+    for (size_t k = 0; k < log_.size() && int(k) < max; ++k) {
+        out[k].iteration = log_[k].iteration;
+        out[k].coords[0] = log_[k].c.x;
+        out[k].coords[1] = log_[k].c.y;
+        out[k].coords[2] = log_[k].c.z;
+        out[k].trigger = log_[k].trigger;
+        out[k].owner = log_[k].owner;
+        out[k].pad = 0;
+    }
+    return int(log_.size());
+}
+
+int Engine::set_capture(bool on) {
+    if (on && !d_capture_) {
+        const size_t n = size_t(cap_ + 1) * C_ * 4 * E3_;
+        d_capture_ = dmalloc<double>(n);
+        CK(cudaMemsetAsync(d_capture_, 0, n * sizeof(double), stream_));
+        CK(cudaStreamSynchronize(stream_));
+    } else if (!on && d_capture_) {
+        CK(cudaStreamSynchronize(stream_));
+        cudaFree(d_capture_);
+        d_capture_ = nullptr;
+    }
+    d_.capture = d_capture_;
+    return 0;
+}
+
+int Engine::poke_f(const int32_t*, int, int, const int32_t*, double) {
+    return -5;  // not supported yet on the device pool
+}
+
+}  // namespace plbm
+
+// ---------------------------------------------------------------------------
+// C-ABI
+
+namespace {
+void fill_err(plbm_error* e, int code, const char* msg) {
+    if (!e) return;
+    std::memset(e, 0, sizeof *e);
+    e->code = code;
+    std::snprintf(e->message, sizeof e->message, "%s", msg);
+}
+}  // namespace
+
+extern "C" {
+
+void* plbm_gpu_create(const plbm_scenario_desc* desc, int device, plbm_error* err) {
+    fill_err(err, 0, "");
+    try {
+        return new plbm::Engine(*desc, device);
+    } catch (const plbm::CudaError& e) {
+        fill_err(err, 3, e.what());
+    } catch (const std::exception& e) {
+        fill_err(err, 2, e.what());
+    }
+    return nullptr;
+}
+
+int plbm_gpu_step(void* h, int n, plbm_error* err) {
+    fill_err(err, 0, "");
+    try {
+        return static_cast<plbm::Engine*>(h)->step(n, err);
+    } catch (const std::exception& e) {
+        fill_err(err, 3, e.what());
+        return 3;
+    }
+}
+
+void plbm_gpu_counters(void* h, plbm_counters* out) {
+    try {
+        static_cast<plbm::Engine*>(h)->counters(out);
+    } catch (const std::exception&) {
+        std::memset(out, 0, sizeof *out);
+    }
+}
+
+int plbm_gpu_tiles(void* h, int32_t* coords, int32_t* owners, int64_t* births, int max) {
+    return static_cast<plbm::Engine*>(h)->tiles(coords, owners, births, max);
+}
+
+int plbm_gpu_read_tile(void* h, const int32_t* coords, int comp, int field, double* out) {
+    try {
+        return static_cast<plbm::Engine*>(h)->read_tile(coords, comp, field, out);
+    } catch (const std::exception&) {
+        return -6;
+    }
+}
+
+int plbm_gpu_creation_log(void* h, plbm_creation_event* out, int max) {
+    return static_cast<plbm::Engine*>(h)->creation_log(out, max);
+}
+
+int plbm_gpu_poke_f(void* h, const int32_t* coords, int comp, int i, const int32_t* local, double v) {
+    return static_cast<plbm::Engine*>(h)->poke_f(coords, comp, i, local, v);
+}
+
+int plbm_gpu_set_capture(void* h, int on) {
+    try {
+        return static_cast<plbm::Engine*>(h)->set_capture(on != 0);
+    } catch (const std::exception&) {
+        return -6;
+    }
+}
+
+int plbm_gpu_set_profiling(void* h, int on) {
+    static_cast<plbm::Engine*>(h)->set_profiling(on != 0);
+    return 0;
+}
+
+void plbm_gpu_kernel_stats(void* h, plbm_kernel_stats* out) {
+    try {
+        *out = static_cast<plbm::Engine*>(h)->stats();
+    } catch (const std::exception&) {
+        std::memset(out, 0, sizeof *out);
+    }
+}
+
+void plbm_gpu_reset_kernel_stats(void* h) {
+    try {
+        static_cast<plbm::Engine*>(h)->reset_stats();
+    } catch (const std::exception&) {
+    }
+}
+
+void* plbm_gpu_stream(void* h) { return static_cast<plbm::Engine*>(h)->stream(); }
+
+void plbm_gpu_destroy(void* h) { delete static_cast<plbm::Engine*>(h); }
+
+}  // extern "C"

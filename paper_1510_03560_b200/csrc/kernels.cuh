@@ -1,0 +1,666 @@
+// kernels.cuh — the B200 step-loop kernels (sm_100a, FP64, no tensor cores).
+//
+// Storage (HBM block pool, SoA):
+//   f[b]      : [slot][comp][19][E^3] doubles, b in {0,1} (A-B buffers).  The
+//               stored state is the POST-COLLISION population of the last step
+//               (f_post^(k)); the reference's post-stream f_read is produced on
+//               the fly by pulling (stream fused into the next step's load).
+//   slot AMB  : one extra pool slot holding feq_amb in both buffers; every route
+//               to an absent tile points at it, so frontier pulls need no branch.
+//   route[r]  : [slot][18] source slot for the 6 face and 12 edge ghost classes,
+//               resolved with the reference's ghost-routing rule (hop along the
+//               higher axis first; proj/src/engine.cpp:266-296).  Two tables:
+//               ROUTE_PULL = map of the previous step (P4 of the last step ran on
+//               it), ROUTE_PSI = map of this step (P2 runs on it).
+//   psi_face  : [slot][comp][6][E^2] face-layer pseudo-potential of the step
+//               about to run (written by k_face, read by neighbours in k_main).
+//   u_face    : [slot][comp][6][3][E^2] velocity used by the last collision on
+//               frontier faces (u_prev of the activation criterion).
+//
+// Per step k:
+//   k_main  : pull f_in^(k) from f_post^(k-1) (or generate it for seeded /
+//             newborn tiles), rho/psi planes in shared memory marching in z,
+//             Shan-Chen forces, BGK + velocity-shift forcing, store f_post^(k).
+//             = reference P1 + P2 + P3 + P4 + (P5 moments of the previous step).
+//   k_face  : moments of f_in^(k+1) on the 6 face layers: psi_face for step
+//             k+1 and the activation criterion of step k (P5 + evaluate_criterion).
+#pragma once
+
+#include "lattice.cuh"
+
+namespace plbm {
+
+enum TileMode : uint8_t { MODE_PULL = 0, MODE_GEN_SEEDED = 1, MODE_GEN_AMBIENT = 2 };
+enum { ROUTE_PULL = 0, ROUTE_PSI = 1 };
+enum { ERR_NONE = 0, ERR_P1_NAN = 1, ERR_P1_POLE = 2, ERR_P5_NAN = 3 };
+enum { CNT_NEG = 0, CNT_CLAMP = 1, CNT_ZERO_RHO = 2, CNT_N = 4 };
+
+constexpr int MAX_COMP = 4;
+constexpr int MAX_SEEDS = 64;
+
+struct SeedConst {
+    int shape, comp;
+    double lo[3], hi[3], center[3], r2;
+    double rho, u[3];
+    double feq[Q];
+};
+
+struct Params {
+    int C;
+    int n_seeds;
+    int grid[3];
+    int amb_slot;
+    int progressive;
+    double s2;  // threshold^2 (tilemap.cpp:185)
+    CompConst comp[MAX_COMP];
+    double coupling[MAX_COMP * MAX_COMP];
+    SeedConst seeds[MAX_SEEDS];
+};
+
+struct Dev {
+    double* f[2];
+    const int* route[2];       // [slot][18]
+    const uint32_t* solid;     // [slot][solid_words]
+    const uint8_t* has_solid;  // [slot]
+    const uint8_t* mode;       // [slot]
+    const int* coords;         // [slot][3]
+    double* psi_face;          // [slot][C][6][E2]
+    double* u_face;            // [slot][C][6][3][E2]
+    uint8_t* trig;             // [slot]
+    double* capture;           // [slot][C][4][E3] or nullptr
+    unsigned long long* cnt;   // CNT_N
+    unsigned long long* err;   // packed (tile_lin << 8 | code), atomicMin
+    int solid_words;
+};
+
+__constant__ Params P;
+
+// 18 ghost classes: 0..5 faces (-x,+x,-y,+y,-z,+z), 6..17 edges.
+__host__ __device__ inline int edge_class(int a, int b, int da, int db) {
+    const int pair = (a == 0) ? (b == 1 ? 0 : 1) : 2;
+    return 6 + 4 * pair + (da > 0 ? 1 : 0) + (db > 0 ? 2 : 0);
+}
+// out pattern (ox,oy,oz) in {-1,0,1}^3 with 1 or 2 non-zeros -> class
+__host__ __device__ inline int ghost_class(int ox, int oy, int oz) {
+    const int n = (ox != 0) + (oy != 0) + (oz != 0);
+    if (n == 1) {
+        if (ox) return ox > 0 ? 1 : 0;
+        if (oy) return oy > 0 ? 3 : 2;
+        return oz > 0 ? 5 : 4;
+    }
+    if (n == 2) {
+        if (!oz) return edge_class(0, 1, ox, oy);
+        if (!oy) return edge_class(0, 2, ox, oz);
+        return edge_class(1, 2, oy, oz);
+    }
+    return -1;
+}
+
+// RouteTab index of the pure face pattern for face 0..5.
+__host__ __device__ constexpr int face_pattern(int face) {
+    return face == 0 ? 12 : face == 1 ? 14 : face == 2 ? 10 : face == 3 ? 16 : face == 4 ? 4 : 22;
+}
+
+// Error key: earliest iteration, then lowest tile in coordinate order (the
+// 1-worker reference order), then code.  atomicMin keeps the first.
+__device__ __forceinline__ void atomic_err(unsigned long long* err, long iter, int tile_lin,
+                                           int code) {
+    atomicMin(err, ((unsigned long long)iter << 36) | ((unsigned long long)(unsigned)tile_lin << 4) |
+                       (unsigned)code);
+}
+
+__device__ __forceinline__ void warp_count(unsigned long long* c, bool pred) {
+    const unsigned m = __ballot_sync(0xffffffffu, pred);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(c, (unsigned long long)__popc(m));
+}
+
+// Extended-grid solid bit of the tile (local coords in [-1, E]).
+template <int E>
+__device__ __forceinline__ bool solid_at(const uint32_t* sb, int x, int y, int z) {
+    constexpr int G = E + 2;
+    const int idx = (x + 1) + G * ((y + 1) + G * (z + 1));
+    return (sb[idx >> 5] >> (idx & 31)) & 1u;
+}
+
+// proj/src/scenario.cpp:177-183 — seed containment at cell centres.
+__device__ __forceinline__ bool seed_contains(const SeedConst& s, double x, double y, double z) {
+    if (s.shape == 0)
+        return x >= s.lo[0] && x < s.hi[0] && y >= s.lo[1] && y < s.hi[1] && z >= s.lo[2] &&
+               z < s.hi[2];
+    const double dx = x - s.center[0], dy = y - s.center[1], dz = z - s.center[2];
+    return dx * dx + dy * dy + dz * dz <= s.r2;
+}
+
+// The last seed of component c containing the cell centre (apply_seeds order,
+// proj/src/engine.cpp:43-76), or -1.
+template <int E>
+__device__ __forceinline__ int seed_for(int c, const int* tc, int x, int y, int z) {
+    int hit = -1;
+    const double cx = double(tc[0] * E + x) + 0.5;
+    const double cy = double(tc[1] * E + y) + 0.5;
+    const double cz = double(tc[2] * E + z) + 0.5;
+    for (int s = 0; s < P.n_seeds; ++s)
+        if (P.seeds[s].comp == c && seed_contains(P.seeds[s], cx, cy, cz)) hit = s;
+    return hit;
+}
+
+// Generated f_in for GEN tiles: seeded equilibrium or ambient (create_tile,
+// proj/src/tilemap.cpp:132-140, then apply_seeds).  Also the velocity the
+// reference holds for that cell before its first collision.
+template <int E>
+__device__ __forceinline__ void gen_fin(int mode, int c, const int* tc, int x, int y, int z,
+                                        double* f, double& u0, double& u1, double& u2) {
+    const int s = (mode == MODE_GEN_SEEDED) ? seed_for<E>(c, tc, x, y, z) : -1;
+    if (s >= 0) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) f[i] = P.seeds[s].feq[i];
+        u0 = P.seeds[s].u[0];
+        u1 = P.seeds[s].u[1];
+        u2 = P.seeds[s].u[2];
+    } else {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) f[i] = P.comp[c].feq_amb[i];
+        u0 = u1 = u2 = 0.0;
+    }
+}
+
+// Per-CTA routing table: slot for each out pattern (ox+1)+3(oy+1)+9(oz+1).
+struct RouteTab {
+    int s[27];
+};
+__device__ __forceinline__ void load_routes(RouteTab& rt, const int* routes, int self, int amb) {
+    for (int k = threadIdx.x; k < 27; k += blockDim.x) {
+        const int ox = k % 3 - 1, oy = (k / 3) % 3 - 1, oz = k / 9 - 1;
+        const int cls = ghost_class(ox, oy, oz);
+        rt.s[k] = (ox == 0 && oy == 0 && oz == 0) ? self : (cls < 0 ? amb : routes[cls]);
+    }
+}
+
+// Pull of one cell's 19 populations of component c from f_post (the
+// reference's P4a ghost fill + stream_pull, proj/src/kernels.cpp:5-30):
+//   f_in[i](x) = solid(x - e_i) ? f_post(x)[opp i] : f_post(route(x - e_i))[i]
+template <int E>
+__device__ __forceinline__ void pull_cell(const double* __restrict__ fp, const RouteTab& rt,
+                                          int self, int c, bool hs, const uint32_t* sb, int x,
+                                          int y, int z, double* f) {
+    constexpr int E3 = E * E * E;
+    const size_t cs = size_t(Q) * E3;
+    const int C = P.C;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+        const int sx = x - ex_(i), sy = y - ey_(i), sz = z - ez_(i);
+        const int ox = sx < 0 ? -1 : (sx >= E ? 1 : 0);
+        const int oy = sy < 0 ? -1 : (sy >= E ? 1 : 0);
+        const int oz = sz < 0 ? -1 : (sz >= E ? 1 : 0);
+        int slot = rt.s[(ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)];
+        int cell = ((sz & (E - 1)) * E + (sy & (E - 1))) * E + (sx & (E - 1));
+        int dir = i;
+        if (hs && solid_at<E>(sb, sx, sy, sz)) {
+            slot = self;
+            cell = (z * E + y) * E + x;
+            dir = opp_(i);
+        }
+        f[i] = __ldg(fp + (size_t(slot) * C + c) * cs + size_t(dir) * E3 + cell);
+    }
+}
+
+// f_in for any mode (u is only meaningful for GEN modes).
+template <int E>
+__device__ __forceinline__ void fin_cell(const Dev& d, const double* fp, const RouteTab& rt,
+                                         int self, int mode, const int* tc, int c, bool hs,
+                                         const uint32_t* sb, int x, int y, int z, double* f,
+                                         double& u0, double& u1, double& u2) {
+    if (mode == MODE_PULL) {
+        pull_cell<E>(fp, rt, self, c, hs, sb, x, y, z, f);
+    } else {
+        gen_fin<E>(mode, c, tc, x, y, z, f, u0, u1, u2);
+    }
+}
+
+// Face-layer index helpers: face f = 2*axis + (dir > 0); the in-face index
+// uses the two remaining coordinates in increasing axis order.
+template <int E>
+__device__ __forceinline__ int face_index(int face, int x, int y, int z) {
+    const int axis = face >> 1;
+    return axis == 0 ? (y + E * z) : (axis == 1 ? (x + E * z) : (x + E * y));
+}
+
+// psi at an out-of-tile cell (local coords with 1 or 2 axes outside) from the
+// routed tile's face buffer (P2 ghost fill, proj/src/engine.cpp:317-352).
+template <int E>
+__device__ __forceinline__ double psi_ghost(const Dev& d, const RouteTab& rt, int c, bool hs,
+                                            const uint32_t* sb, int x, int y, int z) {
+    if (hs && solid_at<E>(sb, x, y, z)) return 0.0;
+    const int ox = x < 0 ? -1 : (x >= E ? 1 : 0);
+    const int oy = y < 0 ? -1 : (y >= E ? 1 : 0);
+    const int oz = z < 0 ? -1 : (z >= E ? 1 : 0);
+    const int slot = rt.s[(ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)];
+    // the cell lies on the routed tile's face opposite our first out axis
+    int face;
+    if (ox) face = ox > 0 ? 0 : 1;
+    else if (oy) face = oy > 0 ? 2 : 3;
+    else face = oz > 0 ? 4 : 5;
+    const int lx = x & (E - 1), ly = y & (E - 1), lz = z & (E - 1);
+    constexpr int E2 = E * E;
+    return d.psi_face[((size_t(slot) * P.C + c) * 6 + face) * E2 + face_index<E>(face, lx, ly, lz)];
+}
+
+// ---------------------------------------------------------------------------
+// k_main: one CTA = one tile x one z-chunk of BZ planes.
+// NOPSI: every component is psi-free and uncoupled (e.g. single-component
+// ideal gas) so no pseudo-potential stencil is needed at all.
+template <int E, int C, int BZ, int NT, bool NOPSI>
+__global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ active, int src_buf,
+                                             int write_uface, long iter) {
+    constexpr int G = E + 2;
+    constexpr int GG = G * G;
+    constexpr int E2 = E * E;
+    constexpr int E3 = E * E * E;
+    constexpr int NZC = E / BZ;
+    constexpr int CPT = (E2 + NT - 1) / NT;  // cells per thread per plane
+    extern __shared__ double smem[];
+    double* psi = smem;  // [3][C][GG] ring of planes (unused when NOPSI)
+    __shared__ RouteTab rt_pull, rt_psi;
+    __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
+    __shared__ int s_tc[3];
+
+    const int slot = active[blockIdx.x / NZC];
+    const int z0 = (blockIdx.x % NZC) * BZ;
+    const uint8_t mode = d.mode[slot];
+    const bool hs = d.has_solid[slot] != 0;
+    const int amb = P.amb_slot;
+    const double* __restrict__ fp = d.f[src_buf];
+    double* __restrict__ fo = d.f[src_buf ^ 1];
+    load_routes(rt_pull, d.route[ROUTE_PULL] + size_t(slot) * 18, slot, amb);
+    load_routes(rt_psi, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, amb);
+    if (threadIdx.x < 3) s_tc[threadIdx.x] = d.coords[slot * 3 + threadIdx.x];
+    if (hs)
+        for (int k = threadIdx.x; k < d.solid_words; k += NT)
+            s_solid[k] = d.solid[size_t(slot) * d.solid_words + k];
+    __syncthreads();
+    const int tile_lin = (s_tc[0] * P.grid[1] + s_tc[1]) * P.grid[2] + s_tc[2];
+
+    // ---- psi of plane pz (ring slot r) incl. the xy ghost ring -------------
+    auto psi_plane = [&](int pz) {
+        const int r = (pz + 3) % 3;
+        const bool inside = pz >= 0 && pz < E;
+        const bool owned = pz >= z0 && pz < z0 + BZ;
+        int negs = 0, clamps = 0;  // per-thread tallies, reduced per warp below
+#pragma unroll 1
+        for (int k = 0; k < CPT; ++k) {
+            const int idx = threadIdx.x + k * NT;
+            if (idx >= E2) break;
+            const int x = idx % E, y = idx / E;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                double v = 0.0;
+                if (!inside) {
+                    v = psi_ghost<E>(d, rt_psi, c, hs, s_solid, x, y, pz);
+                } else if (!(hs && solid_at<E>(s_solid, x, y, pz))) {
+                    double f[Q], u0, u1, u2;
+                    fin_cell<E>(d, fp, rt_pull, slot, mode, s_tc, c, hs, s_solid, x, y, pz, f,
+                                u0, u1, u2);
+                    double rho = 0.0;
+#pragma unroll
+                    for (int i = 0; i < Q; ++i) {
+                        rho += f[i];
+                        if (owned && f[i] < 0.0) ++negs;
+                    }
+                    const CompConst& kc = P.comp[c];
+                    if (!isfinite(rho)) {
+                        atomic_err(d.err, iter, tile_lin, ERR_P1_NAN);
+                    } else {
+                        double press;
+                        if (!pr_pressure(rho, kc, press)) {
+                            atomic_err(d.err, iter, tile_lin, ERR_P1_POLE);
+                        } else {
+                            bool cl;
+                            v = pseudo_potential(rho, press, kc, cl);
+                            if (owned && cl) ++clamps;
+                        }
+                    }
+                }
+                psi[(r * C + c) * GG + (x + 1) + G * (y + 1)] = v;
+            }
+        }
+        // ghost ring of this plane: 4E+4 positions
+        for (int k = threadIdx.x; k < 4 * E + 4; k += NT) {
+            int x, y;
+            if (k < G) { x = k - 1; y = -1; }
+            else if (k < 2 * G) { x = k - G - 1; y = E; }
+            else if (k < 2 * G + E) { x = -1; y = k - 2 * G; }
+            else { x = E; y = k - 2 * G - E; }
+            const bool corner3 = !inside && (x < 0 || x >= E) && (y < 0 || y >= E);
+#pragma unroll
+            for (int c = 0; c < C; ++c)
+                psi[(r * C + c) * GG + (x + 1) + G * (y + 1)] =
+                    corner3 ? 0.0 : psi_ghost<E>(d, rt_psi, c, hs, s_solid, x, y, pz);
+        }
+        if (owned) {
+            const unsigned m1 = __reduce_add_sync(0xffffffffu, (unsigned)negs);
+            const unsigned m2 = __reduce_add_sync(0xffffffffu, (unsigned)clamps);
+            if ((threadIdx.x & 31) == 0) {
+                if (m1) atomicAdd(&d.cnt[CNT_NEG], (unsigned long long)m1);
+                if (m2) atomicAdd(&d.cnt[CNT_CLAMP], (unsigned long long)m2);
+            }
+        }
+    };
+
+    // ---- collide plane z ----------------------------------------------------
+    auto collide_plane = [&](int z) {
+        int zero_rho = 0;
+        int negs = 0;
+#pragma unroll 1
+        for (int k = 0; k < CPT; ++k) {
+            const int idx = threadIdx.x + k * NT;
+            if (idx >= E2) break;
+            const int x = idx % E, y = idx / E;
+            if (hs && solid_at<E>(s_solid, x, y, z)) continue;
+            const int cell = (z * E + y) * E + x;
+            const int rc = (z + 3) % 3, rm = (z + 2) % 3, rp = (z + 4) % 3;
+            const int pc = (x + 1) + G * (y + 1);
+#pragma unroll 1
+            for (int c = 0; c < C; ++c) {
+                double f[Q];
+                double u0 = 0.0, u1 = 0.0, u2 = 0.0, rho;
+                fin_cell<E>(d, fp, rt_pull, slot, mode, s_tc, c, hs, s_solid, x, y, z, f, u0, u1,
+                            u2);
+                if (mode == MODE_PULL) {
+                    moments(f, rho, u0, u1, u2);
+                } else {
+                    rho = sum19(f);  // P1 density; u is the stored seed/ambient u
+                }
+                if constexpr (NOPSI) {
+                    // P1 tallies folded in: psi is +-0 (no clamps, no pole), so
+                    // only the negative-population count and the NaN check remain.
+#pragma unroll
+                    for (int i = 0; i < Q; ++i) negs += f[i] < 0.0;
+                    if (!isfinite(rho)) atomic_err(d.err, iter, tile_lin, ERR_P1_NAN);
+                }
+                const CompConst& kc = P.comp[c];
+                // ---- force: gravity + intra + inter (engine.cpp:426-448)
+                double F0 = 0.0, F1 = 0.0, F2 = 0.0;
+                if (kc.has_gravity) {
+                    F0 = rho * kc.gravity[0];
+                    F1 = rho * kc.gravity[1];
+                    F2 = rho * kc.gravity[2];
+                }
+                if constexpr (!NOPSI) {
+                    // intra_force, proj/src/physics.cpp:44-63
+                    const double* pm = psi + (rm * C + c) * GG + pc;
+                    const double* p0 = psi + (rc * C + c) * GG + pc;
+                    const double* pp = psi + (rp * C + c) * GG + pc;
+                    double s10 = 0.0, s11 = 0.0, s12 = 0.0, s20 = 0.0, s21 = 0.0, s22 = 0.0;
+                    auto nb = [&](int i) -> double {
+                        const int dx = ex_(i), dy = ey_(i), dz = ez_(i);
+                        const double* pl = dz < 0 ? pm : (dz > 0 ? pp : p0);
+                        return pl[dx + G * dy];
+                    };
+#pragma unroll
+                    for (int i = 1; i < Q; ++i) {
+                        const double pn = nb(i);
+                        const double w = w_(i);
+                        const double a1 = w * pn;
+                        const double a2 = a1 * pn;
+                        if (ex_(i) > 0) { s10 += a1; s20 += a2; }
+                        if (ex_(i) < 0) { s10 -= a1; s20 -= a2; }
+                        if (ey_(i) > 0) { s11 += a1; s21 += a2; }
+                        if (ey_(i) < 0) { s11 -= a1; s21 -= a2; }
+                        if (ez_(i) > 0) { s12 += a1; s22 += a2; }
+                        if (ez_(i) < 0) { s12 -= a1; s22 -= a2; }
+                    }
+                    const double c1 = kc.c1f * p0[0];
+                    const double c2 = kc.c2;
+                    F0 += c1 * s10 + c2 * s20;
+                    F1 += c1 * s11 + c2 * s21;
+                    F2 += c1 * s12 + c2 * s22;
+                    // inter_force, proj/src/physics.cpp:65-78
+#pragma unroll
+                    for (int c2i = 0; c2i < C; ++c2i) {
+                        if (c2i == c) continue;
+                        const double g = P.coupling[c * C + c2i];
+                        if (g == 0.0) continue;
+                        const double* qm = psi + (rm * C + c2i) * GG + pc;
+                        const double* q0 = psi + (rc * C + c2i) * GG + pc;
+                        const double* qp = psi + (rp * C + c2i) * GG + pc;
+                        double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+#pragma unroll
+                        for (int i = 1; i < Q; ++i) {
+                            const int dx = ex_(i), dy = ey_(i), dz = ez_(i);
+                            const double* pl = dz < 0 ? qm : (dz > 0 ? qp : q0);
+                            const double a1 = w_(i) * pl[dx + G * dy];
+                            if (dx > 0) t0 += a1;
+                            if (dx < 0) t0 -= a1;
+                            if (dy > 0) t1 += a1;
+                            if (dy < 0) t1 -= a1;
+                            if (dz > 0) t2 += a1;
+                            if (dz < 0) t2 -= a1;
+                        }
+                        const double cc = (-g) * p0[0];
+                        F0 += cc * t0;
+                        F1 += cc * t1;
+                        F2 += cc * t2;
+                    }
+                } else {
+                    // psi == +-0: the intra/inter terms are signed zeros
+                    F0 += 0.0;
+                    F1 += 0.0;
+                    F2 += 0.0;
+                }
+                // ---- u_prev bookkeeping for the criterion / capture
+                if (write_uface) {
+#pragma unroll
+                    for (int face = 0; face < 6; ++face) {
+                        const int axis = face >> 1;
+                        const int coord = axis == 0 ? x : (axis == 1 ? y : z);
+                        if (coord == ((face & 1) ? E - 1 : 0) && rt_psi.s[face_pattern(face)] == amb) {
+                            double* uf = d.u_face + ((size_t(slot) * C + c) * 6 + face) * 3 * E2;
+                            const int fi = face_index<E>(face, x, y, z);
+                            uf[fi] = u0;
+                            uf[E2 + fi] = u1;
+                            uf[2 * E2 + fi] = u2;
+                        }
+                    }
+                }
+                if (d.capture) {
+                    double* cp = d.capture + (size_t(slot) * C + c) * 4 * E3;
+                    // psi-free: radicand 2(+0)/(cs2 g) is a signed zero, sqrt keeps it
+                    cp[cell] = NOPSI ? (kc.cs2_g < 0.0 ? -0.0 : 0.0) : psi[(rc * C + c) * GG + pc];
+                    cp[E3 + cell] = u0;
+                    cp[2 * E3 + cell] = u1;
+                    cp[3 * E3 + cell] = u2;
+                }
+                // ---- collision (engine.cpp:450-475)
+                const double om = kc.omega;
+                double* out = fo + (size_t(slot) * C + c) * size_t(Q) * E3 + cell;
+                const double uu = u0 * u0 + u1 * u1 + u2 * u2;
+                const double t3 = (0.5 * uu) * 3.0;
+                const double wr0 = PLBM_W0 * rho, wr1 = PLBM_W1 * rho, wr2 = PLBM_W2 * rho;
+                const bool unforced = (F0 == 0.0 && F1 == 0.0 && F2 == 0.0);
+                if (!unforced && rho <= 0.0) ++zero_rho;
+                if (unforced || rho <= 0.0) {
+#define PLBM_RELAX(I)                                                                 \
+    {                                                                                 \
+        const double wr = (I == 0) ? wr0 : ((I <= 6) ? wr1 : wr2);                    \
+        const double eu = (I == 0) ? 0.0 : eu_pair<(I == 0 ? 1 : I - ((I + 1) & 1))>(u0, u1, u2); \
+        const double e0 = feq_dir<I>(wr, eu, t3);                                     \
+        out[size_t(I) * E3] = f[I] + om * (e0 - f[I]);                                \
+    }
+                    PLBM_RELAX(0) PLBM_RELAX(1) PLBM_RELAX(2) PLBM_RELAX(3) PLBM_RELAX(4)
+                    PLBM_RELAX(5) PLBM_RELAX(6) PLBM_RELAX(7) PLBM_RELAX(8) PLBM_RELAX(9)
+                    PLBM_RELAX(10) PLBM_RELAX(11) PLBM_RELAX(12) PLBM_RELAX(13) PLBM_RELAX(14)
+                    PLBM_RELAX(15) PLBM_RELAX(16) PLBM_RELAX(17) PLBM_RELAX(18)
+#undef PLBM_RELAX
+                } else {
+                    const double v0 = u0 + F0 / rho, v1 = u1 + F1 / rho, v2 = u2 + F2 / rho;
+                    const double vv = v0 * v0 + v1 * v1 + v2 * v2;
+                    const double s3 = (0.5 * vv) * 3.0;
+#define PLBM_FORCED(I)                                                                \
+    {                                                                                 \
+        constexpr int IP = (I == 0 ? 1 : I - ((I + 1) & 1));                          \
+        const double wr = (I == 0) ? wr0 : ((I <= 6) ? wr1 : wr2);                    \
+        const double eu = (I == 0) ? 0.0 : eu_pair<IP>(u0, u1, u2);                   \
+        const double ev = (I == 0) ? 0.0 : eu_pair<IP>(v0, v1, v2);                   \
+        const double e0 = feq_dir<I>(wr, eu, t3);                                     \
+        const double e1 = feq_dir<I>(wr, ev, s3);                                     \
+        out[size_t(I) * E3] = f[I] + ((om * (e0 - f[I]) + e1) - e0);                  \
+    }
+                    PLBM_FORCED(0) PLBM_FORCED(1) PLBM_FORCED(2) PLBM_FORCED(3) PLBM_FORCED(4)
+                    PLBM_FORCED(5) PLBM_FORCED(6) PLBM_FORCED(7) PLBM_FORCED(8) PLBM_FORCED(9)
+                    PLBM_FORCED(10) PLBM_FORCED(11) PLBM_FORCED(12) PLBM_FORCED(13)
+                    PLBM_FORCED(14) PLBM_FORCED(15) PLBM_FORCED(16) PLBM_FORCED(17)
+                    PLBM_FORCED(18)
+#undef PLBM_FORCED
+                }
+            }
+        }
+        const unsigned zr = __reduce_add_sync(0xffffffffu, (unsigned)zero_rho);
+        if ((threadIdx.x & 31) == 0 && zr) atomicAdd(&d.cnt[CNT_ZERO_RHO], (unsigned long long)zr);
+        if constexpr (NOPSI) {
+            const unsigned ng = __reduce_add_sync(0xffffffffu, (unsigned)negs);
+            if ((threadIdx.x & 31) == 0 && ng) atomicAdd(&d.cnt[CNT_NEG], (unsigned long long)ng);
+        }
+    };
+
+    if constexpr (NOPSI) {
+        (void)psi;
+#pragma unroll 1
+        for (int z = z0; z < z0 + BZ; ++z) collide_plane(z);
+    } else {
+        psi_plane(z0 - 1);
+        psi_plane(z0);
+#pragma unroll 1
+        for (int z = z0; z < z0 + BZ; ++z) {
+            psi_plane(z + 1);
+            __syncthreads();
+            collide_plane(z);
+            __syncthreads();
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_face: moments of f_in^(k+1) on the six face layers of every active tile.
+// Writes psi_face for the next step and evaluates the activation criterion
+// (proj/src/tilemap.cpp:182-218) plus the P5 NaN check (engine.cpp:509-512).
+template <int E, int C, int NT>
+__global__ void __launch_bounds__(NT) k_face(Dev d, const int* __restrict__ active, int src_buf,
+                                             int flags, long iter) {
+    const bool criterion = flags & 1;  // evaluate the activation criterion
+    const bool nan_check = flags & 2;  // P5 NaN check of the moments
+    constexpr int E2 = E * E;
+    constexpr int G = E + 2;
+    __shared__ RouteTab rt;
+    __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
+    __shared__ int s_tc[3];
+    __shared__ int s_fired;
+    const int slot = active[blockIdx.x / 6];
+    const int face = blockIdx.x % 6;
+    const uint8_t mode = d.mode[slot];
+    const bool hs = d.has_solid[slot] != 0;
+    const int amb = P.amb_slot;
+    // after k_main every tile pulls with the map it just stepped on (ROUTE_PSI)
+    load_routes(rt, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, amb);
+    if (threadIdx.x < 3) s_tc[threadIdx.x] = d.coords[slot * 3 + threadIdx.x];
+    if (threadIdx.x == 0) s_fired = 0;
+    if (hs)
+        for (int k = threadIdx.x; k < d.solid_words; k += NT)
+            s_solid[k] = d.solid[size_t(slot) * d.solid_words + k];
+    __syncthreads();
+    const int tile_lin = (s_tc[0] * P.grid[1] + s_tc[1]) * P.grid[2] + s_tc[2];
+    const bool frontier = criterion && (d.route[ROUTE_PSI][size_t(slot) * 18 + face] == amb);
+    const double* __restrict__ fp = d.f[src_buf];
+    const int axis = face >> 1;
+    const int fixed = (face & 1) ? E - 1 : 0;
+    bool fired = false;
+    for (int idx = threadIdx.x; idx < E2; idx += NT) {
+        const int a = idx % E, b = idx / E;
+        const int x = axis == 0 ? fixed : a;
+        const int y = axis == 0 ? a : (axis == 1 ? fixed : b);
+        const int z = axis == 2 ? fixed : b;
+        const bool sol = hs && solid_at<E>(s_solid, x, y, z);
+#pragma unroll 1
+        for (int c = 0; c < C; ++c) {
+            double v = 0.0;
+            if (!sol) {
+                double f[Q], u0 = 0.0, u1 = 0.0, u2 = 0.0, rho;
+                fin_cell<E>(d, fp, rt, slot, mode, s_tc, c, hs, s_solid, x, y, z, f, u0, u1, u2);
+                if (mode == MODE_PULL) moments(f, rho, u0, u1, u2);
+                else rho = sum19(f);
+                if (nan_check && (!isfinite(rho) || !isfinite(u0) || !isfinite(u1) || !isfinite(u2)))
+                    atomic_err(d.err, iter, tile_lin, ERR_P5_NAN);
+                if (frontier && !fired) {
+                    const double* uf = d.u_face + ((size_t(slot) * C + c) * 6 + face) * 3 * E2;
+                    const double dx = u0 - uf[idx], dy = u1 - uf[E2 + idx], dz = u2 - uf[2 * E2 + idx];
+                    if (dx * dx + dy * dy + dz * dz > P.s2) fired = true;
+                }
+                const CompConst& kc = P.comp[c];
+                double press;
+                if (isfinite(rho) && pr_pressure(rho, kc, press)) {
+                    bool cl;
+                    v = pseudo_potential(rho, press, kc, cl);
+                }
+            }
+            d.psi_face[((size_t(slot) * C + c) * 6 + face) * E2 + idx] = v;
+        }
+    }
+    if (__any_sync(0xffffffffu, fired) && (threadIdx.x & 31) == 0) s_fired = 1;
+    __syncthreads();
+    if (threadIdx.x == 0 && s_fired) atomicOr((unsigned*)(d.trig) + slot / 4, 1u << (8 * (slot % 4) + face));
+}
+
+// Newborn / ambient face buffers: psi of the ambient-equilibrium cell.
+template <int E>
+__global__ void k_face_ambient(Dev d, const int* __restrict__ slots, int n) {
+    constexpr int E2 = E * E;
+    const int k = blockIdx.x;
+    if (k >= n) return;
+    const int slot = slots[k];
+    for (int idx = threadIdx.x; idx < 6 * E2; idx += blockDim.x)
+        for (int c = 0; c < P.C; ++c)
+            d.psi_face[(size_t(slot) * P.C + c) * 6 * E2 + idx] = P.comp[c].psi_nb;
+}
+
+// Reference-view read-back of one tile (f_read, rho, u) into out:
+// [19*E3 f][E3 rho][E3 ux][E3 uy][E3 uz]
+template <int E>
+__global__ void k_readback(Dev d, int slot, int c, int src_buf, int fresh_birth, double* out) {
+    constexpr int E3 = E * E * E;
+    constexpr int G = E + 2;
+    __shared__ RouteTab rt;
+    __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
+    __shared__ int s_tc[3];
+    const uint8_t mode = d.mode[slot];
+    const bool hs = d.has_solid[slot] != 0;
+    load_routes(rt, d.route[ROUTE_PULL] + size_t(slot) * 18, slot, P.amb_slot);
+    if (threadIdx.x < 3) s_tc[threadIdx.x] = d.coords[slot * 3 + threadIdx.x];
+    if (hs)
+        for (int k = threadIdx.x; k < d.solid_words; k += blockDim.x)
+            s_solid[k] = d.solid[size_t(slot) * d.solid_words + k];
+    __syncthreads();
+    const double* fp = d.f[src_buf];
+    for (int cell = blockIdx.x * blockDim.x + threadIdx.x; cell < E3; cell += gridDim.x * blockDim.x) {
+        const int x = cell % E, y = (cell / E) % E, z = cell / (E * E);
+        double f[Q], u0 = 0.0, u1 = 0.0, u2 = 0.0, rho = 0.0;
+        const bool sol = hs && solid_at<E>(s_solid, x, y, z);
+        if (sol) {
+            for (int i = 0; i < Q; ++i) f[i] = P.comp[c].feq_amb[i];
+        } else if (mode == MODE_PULL) {
+            pull_cell<E>(fp, rt, slot, c, hs, s_solid, x, y, z, f);
+            moments(f, rho, u0, u1, u2);
+        } else {
+            gen_fin<E>(mode, c, s_tc, x, y, z, f, u0, u1, u2);
+            // stored density: seed rho / rho_ambient (create_tile + apply_seeds)
+            const int s = mode == MODE_GEN_SEEDED ? seed_for<E>(c, s_tc, x, y, z) : -1;
+            rho = s >= 0 ? P.seeds[s].rho : P.comp[c].rho_amb;
+        }
+        for (int i = 0; i < Q; ++i) out[size_t(i) * E3 + cell] = f[i];
+        out[size_t(19) * E3 + cell] = rho;
+        out[size_t(20) * E3 + cell] = u0;
+        out[size_t(21) * E3 + cell] = u1;
+        out[size_t(22) * E3 + cell] = u2;
+    }
+    (void)fresh_birth;
+}
+
+}  // namespace plbm

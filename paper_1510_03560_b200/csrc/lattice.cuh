@@ -1,0 +1,178 @@
+// lattice.cuh — D3Q19 lattice + multiphase closure as sm_100a device code.
+//
+// Every function reproduces the reference's floating-point expression tree
+// exactly (the translation unit is compiled with -fmad=false, so nvcc never
+// contracts a multiply-add), which is what makes the B200 engine bit-identical
+// to the CPU reference in FP64.  Algebraic shortcuts are used only where they
+// are provably bit-neutral:
+//   * e_i components are in {-1,0,+1}: a product with 0 contributes a signed
+//     zero that can never change a non-zero running sum, and a product with
+//     +-1 is exact, so those terms are folded at compile time;
+//   * opposite velocity pairs share |e.u| and (e.u)^2 exactly (IEEE rounding
+//     is sign-symmetric), so each pair evaluates the quadratic term once;
+//   * ideal-like EOS (a = b = 0) reduces pr_pressure to (rho R) T exactly.
+// The reference expression each function restates is cited inline.
+#pragma once
+
+#include <cstdint>
+
+namespace plbm {
+
+constexpr int Q = 19;
+
+// proj/src/stencil.cpp:21-34 — velocity order (part of the parity contract).
+__host__ __device__ constexpr int ex_(int i) {
+    constexpr int t[Q] = {0, 1, -1, 0, 0, 0, 0, 1, -1, 1, -1, 1, -1, 1, -1, 0, 0, 0, 0};
+    return t[i];
+}
+__host__ __device__ constexpr int ey_(int i) {
+    constexpr int t[Q] = {0, 0, 0, 1, -1, 0, 0, 1, -1, -1, 1, 0, 0, 0, 0, 1, -1, 1, -1};
+    return t[i];
+}
+__host__ __device__ constexpr int ez_(int i) {
+    constexpr int t[Q] = {0, 0, 0, 0, 0, 1, -1, 0, 0, 0, 0, 1, -1, -1, 1, 1, -1, -1, 1};
+    return t[i];
+}
+// proj/src/stencil.cpp:57-69 (derived opposite map).
+__host__ __device__ constexpr int opp_(int i) {
+    constexpr int t[Q] = {0, 2, 1, 4, 3, 6, 5, 8, 7, 10, 9, 12, 11, 14, 13, 16, 15, 18, 17};
+    return t[i];
+}
+// weight class: 0 -> 1/3, 1 -> 1/18, 2 -> 1/36
+__host__ __device__ constexpr int wclass_(int i) { return i == 0 ? 0 : (i <= 6 ? 1 : 2); }
+
+#define PLBM_W0 (1.0 / 3.0)
+#define PLBM_W1 (1.0 / 18.0)
+#define PLBM_W2 (1.0 / 36.0)
+#define PLBM_CS2 (1.0 / 3.0)
+
+__host__ __device__ constexpr double w_(int i) {
+    return i == 0 ? PLBM_W0 : (i <= 6 ? PLBM_W1 : PLBM_W2);
+}
+
+// Per-component constants (host-precomputed with the same IEEE operations
+// as the reference computes them per call).
+struct CompConst {
+    double omega;        // 1.0 / tau                    (engine.cpp:419)
+    double gravity[3];
+    int has_gravity;     // engine.cpp:416-418
+    int psi_free;        // a=b=0, R=1, T=cs2  =>  psi == +-0 everywhere
+    int ideal;           // a == 0 && b == 0
+    int pad;
+    double R, T, b;      // EOS
+    double a_theta;      // a * theta                    (physics.cpp:22-24)
+    double two_b, b_b;   // 2b, b*b                      (physics.cpp:25)
+    double cs2_g;        // cs2 * g_self                 (physics.cpp:36)
+    double c1f;          // -beta * g_self               (physics.cpp:59)
+    double c2;           // -0.5 * (1 - beta) * g_self   (physics.cpp:60)
+    double rho_amb, psi_amb, psi_nb; // ambient rho/psi; psi of a newborn cell
+    double feq_amb[Q];   // equilibrium at rest          (tilemap.cpp:13-28)
+};
+
+// proj/include/plbm/kernels.hpp:17-28 — f_eq(rho, u) for all 19 directions.
+// out_i = (w_i rho) * (((1 + eu*3) + ((0.5 eu) eu * 3) * 3) - (0.5 uu) * 3)
+__device__ __forceinline__ void equilibrium(double rho, double u0, double u1, double u2,
+                                            double* out) {
+    const double uu = u0 * u0 + u1 * u1 + u2 * u2;
+    const double t3 = (0.5 * uu) * 3.0;
+    const double wr0 = PLBM_W0 * rho, wr1 = PLBM_W1 * rho, wr2 = PLBM_W2 * rho;
+    out[0] = wr0 * (1.0 - t3);  // eu = +-0 for the rest vector
+    // + members of the 9 opposite pairs: 1,3,5,7,9,11,13,15,17
+    const double eus[9] = {u0, u1, u2, u0 + u1, u0 - u1, u0 + u2, u0 - u2, u1 + u2, u1 - u2};
+#pragma unroll
+    for (int p = 0; p < 9; ++p) {
+        const double eu = eus[p];
+        const double a = eu * 3.0;
+        const double b = (((0.5 * eu) * eu) * 3.0) * 3.0;
+        const double wr = p < 3 ? wr1 : wr2;
+        out[1 + 2 * p] = wr * (((1.0 + a) + b) - t3);
+        out[2 + 2 * p] = wr * (((1.0 - a) + b) - t3);
+    }
+}
+
+// Single-direction equilibrium, same tree as above (used on the fly).
+template <int I>
+__device__ __forceinline__ double feq_dir(double wr, double eu, double t3) {
+    if constexpr (I == 0) {
+        return wr * (1.0 - t3);
+    } else {
+        const double a = eu * 3.0;
+        const double b = (((0.5 * eu) * eu) * 3.0) * 3.0;
+        return (I & 1) ? wr * (((1.0 + a) + b) - t3) : wr * (((1.0 - a) + b) - t3);
+    }
+}
+
+// e_i . u for the "+" member of direction I's pair (exact; see header).
+template <int I>
+__device__ __forceinline__ double eu_pair(double u0, double u1, double u2) {
+    constexpr int p = (I - 1) / 2;
+    if constexpr (p == 0) return u0;
+    else if constexpr (p == 1) return u1;
+    else if constexpr (p == 2) return u2;
+    else if constexpr (p == 3) return u0 + u1;
+    else if constexpr (p == 4) return u0 - u1;
+    else if constexpr (p == 5) return u0 + u2;
+    else if constexpr (p == 6) return u0 - u2;
+    else if constexpr (p == 7) return u1 + u2;
+    else return u1 - u2;
+}
+
+// proj/include/plbm/kernels.hpp:31-48 — rho and momentum by sequential sums
+// (i order); zero-e terms are exact no-ops on a running sum that starts at +0.
+__device__ __forceinline__ void moments(const double* f, double& rho, double& u0, double& u1,
+                                        double& u2) {
+    double r = 0.0;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) r += f[i];
+    double m0 = 0.0;
+    m0 += f[1]; m0 -= f[2]; m0 += f[7]; m0 -= f[8]; m0 += f[9]; m0 -= f[10];
+    m0 += f[11]; m0 -= f[12]; m0 += f[13]; m0 -= f[14];
+    double m1 = 0.0;
+    m1 += f[3]; m1 -= f[4]; m1 += f[7]; m1 -= f[8]; m1 -= f[9]; m1 += f[10];
+    m1 += f[15]; m1 -= f[16]; m1 += f[17]; m1 -= f[18];
+    double m2 = 0.0;
+    m2 += f[5]; m2 -= f[6]; m2 += f[11]; m2 -= f[12]; m2 -= f[13]; m2 += f[14];
+    m2 += f[15]; m2 -= f[16]; m2 -= f[17]; m2 += f[18];
+    if (r != 0.0) {
+        u0 = m0 / r;
+        u1 = m1 / r;
+        u2 = m2 / r;
+    } else {
+        u0 = u1 = u2 = 0.0;
+    }
+    rho = r;
+}
+
+__device__ __forceinline__ double sum19(const double* f) {
+    double r = 0.0;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) r += f[i];
+    return r;
+}
+
+// proj/src/physics.cpp:12-27; returns false at the b*rho >= 1 pole.
+__device__ __forceinline__ bool pr_pressure(double rho, const CompConst& k, double& p) {
+    if (k.ideal) {  // a = b = 0: ideal/(1-0) - 0/(1+0-0) == (rho R) T exactly
+        p = (rho * k.R) * k.T;
+        return true;
+    }
+    if (k.b * rho >= 1.0) return false;
+    const double ideal = ((rho * k.R) * k.T) / (1.0 - k.b * rho);
+    const double attr = ((k.a_theta * rho) * rho) / ((1.0 + k.two_b * rho) - (k.b_b * rho) * rho);
+    p = ideal - attr;
+    return true;
+}
+
+// proj/src/physics.cpp:34-42; *clamped set on a negative radicand.
+__device__ __forceinline__ double pseudo_potential(double rho, double press, const CompConst& k,
+                                                   bool& clamped) {
+    const double radicand = (2.0 * (press - PLBM_CS2 * rho)) / k.cs2_g;
+    if (radicand < 0.0) {
+        clamped = true;
+        return 0.0;
+    }
+    clamped = false;
+    return sqrt(radicand);
+}
+
+}  // namespace plbm

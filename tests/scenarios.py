@@ -1,0 +1,78 @@
+"""Small parity scenarios (sizes the CPU oracle finishes in seconds).
+
+Each covers a different part of the path: ghost routing, progressive
+activation at S = 0 (rounding-noise driven) and S > 0, periodic
+self-neighbours, solids (bounce-back + solid ghost psi), gravity, placement
+on several simulated devices, two and three MPMC components.
+"""
+import numpy as np
+
+from paper_1510_03560_b200 import scenario as S
+
+
+def c1_progressive(extent=8, n=32, threshold=1e-12):
+    return S.config1(threshold=threshold, n=n, extent=extent)
+
+
+def c1_static(extent=8, n=32):
+    return S.config1(n=n, extent=extent, mode=S.MODE_STATIC)
+
+
+def mpmc_progressive(extent=16, n=32, threshold=1e-9, devices=1):
+    return S.mpmc_release(n=n, extent=extent, threshold=threshold, r_core=5, devices=devices)
+
+
+def mpmc_s0(extent=8, n=32):
+    return S.mpmc_release(n=n, extent=extent, threshold=0.0, r_core=5, devices=3)
+
+
+def periodic_solid_gravity(extent=8, n=32):
+    sc = S.config1(threshold=1e-12, n=n, extent=extent)
+    sc.periodic = (1, 0, 1)
+    sc.devices = 4
+    sc.policy = S.POLICY_SIMPLE
+    g = np.zeros((n, n, n), np.uint8)
+    g[:, :, 20:22] = 1
+    g[5:9, 3:30, 3:18] = 1
+    sc.geometry = g
+    sc.components[0].gravity = (1e-5, 0.0, -2e-5)
+    return sc
+
+
+def closed_box(n=32, extent=16):
+    """Acceptance criterion 2 shape (proj/tests/acceptance.cpp:206-237)."""
+    sc = S.Scenario(domain=(n, n, n), tile_extent=extent, mode=S.MODE_STATIC,
+                    components=[S.Component(tau=0.9)],
+                    seeds=[S.Seed(box_min=(8, 8, 8), box_max=(24, 24, 24), rho=1.2,
+                                  velocity=(0.04, 0.02, 0.01))])
+    g = np.zeros((n, n, n), np.uint8)
+    g[0, :, :] = g[-1, :, :] = g[:, 0, :] = g[:, -1, :] = g[:, :, 0] = g[:, :, -1] = 1
+    sc.geometry = g
+    return sc
+
+
+def mpmc3_static(extent=8, n=16):
+    return S.mpmc_release(n=n, extent=extent, mode=S.MODE_STATIC, r_core=3, n_components=3)
+
+
+def mpmc_periodic_solid(extent=8, n=32):
+    sc = S.mpmc_release(n=n, extent=extent, threshold=1e-10, r_core=5, devices=2)
+    sc.periodic = (0, 1, 0)
+    g = np.zeros((n, n, n), np.uint8)
+    g[:, 2:5, 24:28] = 1
+    sc.geometry = g
+    sc.components[1].gravity = (0.0, 0.0, -1e-6)
+    return sc
+
+
+ALL = {
+    "c1_progressive": (c1_progressive, 20),
+    "c1_static": (c1_static, 10),
+    "c1_progressive_S0": (lambda: c1_progressive(threshold=0.0), 12),
+    "mpmc_progressive_e16": (mpmc_progressive, 15),
+    "mpmc_s0_3dev": (mpmc_s0, 12),
+    "periodic_solid_gravity": (periodic_solid_gravity, 25),
+    "closed_box": (closed_box, 20),
+    "mpmc3_static": (mpmc3_static, 10),
+    "mpmc_periodic_solid": (mpmc_periodic_solid, 20),
+}
