@@ -175,6 +175,7 @@ class GpuEngine(StepEngine):
         lib.plbm_gpu_reset_kernel_stats.argtypes = [C.c_void_p]
         lib.plbm_gpu_stream.argtypes = [C.c_void_p]
         lib.plbm_gpu_stream.restype = C.c_void_p
+        lib.plbm_gpu_set_kernel_variant.argtypes = [C.c_void_p, C.c_int]
         if capture:
             self.set_capture(True)
 
@@ -192,6 +193,10 @@ class GpuEngine(StepEngine):
 
     def reset_kernel_stats(self) -> None:
         self.lib.plbm_gpu_reset_kernel_stats(self._h)
+
+    def set_kernel_variant(self, variant: int) -> None:
+        """0 = TMEM-stash cluster kernel where it applies, 1 = plain kernel."""
+        self.lib.plbm_gpu_set_kernel_variant(self._h, int(variant))
 
     def stream(self) -> int:
         return self.lib.plbm_gpu_stream(self._h)

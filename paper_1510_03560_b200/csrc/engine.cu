@@ -7,6 +7,7 @@
 // and placement (proj/src/assign.cpp:8-38, engine.cpp:30-41) run on this
 // mirror from the per-face trigger bits the device criterion produced.
 #include "kernels.cuh"
+#include "kernels_tm.cuh"
 #include "plbm_gpu.h"
 
 #include <cuda_runtime.h>
@@ -93,9 +94,30 @@ struct Kernels {
     void (*face)(Dev, const int*, int, int, long, dim3, cudaStream_t);
     void (*face_amb)(Dev, const int*, int, cudaStream_t);
     void (*readback)(Dev, int, int, int, double*, cudaStream_t);
+    void (*main_tm)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
     int nt, bz;
     size_t smem;
 };
+
+// The TMEM-stash cluster kernel serves E in {16, 32} with a psi stencil; the
+// plain kernel serves psi-free scenarios (no stencil: one pass already) and E = 8.
+template <int E, int C>
+void launch_tm(Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
+    using T = TmCfg<E, C>;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ntiles * T::NB);
+    cfg.blockDim = dim3(T::NT);
+    cfg.dynamicSmemBytes = T::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = T::NB;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_main_tm<E, C>, d, act, src, wu, it);
+}
 
 template <int E, int C, bool NOPSI>
 Kernels make_kernels() {
@@ -111,6 +133,12 @@ Kernels make_kernels() {
                              int(k.smem));
     k.main = [](Dev d, const int* act, int src, int wu, long it, dim3 g, dim3 b, size_t sm,
                 cudaStream_t s) { k_main<E, C, BZ, NT, NOPSI><<<g, b, sm, s>>>(d, act, src, wu, it); };
+    k.main_tm = nullptr;
+    if constexpr (!NOPSI && (E == 16 || E == 32)) {
+        cudaFuncSetAttribute(k_main_tm<E, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             TmCfg<E, C>::SMEM);
+        k.main_tm = launch_tm<E, C>;
+    }
     k.face = [](Dev d, const int* act, int src, int flags, long it, dim3 g, cudaStream_t s) {
         k_face<E, C, NT><<<g, NT, 0, s>>>(d, act, src, flags, it);
     };
@@ -184,6 +212,7 @@ class Engine {
     int set_capture(bool on);
     int poke_f(const int32_t* coords, int comp, int i, const int32_t* local, double v);
     void set_profiling(bool on) { profiling_ = on; }
+    void set_variant(int v) { use_tm_ = v == 0; }
     plbm_kernel_stats stats();
     void reset_stats() {
         resolve_events();
@@ -250,6 +279,7 @@ class Engine {
     int cur_ = 0;  // buffer holding the latest f_post (or unused before step 1)
     int solid_words_ = 0;
     bool profiling_ = false;
+    bool use_tm_ = true;
     plbm_kernel_stats stats_{};
     struct EvPair {
         cudaEvent_t a = nullptr, b = nullptr;
@@ -731,8 +761,11 @@ void Engine::launch_main(long iter) {
     const dim3 grid(unsigned(active_.size() * (E_ / K_.bz)));
     EvPair* ev = profiling_ ? &next_event(0, active_cells_) : nullptr;
     if (ev) CK(cudaEventRecord(ev->a, stream_));
-    K_.main(d_, d_active_, cur_, mode_ == PLBM_MODE_PROGRESSIVE ? 1 : 0, iter, grid, dim3(K_.nt),
-            K_.smem, stream_);
+    const int wu = mode_ == PLBM_MODE_PROGRESSIVE ? 1 : 0;
+    if (K_.main_tm && use_tm_)
+        K_.main_tm(d_, d_active_, cur_, wu, iter, unsigned(active_.size()), stream_);
+    else
+        K_.main(d_, d_active_, cur_, wu, iter, grid, dim3(K_.nt), K_.smem, stream_);
     CK(cudaGetLastError());
     ++stats_.kernels_launched;
     if (ev) CK(cudaEventRecord(ev->b, stream_));
@@ -1105,6 +1138,11 @@ void plbm_gpu_reset_kernel_stats(void* h) {
 }
 
 void* plbm_gpu_stream(void* h) { return static_cast<plbm::Engine*>(h)->stream(); }
+
+int plbm_gpu_set_kernel_variant(void* h, int variant) {
+    static_cast<plbm::Engine*>(h)->set_variant(variant);
+    return 0;
+}
 
 void plbm_gpu_destroy(void* h) { delete static_cast<plbm::Engine*>(h); }
 

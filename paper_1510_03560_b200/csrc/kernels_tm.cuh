@@ -1,0 +1,484 @@
+// kernels_tm.cuh — k_main_tm: the fused step kernel with a TMEM stash.
+//
+// Why: the Shan-Chen force needs psi of all 18 neighbours, and psi needs the
+// density of the POST-STREAM populations, so every cell's pulled f_in is used
+// twice — once for rho -> psi (one plane ahead), once for the collision.  The
+// plain kernel (k_main) pulls twice; the second pull misses L2 (reuse
+// distance ~90 MB chip-wide) and DRAM reads run at 2.4x the algorithmic
+// bytes.  Here the first pull is the only one: its 19*C doubles per cell go to
+// Tensor Memory (tcgen05.st, 32x32b, one TMEM lane per thread) and come back
+// for the collision two planes later (tcgen05.ld).  TMEM is 256 KB per SM that
+// this FP64 stencil otherwise never uses.
+//
+// Decomposition: one CTA = a 32 x 8 (x, y) column block of one 32^3 tile,
+// marching z over the whole tile; the four blocks of a tile form a thread-block
+// cluster and exchange their psi boundary rows through distributed shared
+// memory (no halo recompute).  Halo planes/rows outside the tile come from the
+// neighbours' face buffers (psi_face, k_face) through the ghost routing table.
+//
+// Pipeline per plane z (all on-chip except the f loads / stores):
+//   issue the pull loads of plane z+2           (in flight during the collide)
+//   collide plane z  : f(z) <- TMEM slot z&1, psi planes z-1..z+1 from smem
+//   rho/psi of plane z+2 -> smem ring slot (z+2)&3; f(z+2) -> TMEM slot z&1
+//   cluster barrier; copy the neighbour blocks' boundary rows of psi(z+2)
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "kernels.cuh"
+
+namespace plbm {
+
+namespace cg = cooperative_groups;
+
+template <int E, int C>
+struct TmCfg {
+    static constexpr int NT = 256;
+    static constexpr int BY = NT / E;            // rows per CTA
+    static constexpr int NB = E / BY;            // CTAs per tile = cluster size
+    static constexpr int CB = 40;                // TMEM columns per component (38 used)
+    static constexpr int SCOLS = CB * C;         // TMEM columns per stash slot
+    static constexpr int WCOLS = 2 * SCOLS;      // two slots per thread
+    static constexpr int NCOLS = (2 * WCOLS <= 256) ? 256 : 512;  // 2 warps per lane quarter
+    static constexpr int HALF = NCOLS / 2;
+    static constexpr int PW = E + 2;             // psi plane row pitch (x + ring)
+    static constexpr int PH = BY + 2;
+    static constexpr int PP = PW * PH;
+    static constexpr int PSI_BYTES = 4 * C * PP * 8;
+    // >= 116 KB of dynamic shared memory pins one CTA per SM, so a CTA that
+    // waits in tcgen05.alloc can never block a co-resident cluster peer.
+    static constexpr int SMEM = PSI_BYTES > 118 * 1024 ? PSI_BYTES : 118 * 1024;
+    static_assert(WCOLS <= HALF, "TMEM stash does not fit");
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 19 doubles = 38 TMEM columns of this thread's lane, written as 32x32b
+// x8,x8,x8,x8,x4,x2 chunks at offsets aligned to the chunk width (each
+// component block starts on an 8-column boundary: CB = 40 columns).
+#define PLBM_TM_ST8(A, R, o)                                                                     \
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" \
+                 ::"r"(A), "r"(R[o]), "r"(R[o + 1]), "r"(R[o + 2]), "r"(R[o + 3]), "r"(R[o + 4]), \
+                 "r"(R[o + 5]), "r"(R[o + 6]), "r"(R[o + 7]))
+#define PLBM_TM_LD8(A, R, o)                                                                     \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n" \
+                 : "=r"(R[o]), "=r"(R[o + 1]), "=r"(R[o + 2]), "=r"(R[o + 3]), "=r"(R[o + 4]),    \
+                   "=r"(R[o + 5]), "=r"(R[o + 6]), "=r"(R[o + 7])                                 \
+                 : "r"(A))
+
+__device__ __forceinline__ void tm_store19(uint32_t taddr, const double* f) {
+    uint32_t r[38];
+#pragma unroll
+    for (int i = 0; i < 19; ++i) {
+        r[2 * i] = uint32_t(__double2loint(f[i]));
+        r[2 * i + 1] = uint32_t(__double2hiint(f[i]));
+    }
+    PLBM_TM_ST8(taddr, r, 0);
+    PLBM_TM_ST8(taddr + 8, r, 8);
+    PLBM_TM_ST8(taddr + 16, r, 16);
+    PLBM_TM_ST8(taddr + 24, r, 24);
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(taddr + 32),
+                 "r"(r[32]), "r"(r[33]), "r"(r[34]), "r"(r[35]));
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(taddr + 36),
+                 "r"(r[36]), "r"(r[37]));
+}
+
+__device__ __forceinline__ void tm_load19(uint32_t taddr, double* f) {
+    uint32_t r[38];
+    PLBM_TM_LD8(taddr, r, 0);
+    PLBM_TM_LD8(taddr + 8, r, 8);
+    PLBM_TM_LD8(taddr + 16, r, 16);
+    PLBM_TM_LD8(taddr + 24, r, 24);
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35])
+                 : "r"(taddr + 32));
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];\n"
+                 : "=r"(r[36]), "=r"(r[37])
+                 : "r"(taddr + 36));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 19; ++i) f[i] = __hiloint2double(int(r[2 * i + 1]), int(r[2 * i]));
+}
+
+// One component's collision at one cell (engine.cpp:420-476): gravity +
+// intra + inter force, then BGK with the velocity-shift forcing.  psi is a
+// [C] array of plane pointers at the cell centre for planes z-1, z, z+1.
+template <int C, int PW>
+__device__ __forceinline__ void collide_comp(const double* f, double rho, double u0, double u1,
+                                             double u2, int c, const double* const* pm,
+                                             const double* const* p0, const double* const* pp,
+                                             double* out, size_t dstride, int& zero_rho) {
+    const CompConst& kc = P.comp[c];
+    double F0 = 0.0, F1 = 0.0, F2 = 0.0;
+    if (kc.has_gravity) {
+        F0 = rho * kc.gravity[0];
+        F1 = rho * kc.gravity[1];
+        F2 = rho * kc.gravity[2];
+    }
+    {  // intra_force, proj/src/physics.cpp:44-63
+        double s10 = 0.0, s11 = 0.0, s12 = 0.0, s20 = 0.0, s21 = 0.0, s22 = 0.0;
+#pragma unroll
+        for (int i = 1; i < Q; ++i) {
+            const int dx = ex_(i), dy = ey_(i), dz = ez_(i);
+            const double* pl = dz < 0 ? pm[c] : (dz > 0 ? pp[c] : p0[c]);
+            const double pn = pl[dx + PW * dy];
+            const double a1 = w_(i) * pn;
+            const double a2 = a1 * pn;
+            if (dx > 0) { s10 += a1; s20 += a2; }
+            if (dx < 0) { s10 -= a1; s20 -= a2; }
+            if (dy > 0) { s11 += a1; s21 += a2; }
+            if (dy < 0) { s11 -= a1; s21 -= a2; }
+            if (dz > 0) { s12 += a1; s22 += a2; }
+            if (dz < 0) { s12 -= a1; s22 -= a2; }
+        }
+        const double c1 = kc.c1f * p0[c][0];
+        const double c2 = kc.c2;
+        F0 += c1 * s10 + c2 * s20;
+        F1 += c1 * s11 + c2 * s21;
+        F2 += c1 * s12 + c2 * s22;
+    }
+#pragma unroll
+    for (int c2i = 0; c2i < C; ++c2i) {  // inter_force, proj/src/physics.cpp:65-78
+        if (c2i == c) continue;
+        const double g = P.coupling[c * C + c2i];
+        if (g == 0.0) continue;
+        double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+#pragma unroll
+        for (int i = 1; i < Q; ++i) {
+            const int dx = ex_(i), dy = ey_(i), dz = ez_(i);
+            const double* pl = dz < 0 ? pm[c2i] : (dz > 0 ? pp[c2i] : p0[c2i]);
+            const double a1 = w_(i) * pl[dx + PW * dy];
+            if (dx > 0) t0 += a1;
+            if (dx < 0) t0 -= a1;
+            if (dy > 0) t1 += a1;
+            if (dy < 0) t1 -= a1;
+            if (dz > 0) t2 += a1;
+            if (dz < 0) t2 -= a1;
+        }
+        const double cc = (-g) * p0[c][0];
+        F0 += cc * t0;
+        F1 += cc * t1;
+        F2 += cc * t2;
+    }
+    // ---- collision (engine.cpp:450-475)
+    const double om = kc.omega;
+    const double uu = u0 * u0 + u1 * u1 + u2 * u2;
+    const double t3 = (0.5 * uu) * 3.0;
+    const double wr0 = PLBM_W0 * rho, wr1 = PLBM_W1 * rho, wr2 = PLBM_W2 * rho;
+    const bool unforced = (F0 == 0.0 && F1 == 0.0 && F2 == 0.0);
+    if (!unforced && rho <= 0.0) ++zero_rho;
+    if (unforced || rho <= 0.0) {
+#define PLBM_TM_RELAX(I)                                                                      \
+    {                                                                                         \
+        constexpr int IP = (I == 0 ? 1 : I - ((I + 1) & 1));                                  \
+        const double wr = (I == 0) ? wr0 : ((I <= 6) ? wr1 : wr2);                            \
+        const double eu = (I == 0) ? 0.0 : eu_pair<IP>(u0, u1, u2);                           \
+        const double e0 = feq_dir<I>(wr, eu, t3);                                             \
+        out[size_t(I) * dstride] = f[I] + om * (e0 - f[I]);                                   \
+    }
+        PLBM_TM_RELAX(0) PLBM_TM_RELAX(1) PLBM_TM_RELAX(2) PLBM_TM_RELAX(3) PLBM_TM_RELAX(4)
+        PLBM_TM_RELAX(5) PLBM_TM_RELAX(6) PLBM_TM_RELAX(7) PLBM_TM_RELAX(8) PLBM_TM_RELAX(9)
+        PLBM_TM_RELAX(10) PLBM_TM_RELAX(11) PLBM_TM_RELAX(12) PLBM_TM_RELAX(13) PLBM_TM_RELAX(14)
+        PLBM_TM_RELAX(15) PLBM_TM_RELAX(16) PLBM_TM_RELAX(17) PLBM_TM_RELAX(18)
+#undef PLBM_TM_RELAX
+    } else {
+        const double v0 = u0 + F0 / rho, v1 = u1 + F1 / rho, v2 = u2 + F2 / rho;
+        const double vv = v0 * v0 + v1 * v1 + v2 * v2;
+        const double s3 = (0.5 * vv) * 3.0;
+#define PLBM_TM_FORCED(I)                                                                     \
+    {                                                                                         \
+        constexpr int IP = (I == 0 ? 1 : I - ((I + 1) & 1));                                  \
+        const double wr = (I == 0) ? wr0 : ((I <= 6) ? wr1 : wr2);                            \
+        const double eu = (I == 0) ? 0.0 : eu_pair<IP>(u0, u1, u2);                           \
+        const double ev = (I == 0) ? 0.0 : eu_pair<IP>(v0, v1, v2);                           \
+        const double e0 = feq_dir<I>(wr, eu, t3);                                             \
+        const double e1 = feq_dir<I>(wr, ev, s3);                                             \
+        out[size_t(I) * dstride] = f[I] + ((om * (e0 - f[I]) + e1) - e0);                     \
+    }
+        PLBM_TM_FORCED(0) PLBM_TM_FORCED(1) PLBM_TM_FORCED(2) PLBM_TM_FORCED(3)
+        PLBM_TM_FORCED(4) PLBM_TM_FORCED(5) PLBM_TM_FORCED(6) PLBM_TM_FORCED(7)
+        PLBM_TM_FORCED(8) PLBM_TM_FORCED(9) PLBM_TM_FORCED(10) PLBM_TM_FORCED(11)
+        PLBM_TM_FORCED(12) PLBM_TM_FORCED(13) PLBM_TM_FORCED(14) PLBM_TM_FORCED(15)
+        PLBM_TM_FORCED(16) PLBM_TM_FORCED(17) PLBM_TM_FORCED(18)
+#undef PLBM_TM_FORCED
+    }
+}
+
+// Seed / ambient velocity of a GEN-mode cell (the u the reference holds
+// before a tile's first collision).
+template <int E>
+__device__ __forceinline__ void gen_u(int mode, int c, const int* tc, int x, int y, int z,
+                                      double& u0, double& u1, double& u2) {
+    const int s = (mode == MODE_GEN_SEEDED) ? seed_for<E>(c, tc, x, y, z) : -1;
+    if (s >= 0) {
+        u0 = P.seeds[s].u[0];
+        u1 = P.seeds[s].u[1];
+        u2 = P.seeds[s].u[2];
+    } else {
+        u0 = u1 = u2 = 0.0;
+    }
+}
+
+template <int E, int C>
+__global__ void __launch_bounds__(256, 1) k_main_tm(Dev d, const int* __restrict__ active,
+                                                    int src_buf, int write_uface, long iter) {
+    using T = TmCfg<E, C>;
+    constexpr int NT = T::NT, BY = T::BY, NB = T::NB, PW = T::PW, PH = T::PH, PP = T::PP;
+    constexpr int G = E + 2;
+    constexpr int E2 = E * E;
+    constexpr int E3 = E * E * E;
+    extern __shared__ __align__(16) double smem[];
+    double* psi = smem;  // [4 ring slots][C][PH][PW]
+    __shared__ RouteTab rt_pull, rt_psi;
+    __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
+    __shared__ int s_tc[3];
+    __shared__ uint32_t s_tmem;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int tile_i = blockIdx.x / NB;
+    const int yb = blockIdx.x % NB;
+    const int y0 = yb * BY;
+    const int slot = active[tile_i];
+    const uint8_t mode = d.mode[slot];
+    const bool hs = d.has_solid[slot] != 0;
+    const int amb = P.amb_slot;
+    const double* __restrict__ fp = d.f[src_buf];
+    double* __restrict__ fo = d.f[src_buf ^ 1];
+
+    // ---- TMEM: one warp allocates, everyone reads the base after the fence
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                         smem_u32(&s_tmem)),
+                     "n"(T::NCOLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    load_routes(rt_pull, d.route[ROUTE_PULL] + size_t(slot) * 18, slot, amb);
+    load_routes(rt_psi, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, amb);
+    if (tid < 3) s_tc[tid] = d.coords[slot * 3 + tid];
+    if (hs)
+        for (int k = tid; k < d.solid_words; k += NT) s_solid[k] = d.solid[size_t(slot) * d.solid_words + k];
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tbase = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * T::HALF);
+    const int tile_lin = (s_tc[0] * P.grid[1] + s_tc[1]) * P.grid[2] + s_tc[2];
+
+    const int x = tid % E;
+    const int yl = tid / E;
+    const int y = y0 + yl;
+    const bool sol_xy_any = hs;  // per-plane solidity is looked up per z
+    auto pidx = [&](int ring, int c, int xx, int yy_local) {
+        return ((ring * C + c) * PH + (yy_local + 1)) * PW + (xx + 1);
+    };
+
+    // ---- psi of out-of-block positions -------------------------------------
+    // whole plane outside the tile in z (pz = -1 or E)
+    auto fill_zghost = [&](int pz) {
+        const int ring = pz & 3;
+        for (int k = tid; k < PP; k += NT) {
+            const int xx = k % PW - 1, yy = k / PW - 1 + y0;
+            const bool xo = xx < 0 || xx >= E, yo = yy < 0 || yy >= E;
+#pragma unroll
+            for (int c = 0; c < C; ++c)
+                psi[pidx(ring, c, xx, yy - y0)] =
+                    (xo && yo) ? 0.0 : psi_ghost<E>(d, rt_psi, c, hs, s_solid, xx, yy, pz);
+        }
+    };
+    // x ring (both sides, rows -1..BY) and y rows that lie outside the tile
+    auto fill_ring = [&](int pz) {
+        const int ring = pz & 3;
+        for (int k = tid; k < 2 * PH + 2 * E; k += NT) {
+            int xx, yyl;
+            if (k < 2 * PH) {
+                xx = (k & 1) ? E : -1;
+                yyl = (k >> 1) - 1;
+            } else {
+                const int q = k - 2 * PH;
+                xx = q % E;
+                yyl = (q / E) ? BY : -1;
+                const int yy = y0 + yyl;
+                if (yy >= 0 && yy < E) continue;  // in-tile row: cluster neighbour's
+            }
+#pragma unroll
+            for (int c = 0; c < C; ++c)
+                psi[pidx(ring, c, xx, yyl)] = psi_ghost<E>(d, rt_psi, c, hs, s_solid, xx, y0 + yyl, pz);
+        }
+    };
+    // in-tile boundary rows from the cluster neighbours (DSMEM)
+    auto copy_rows = [&](int pz) {
+        if constexpr (NB > 1) {
+            cg::cluster_group cl = cg::this_cluster();
+            const int ring = pz & 3;
+            for (int k = tid; k < 2 * E * C; k += NT) {
+                const int side = k / (E * C);  // 0: row -1 from yb-1, 1: row BY from yb+1
+                const int c = (k / E) % C;
+                const int xx = k % E;
+                const int nb = yb + (side ? 1 : -1);
+                if (nb < 0 || nb >= NB) continue;
+                const double* peer = cl.map_shared_rank(psi, nb);
+                const int src_row = side ? 0 : BY - 1;
+                psi[pidx(ring, c, xx, side ? BY : -1)] = peer[pidx(ring, c, xx, src_row)];
+            }
+        }
+    };
+    auto cluster_sync = [&]() {
+        if constexpr (NB > 1) {
+            asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+            asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+        } else {
+            __syncthreads();
+        }
+    };
+
+    // ---- f_in of this thread's cell in plane pz (pull or generated) ---------
+    double R[C][Q];
+    auto load_plane = [&](int pz) {
+        const bool sol = sol_xy_any && solid_at<E>(s_solid, x, y, pz);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            if (sol) {
+#pragma unroll
+                for (int i = 0; i < Q; ++i) R[c][i] = 0.0;
+            } else if (mode == MODE_PULL) {
+                pull_cell<E>(fp, rt_pull, slot, c, hs, s_solid, x, y, pz, R[c]);
+            } else {
+                double a0, a1, a2;
+                gen_fin<E>(mode, c, s_tc, x, y, pz, R[c], a0, a1, a2);
+            }
+        }
+    };
+    // rho -> psi of the loaded plane (P1: engine.cpp:221-264) and TMEM stash
+    auto finish_plane = [&](int pz, int tslot) {
+        const int ring = pz & 3;
+        const bool sol = sol_xy_any && solid_at<E>(s_solid, x, y, pz);
+        int negs = 0, clamps = 0;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            double v = 0.0;
+            if (!sol) {
+                double rho = 0.0;
+#pragma unroll
+                for (int i = 0; i < Q; ++i) {
+                    rho += R[c][i];
+                    negs += R[c][i] < 0.0;
+                }
+                if (!isfinite(rho)) {
+                    atomic_err(d.err, iter, tile_lin, ERR_P1_NAN);
+                } else {
+                    double press;
+                    if (!pr_pressure(rho, P.comp[c], press)) {
+                        atomic_err(d.err, iter, tile_lin, ERR_P1_POLE);
+                    } else {
+                        bool cl;
+                        v = pseudo_potential(rho, press, P.comp[c], cl);
+                        clamps += cl;
+                    }
+                }
+            }
+            psi[pidx(ring, c, x, yl)] = v;
+            tm_store19(tbase + uint32_t(tslot * T::SCOLS + c * T::CB), R[c]);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        const unsigned m1 = __reduce_add_sync(0xffffffffu, (unsigned)negs);
+        const unsigned m2 = __reduce_add_sync(0xffffffffu, (unsigned)clamps);
+        if ((tid & 31) == 0) {
+            if (m1) atomicAdd(&d.cnt[CNT_NEG], (unsigned long long)m1);
+            if (m2) atomicAdd(&d.cnt[CNT_CLAMP], (unsigned long long)m2);
+        }
+    };
+
+    // ---- collide plane z from the TMEM stash --------------------------------
+    auto collide_plane = [&](int z) {
+        const bool sol = sol_xy_any && solid_at<E>(s_solid, x, y, z);
+        const int cell = (z * E + y) * E + x;
+        const double* pm[C];
+        const double* p0[C];
+        const double* ppl[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            pm[c] = psi + pidx((z - 1) & 3, c, x, yl);
+            p0[c] = psi + pidx(z & 3, c, x, yl);
+            ppl[c] = psi + pidx((z + 1) & 3, c, x, yl);
+        }
+        int zero_rho = 0;
+#pragma unroll 1
+        for (int c = 0; c < C; ++c) {
+            double f[Q];
+            tm_load19(tbase + uint32_t((z & 1) * T::SCOLS + c * T::CB), f);  // warp-convergent
+            if (sol) continue;
+            double rho, u0 = 0.0, u1 = 0.0, u2 = 0.0;
+            if (mode == MODE_PULL) {
+                moments(f, rho, u0, u1, u2);
+            } else {
+                rho = sum19(f);
+                gen_u<E>(mode, c, s_tc, x, y, z, u0, u1, u2);
+            }
+            if (write_uface) {
+#pragma unroll
+                for (int face = 0; face < 6; ++face) {
+                    const int axis = face >> 1;
+                    const int coord = axis == 0 ? x : (axis == 1 ? y : z);
+                    if (coord == ((face & 1) ? E - 1 : 0) && rt_psi.s[face_pattern(face)] == amb) {
+                        double* uf = d.u_face + ((size_t(slot) * C + c) * 6 + face) * 3 * E2;
+                        const int fi = face_index<E>(face, x, y, z);
+                        uf[fi] = u0;
+                        uf[E2 + fi] = u1;
+                        uf[2 * E2 + fi] = u2;
+                    }
+                }
+            }
+            if (d.capture) {
+                double* cp = d.capture + (size_t(slot) * C + c) * 4 * E3;
+                cp[cell] = p0[c][0];
+                cp[E3 + cell] = u0;
+                cp[2 * E3 + cell] = u1;
+                cp[3 * E3 + cell] = u2;
+            }
+            double* out = fo + (size_t(slot) * C + c) * size_t(Q) * E3 + cell;
+            collide_comp<C, PW>(f, rho, u0, u1, u2, c, pm, p0, ppl, out, size_t(E3), zero_rho);
+        }
+        const unsigned zr = __reduce_add_sync(0xffffffffu, (unsigned)zero_rho);
+        if ((tid & 31) == 0 && zr) atomicAdd(&d.cnt[CNT_ZERO_RHO], (unsigned long long)zr);
+    };
+
+    // ---- prologue: psi planes -1, 0, 1; f(0), f(1) stashed -------------------
+    fill_zghost(-1);
+    load_plane(0);
+    finish_plane(0, 0);
+    fill_ring(0);
+    load_plane(1);
+    finish_plane(1, 1);
+    fill_ring(1);
+    cluster_sync();
+    copy_rows(0);
+    copy_rows(1);
+    __syncthreads();
+
+#pragma unroll 1
+    for (int z = 0; z < E; ++z) {
+        const bool ahead = z + 2 < E;
+        if (ahead) load_plane(z + 2);  // in flight during the collide
+        collide_plane(z);
+        if (ahead) {
+            finish_plane(z + 2, z & 1);
+            fill_ring(z + 2);
+        } else if (z + 2 == E) {
+            fill_zghost(E);
+        }
+        cluster_sync();
+        if (ahead) copy_rows(z + 2);
+        __syncthreads();
+    }
+
+    // ---- teardown
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    cluster_sync();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(s_tmem),
+                     "n"(T::NCOLS));
+}
+
+}  // namespace plbm

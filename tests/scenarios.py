@@ -76,3 +76,42 @@ ALL = {
     "mpmc3_static": (mpmc3_static, 10),
     "mpmc_periodic_solid": (mpmc_periodic_solid, 20),
 }
+
+
+def mpmc_e32(n=64, threshold=1e-9):
+    """C2 physics at E = 32 (the benchmark tile size; 4-CTA cluster kernel)."""
+    return S.mpmc_release(n=n, extent=32, threshold=threshold, r_core=8)
+
+
+def mpmc_e32_solid_periodic(n=64):
+    sc = S.mpmc_release(n=n, extent=32, mode=S.MODE_STATIC, r_core=8, devices=2)
+    sc.domain = (64, 32, 64)
+    sc.seeds = S.ramped_sphere_seeds((32.0, 16.0, 32.0), 8, 6.5, sc.components[0].rho_ambient, 6)
+    sc.periodic = (1, 1, 0)
+    g = np.zeros((64, 32, 64), np.uint8)
+    g[40:44, :, 10:20] = 1
+    g[:, 5:7, 50:60] = 1
+    sc.geometry = g
+    sc.components[0].gravity = (0.0, 1e-6, 0.0)
+    return sc
+
+
+def mpmc3_e32(n=32):
+    return S.mpmc_release(n=n, extent=32, mode=S.MODE_STATIC, r_core=6, n_components=3)
+
+
+def mpmc_e16_solid(n=32):
+    sc = S.mpmc_release(n=n, extent=16, threshold=0.0, r_core=5, devices=4)
+    g = np.zeros((n, n, n), np.uint8)
+    g[20:23, 3:29, 10:14] = 1
+    sc.geometry = g
+    sc.periodic = (0, 0, 1)
+    return sc
+
+
+ALL.update({
+    "mpmc_e32": (mpmc_e32, 8),
+    "mpmc_e32_solid_periodic": (mpmc_e32_solid_periodic, 6),
+    "mpmc3_e32": (mpmc3_e32, 6),
+    "mpmc_e16_solid_S0": (mpmc_e16_solid, 10),
+})

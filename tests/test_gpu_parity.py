@@ -11,12 +11,14 @@ from tests.compare import assert_same_state
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("variant", [0, 1], ids=["tmem", "plain"])
 @pytest.mark.parametrize("name", sorted(scenarios.ALL))
-def test_gpu_matches_oracle(built, name):
+def test_gpu_matches_oracle(built, name, variant):
     make, steps = scenarios.ALL[name]
     sc = make()
     orc = capi.oracle_engine(sc)
     gpu = capi.gpu_engine(sc, capture=True)
+    gpu.set_kernel_variant(variant)
     assert_same_state(orc, gpu, label=f"{name}@0")
     orc.step(1)
     gpu.step(1)
