@@ -247,11 +247,15 @@ def main():
     peak, peak_kind = hbm_peak()
     achieved = (ks["main_cell_updates"] * C * BYTES_PER_CELL_COMP / (ks["main_ms"] / 1e3) / 1e9
                 if ks["main_ms"] > 0 else None)
+    # DRAM traffic of the fused kernel from the committed ncu --set full capture
+    # (profiles/ncu_kmain_summary.json), per cell update per component, scaled
+    # to this run's average launch.
     traffic = None
     prof = os.path.join(REPO, "profiles", "ncu_kmain_summary.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and ks["main_launches"]:
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            bpc = json.load(open(prof))["dram_bytes_per_cell_comp"]
+            traffic = round(bpc * ks["main_cell_updates"] / ks["main_launches"] * C)
         except Exception:
             traffic = None
     line = {
@@ -272,6 +276,7 @@ def main():
                      "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4) if achieved else None,
                      "traffic": traffic, "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": round(BYTES_PER_CELL_COMP * C * ks["main_cell_updates"] / max(ks["main_launches"], 1)),
                      "kernel": "k_main (fused pull-stream + psi + forces + BGK collide)",
                      "kernel_ms_avg": round(ks["main_ms"] / max(ks["main_launches"], 1), 4),
                      "face_ms_avg": round(ks["face_ms"] / max(ks["face_launches"], 1), 4)},

@@ -77,8 +77,10 @@ typedef struct plbm_kernel_stats {
 void plbm_gpu_kernel_stats(void* h, plbm_kernel_stats* out);
 void plbm_gpu_reset_kernel_stats(void* h);
 
-/* Fused-kernel variant: 0 = TMEM-stash cluster kernel where it applies
- * (default), 1 = plain two-pull kernel (kept for A/B measurement).          */
+/* Fused-kernel variant (A/B measurement; all are bit-identical):
+ *   0 = two CTAs/SM, TMEM + smem alternating stash (default where it applies)
+ *   1 = one CTA/SM, two-slot TMEM stash with register prefetch
+ *   2 = plain kernel that pulls every population twice                       */
 int plbm_gpu_set_kernel_variant(void* h, int variant);
 
 /* The engine's CUDA stream (cudaStream_t) for callers that time with events. */

@@ -95,6 +95,7 @@ struct Kernels {
     void (*face_amb)(Dev, const int*, int, cudaStream_t);
     void (*readback)(Dev, int, int, int, double*, cudaStream_t);
     void (*main_tm)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
+    void (*main_tm2)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
     int nt, bz;
     size_t smem;
 };
@@ -119,6 +120,24 @@ void launch_tm(Dev d, const int* act, int src, int wu, long it, unsigned ntiles,
     cudaLaunchKernelEx(&cfg, k_main_tm<E, C>, d, act, src, wu, it);
 }
 
+template <int E, int C>
+void launch_tm2(Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
+    using T = Tm2Cfg<E, C>;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ntiles * T::NB);
+    cfg.blockDim = dim3(T::NT);
+    cfg.dynamicSmemBytes = T::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = T::NB;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_main_tm2<E, C>, d, act, src, wu, it);
+}
+
 template <int E, int C, bool NOPSI>
 Kernels make_kernels() {
     constexpr int NT = E * E < 256 ? E * E : 256;
@@ -134,10 +153,16 @@ Kernels make_kernels() {
     k.main = [](Dev d, const int* act, int src, int wu, long it, dim3 g, dim3 b, size_t sm,
                 cudaStream_t s) { k_main<E, C, BZ, NT, NOPSI><<<g, b, sm, s>>>(d, act, src, wu, it); };
     k.main_tm = nullptr;
+    k.main_tm2 = nullptr;
     if constexpr (!NOPSI && (E == 16 || E == 32)) {
         cudaFuncSetAttribute(k_main_tm<E, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              TmCfg<E, C>::SMEM);
         k.main_tm = launch_tm<E, C>;
+        if constexpr (C <= 2) {
+            cudaFuncSetAttribute(k_main_tm2<E, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Tm2Cfg<E, C>::SMEM);
+            k.main_tm2 = launch_tm2<E, C>;
+        }
     }
     k.face = [](Dev d, const int* act, int src, int flags, long it, dim3 g, cudaStream_t s) {
         k_face<E, C, NT><<<g, NT, 0, s>>>(d, act, src, flags, it);
@@ -212,7 +237,7 @@ class Engine {
     int set_capture(bool on);
     int poke_f(const int32_t* coords, int comp, int i, const int32_t* local, double v);
     void set_profiling(bool on) { profiling_ = on; }
-    void set_variant(int v) { use_tm_ = v == 0; }
+    void set_variant(int v) { variant_ = v; }
     plbm_kernel_stats stats();
     void reset_stats() {
         resolve_events();
@@ -279,7 +304,7 @@ class Engine {
     int cur_ = 0;  // buffer holding the latest f_post (or unused before step 1)
     int solid_words_ = 0;
     bool profiling_ = false;
-    bool use_tm_ = true;
+    int variant_ = 0;
     plbm_kernel_stats stats_{};
     struct EvPair {
         cudaEvent_t a = nullptr, b = nullptr;
@@ -762,7 +787,9 @@ void Engine::launch_main(long iter) {
     EvPair* ev = profiling_ ? &next_event(0, active_cells_) : nullptr;
     if (ev) CK(cudaEventRecord(ev->a, stream_));
     const int wu = mode_ == PLBM_MODE_PROGRESSIVE ? 1 : 0;
-    if (K_.main_tm && use_tm_)
+    if (K_.main_tm2 && variant_ == 0)
+        K_.main_tm2(d_, d_active_, cur_, wu, iter, unsigned(active_.size()), stream_);
+    else if (K_.main_tm && variant_ <= 1)
         K_.main_tm(d_, d_active_, cur_, wu, iter, unsigned(active_.size()), stream_);
     else
         K_.main(d_, d_active_, cur_, wu, iter, grid, dim3(K_.nt), K_.smem, stream_);
