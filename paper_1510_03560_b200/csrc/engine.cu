@@ -775,7 +775,8 @@ void Engine::launch_face(int src, int flags, long iter) {
     if (active_.empty()) return;
     EvPair* ev = profiling_ ? &next_event(1, 0) : nullptr;
     if (ev) CK(cudaEventRecord(ev->a, stream_));
-    K_.face(d_, d_active_, src, flags, iter, dim3(unsigned(active_.size() * 6)), stream_);
+    const unsigned nch = unsigned((E2_ + K_.nt - 1) / K_.nt);
+    K_.face(d_, d_active_, src, flags, iter, dim3(unsigned(active_.size() * 6) * nch), stream_);
     CK(cudaGetLastError());
     ++stats_.kernels_launched;
     if (ev) CK(cudaEventRecord(ev->b, stream_));

@@ -204,6 +204,90 @@ __device__ __forceinline__ void pull_cell(const double* __restrict__ fp, const R
     }
 }
 
+// Fast pull for a cell whose y and z neighbours all lie inside the tile and
+// whose tile has no solid cell (warp-uniform in callers: one warp = one x row).
+// Only the x shift can leave the tile; that lane-dependent choice collapses to
+// two base pointers, and every population is a load at a compile-time
+// immediate offset from one of three bases.
+template <int E>
+__device__ __forceinline__ void pull_cell_fast(const double* __restrict__ fp, const RouteTab& rt,
+                                               int self, int c, int x, int y, int z, double* f) {
+    constexpr int E2 = E * E;
+    constexpr int E3 = E * E * E;
+    const size_t cs = size_t(Q) * E3;
+    const int C = P.C;
+    const int row = (z * E + y) * E;
+    const double* own = fp + (size_t(self) * C + c) * cs + row + x;
+    // ex = +1 pulls from x-1: the -x neighbour's column E-1 on lane x == 0
+    const double* bp = x == 0 ? fp + (size_t(rt.s[12]) * C + c) * cs + row + (E - 1) : own - 1;
+    // ex = -1 pulls from x+1: the +x neighbour's column 0 on lane x == E-1
+    const double* bm = x == E - 1 ? fp + (size_t(rt.s[14]) * C + c) * cs + row : own + 1;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+        const int off = i * E3 - ey_(i) * E - ez_(i) * E2;
+        const double* b = ex_(i) > 0 ? bp : (ex_(i) < 0 ? bm : own);
+        f[i] = __ldg(b + off);
+    }
+}
+
+// Address-only variants of the two pulls (same routing/bounce-back), handing
+// each population's source pointer to `op(i, ptr)` — used to issue cp.async.
+template <int E, class Op>
+__device__ __forceinline__ void pull_addr(const double* __restrict__ fp, const RouteTab& rt, int self,
+                                          int c, bool hs, const uint32_t* sb, int x, int y, int z,
+                                          Op&& op) {
+    constexpr int E3 = E * E * E;
+    const size_t cs = size_t(Q) * E3;
+    const int C = P.C;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+        const int sx = x - ex_(i), sy = y - ey_(i), sz = z - ez_(i);
+        const int ox = sx < 0 ? -1 : (sx >= E ? 1 : 0);
+        const int oy = sy < 0 ? -1 : (sy >= E ? 1 : 0);
+        const int oz = sz < 0 ? -1 : (sz >= E ? 1 : 0);
+        int slot = rt.s[(ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)];
+        int cell = ((sz & (E - 1)) * E + (sy & (E - 1))) * E + (sx & (E - 1));
+        int dir = i;
+        if (hs && solid_at<E>(sb, sx, sy, sz)) {
+            slot = self;
+            cell = (z * E + y) * E + x;
+            dir = opp_(i);
+        }
+        op(i, fp + (size_t(slot) * C + c) * cs + size_t(dir) * E3 + cell);
+    }
+}
+
+template <int E, class Op>
+__device__ __forceinline__ void pull_addr_fast(const double* __restrict__ fp, const RouteTab& rt,
+                                               int self, int c, int x, int y, int z, Op&& op) {
+    constexpr int E2 = E * E;
+    constexpr int E3 = E * E * E;
+    const size_t cs = size_t(Q) * E3;
+    const int C = P.C;
+    const int row = (z * E + y) * E;
+    const double* own = fp + (size_t(self) * C + c) * cs + row + x;
+    const double* bp = x == 0 ? fp + (size_t(rt.s[12]) * C + c) * cs + row + (E - 1) : own - 1;
+    const double* bm = x == E - 1 ? fp + (size_t(rt.s[14]) * C + c) * cs + row : own + 1;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+        const int off = i * E3 - ey_(i) * E - ez_(i) * E2;
+        const double* b = ex_(i) > 0 ? bp : (ex_(i) < 0 ? bm : own);
+        op(i, b + off);
+    }
+}
+
+__device__ __forceinline__ void cp_async8(double* dst_smem, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(dst_smem))),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 // f_in for any mode (u is only meaningful for GEN modes).
 template <int E>
 __device__ __forceinline__ void fin_cell(const Dev& d, const double* fp, const RouteTab& rt,
@@ -554,8 +638,10 @@ __global__ void __launch_bounds__(NT) k_face(Dev d, const int* __restrict__ acti
     __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
     __shared__ int s_tc[3];
     __shared__ int s_fired;
-    const int slot = active[blockIdx.x / 6];
-    const int face = blockIdx.x % 6;
+    constexpr int NCH = (E2 + NT - 1) / NT;  // blocks per face (one cell per thread)
+    const int slot = active[blockIdx.x / (6 * NCH)];
+    const int face = (blockIdx.x / NCH) % 6;
+    const int chunk = blockIdx.x % NCH;
     const uint8_t mode = d.mode[slot];
     const bool hs = d.has_solid[slot] != 0;
     const int amb = P.amb_slot;
@@ -573,7 +659,7 @@ __global__ void __launch_bounds__(NT) k_face(Dev d, const int* __restrict__ acti
     const int axis = face >> 1;
     const int fixed = (face & 1) ? E - 1 : 0;
     bool fired = false;
-    for (int idx = threadIdx.x; idx < E2; idx += NT) {
+    for (int idx = chunk * NT + threadIdx.x; idx < E2 && idx < (chunk + 1) * NT; idx += NT) {
         const int a = idx % E, b = idx / E;
         const int x = axis == 0 ? fixed : a;
         const int y = axis == 0 ? a : (axis == 1 ? fixed : b);

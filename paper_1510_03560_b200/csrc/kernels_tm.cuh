@@ -105,11 +105,16 @@ __device__ __forceinline__ void tm_load19(uint32_t taddr, double* f) {
 // One component's collision at one cell (engine.cpp:420-476): gravity +
 // intra + inter force, then BGK with the velocity-shift forcing.  psi is a
 // [C] array of plane pointers at the cell centre for planes z-1, z, z+1.
-template <int C, int PW>
+template <int C, int PW, int CP>
 __device__ __forceinline__ void collide_comp(const double* f, double rho, double u0, double u1,
-                                             double u2, int c, const double* const* pm,
-                                             const double* const* p0, const double* const* pp,
+                                             double u2, int c, const double* pm0,
+                                             const double* p00, const double* pp0,
                                              double* out, size_t dstride, int& zero_rho) {
+    // pm0/p00/pp0: psi at this cell in planes z-1, z, z+1 for component 0;
+    // component k is CP doubles further.
+    const double* pm_c = pm0 + c * CP;
+    const double* p0_c = p00 + c * CP;
+    const double* pp_c = pp0 + c * CP;
     const CompConst& kc = P.comp[c];
     double F0 = 0.0, F1 = 0.0, F2 = 0.0;
     if (kc.has_gravity) {
@@ -122,7 +127,7 @@ __device__ __forceinline__ void collide_comp(const double* f, double rho, double
 #pragma unroll
         for (int i = 1; i < Q; ++i) {
             const int dx = ex_(i), dy = ey_(i), dz = ez_(i);
-            const double* pl = dz < 0 ? pm[c] : (dz > 0 ? pp[c] : p0[c]);
+            const double* pl = dz < 0 ? pm_c : (dz > 0 ? pp_c : p0_c);
             const double pn = pl[dx + PW * dy];
             const double a1 = w_(i) * pn;
             const double a2 = a1 * pn;
@@ -133,7 +138,7 @@ __device__ __forceinline__ void collide_comp(const double* f, double rho, double
             if (dz > 0) { s12 += a1; s22 += a2; }
             if (dz < 0) { s12 -= a1; s22 -= a2; }
         }
-        const double c1 = kc.c1f * p0[c][0];
+        const double c1 = kc.c1f * p0_c[0];
         const double c2 = kc.c2;
         F0 += c1 * s10 + c2 * s20;
         F1 += c1 * s11 + c2 * s21;
@@ -148,7 +153,7 @@ __device__ __forceinline__ void collide_comp(const double* f, double rho, double
 #pragma unroll
         for (int i = 1; i < Q; ++i) {
             const int dx = ex_(i), dy = ey_(i), dz = ez_(i);
-            const double* pl = dz < 0 ? pm[c2i] : (dz > 0 ? pp[c2i] : p0[c2i]);
+            const double* pl = (dz < 0 ? pm0 : (dz > 0 ? pp0 : p00)) + c2i * CP;
             const double a1 = w_(i) * pl[dx + PW * dy];
             if (dx > 0) t0 += a1;
             if (dx < 0) t0 -= a1;
@@ -157,7 +162,7 @@ __device__ __forceinline__ void collide_comp(const double* f, double rho, double
             if (dz > 0) t2 += a1;
             if (dz < 0) t2 -= a1;
         }
-        const double cc = (-g) * p0[c][0];
+        const double cc = (-g) * p0_c[0];
         F0 += cc * t0;
         F1 += cc * t1;
         F2 += cc * t2;
@@ -394,14 +399,19 @@ __global__ void __launch_bounds__(256, 1) k_main_tm(Dev d, const int* __restrict
     auto collide_plane = [&](int z) {
         const bool sol = sol_xy_any && solid_at<E>(s_solid, x, y, z);
         const int cell = (z * E + y) * E + x;
-        const double* pm[C];
-        const double* p0[C];
-        const double* ppl[C];
+        const double* pm = psi + pidx((z - 1) & 3, 0, x, yl);
+        const double* p0 = psi + pidx(z & 3, 0, x, yl);
+        const double* ppl = psi + pidx((z + 1) & 3, 0, x, yl);
+        // frontier faces this cell lies on (u_prev of the activation criterion)
+        unsigned fmask = 0;
+        if (write_uface) {
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-            pm[c] = psi + pidx((z - 1) & 3, c, x, yl);
-            p0[c] = psi + pidx(z & 3, c, x, yl);
-            ppl[c] = psi + pidx((z + 1) & 3, c, x, yl);
+            for (int face = 0; face < 6; ++face) {
+                const int axis = face >> 1;
+                const int coord = axis == 0 ? x : (axis == 1 ? y : z);
+                if (coord == ((face & 1) ? E - 1 : 0) && rt_psi.s[face_pattern(face)] == amb)
+                    fmask |= 1u << face;
+            }
         }
         int zero_rho = 0;
 #pragma unroll 1
@@ -416,29 +426,26 @@ __global__ void __launch_bounds__(256, 1) k_main_tm(Dev d, const int* __restrict
                 rho = sum19(f);
                 gen_u<E>(mode, c, s_tc, x, y, z, u0, u1, u2);
             }
-            if (write_uface) {
-#pragma unroll
+            if (fmask) {
+#pragma unroll 1
                 for (int face = 0; face < 6; ++face) {
-                    const int axis = face >> 1;
-                    const int coord = axis == 0 ? x : (axis == 1 ? y : z);
-                    if (coord == ((face & 1) ? E - 1 : 0) && rt_psi.s[face_pattern(face)] == amb) {
-                        double* uf = d.u_face + ((size_t(slot) * C + c) * 6 + face) * 3 * E2;
-                        const int fi = face_index<E>(face, x, y, z);
-                        uf[fi] = u0;
-                        uf[E2 + fi] = u1;
-                        uf[2 * E2 + fi] = u2;
-                    }
+                    if (!(fmask & (1u << face))) continue;
+                    double* uf = d.u_face + ((size_t(slot) * C + c) * 6 + face) * 3 * E2;
+                    const int fi = face_index<E>(face, x, y, z);
+                    uf[fi] = u0;
+                    uf[E2 + fi] = u1;
+                    uf[2 * E2 + fi] = u2;
                 }
             }
             if (d.capture) {
                 double* cp = d.capture + (size_t(slot) * C + c) * 4 * E3;
-                cp[cell] = p0[c][0];
+                cp[cell] = p0[c * PP];
                 cp[E3 + cell] = u0;
                 cp[2 * E3 + cell] = u1;
                 cp[3 * E3 + cell] = u2;
             }
             double* out = fo + (size_t(slot) * C + c) * size_t(Q) * E3 + cell;
-            collide_comp<C, PW>(f, rho, u0, u1, u2, c, pm, p0, ppl, out, size_t(E3), zero_rho);
+            collide_comp<C, PW, PP>(f, rho, u0, u1, u2, c, pm, p0, ppl, out, size_t(E3), zero_rho);
         }
         const unsigned zr = __reduce_add_sync(0xffffffffu, (unsigned)zero_rho);
         if ((tid & 31) == 0 && zr) atomicAdd(&d.cnt[CNT_ZERO_RHO], (unsigned long long)zr);
@@ -559,6 +566,9 @@ __global__ void __launch_bounds__(256, 2) k_main_tm2(Dev d, const int* __restric
     const int x = tid % E;
     const int yl = tid / E;
     const int y = y0 + yl;
+    // fast pull applies to this warp's row(s): no solids, y+-1 inside the tile
+    // (E = 32: one warp is one row, so the test is warp-uniform)
+    const bool fast_rows = mode == MODE_PULL && !hs && y >= 1 && y <= E - 2;
     auto pidx = [&](int ring, int c, int xx, int yy_local) {
         return ((ring * C + c) * PH + (yy_local + 1)) * PW + (xx + 1);
     };
@@ -629,7 +639,9 @@ __global__ void __launch_bounds__(256, 2) k_main_tm2(Dev d, const int* __restric
 #pragma unroll
                 for (int i = 0; i < Q; ++i) f[i] = 0.0;
             } else {
-                if (mode == MODE_PULL) {
+                if (fast_rows && pz >= 1 && pz <= E - 2) {
+                    pull_cell_fast<E>(fp, rt_pull, slot, c, x, y, pz, f);
+                } else if (mode == MODE_PULL) {
                     pull_cell<E>(fp, rt_pull, slot, c, hs, s_solid, x, y, pz, f);
                 } else {
                     double a0, a1, a2;
@@ -675,14 +687,19 @@ __global__ void __launch_bounds__(256, 2) k_main_tm2(Dev d, const int* __restric
     auto collide_plane = [&](int z) {
         const bool sol = hs && solid_at<E>(s_solid, x, y, z);
         const int cell = (z * E + y) * E + x;
-        const double* pm[C];
-        const double* p0[C];
-        const double* ppl[C];
+        const double* pm = psi + pidx((z - 1) & 3, 0, x, yl);
+        const double* p0 = psi + pidx(z & 3, 0, x, yl);
+        const double* ppl = psi + pidx((z + 1) & 3, 0, x, yl);
+        // frontier faces this cell lies on (u_prev of the activation criterion)
+        unsigned fmask = 0;
+        if (write_uface) {
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-            pm[c] = psi + pidx((z - 1) & 3, c, x, yl);
-            p0[c] = psi + pidx(z & 3, c, x, yl);
-            ppl[c] = psi + pidx((z + 1) & 3, c, x, yl);
+            for (int face = 0; face < 6; ++face) {
+                const int axis = face >> 1;
+                const int coord = axis == 0 ? x : (axis == 1 ? y : z);
+                if (coord == ((face & 1) ? E - 1 : 0) && rt_psi.s[face_pattern(face)] == amb)
+                    fmask |= 1u << face;
+            }
         }
         int zero_rho = 0;
 #pragma unroll 1
@@ -703,29 +720,26 @@ __global__ void __launch_bounds__(256, 2) k_main_tm2(Dev d, const int* __restric
                 rho = sum19(f);
                 gen_u<E>(mode, c, s_tc, x, y, z, u0, u1, u2);
             }
-            if (write_uface) {
+            if (fmask) {
 #pragma unroll 1
                 for (int face = 0; face < 6; ++face) {
-                    const int axis = face >> 1;
-                    const int coord = axis == 0 ? x : (axis == 1 ? y : z);
-                    if (coord == ((face & 1) ? E - 1 : 0) && rt_psi.s[face_pattern(face)] == amb) {
-                        double* uf = d.u_face + ((size_t(slot) * C + c) * 6 + face) * 3 * E2;
-                        const int fi = face_index<E>(face, x, y, z);
-                        uf[fi] = u0;
-                        uf[E2 + fi] = u1;
-                        uf[2 * E2 + fi] = u2;
-                    }
+                    if (!(fmask & (1u << face))) continue;
+                    double* uf = d.u_face + ((size_t(slot) * C + c) * 6 + face) * 3 * E2;
+                    const int fi = face_index<E>(face, x, y, z);
+                    uf[fi] = u0;
+                    uf[E2 + fi] = u1;
+                    uf[2 * E2 + fi] = u2;
                 }
             }
             if (d.capture) {
                 double* cp = d.capture + (size_t(slot) * C + c) * 4 * E3;
-                cp[cell] = p0[c][0];
+                cp[cell] = p0[c * PP];
                 cp[E3 + cell] = u0;
                 cp[2 * E3 + cell] = u1;
                 cp[3 * E3 + cell] = u2;
             }
             double* out = fo + (size_t(slot) * C + c) * size_t(Q) * E3 + cell;
-            collide_comp<C, PW>(f, rho, u0, u1, u2, c, pm, p0, ppl, out, size_t(E3), zero_rho);
+            collide_comp<C, PW, PP>(f, rho, u0, u1, u2, c, pm, p0, ppl, out, size_t(E3), zero_rho);
         }
         const unsigned zr = __reduce_add_sync(0xffffffffu, (unsigned)zero_rho);
         if ((tid & 31) == 0 && zr) atomicAdd(&d.cnt[CNT_ZERO_RHO], (unsigned long long)zr);
