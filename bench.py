@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--pre-steps", type=int, default=100)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--variant", type=int, default=0, help="fused-kernel variant (plbm_gpu.h)")
     return p.parse_args()
 
 
@@ -185,6 +186,7 @@ def main():
     sc, name = workload(a.config)
     C = sc.n_components
     eng = capi.gpu_engine(sc, device=local)
+    eng.set_kernel_variant(a.variant)
     stream = torch.cuda.ExternalStream(eng.stream(), device=torch.device("cuda", local))
 
     eng.step(a.pre_steps)

@@ -80,7 +80,9 @@ void plbm_gpu_reset_kernel_stats(void* h);
 /* Fused-kernel variant (A/B measurement; all are bit-identical):
  *   0 = two CTAs/SM, TMEM + smem alternating stash (default where it applies)
  *   1 = one CTA/SM, two-slot TMEM stash with register prefetch
- *   2 = plain kernel that pulls every population twice                       */
+ *   2 = plain kernel that pulls every population twice
+ *   3 = one CTA/SM, cp.async prefetch two planes ahead + two TMEM slots
+ *   4 = as 0, psi rows pushed with st.async + mbarrier (no cluster barrier)  */
 int plbm_gpu_set_kernel_variant(void* h, int variant);
 
 /* The engine's CUDA stream (cudaStream_t) for callers that time with events. */

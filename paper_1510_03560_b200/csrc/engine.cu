@@ -96,6 +96,8 @@ struct Kernels {
     void (*readback)(Dev, int, int, int, double*, cudaStream_t);
     void (*main_tm)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
     void (*main_tm2)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
+    void (*main_tm3)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
+    void (*main_tm4)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
     int nt, bz;
     size_t smem;
 };
@@ -138,6 +140,42 @@ void launch_tm2(Dev d, const int* act, int src, int wu, long it, unsigned ntiles
     cudaLaunchKernelEx(&cfg, k_main_tm2<E, C>, d, act, src, wu, it);
 }
 
+template <int E, int C>
+void launch_tm3(Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
+    using T = Tm3Cfg<E, C>;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ntiles * T::NB);
+    cfg.blockDim = dim3(T::NT);
+    cfg.dynamicSmemBytes = T::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = T::NB;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_main_tm3<E, C>, d, act, src, wu, it);
+}
+
+template <int E, int C>
+void launch_tm4(Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
+    using T = Tm2Cfg<E, C>;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ntiles * T::NB);
+    cfg.blockDim = dim3(T::NT);
+    cfg.dynamicSmemBytes = T::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = T::NB;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_main_tm4<E, C>, d, act, src, wu, it);
+}
+
 template <int E, int C, bool NOPSI>
 Kernels make_kernels() {
     constexpr int NT = E * E < 256 ? E * E : 256;
@@ -154,6 +192,8 @@ Kernels make_kernels() {
                 cudaStream_t s) { k_main<E, C, BZ, NT, NOPSI><<<g, b, sm, s>>>(d, act, src, wu, it); };
     k.main_tm = nullptr;
     k.main_tm2 = nullptr;
+    k.main_tm3 = nullptr;
+    k.main_tm4 = nullptr;
     if constexpr (!NOPSI && (E == 16 || E == 32)) {
         cudaFuncSetAttribute(k_main_tm<E, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              TmCfg<E, C>::SMEM);
@@ -162,6 +202,12 @@ Kernels make_kernels() {
             cudaFuncSetAttribute(k_main_tm2<E, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Tm2Cfg<E, C>::SMEM);
             k.main_tm2 = launch_tm2<E, C>;
+            cudaFuncSetAttribute(k_main_tm3<E, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Tm3Cfg<E, C>::SMEM);
+            k.main_tm3 = launch_tm3<E, C>;
+            cudaFuncSetAttribute(k_main_tm4<E, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Tm2Cfg<E, C>::SMEM);
+            k.main_tm4 = launch_tm4<E, C>;
         }
     }
     k.face = [](Dev d, const int* act, int src, int flags, long it, dim3 g, cudaStream_t s) {
@@ -790,6 +836,10 @@ void Engine::launch_main(long iter) {
     const int wu = mode_ == PLBM_MODE_PROGRESSIVE ? 1 : 0;
     if (K_.main_tm2 && variant_ == 0)
         K_.main_tm2(d_, d_active_, cur_, wu, iter, unsigned(active_.size()), stream_);
+    else if (K_.main_tm4 && variant_ == 4)
+        K_.main_tm4(d_, d_active_, cur_, wu, iter, unsigned(active_.size()), stream_);
+    else if (K_.main_tm3 && variant_ == 3)
+        K_.main_tm3(d_, d_active_, cur_, wu, iter, unsigned(active_.size()), stream_);
     else if (K_.main_tm && variant_ <= 1)
         K_.main_tm(d_, d_active_, cur_, wu, iter, unsigned(active_.size()), stream_);
     else

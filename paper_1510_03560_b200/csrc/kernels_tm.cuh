@@ -771,4 +771,608 @@ __global__ void __launch_bounds__(256, 2) k_main_tm2(Dev d, const int* __restric
                      "n"(T::NCOLS));
 }
 
+
+template <int E, int C>
+__global__ void __launch_bounds__(256, 2) k_main_tm4(Dev d, const int* __restrict__ active,
+                                                     int src_buf, int write_uface, long iter) {
+    using T = Tm2Cfg<E, C>;  // same footprint + 2 mbarriers
+    constexpr int NT = T::NT, BY = T::BY, NB = T::NB, PW = T::PW, PH = T::PH, PP = T::PP;
+    constexpr int G = E + 2;
+    constexpr int E2 = E * E;
+    constexpr int E3 = E * E * E;
+    extern __shared__ __align__(16) double smem[];
+    double* psi = smem;                        // [4][C][PH][PW]
+    double* stage = smem + 4 * C * PP;         // [C][Q][NT]
+    __shared__ RouteTab rt_pull, rt_psi;
+    __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
+    __shared__ int s_tc[3];
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(8) uint64_t s_mbar[2];  // psi-row arrival, by plane parity
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int tile_i = blockIdx.x / NB;
+    const int yb = blockIdx.x % NB;
+    const int y0 = yb * BY;
+    const int slot = active[tile_i];
+    const uint8_t mode = d.mode[slot];
+    const bool hs = d.has_solid[slot] != 0;
+    const int amb = P.amb_slot;
+    const double* __restrict__ fp = d.f[src_buf];
+    double* __restrict__ fo = d.f[src_buf ^ 1];
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                         smem_u32(&s_tmem)),
+                     "n"(T::NCOLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    load_routes(rt_pull, d.route[ROUTE_PULL] + size_t(slot) * 18, slot, amb);
+    load_routes(rt_psi, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, amb);
+    if (tid < 3) s_tc[tid] = d.coords[slot * 3 + tid];
+    if (hs)
+        for (int k = tid; k < d.solid_words; k += NT) s_solid[k] = d.solid[size_t(slot) * d.solid_words + k];
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&s_mbar[0])), "r"(1));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&s_mbar[1])), "r"(1));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    // peers must see our initialised mbarriers before they push rows at us
+    if constexpr (NB > 1) {
+        asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    }
+    const uint32_t tbase = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * T::HALF);
+    const int tile_lin = (s_tc[0] * P.grid[1] + s_tc[1]) * P.grid[2] + s_tc[2];
+
+    const int x = tid % E;
+    const int yl = tid / E;
+    const int y = y0 + yl;
+    // fast pull applies to this warp's row(s): no solids, y+-1 inside the tile
+    // (E = 32: one warp is one row, so the test is warp-uniform)
+    const bool fast_rows = mode == MODE_PULL && !hs && y >= 1 && y <= E - 2;
+    auto pidx = [&](int ring, int c, int xx, int yy_local) {
+        return ((ring * C + c) * PH + (yy_local + 1)) * PW + (xx + 1);
+    };
+    // ---- push-based psi row exchange (no per-plane cluster barrier) ---------
+    // Block row 0 feeds the -y neighbour's ring row BY, block row BY-1 feeds
+    // the +y neighbour's ring row -1: each value goes out as an 8-byte
+    // st.async that completes a transaction on the receiver's mbarrier.
+    const bool push_lo = NB > 1 && yl == 0 && yb > 0;
+    const bool push_hi = NB > 1 && yl == BY - 1 && yb < NB - 1;
+    const uint32_t psi_sh = smem_u32(psi);
+    uint32_t peer_psi = 0, peer_mbar = 0;
+    if (push_lo || push_hi) {
+        const uint32_t nb = uint32_t(yb + (push_lo ? -1 : 1));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(peer_psi) : "r"(psi_sh), "r"(nb));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n"
+                     : "=r"(peer_mbar)
+                     : "r"(smem_u32(&s_mbar[0])), "r"(nb));
+    }
+    const uint32_t rows_bytes = uint32_t(((yb > 0) + (yb < NB - 1)) * E * C * 8);
+    auto push_row = [&](int pz, int c, double v) {
+        if (!(push_lo || push_hi)) return;
+        const int idx = pidx(pz & 3, c, x, push_lo ? BY : -1);
+        asm volatile(
+            "st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n" ::"r"(
+                peer_psi + uint32_t(idx) * 8u),
+            "l"(__double_as_longlong(v)), "r"(peer_mbar + uint32_t((pz & 1) * 8))
+            : "memory");
+    };
+    auto expect_rows = [&](int pz) {
+        if (NB > 1 && tid == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                             smem_u32(&s_mbar[pz & 1])),
+                         "r"(rows_bytes)
+                         : "memory");
+    };
+    // only the rows that read a pushed ring row wait for it
+    const bool needs_rows = NB > 1 && ((yl == 0 && yb > 0) || (yl == BY - 1 && yb < NB - 1));
+    auto wait_rows = [&](int pz) {
+        if (!needs_rows) return;
+        const uint32_t bar = smem_u32(&s_mbar[pz & 1]);
+        const uint32_t parity = uint32_t((pz >> 1) & 1);
+        uint32_t ok = 0;
+        while (!ok)
+            asm volatile(
+                "{\n .reg .pred q;\n mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n"
+                " selp.u32 %0, 1, 0, q;\n}\n"
+                : "=r"(ok)
+                : "r"(bar), "r"(parity)
+                : "memory");
+    };
+    auto fill_zghost = [&](int pz) {
+        const int ring = pz & 3;
+        for (int k = tid; k < PP; k += NT) {
+            const int xx = k % PW - 1, yy = k / PW - 1 + y0;
+            const bool xo = xx < 0 || xx >= E, yo = yy < 0 || yy >= E;
+#pragma unroll 1
+            for (int c = 0; c < C; ++c)
+                psi[pidx(ring, c, xx, yy - y0)] =
+                    (xo && yo) ? 0.0 : psi_ghost<E>(d, rt_psi, c, hs, s_solid, xx, yy, pz);
+        }
+    };
+    auto fill_ring = [&](int pz) {
+        const int ring = pz & 3;
+        for (int k = tid; k < 2 * PH + 2 * E; k += NT) {
+            int xx, yyl;
+            if (k < 2 * PH) {
+                xx = (k & 1) ? E : -1;
+                yyl = (k >> 1) - 1;
+            } else {
+                const int q = k - 2 * PH;
+                xx = q % E;
+                yyl = (q / E) ? BY : -1;
+                const int yy = y0 + yyl;
+                if (yy >= 0 && yy < E) continue;
+            }
+#pragma unroll 1
+            for (int c = 0; c < C; ++c)
+                psi[pidx(ring, c, xx, yyl)] = psi_ghost<E>(d, rt_psi, c, hs, s_solid, xx, y0 + yyl, pz);
+        }
+    };
+    auto copy_rows = [&](int pz) {
+        if constexpr (NB > 1) {
+            cg::cluster_group cl = cg::this_cluster();
+            const int ring = pz & 3;
+            for (int k = tid; k < 2 * E * C; k += NT) {
+                const int side = k / (E * C);
+                const int c = (k / E) % C;
+                const int xx = k % E;
+                const int nb = yb + (side ? 1 : -1);
+                if (nb < 0 || nb >= NB) continue;
+                const double* peer = cl.map_shared_rank(psi, nb);
+                psi[pidx(ring, c, xx, side ? BY : -1)] = peer[pidx(ring, c, xx, side ? 0 : BY - 1)];
+            }
+        }
+    };
+    auto cluster_sync = [&]() {
+        if constexpr (NB > 1) {
+            asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+            asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+        } else {
+            __syncthreads();
+        }
+    };
+
+    // psi pass of plane pz: pull (or generate) f_in, rho -> psi, stash f_in
+    auto psi_pass = [&](int pz) {
+        const int ring = pz & 3;
+        const bool sol = hs && solid_at<E>(s_solid, x, y, pz);
+        int negs = 0, clamps = 0;
+#pragma unroll 1
+        for (int c = 0; c < C; ++c) {
+            double f[Q];
+            double v = 0.0;
+            if (sol) {
+#pragma unroll
+                for (int i = 0; i < Q; ++i) f[i] = 0.0;
+            } else {
+                if (fast_rows && pz >= 1 && pz <= E - 2) {
+                    pull_cell_fast<E>(fp, rt_pull, slot, c, x, y, pz, f);
+                } else if (mode == MODE_PULL) {
+                    pull_cell<E>(fp, rt_pull, slot, c, hs, s_solid, x, y, pz, f);
+                } else {
+                    double a0, a1, a2;
+                    gen_fin<E>(mode, c, s_tc, x, y, pz, f, a0, a1, a2);
+                }
+                double rho = 0.0;
+#pragma unroll
+                for (int i = 0; i < Q; ++i) {
+                    rho += f[i];
+                    negs += f[i] < 0.0;
+                }
+                if (!isfinite(rho)) {
+                    atomic_err(d.err, iter, tile_lin, ERR_P1_NAN);
+                } else {
+                    double press;
+                    if (!pr_pressure(rho, P.comp[c], press)) {
+                        atomic_err(d.err, iter, tile_lin, ERR_P1_POLE);
+                    } else {
+                        bool cl;
+                        v = pseudo_potential(rho, press, P.comp[c], cl);
+                        clamps += cl;
+                    }
+                }
+            }
+            psi[pidx(ring, c, x, yl)] = v;
+            push_row(pz, c, v);
+            if ((pz & 1) == 0) {
+                tm_store19(tbase + uint32_t(c * T::CB), f);
+            } else {
+                double* st = stage + size_t(c) * Q * NT + tid;
+#pragma unroll
+                for (int i = 0; i < Q; ++i) st[i * NT] = f[i];
+            }
+        }
+        if ((pz & 1) == 0) asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        const unsigned m1 = __reduce_add_sync(0xffffffffu, (unsigned)negs);
+        const unsigned m2 = __reduce_add_sync(0xffffffffu, (unsigned)clamps);
+        if ((tid & 31) == 0) {
+            if (m1) atomicAdd(&d.cnt[CNT_NEG], (unsigned long long)m1);
+            if (m2) atomicAdd(&d.cnt[CNT_CLAMP], (unsigned long long)m2);
+        }
+    };
+
+    auto collide_plane = [&](int z) {
+        const bool sol = hs && solid_at<E>(s_solid, x, y, z);
+        const int cell = (z * E + y) * E + x;
+        const double* pm = psi + pidx((z - 1) & 3, 0, x, yl);
+        const double* p0 = psi + pidx(z & 3, 0, x, yl);
+        const double* ppl = psi + pidx((z + 1) & 3, 0, x, yl);
+        // frontier faces this cell lies on (u_prev of the activation criterion)
+        unsigned fmask = 0;
+        if (write_uface) {
+#pragma unroll
+            for (int face = 0; face < 6; ++face) {
+                const int axis = face >> 1;
+                const int coord = axis == 0 ? x : (axis == 1 ? y : z);
+                if (coord == ((face & 1) ? E - 1 : 0) && rt_psi.s[face_pattern(face)] == amb)
+                    fmask |= 1u << face;
+            }
+        }
+        int zero_rho = 0;
+#pragma unroll 1
+        for (int c = 0; c < C; ++c) {
+            double f[Q];
+            if ((z & 1) == 0) {
+                tm_load19(tbase + uint32_t(c * T::CB), f);  // warp-convergent
+            } else {
+                const double* st = stage + size_t(c) * Q * NT + tid;
+#pragma unroll
+                for (int i = 0; i < Q; ++i) f[i] = st[i * NT];
+            }
+            if (sol) continue;
+            double rho, u0 = 0.0, u1 = 0.0, u2 = 0.0;
+            if (mode == MODE_PULL) {
+                moments(f, rho, u0, u1, u2);
+            } else {
+                rho = sum19(f);
+                gen_u<E>(mode, c, s_tc, x, y, z, u0, u1, u2);
+            }
+            if (fmask) {
+#pragma unroll 1
+                for (int face = 0; face < 6; ++face) {
+                    if (!(fmask & (1u << face))) continue;
+                    double* uf = d.u_face + ((size_t(slot) * C + c) * 6 + face) * 3 * E2;
+                    const int fi = face_index<E>(face, x, y, z);
+                    uf[fi] = u0;
+                    uf[E2 + fi] = u1;
+                    uf[2 * E2 + fi] = u2;
+                }
+            }
+            if (d.capture) {
+                double* cp = d.capture + (size_t(slot) * C + c) * 4 * E3;
+                cp[cell] = p0[c * PP];
+                cp[E3 + cell] = u0;
+                cp[2 * E3 + cell] = u1;
+                cp[3 * E3 + cell] = u2;
+            }
+            double* out = fo + (size_t(slot) * C + c) * size_t(Q) * E3 + cell;
+            collide_comp<C, PW, PP>(f, rho, u0, u1, u2, c, pm, p0, ppl, out, size_t(E3), zero_rho);
+        }
+        const unsigned zr = __reduce_add_sync(0xffffffffu, (unsigned)zero_rho);
+        if ((tid & 31) == 0 && zr) atomicAdd(&d.cnt[CNT_ZERO_RHO], (unsigned long long)zr);
+    };
+
+    fill_zghost(-1);
+    expect_rows(0);
+    psi_pass(0);
+    fill_ring(0);
+    __syncthreads();
+    wait_rows(0);
+#pragma unroll 1
+    for (int z = 0; z < E; ++z) {
+        if (z + 1 < E) {
+            expect_rows(z + 1);
+            psi_pass(z + 1);
+            fill_ring(z + 1);
+        } else {
+            fill_zghost(E);
+        }
+        __syncthreads();
+        if (z + 1 < E) wait_rows(z + 1);
+        collide_plane(z);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    cluster_sync();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(s_tmem),
+                     "n"(T::NCOLS));
+}
+
+
+// ---------------------------------------------------------------------------
+// k_main_tm3: one CTA (8 warps) per SM, memory latency hidden by cp.async.
+// The pulls of plane z+2 are issued as 8-byte cp.async copies (no registers
+// held) into a shared-memory landing buffer while plane z+1's psi pass and
+// plane z's collide run; the psi pass reads the landed plane, stashes it in
+// TMEM (two slots), and the collide reads TMEM.
+template <int E, int C>
+struct Tm3Cfg {
+    static constexpr int NT = 256;
+    static constexpr int BY = NT / E;
+    static constexpr int NB = E / BY;
+    static constexpr int CB = 40;
+    static constexpr int SCOLS = CB * C;
+    static constexpr int NCOLS = (4 * SCOLS <= 256) ? 256 : 512;
+    static constexpr int HALF = NCOLS / 2;
+    static constexpr int PW = E + 2;
+    static constexpr int PH = BY + 2;
+    static constexpr int PP = PW * PH;
+    static constexpr int PSI_BYTES = 4 * C * PP * 8;
+    static constexpr int LAND_BYTES = 2 * Q * C * NT * 8;
+    static constexpr int RAW = PSI_BYTES + LAND_BYTES;
+    static constexpr int SMEM = RAW > 118 * 1024 ? RAW : 118 * 1024;  // one CTA per SM
+    static_assert(2 * SCOLS <= HALF, "TMEM stash does not fit");
+    static_assert(RAW + 8 * 1024 <= 227 * 1024, "shared memory");
+};
+
+template <int E, int C>
+__global__ void __launch_bounds__(256, 1) k_main_tm3(Dev d, const int* __restrict__ active,
+                                                     int src_buf, int write_uface, long iter) {
+    using T = Tm3Cfg<E, C>;
+    constexpr int NT = T::NT, BY = T::BY, NB = T::NB, PW = T::PW, PH = T::PH, PP = T::PP;
+    constexpr int G = E + 2;
+    constexpr int E2 = E * E;
+    constexpr int E3 = E * E * E;
+    extern __shared__ __align__(16) double smem[];
+    double* psi = smem;                   // [4][C][PH][PW]
+    double* land = smem + 4 * C * PP;     // [2][C][Q][NT]
+    __shared__ RouteTab rt_pull, rt_psi;
+    __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
+    __shared__ int s_tc[3];
+    __shared__ uint32_t s_tmem;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int tile_i = blockIdx.x / NB;
+    const int yb = blockIdx.x % NB;
+    const int y0 = yb * BY;
+    const int slot = active[tile_i];
+    const uint8_t mode = d.mode[slot];
+    const bool hs = d.has_solid[slot] != 0;
+    const int amb = P.amb_slot;
+    const double* __restrict__ fp = d.f[src_buf];
+    double* __restrict__ fo = d.f[src_buf ^ 1];
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                         smem_u32(&s_tmem)),
+                     "n"(T::NCOLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    load_routes(rt_pull, d.route[ROUTE_PULL] + size_t(slot) * 18, slot, amb);
+    load_routes(rt_psi, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, amb);
+    if (tid < 3) s_tc[tid] = d.coords[slot * 3 + tid];
+    if (hs)
+        for (int k = tid; k < d.solid_words; k += NT) s_solid[k] = d.solid[size_t(slot) * d.solid_words + k];
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tbase = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * T::HALF);
+    const int tile_lin = (s_tc[0] * P.grid[1] + s_tc[1]) * P.grid[2] + s_tc[2];
+
+    const int x = tid % E;
+    const int yl = tid / E;
+    const int y = y0 + yl;
+    const bool fast_rows = mode == MODE_PULL && !hs && y >= 1 && y <= E - 2;
+    auto pidx = [&](int ring, int c, int xx, int yy_local) {
+        return ((ring * C + c) * PH + (yy_local + 1)) * PW + (xx + 1);
+    };
+    auto lidx = [&](int buf, int c, int i) { return ((buf * C + c) * Q + i) * NT + tid; };
+    auto fill_zghost = [&](int pz) {
+        const int ring = pz & 3;
+        for (int k = tid; k < PP; k += NT) {
+            const int xx = k % PW - 1, yy = k / PW - 1 + y0;
+            const bool xo = xx < 0 || xx >= E, yo = yy < 0 || yy >= E;
+#pragma unroll 1
+            for (int c = 0; c < C; ++c)
+                psi[pidx(ring, c, xx, yy - y0)] =
+                    (xo && yo) ? 0.0 : psi_ghost<E>(d, rt_psi, c, hs, s_solid, xx, yy, pz);
+        }
+    };
+    auto fill_ring = [&](int pz) {
+        const int ring = pz & 3;
+        for (int k = tid; k < 2 * PH + 2 * E; k += NT) {
+            int xx, yyl;
+            if (k < 2 * PH) {
+                xx = (k & 1) ? E : -1;
+                yyl = (k >> 1) - 1;
+            } else {
+                const int q = k - 2 * PH;
+                xx = q % E;
+                yyl = (q / E) ? BY : -1;
+                const int yy = y0 + yyl;
+                if (yy >= 0 && yy < E) continue;
+            }
+#pragma unroll 1
+            for (int c = 0; c < C; ++c)
+                psi[pidx(ring, c, xx, yyl)] = psi_ghost<E>(d, rt_psi, c, hs, s_solid, xx, y0 + yyl, pz);
+        }
+    };
+    auto copy_rows = [&](int pz) {
+        if constexpr (NB > 1) {
+            cg::cluster_group cl = cg::this_cluster();
+            const int ring = pz & 3;
+            for (int k = tid; k < 2 * E * C; k += NT) {
+                const int side = k / (E * C);
+                const int c = (k / E) % C;
+                const int xx = k % E;
+                const int nb = yb + (side ? 1 : -1);
+                if (nb < 0 || nb >= NB) continue;
+                const double* peer = cl.map_shared_rank(psi, nb);
+                psi[pidx(ring, c, xx, side ? BY : -1)] = peer[pidx(ring, c, xx, side ? 0 : BY - 1)];
+            }
+        }
+    };
+    auto cluster_sync = [&]() {
+        if constexpr (NB > 1) {
+            asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+            asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+        } else {
+            __syncthreads();
+        }
+    };
+
+    // issue the pulls of plane pz into landing buffer pz & 1
+    auto issue = [&](int pz) {
+        const int buf = pz & 1;
+        const bool sol = hs && solid_at<E>(s_solid, x, y, pz);
+#pragma unroll 1
+        for (int c = 0; c < C; ++c) {
+            if (sol) continue;
+            if (fast_rows && pz >= 1 && pz <= E - 2) {
+                pull_addr_fast<E>(fp, rt_pull, slot, c, x, y, pz,
+                                  [&](int i, const double* p) { cp_async8(&land[lidx(buf, c, i)], p); });
+            } else if (mode == MODE_PULL) {
+                pull_addr<E>(fp, rt_pull, slot, c, hs, s_solid, x, y, pz,
+                             [&](int i, const double* p) { cp_async8(&land[lidx(buf, c, i)], p); });
+            } else {
+                double f[Q], a0, a1, a2;
+                gen_fin<E>(mode, c, s_tc, x, y, pz, f, a0, a1, a2);
+#pragma unroll
+                for (int i = 0; i < Q; ++i) land[lidx(buf, c, i)] = f[i];
+            }
+        }
+        cp_async_commit();
+    };
+
+    // psi pass of a landed plane + TMEM stash (slot pz & 1)
+    auto psi_pass = [&](int pz) {
+        const int ring = pz & 3;
+        const int buf = pz & 1;
+        const bool sol = hs && solid_at<E>(s_solid, x, y, pz);
+        int negs = 0, clamps = 0;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            double f[Q];
+            double v = 0.0;
+            if (sol) {
+#pragma unroll
+                for (int i = 0; i < Q; ++i) f[i] = 0.0;
+            } else {
+#pragma unroll
+                for (int i = 0; i < Q; ++i) f[i] = land[lidx(buf, c, i)];
+                double rho = 0.0;
+#pragma unroll
+                for (int i = 0; i < Q; ++i) {
+                    rho += f[i];
+                    negs += f[i] < 0.0;
+                }
+                if (!isfinite(rho)) {
+                    atomic_err(d.err, iter, tile_lin, ERR_P1_NAN);
+                } else {
+                    double press;
+                    if (!pr_pressure(rho, P.comp[c], press)) {
+                        atomic_err(d.err, iter, tile_lin, ERR_P1_POLE);
+                    } else {
+                        bool cl;
+                        v = pseudo_potential(rho, press, P.comp[c], cl);
+                        clamps += cl;
+                    }
+                }
+            }
+            psi[pidx(ring, c, x, yl)] = v;
+            tm_store19(tbase + uint32_t((pz & 1) * T::SCOLS + c * T::CB), f);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        const unsigned m1 = __reduce_add_sync(0xffffffffu, (unsigned)negs);
+        const unsigned m2 = __reduce_add_sync(0xffffffffu, (unsigned)clamps);
+        if ((tid & 31) == 0) {
+            if (m1) atomicAdd(&d.cnt[CNT_NEG], (unsigned long long)m1);
+            if (m2) atomicAdd(&d.cnt[CNT_CLAMP], (unsigned long long)m2);
+        }
+    };
+
+    auto collide_plane = [&](int z) {
+        const bool sol = hs && solid_at<E>(s_solid, x, y, z);
+        const int cell = (z * E + y) * E + x;
+        const double* pm = psi + pidx((z - 1) & 3, 0, x, yl);
+        const double* p0 = psi + pidx(z & 3, 0, x, yl);
+        const double* ppl = psi + pidx((z + 1) & 3, 0, x, yl);
+        unsigned fmask = 0;
+        if (write_uface) {
+#pragma unroll
+            for (int face = 0; face < 6; ++face) {
+                const int axis = face >> 1;
+                const int coord = axis == 0 ? x : (axis == 1 ? y : z);
+                if (coord == ((face & 1) ? E - 1 : 0) && rt_psi.s[face_pattern(face)] == amb)
+                    fmask |= 1u << face;
+            }
+        }
+        int zero_rho = 0;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            double f[Q];
+            tm_load19(tbase + uint32_t((z & 1) * T::SCOLS + c * T::CB), f);  // warp-convergent
+            if (sol) continue;
+            double rho, u0 = 0.0, u1 = 0.0, u2 = 0.0;
+            if (mode == MODE_PULL) {
+                moments(f, rho, u0, u1, u2);
+            } else {
+                rho = sum19(f);
+                gen_u<E>(mode, c, s_tc, x, y, z, u0, u1, u2);
+            }
+            if (fmask) {
+#pragma unroll 1
+                for (int face = 0; face < 6; ++face) {
+                    if (!(fmask & (1u << face))) continue;
+                    double* uf = d.u_face + ((size_t(slot) * C + c) * 6 + face) * 3 * E2;
+                    const int fi = face_index<E>(face, x, y, z);
+                    uf[fi] = u0;
+                    uf[E2 + fi] = u1;
+                    uf[2 * E2 + fi] = u2;
+                }
+            }
+            if (d.capture) {
+                double* cp = d.capture + (size_t(slot) * C + c) * 4 * E3;
+                cp[cell] = p0[c * PP];
+                cp[E3 + cell] = u0;
+                cp[2 * E3 + cell] = u1;
+                cp[3 * E3 + cell] = u2;
+            }
+            double* out = fo + (size_t(slot) * C + c) * size_t(Q) * E3 + cell;
+            collide_comp<C, PW, PP>(f, rho, u0, u1, u2, c, pm, p0, ppl, out, size_t(E3), zero_rho);
+        }
+        const unsigned zr = __reduce_add_sync(0xffffffffu, (unsigned)zero_rho);
+        if ((tid & 31) == 0 && zr) atomicAdd(&d.cnt[CNT_ZERO_RHO], (unsigned long long)zr);
+    };
+
+    issue(0);
+    issue(1);
+    fill_zghost(-1);
+    cp_async_wait<1>();
+    psi_pass(0);
+    fill_ring(0);
+    cluster_sync();
+    copy_rows(0);
+    __syncthreads();
+#pragma unroll 1
+    for (int z = 0; z < E; ++z) {
+        if (z + 2 < E) issue(z + 2);
+        else cp_async_commit();  // keep one group per iteration
+        cp_async_wait<1>();
+        if (z + 1 < E) {
+            psi_pass(z + 1);
+            fill_ring(z + 1);
+        } else {
+            fill_zghost(E);
+        }
+        cluster_sync();
+        if (z + 1 < E) copy_rows(z + 1);
+        __syncthreads();
+        collide_plane(z);
+    }
+    cp_async_wait<0>();
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    cluster_sync();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(s_tmem),
+                     "n"(T::NCOLS));
+}
+
 }  // namespace plbm
