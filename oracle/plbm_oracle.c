@@ -958,3 +958,39 @@ void plbm_oracle_destroy(void* h) {
     free(o->tiles); free(o->log); free(o->geom); free(o->p2p); free(o->per_dev);
     free(o);
 }
+
+/* ---------------------------------------------------------------- KATs
+ * Single-function entry points so the restatement can be checked against
+ * the reference's own known-answer unit tests (tests/test_golden.py). */
+double plbm_oracle_kat_pr_pressure(double rho, const plbm_component_desc* p, int* pole) {
+    double out = 0.0;
+    *pole = pr_pressure(rho, p, &out);
+    return out;
+}
+double plbm_oracle_kat_psi(double rho, double press, double g_self, int* clamped) {
+    unsigned long long c = 0;
+    const double v = pseudo_potential(rho, press, g_self, &c);
+    *clamped = (int)c;
+    return v;
+}
+void plbm_oracle_kat_equilibrium(double rho, const double* u, double* out) {
+    init_opp();
+    equilibrium(rho, u, out);
+}
+void plbm_oracle_kat_moments(const double* f, double* rho, double* u) { moments(f, rho, u); }
+void plbm_oracle_kat_intra_force(const double* psi, long cell, const long* stride,
+                                 const plbm_component_desc* p, double* F) {
+    intra_force(psi, cell, stride, p, F);
+}
+void plbm_oracle_kat_inter_force(double psi_self, const double* psi_other, long cell,
+                                 const long* stride, double g, double* F) {
+    inter_force(psi_self, psi_other, cell, stride, g, F);
+}
+void plbm_oracle_kat_stencil(int* e, double* w, int* opp) {
+    init_opp();
+    for (int i = 0; i < Q; ++i) {
+        for (int a = 0; a < 3; ++a) e[3 * i + a] = E3[i][a];
+        w[i] = W3[i];
+        opp[i] = OPP[i];
+    }
+}

@@ -14,6 +14,8 @@
 //   plbm_ref_read_tile / counters / creation_log -> the state callers read
 //                       between steps (SURVEY §8b "State read by callers").
 #include "plbm/engine.hpp"
+#include "plbm/kernels.hpp"
+#include "plbm/physics.hpp"
 #include "plbm/geometry.hpp"
 #include "plbm/topology.hpp"
 
@@ -282,6 +284,70 @@ void plbm_ref_destroy(void* hp) {
     h->st.reset();
     std::filesystem::remove_all(h->tmpdir);
     delete h;
+}
+
+
+// ---- known-answer entry points straight into the reference's functions
+namespace {
+physics::ComponentParams to_params(const plbm_component_desc* c) {
+    physics::ComponentParams p;
+    p.tau = c->tau;
+    p.rho_ambient = c->rho_ambient;
+    p.g_self = c->g_self;
+    p.beta = c->beta;
+    p.gravity = {c->gravity[0], c->gravity[1], c->gravity[2]};
+    p.eos.a = c->a;
+    p.eos.b = c->b;
+    p.eos.R = c->R;
+    p.eos.T = c->T;
+    p.eos.Tc = c->Tc;
+    p.eos.omega = c->omega;
+    return p;
+}
+const lattice::Stencil& st3() {
+    static const lattice::Stencil s = lattice::make_stencil(lattice::StencilKind::D3Q19);
+    return s;
+}
+}  // namespace
+
+double plbm_ref_kat_pr_pressure(double rho, const plbm_component_desc* c, int* pole) {
+    *pole = 0;
+    try {
+        return physics::pr_pressure(rho, to_params(c));
+    } catch (const std::domain_error&) {
+        *pole = 1;
+        return 0.0;
+    }
+}
+double plbm_ref_kat_psi(double rho, double press, double g_self, int* clamped) {
+    std::uint64_t n = 0;
+    const double v = physics::pseudo_potential(rho, press, g_self, st3().cs2, &n);
+    *clamped = int(n);
+    return v;
+}
+void plbm_ref_kat_equilibrium(double rho, const double* u, double* out) {
+    lattice::equilibrium(rho, u, st3(), out);
+}
+void plbm_ref_kat_moments(const double* f, double* rho, double* u) {
+    lattice::moments(f, st3(), *rho, u);
+}
+void plbm_ref_kat_intra_force(const double* psi, long cell, const long* stride,
+                              const plbm_component_desc* c, double* F) {
+    const auto r = physics::intra_force(psi, cell, stride, to_params(c), st3());
+    F[0] = r[0]; F[1] = r[1]; F[2] = r[2];
+}
+void plbm_ref_kat_inter_force(double psi_self, const double* psi_other, long cell,
+                              const long* stride, double g, double* F) {
+    const auto r = physics::inter_force(psi_self, psi_other, cell, stride, g, st3());
+    F[0] = r[0]; F[1] = r[1]; F[2] = r[2];
+}
+void plbm_ref_kat_stencil(int* e, double* w, int* opp) {
+    const auto& s = st3();
+    for (int i = 0; i < 19; ++i) {
+        for (int a = 0; a < 3; ++a) e[3 * i + a] = s.e[i][a];
+        w[i] = s.w[i];
+        opp[i] = s.opp[i];
+    }
 }
 
 } // extern "C"

@@ -26,3 +26,13 @@ def test_gpu_matches_oracle(built, name, variant):
     orc.step(steps - 1)
     gpu.step(steps - 1)
     assert_same_state(orc, gpu, label=f"{name}@{steps}")
+
+
+@pytest.mark.parametrize("name", sorted(__import__("tests.golden_check", fromlist=["x"]).load_golden()))
+def test_gpu_reproduces_reference_golden_states(built, name):
+    """Against the state the reference itself produced (tests/golden/)."""
+    from tests.golden_check import assert_matches_golden
+    make, steps = scenarios.ALL[name]
+    gpu = capi.gpu_engine(make(), capture=True)
+    gpu.step(steps)
+    assert_matches_golden(gpu, name)
