@@ -51,10 +51,14 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     p.add_argument("--variant", type=int, default=0, help="fused-kernel variant (plbm_gpu.h)")
+    p.add_argument("--dist-backend", default="nccl", help="nccl (one GPU per rank) or gloo (tests)")
     return p.parse_args()
 
 
-def workload(cfg: str):
+def workload(cfg: str, world: int = 1):
+    if cfg == "c2" and world > 1:
+        return S.mpmc_release_weak(world), \
+            f"C2 weak-scaled: {world} x (256^3 2-comp MPMC sphere release) along x, 32^3 subdomains, progressive S=1e-9, owners sharded over {world} GPUs"
     if cfg == "c2":
         return S.mpmc_release(n=256, extent=32, threshold=1e-9), \
             "C2: D3Q19 2-comp MPMC (PR liquid/vapour + ideal-like) sphere release, 256^3, 32^3 subdomains, progressive S=1e-9"
@@ -177,20 +181,31 @@ def main():
         return
 
     import torch
-    torch.cuda.set_device(local)
+    ndev = torch.cuda.device_count()
+    gpu = local % max(ndev, 1)
+    torch.cuda.set_device(gpu)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if a.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group(a.dist_backend)
     from paper_1510_03560_b200 import capi
-    sc, name = workload(a.config)
+    from paper_1510_03560_b200.dist import DistStepper
+    sc, name = workload(a.config, world)
     C = sc.n_components
-    eng = capi.gpu_engine(sc, device=local)
+    eng = capi.gpu_engine(sc, device=gpu, rank=rank, world=world)
     eng.set_kernel_variant(a.variant)
-    stream = torch.cuda.ExternalStream(eng.stream(), device=torch.device("cuda", local))
+    stream = torch.cuda.ExternalStream(eng.stream(), device=torch.device("cuda", gpu))
+    if world > 1:
+        stepper = DistStepper(eng, dist, gpu)
+        run = stepper.step
+    else:
+        run = eng.step
 
-    eng.step(a.pre_steps)
-    eng.step(a.warmup)
+    run(a.pre_steps)
+    run(a.warmup)
     tiles_at_start = eng.counters()["tiles"]
 
     def barrier():
@@ -208,7 +223,7 @@ def main():
     with ClockSampler(os.path.join(REPO, "gpurun_out", f"clocks_r{rank}.csv"), local) as clk:
         barrier()
         ev0.record(stream)
-        eng.step(a.steps)
+        run(a.steps)
         ev1.record(stream)
         barrier()
     ms = ev0.elapsed_time(ev1)
@@ -224,7 +239,7 @@ def main():
     barrier()
     t0 = time.perf_counter()
     for _ in range(a.steps):
-        eng.step(1)
+        run(1)
         eng.counters()
     barrier()
     e_dt = time.perf_counter() - t0
@@ -232,13 +247,14 @@ def main():
     e_ks = eng.kernel_stats()
 
     # ---- max over ranks / sums -------------------------------------------------
-    t = torch.tensor([ms, e_dt], dtype=torch.float64, device="cuda")
-    tot = torch.tensor([float(cells), float(e_cells)], dtype=torch.float64, device="cuda")
+    # cell_updates is a global count (every rank's mirror sees all tiles), so
+    # the job total is taken once; times are the max over ranks.
+    tdev = "cuda" if (dist is None or a.dist_backend == "nccl") else "cpu"
+    t = torch.tensor([ms, e_dt], dtype=torch.float64, device=tdev)
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
     ms_max, e_dt_max = float(t[0]), float(t[1])
-    cells_all, e_cells_all = float(tot[0]), float(tot[1])
+    cells_all, e_cells_all = float(cells), float(e_cells)
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -267,7 +283,7 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": name, "pre_steps": a.pre_steps, "tiles": [tiles_at_start, tiles_at_end],
                    "components": C, "tile_extent": sc.tile_extent,
-                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "parallelism": f"tile-sharded x{world} (owner % world), NVLink peer loads" if world > 1 else "1 GPU",
                    "l2": "per-step working set ~10 GB >> 126 MB L2 (no flush needed)",
                    "mlups_cells": round(value / C, 2)},
         "e2e": {"value": round(e2e, 2), "unit": "MLUPS/comp",

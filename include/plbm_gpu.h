@@ -45,7 +45,8 @@ int plbm_gpu_tiles(void* h, int32_t* coords, int32_t* owners, int64_t* births, i
 /* Reads one field of one tile as the reference holds it between steps
  * (Tile / ComponentState, tile.hpp:38-82): interior cells, x-fastest.
  * PLBM_FIELD_PSI / PUX..PUZ need plbm_gpu_set_capture(h, 1) before the step.
- * 0 ok, -1 no such tile, -2 bad component, -3 bad field, -4 not captured.  */
+ * 0 ok, -1 no such tile, -2 bad component, -3 bad field, -4 not captured,
+ * -7 tile owned by another rank.                                             */
 int plbm_gpu_read_tile(void* h, const int32_t* coords, int comp, int field, double* out);
 
 /* TileMap::creation_log() (tilemap.hpp:94-96).  Returns the row count.      */
@@ -77,16 +78,54 @@ typedef struct plbm_kernel_stats {
 void plbm_gpu_kernel_stats(void* h, plbm_kernel_stats* out);
 void plbm_gpu_reset_kernel_stats(void* h);
 
-/* Fused-kernel variant (A/B measurement; all are bit-identical):
- *   0 = two CTAs/SM, TMEM + smem alternating stash (default where it applies)
- *   1 = one CTA/SM, two-slot TMEM stash with register prefetch
- *   2 = plain kernel that pulls every population twice
- *   3 = one CTA/SM, cp.async prefetch two planes ahead + two TMEM slots
- *   4 = as 0, psi rows pushed with st.async + mbarrier (no cluster barrier)  */
+/* Fused-kernel variant (A/B measurement; both are bit-identical):
+ *   0 = TMEM + smem alternating stash, 4-CTA cluster, psi rows pushed with
+ *       st.async + mbarrier (default where it applies: E in {16,32}, C <= 2,
+ *       a psi stencil)
+ *   1 = plain kernel that pulls every population twice (always used for
+ *       E = 8 and psi-free scenarios)                                        */
 int plbm_gpu_set_kernel_variant(void* h, int variant);
 
 /* The engine's CUDA stream (cudaStream_t) for callers that time with events. */
 void* plbm_gpu_stream(void* h);
+
+/* ---- multi-GPU (one process per GPU) -----------------------
+ * Every rank builds the same deterministic host mirror from the same
+ * descriptor; tile owner o (assign_device) lives on rank o % world.  Each
+ * rank's block pool is exported as CUDA IPC handles; peers map it and the
+ * fused kernel reads remote neighbour tiles over NVLink in place.
+ *
+ *   h = plbm_gpu_create_dist(desc, local_device, rank, world, &err)
+ *   plbm_gpu_ipc_handles(h, buf)           -> exchange (all_gather) ->
+ *   plbm_gpu_open_peer(h, r, handles_r)    for every other rank r
+ *   plbm_gpu_prepare(h)                    then a barrier across ranks
+ *   per step: plbm_gpu_step_main(h)        (fused kernel of this rank's tiles)
+ *             barrier across ranks          (k_face pulls peers' new f_post)
+ *             plbm_gpu_step_face(h)        (psi faces, criterion, trigger bits)
+ *             all-reduce(MAX) the plbm_gpu_trigger_bytes(h) bytes at
+ *             plbm_gpu_triggers_device(h) on plbm_gpu_stream(h)
+ *             plbm_gpu_step_end(h, merged)  (expansion on the merged bits)
+ * The two stream-ordered collectives also order the ranks' double-buffered
+ * pools; step_end writes nothing a peer reads.  plbm_gpu_step_begin =
+ * step_main + step_face (single rank).                                      */
+void* plbm_gpu_create_dist(const plbm_scenario_desc* desc, int device, int rank, int world,
+                           plbm_error* err);
+int plbm_gpu_prepare(void* h);
+int plbm_gpu_step_begin(void* h, plbm_error* err);
+int plbm_gpu_step_main(void* h, plbm_error* err);
+int plbm_gpu_step_face(void* h);
+int plbm_gpu_step_end(void* h, const uint8_t* merged_triggers, plbm_error* err);
+int plbm_gpu_trigger_bytes(void* h);
+void* plbm_gpu_triggers_device(void* h);
+int plbm_gpu_local_triggers(void* h, uint8_t* out, int n);   /* D2H copy, syncs */
+int plbm_gpu_ipc_handles(void* h, void* out);                /* 2 x cudaIpcMemHandle_t */
+int plbm_gpu_open_peer(void* h, int rank, const void* handles);
+/* Same-process peers (several ranks' engines in one process on one GPU):
+ * attach another engine's pools directly.                                    */
+int plbm_gpu_set_peer_pools(void* h, int rank, void* pool_f, void* pool_pf);
+void plbm_gpu_pool_pointers(void* h, void** pool_f, void** pool_pf);
+int plbm_gpu_tile_rank(void* h, const int32_t* coords);      /* -1 if absent */
+int plbm_gpu_sync(void* h);
 
 /* Engine::~Engine + SimulationState release.                                 */
 void plbm_gpu_destroy(void* h);

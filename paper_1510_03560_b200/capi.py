@@ -164,11 +164,47 @@ class KernelStats(C.Structure):
 
 class GpuEngine(StepEngine):
     """The product engine (libplbm_gpu.so).  There is no fallback: a missing
-    library or CUDA device raises."""
+    library or CUDA device raises.  rank/world > 1 builds one rank of a
+    multi-GPU run (include/plbm_gpu.h, "multi-GPU")."""
 
-    def __init__(self, sc: Scenario, device: int = 0, capture: bool = False):
-        super().__init__(sc, GPU_LIB, "plbm_gpu", device)
+    def __init__(self, sc: Scenario, device: int = 0, capture: bool = False,
+                 rank: int = 0, world: int = 1):
+        self.rank, self.world = rank, world
+        if world == 1:
+            super().__init__(sc, GPU_LIB, "plbm_gpu", device)
+        else:
+            self.scenario, self.prefix = sc, "plbm_gpu"
+            self.lib = load(GPU_LIB, "plbm_gpu")
+            self.lib.plbm_gpu_create_dist.restype = C.c_void_p
+            self.lib.plbm_gpu_create_dist.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                                      C.POINTER(Error)]
+            self._c = sc.to_c()
+            err = Error()
+            self._h = self.lib.plbm_gpu_create_dist(C.cast(self._c.ptr(), C.c_void_p), device,
+                                                    rank, world, C.byref(err))
+            if not self._h:
+                raise ValueError(f"plbm_gpu_create_dist failed: {err.message.decode()}")
+            self.ncell = sc.tile_extent ** 3
         lib = self.lib
+        P = C.c_void_p
+        for name, res, args in [
+                ("prepare", C.c_int, [P]),
+                ("step_begin", C.c_int, [P, C.POINTER(Error)]),
+                ("step_main", C.c_int, [P, C.POINTER(Error)]),
+                ("step_face", C.c_int, [P]),
+                ("step_end", C.c_int, [P, C.c_void_p, C.POINTER(Error)]),
+                ("trigger_bytes", C.c_int, [P]),
+                ("triggers_device", C.c_void_p, [P]),
+                ("local_triggers", C.c_int, [P, C.c_void_p, C.c_int]),
+                ("ipc_handles", C.c_int, [P, C.c_void_p]),
+                ("open_peer", C.c_int, [P, C.c_int, C.c_void_p]),
+                ("set_peer_pools", C.c_int, [P, C.c_int, C.c_void_p, C.c_void_p]),
+                ("pool_pointers", None, [P, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+                ("tile_rank", C.c_int, [P, C.POINTER(C.c_int32)]),
+                ("sync", C.c_int, [P])]:
+            fn = getattr(lib, f"plbm_gpu_{name}")
+            fn.restype = res
+            fn.argtypes = args
         lib.plbm_gpu_set_capture.argtypes = [C.c_void_p, C.c_int]
         lib.plbm_gpu_set_profiling.argtypes = [C.c_void_p, C.c_int]
         lib.plbm_gpu_kernel_stats.argtypes = [C.c_void_p, C.POINTER(KernelStats)]
@@ -194,13 +230,76 @@ class GpuEngine(StepEngine):
     def reset_kernel_stats(self) -> None:
         self.lib.plbm_gpu_reset_kernel_stats(self._h)
 
+    # ---- multi-rank protocol (include/plbm_gpu.h "multi-GPU") ----------------
+    def prepare(self) -> None:
+        if self.lib.plbm_gpu_prepare(self._h) != 0:
+            raise RuntimeError("plbm_gpu_prepare failed (peers attached?)")
+
+    def step_begin(self) -> None:
+        err = Error()
+        if self.lib.plbm_gpu_step_begin(self._h, C.byref(err)) != 0:
+            raise EngineError(err)
+
+    def step_main(self) -> None:
+        err = Error()
+        if self.lib.plbm_gpu_step_main(self._h, C.byref(err)) != 0:
+            raise EngineError(err)
+
+    def step_face(self) -> None:
+        self.lib.plbm_gpu_step_face(self._h)
+
+    def step_end(self, merged: "np.ndarray | None" = None) -> None:
+        err = Error()
+        ptr = None if merged is None else merged.ctypes.data_as(C.c_void_p)
+        if self.lib.plbm_gpu_step_end(self._h, ptr, C.byref(err)) != 0:
+            raise EngineError(err)
+
+    def trigger_bytes(self) -> int:
+        return self.lib.plbm_gpu_trigger_bytes(self._h)
+
+    def triggers_device(self) -> int:
+        return self.lib.plbm_gpu_triggers_device(self._h)
+
+    def local_triggers(self) -> np.ndarray:
+        out = np.zeros(self.trigger_bytes(), np.uint8)
+        self.lib.plbm_gpu_local_triggers(self._h, out.ctypes.data_as(C.c_void_p), out.size)
+        return out
+
+    def ipc_handles(self) -> bytes:
+        buf = (C.c_char * 256)()
+        n = self.lib.plbm_gpu_ipc_handles(self._h, buf)
+        if n <= 0:
+            raise RuntimeError("plbm_gpu_ipc_handles failed")
+        return bytes(buf[:n])
+
+    def open_peer(self, rank: int, handles: bytes) -> None:
+        buf = (C.c_char * len(handles)).from_buffer_copy(handles)
+        if self.lib.plbm_gpu_open_peer(self._h, rank, buf) != 0:
+            raise RuntimeError(f"plbm_gpu_open_peer({rank}) failed")
+
+    def pool_pointers(self):
+        f, pf = C.c_void_p(), C.c_void_p()
+        self.lib.plbm_gpu_pool_pointers(self._h, C.byref(f), C.byref(pf))
+        return f.value, pf.value
+
+    def set_peer_pools(self, rank: int, pools) -> None:
+        if self.lib.plbm_gpu_set_peer_pools(self._h, rank, pools[0], pools[1]) != 0:
+            raise RuntimeError("plbm_gpu_set_peer_pools failed")
+
+    def tile_rank(self, coords) -> int:
+        return self.lib.plbm_gpu_tile_rank(self._h, (C.c_int32 * 3)(*coords))
+
+    def sync(self) -> None:
+        self.lib.plbm_gpu_sync(self._h)
+
     def set_kernel_variant(self, variant: int) -> None:
-        """0 = TMEM-stash cluster kernel where it applies, 1 = plain kernel."""
+        """0 = TMEM/smem-stash cluster kernel where it applies, 1 = plain kernel."""
         self.lib.plbm_gpu_set_kernel_variant(self._h, int(variant))
 
     def stream(self) -> int:
         return self.lib.plbm_gpu_stream(self._h)
 
 
-def gpu_engine(sc: Scenario, device: int = 0, capture: bool = False) -> GpuEngine:
-    return GpuEngine(sc, device, capture)
+def gpu_engine(sc: Scenario, device: int = 0, capture: bool = False, rank: int = 0,
+               world: int = 1) -> GpuEngine:
+    return GpuEngine(sc, device, capture, rank, world)

@@ -3,9 +3,19 @@
 // The host keeps only METADATA (the reference's TileMap / AssignmentState /
 // DeviceTopology counters without any field buffer): tile coordinates, owners,
 // creation log, per-device counts, byte classes.  All field state lives in
-// the device block pool (kernels.cuh).  Expansion (proj/src/tilemap.cpp:220-266)
+// device block pools (kernels.cuh).  Expansion (proj/src/tilemap.cpp:220-266)
 // and placement (proj/src/assign.cpp:8-38, engine.cpp:30-41) run on this
 // mirror from the per-face trigger bits the device criterion produced.
+//
+// Multi-GPU (one process per GPU): every rank runs the same deterministic
+// mirror, so global slot ids, owners and per-rank local pool indices agree on
+// all ranks without communication.  Tile owner `o` (assign_device) lives on
+// rank `o % world` (the reference's worker mapping, engine.cpp:214-218).  Each
+// rank allocates a pool only for its own tiles; the per-slot pointer tables
+// point remote slots at the owner's pool (CUDA IPC, read over NVLink inside
+// the fused kernel).  Between step_begin and step_end the caller merges the
+// trigger bits of all ranks (one small all-reduce), which also orders the
+// ranks' double-buffered reads and writes.
 #include "kernels.cuh"
 #include "kernels_tm.cuh"
 #include "plbm_gpu.h"
@@ -50,20 +60,7 @@ void host_equilibrium(double rho, const double u[3], double* out) {
     }
 }
 
-// proj/src/physics.cpp:12-27
-double host_pr_pressure(double rho, const plbm_component_desc& e) {
-    if (e.b * rho >= 1.0) throw std::domain_error("pr_pressure: b*rho >= 1 (EOS pole)");
-    double theta = 1.0;
-    if (e.Tc > 0.0) {
-        const double kappa = 0.37464 + 1.54226 * e.omega - 0.26992 * e.omega * e.omega;
-        const double root = 1.0 + kappa * (1.0 - std::sqrt(e.T / e.Tc));
-        theta = root * root;
-    }
-    const double ideal = rho * e.R * e.T / (1.0 - e.b * rho);
-    const double attr = e.a * theta * rho * rho / (1.0 + 2.0 * e.b * rho - e.b * e.b * rho * rho);
-    return ideal - attr;
-}
-
+// theta(T) of proj/src/physics.cpp:16-21
 double host_theta(const plbm_component_desc& e) {
     double theta = 1.0;
     if (e.Tc > 0.0) {
@@ -72,6 +69,15 @@ double host_theta(const plbm_component_desc& e) {
         theta = root * root;
     }
     return theta;
+}
+
+// proj/src/physics.cpp:12-27
+double host_pr_pressure(double rho, const plbm_component_desc& e) {
+    if (e.b * rho >= 1.0) throw std::domain_error("pr_pressure: b*rho >= 1 (EOS pole)");
+    const double theta = host_theta(e);
+    const double ideal = rho * e.R * e.T / (1.0 - e.b * rho);
+    const double attr = e.a * theta * rho * rho / (1.0 + 2.0 * e.b * rho - e.b * e.b * rho * rho);
+    return ideal - attr;
 }
 
 // proj/src/physics.cpp:34-42
@@ -89,21 +95,15 @@ T* dmalloc(size_t n) {
 }
 
 // ---- kernel dispatch over (E, C, NOPSI) --------------------------------------
+using MainFn = void (*)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
 struct Kernels {
-    void (*main)(Dev, const int*, int, int, long, dim3, dim3, size_t, cudaStream_t);
-    void (*face)(Dev, const int*, int, int, long, dim3, cudaStream_t);
-    void (*face_amb)(Dev, const int*, int, cudaStream_t);
+    MainFn main_plain;  // variant 1 (and the only kernel for E = 8 / psi-free)
+    MainFn main_tm;     // variant 0: TMEM/smem stash, 4-CTA cluster
+    void (*face)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
     void (*readback)(Dev, int, int, int, double*, cudaStream_t);
-    void (*main_tm)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
-    void (*main_tm2)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
-    void (*main_tm3)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
-    void (*main_tm4)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
-    int nt, bz;
-    size_t smem;
+    int nt;
 };
 
-// The TMEM-stash cluster kernel serves E in {16, 32} with a psi stencil; the
-// plain kernel serves psi-free scenarios (no stencil: one pass already) and E = 8.
 template <int E, int C>
 void launch_tm(Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
     using T = TmCfg<E, C>;
@@ -122,102 +122,32 @@ void launch_tm(Dev d, const int* act, int src, int wu, long it, unsigned ntiles,
     cudaLaunchKernelEx(&cfg, k_main_tm<E, C>, d, act, src, wu, it);
 }
 
-template <int E, int C>
-void launch_tm2(Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
-    using T = Tm2Cfg<E, C>;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ntiles * T::NB);
-    cfg.blockDim = dim3(T::NT);
-    cfg.dynamicSmemBytes = T::SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = T::NB;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_main_tm2<E, C>, d, act, src, wu, it);
-}
-
-template <int E, int C>
-void launch_tm3(Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
-    using T = Tm3Cfg<E, C>;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ntiles * T::NB);
-    cfg.blockDim = dim3(T::NT);
-    cfg.dynamicSmemBytes = T::SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = T::NB;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_main_tm3<E, C>, d, act, src, wu, it);
-}
-
-template <int E, int C>
-void launch_tm4(Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
-    using T = Tm2Cfg<E, C>;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ntiles * T::NB);
-    cfg.blockDim = dim3(T::NT);
-    cfg.dynamicSmemBytes = T::SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = T::NB;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_main_tm4<E, C>, d, act, src, wu, it);
-}
-
 template <int E, int C, bool NOPSI>
 Kernels make_kernels() {
     constexpr int NT = E * E < 256 ? E * E : 256;
     constexpr int BZ = E < 8 ? E : 8;
     constexpr int G = E + 2;
+    constexpr size_t SMEM_PLAIN = NOPSI ? 0 : size_t(3) * C * G * G * sizeof(double);
     Kernels k;
     k.nt = NT;
-    k.bz = BZ;
-    k.smem = NOPSI ? 0 : size_t(3) * C * G * G * sizeof(double);
-    if (k.smem > 48 * 1024)
+    if (SMEM_PLAIN > 48 * 1024)
         cudaFuncSetAttribute(k_main<E, C, BZ, NT, NOPSI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(k.smem));
-    k.main = [](Dev d, const int* act, int src, int wu, long it, dim3 g, dim3 b, size_t sm,
-                cudaStream_t s) { k_main<E, C, BZ, NT, NOPSI><<<g, b, sm, s>>>(d, act, src, wu, it); };
+                             int(SMEM_PLAIN));
+    k.main_plain = [](Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
+        k_main<E, C, BZ, NT, NOPSI><<<ntiles * (E / BZ), NT, SMEM_PLAIN, s>>>(d, act, src, wu, it);
+    };
     k.main_tm = nullptr;
-    k.main_tm2 = nullptr;
-    k.main_tm3 = nullptr;
-    k.main_tm4 = nullptr;
-    if constexpr (!NOPSI && (E == 16 || E == 32)) {
+    if constexpr (!NOPSI && (E == 16 || E == 32) && C <= 2) {
         cudaFuncSetAttribute(k_main_tm<E, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              TmCfg<E, C>::SMEM);
         k.main_tm = launch_tm<E, C>;
-        if constexpr (C <= 2) {
-            cudaFuncSetAttribute(k_main_tm2<E, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Tm2Cfg<E, C>::SMEM);
-            k.main_tm2 = launch_tm2<E, C>;
-            cudaFuncSetAttribute(k_main_tm3<E, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Tm3Cfg<E, C>::SMEM);
-            k.main_tm3 = launch_tm3<E, C>;
-            cudaFuncSetAttribute(k_main_tm4<E, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Tm2Cfg<E, C>::SMEM);
-            k.main_tm4 = launch_tm4<E, C>;
-        }
     }
-    k.face = [](Dev d, const int* act, int src, int flags, long it, dim3 g, cudaStream_t s) {
-        k_face<E, C, NT><<<g, NT, 0, s>>>(d, act, src, flags, it);
-    };
-    k.face_amb = [](Dev d, const int* slots, int n, cudaStream_t s) {
-        if (n) k_face_ambient<E><<<n, 256, 0, s>>>(d, slots, n);
+    k.face = [](Dev d, const int* act, int src, int flags, long it, unsigned ntiles, cudaStream_t s) {
+        constexpr unsigned NCH = (E * E + NT - 1) / NT;
+        k_face<E, C, NT><<<ntiles * 6 * NCH, NT, 0, s>>>(d, act, src, flags, it);
     };
     k.readback = [](Dev d, int slot, int c, int src, double* out, cudaStream_t s) {
-        k_readback<E><<<(E * E * E + 255) / 256, 256, 0, s>>>(d, slot, c, src, 0, out);
+        k_readback<E><<<(E * E * E + 255) / 256, 256, 0, s>>>(d, slot, c, src, out);
     };
     return k;
 }
@@ -254,7 +184,9 @@ struct Coord {
 
 struct SlotInfo {
     Coord c{};
-    int owner = -1;
+    int owner = -1;  // assign_device result (simulated device)
+    int rank = -1;   // GPU rank holding the fields (owner % world)
+    int local = -1;  // index in the owner rank's pool
     long birth = 0;
     size_t log_index = 0;
     int fluid = 0;
@@ -272,10 +204,17 @@ struct LogRow {
 
 class Engine {
   public:
-    Engine(const plbm_scenario_desc& d, int device) { init(d, device); }
+    Engine(const plbm_scenario_desc& d, int device, int rank, int world) {
+        init(d, device, rank, world);
+    }
     ~Engine() { release(); }
 
+    int prepare();
     int step(int n, plbm_error* err);
+    int step_begin(plbm_error* err);
+    int step_main(plbm_error* err);
+    int step_face();
+    int step_end(const uint8_t* merged, plbm_error* err);
     void counters(plbm_counters* out);
     int tiles(int32_t* coords, int32_t* owners, int64_t* births, int max) const;
     int read_tile(const int32_t* coords, int comp, int field, double* out);
@@ -290,10 +229,25 @@ class Engine {
         stats_ = plbm_kernel_stats{};
     }
     cudaStream_t stream() const { return stream_; }
+    int trig_bytes() const { return int(trig_bytes_); }
+    uint8_t* trig_device() const { return d_trig_; }
+    int local_triggers(uint8_t* out, int n);
+    void pool_pointers(void** f, void** pf) const {
+        *f = d_pool_f_;
+        *pf = d_pool_pf_;
+    }
+    int ipc_handles(void* out) const;
+    int open_peer(int rank, const void* handles);
+    int set_peer(int rank, void* pool_f, void* pool_pf);
+    int rank_of(const int32_t* coords) const;
+    int sync() {
+        CK(cudaStreamSynchronize(stream_));
+        return 0;
+    }
 
   private:
     // configuration
-    int dev_ = 0;
+    int dev_ = 0, rank_ = 0, world_ = 1;
     int E_ = 0, C_ = 0, E3_ = 0, E2_ = 0;
     int dom_[3]{}, grid_[3]{}, periodic_[3]{};
     int mode_ = 0, devices_ = 1, policy_ = 1;
@@ -308,37 +262,48 @@ class Engine {
     Kernels K_{};
     Params params_{};
 
-    // host mirror
-    std::vector<int> grid_slot_;  // lin -> slot or -1
+    // host mirror (replicated on every rank)
+    std::vector<int> grid_slot_;  // lin -> global slot or -1
     std::vector<SlotInfo> slots_;
     std::vector<int> free_slots_;
-    std::vector<int> active_;     // slots in coordinate order
+    std::vector<int> all_active_;   // global slots in coordinate order
+    std::vector<int> active_;       // this rank's slots in coordinate order
+    std::vector<int> next_local_;   // per rank: next pool index
     std::vector<LogRow> log_;
     std::vector<uint64_t> per_dev_;
-    uint64_t suppressed_ = 0, active_cells_ = 0;
+    uint64_t suppressed_ = 0, active_cells_ = 0, local_cells_ = 0;
     uint64_t bytes_[3]{};
     uint64_t step_bytes_[3]{};
     long iteration_ = 0;
     uint64_t cell_updates_ = 0;
-    uint64_t dev_cnt_[CNT_N]{};
-    bool any_gen_ = true;     // some tile is in a GEN mode this step
+    bool any_gen_ = true;
     bool routes_differ_ = false;
-    std::vector<uint8_t> h_mode_;      // [slot]
-    std::vector<uint8_t> h_has_solid_; // [slot]
-    std::vector<int> h_coords_;        // [slot][3]
-    std::vector<uint32_t> h_solid_;    // [slot][solid_words]
-    int cap_ = 0, amb_ = 0;
+    bool prepared_ = false;
+    int phase_ = 0;  // 0 idle, 1 main queued, 2 face queued
+    std::vector<uint8_t> h_mode_;
+    std::vector<uint8_t> h_has_solid_;
+    std::vector<int> h_coords_;
+    std::vector<uint32_t> h_solid_;
+    std::vector<int> h_lidx_;
+    int cap_ = 0, amb_ = 0, lcap_ = 0;
+    size_t per_slot_ = 0, per_pf_ = 0;
+    size_t trig_bytes_ = 0;
 
     // device
     cudaStream_t stream_ = nullptr;
     Dev d_{};
-    double* d_f_[2]{};
+    double* d_pool_f_ = nullptr;   // [2][lcap+1][per_slot]  (local index lcap = ambient)
+    double* d_pool_pf_ = nullptr;  // [2][lcap+1][per_pf]
+    std::vector<double*> peer_f_, peer_pf_;  // pool bases per rank (self = own)
+    std::vector<bool> peer_opened_;
+    double** d_slot_f_[2]{};
+    double** d_slot_pf_[2]{};
     int* d_route_[2]{};
+    int* d_lidx_ = nullptr;
     uint32_t* d_solid_ = nullptr;
     uint8_t* d_has_solid_ = nullptr;
     uint8_t* d_mode_ = nullptr;
     int* d_coords_ = nullptr;
-    double* d_psi_face_ = nullptr;
     double* d_u_face_ = nullptr;
     uint8_t* d_trig_ = nullptr;
     double* d_capture_ = nullptr;
@@ -359,10 +324,8 @@ class Engine {
     };
     std::vector<EvPair> ev_pool_;
     size_t ev_used_ = 0;
-    EvPair& next_event(int kind, uint64_t cells);
-    void resolve_events();
 
-    void init(const plbm_scenario_desc& d, int device);
+    void init(const plbm_scenario_desc& d, int device, int rank, int world);
     void release();
     size_t lin(const Coord& c) const { return (size_t(c.x) * grid_[1] + c.y) * grid_[2] + c.z; }
     int slot_at(const Coord& c) const { return grid_slot_[lin(c)]; }
@@ -375,18 +338,29 @@ class Engine {
     }
     void compute_routes(int slot, int* out) const;
     void upload_map(const std::vector<int>& new_slots, bool initial);
-    void check_error(plbm_error* err, bool& failed);
+    void upload_pointers();
     void recompute_step_bytes();
     void launch_face(int src, int flags, long iter);
     void launch_main(long iter);
     void expand(const std::vector<std::pair<Coord, int>>& triggers, long iteration,
                 std::vector<int>& created);
+    void check_error(plbm_error* err, bool& failed);
+    EvPair& next_event(int kind, uint64_t cells);
+    void resolve_events();
+    bool peers_ready() const {
+        for (int r = 0; r < world_; ++r)
+            if (!peer_f_[r]) return false;
+        return true;
+    }
 };
 
 // ---------------------------------------------------------------------------
 
-void Engine::init(const plbm_scenario_desc& d, int device) {
+void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) {
     dev_ = device;
+    rank_ = rank;
+    world_ = world;
+    if (world_ < 1 || rank_ < 0 || rank_ >= world_) throw std::invalid_argument("bad rank/world");
     E_ = d.tile_extent;
     C_ = d.n_components;
     E2_ = E_ * E_;
@@ -460,7 +434,7 @@ void Engine::init(const plbm_scenario_desc& d, int device) {
         for (int i = 0; i < Q; ++i) rnb += k.feq_amb[i];
         k.psi_nb = host_psi(rnb, host_pr_pressure(rnb, s), s.g_self);
     }
-    for (int k = 0; k < C_ * C_; ++k) p.coupling[(k / C_) * C_ + (k % C_)] = coupling_[k];
+    for (int k = 0; k < C_ * C_; ++k) p.coupling[k] = coupling_[k];
     for (size_t s = 0; s < seeds_.size(); ++s) {
         const plbm_seed_desc& sd = seeds_[s];
         SeedConst& sc = p.seeds[s];
@@ -477,69 +451,88 @@ void Engine::init(const plbm_scenario_desc& d, int device) {
         host_equilibrium(sd.rho, sd.velocity, sc.feq);
     }
 
-    // ---- device memory
-    CK(cudaSetDevice(dev_));
-    CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-    K_ = pick_kernels(E_, C_, nopsi_);
+    // ---- capacities: global slots (all tiles) + per-rank local pools
     const size_t n_tiles = size_t(grid_[0]) * grid_[1] * grid_[2];
     cap_ = int(n_tiles);
     amb_ = cap_;
     p.amb_slot = amb_;
+    // owners are balanced over `devices` (spread <= 1, assign.cpp:8-15) and
+    // owner o lives on rank o % world: the busiest rank holds at most
+    // ceil(devices/world) owners x ceil(tiles/devices) tiles.
+    {
+        const int owners_per_rank = (devices_ + world_ - 1) / world_;
+        const int tiles_per_owner = int((n_tiles + devices_ - 1) / devices_);
+        lcap_ = std::min(int(n_tiles), owners_per_rank * tiles_per_owner);
+        if (world_ == 1) lcap_ = int(n_tiles);
+    }
+    per_slot_ = size_t(C_) * Q * E3_;
+    per_pf_ = size_t(C_) * 6 * E2_;
     const int nslot = cap_ + 1;
-    const size_t per_slot = size_t(C_) * Q * E3_;
     const int G = E_ + 2;
     solid_words_ = (G * G * G + 31) / 32;
-    d_f_[0] = dmalloc<double>(per_slot * nslot);
-    d_f_[1] = dmalloc<double>(per_slot * nslot);
+    trig_bytes_ = (size_t(nslot) + 3) / 4 * 4;
+
+    CK(cudaSetDevice(dev_));
+    CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    K_ = pick_kernels(E_, C_, nopsi_);
+    d_pool_f_ = dmalloc<double>(2 * per_slot_ * size_t(lcap_ + 1));
+    d_pool_pf_ = dmalloc<double>(2 * per_pf_ * size_t(lcap_ + 1));
+    for (int b = 0; b < 2; ++b) {
+        d_slot_f_[b] = dmalloc<double*>(nslot);
+        d_slot_pf_[b] = dmalloc<double*>(nslot);
+    }
     d_route_[0] = dmalloc<int>(size_t(nslot) * 18);
     d_route_[1] = dmalloc<int>(size_t(nslot) * 18);
+    d_lidx_ = dmalloc<int>(nslot);
     d_solid_ = dmalloc<uint32_t>(size_t(nslot) * solid_words_);
     d_has_solid_ = dmalloc<uint8_t>(nslot);
     d_mode_ = dmalloc<uint8_t>(nslot);
     d_coords_ = dmalloc<int>(size_t(nslot) * 3);
-    d_psi_face_ = dmalloc<double>(size_t(nslot) * C_ * 6 * E2_);
-    d_u_face_ = dmalloc<double>(size_t(nslot) * C_ * 6 * 3 * E2_);
-    const size_t trig_bytes = (size_t(nslot) + 3) / 4 * 4;
-    d_trig_ = dmalloc<uint8_t>(trig_bytes);
+    d_u_face_ = dmalloc<double>(size_t(lcap_ + 1) * C_ * 6 * 3 * E2_);
+    d_trig_ = dmalloc<uint8_t>(trig_bytes_);
     d_cnt_ = dmalloc<unsigned long long>(CNT_N);
     d_err_ = dmalloc<unsigned long long>(1);
     d_active_ = dmalloc<int>(nslot);
     d_scratch_slots_ = dmalloc<int>(nslot);
     d_readback_ = dmalloc<double>(size_t(23) * E3_);
-    CK(cudaMemsetAsync(d_has_solid_, 0, nslot, stream_));
-    CK(cudaMemsetAsync(d_mode_, 0, nslot, stream_));
-    CK(cudaMemsetAsync(d_u_face_, 0, size_t(nslot) * C_ * 6 * 3 * E2_ * sizeof(double), stream_));
-    CK(cudaMemsetAsync(d_trig_, 0, trig_bytes, stream_));
+    CK(cudaMemsetAsync(d_u_face_, 0, size_t(lcap_ + 1) * C_ * 6 * 3 * E2_ * sizeof(double), stream_));
+    CK(cudaMemsetAsync(d_trig_, 0, trig_bytes_, stream_));
     CK(cudaMemsetAsync(d_cnt_, 0, CNT_N * sizeof(unsigned long long), stream_));
     CK(cudaMemsetAsync(d_err_, 0xff, sizeof(unsigned long long), stream_));
     CK(cudaMemcpyToSymbolAsync(P, &params_, sizeof(Params), 0, cudaMemcpyHostToDevice, stream_));
-    // the ambient slot: feq_amb in both buffers, psi_amb on its faces
+    // this rank's ambient slot (local index lcap): feq_amb in both buffers and
+    // psi_amb on its faces for both parities
     {
-        std::vector<double> amb(per_slot);
+        std::vector<double> amb(per_slot_);
         for (int c = 0; c < C_; ++c)
             for (int i = 0; i < Q; ++i)
                 std::fill_n(amb.begin() + (size_t(c) * Q + i) * E3_, E3_, p.comp[c].feq_amb[i]);
-        CK(cudaMemcpy(d_f_[0] + per_slot * amb_, amb.data(), per_slot * sizeof(double),
-                      cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(d_f_[1] + per_slot * amb_, amb.data(), per_slot * sizeof(double),
-                      cudaMemcpyHostToDevice));
-        std::vector<double> pf(size_t(C_) * 6 * E2_);
+        std::vector<double> pf(per_pf_);
         for (int c = 0; c < C_; ++c)
             std::fill_n(pf.begin() + size_t(c) * 6 * E2_, 6 * E2_, p.comp[c].psi_amb);
-        CK(cudaMemcpy(d_psi_face_ + size_t(amb_) * C_ * 6 * E2_, pf.data(), pf.size() * sizeof(double),
-                      cudaMemcpyHostToDevice));
-        const int zc[3] = {-1000000, -1000000, -1000000};
-        CK(cudaMemcpy(d_coords_ + 3 * amb_, zc, sizeof zc, cudaMemcpyHostToDevice));
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaMemcpy(d_pool_f_ + (size_t(b) * (lcap_ + 1) + lcap_) * per_slot_, amb.data(),
+                          per_slot_ * sizeof(double), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(d_pool_pf_ + (size_t(b) * (lcap_ + 1) + lcap_) * per_pf_, pf.data(),
+                          per_pf_ * sizeof(double), cudaMemcpyHostToDevice));
+        }
     }
-    d_.f[0] = d_f_[0];
-    d_.f[1] = d_f_[1];
+    peer_f_.assign(world_, nullptr);
+    peer_pf_.assign(world_, nullptr);
+    peer_opened_.assign(world_, false);
+    peer_f_[rank_] = d_pool_f_;
+    peer_pf_[rank_] = d_pool_pf_;
+    for (int b = 0; b < 2; ++b) {
+        d_.slot_f[b] = d_slot_f_[b];
+        d_.slot_pf[b] = d_slot_pf_[b];
+    }
     d_.route[0] = d_route_[0];
     d_.route[1] = d_route_[1];
+    d_.lidx = d_lidx_;
     d_.solid = d_solid_;
     d_.has_solid = d_has_solid_;
     d_.mode = d_mode_;
     d_.coords = d_coords_;
-    d_.psi_face = d_psi_face_;
     d_.u_face = d_u_face_;
     d_.trig = d_trig_;
     d_.capture = nullptr;
@@ -552,11 +545,14 @@ void Engine::init(const plbm_scenario_desc& d, int device) {
     slots_.assign(nslot, SlotInfo{});
     free_slots_.clear();
     for (int s = cap_ - 1; s >= 0; --s) free_slots_.push_back(s);
+    next_local_.assign(world_, 0);
     per_dev_.assign(devices_, 0);
     h_mode_.assign(nslot, MODE_PULL);
     h_has_solid_.assign(nslot, 0);
     h_coords_.assign(size_t(nslot) * 3, -1000000);
     h_solid_.assign(size_t(nslot) * solid_words_, 0u);
+    h_lidx_.assign(nslot, -1);
+    h_lidx_[amb_] = lcap_;
     std::vector<uint8_t> initial(n_tiles, 0);
     if (mode_ == PLBM_MODE_STATIC) {
         std::fill(initial.begin(), initial.end(), 1);
@@ -606,16 +602,32 @@ void Engine::init(const plbm_scenario_desc& d, int device) {
     }
     for (int s : created) h_mode_[s] = MODE_GEN_SEEDED;
     upload_map(created, true);
-    // psi_face for step 1 from the generated initial state
+    if (world_ == 1) prepare();
+    CK(cudaStreamSynchronize(stream_));
+}
+
+// psi faces of the initial (generated) state for step 1.  Multi-rank callers
+// run this on every rank after attaching peers and synchronise before step 1.
+int Engine::prepare() {
+    if (prepared_) return 0;
+    if (!peers_ready()) return -8;
     launch_face(0, 0, 0);
     CK(cudaStreamSynchronize(stream_));
+    prepared_ = true;
+    return 0;
 }
 
 void Engine::release() {
     if (stream_) cudaStreamSynchronize(stream_);
-    void* ptrs[] = {d_f_[0], d_f_[1], d_route_[0], d_route_[1], d_solid_, d_has_solid_, d_mode_,
-                    d_coords_, d_psi_face_, d_u_face_, d_trig_, d_capture_, d_cnt_, d_err_,
-                    d_active_, d_scratch_slots_, d_readback_};
+    for (int r = 0; r < world_ && r < int(peer_opened_.size()); ++r)
+        if (peer_opened_[r]) {
+            cudaIpcCloseMemHandle(peer_f_[r]);
+            cudaIpcCloseMemHandle(peer_pf_[r]);
+        }
+    void* ptrs[] = {d_pool_f_, d_pool_pf_, d_slot_f_[0], d_slot_f_[1], d_slot_pf_[0], d_slot_pf_[1],
+                    d_route_[0], d_route_[1], d_lidx_, d_solid_, d_has_solid_, d_mode_, d_coords_,
+                    d_u_face_, d_trig_, d_capture_, d_cnt_, d_err_, d_active_, d_scratch_slots_,
+                    d_readback_};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     for (auto& e : ev_pool_) {
@@ -689,7 +701,8 @@ int Engine::create_tile(const Coord& c, long iteration, int trigger) {
     return s;
 }
 
-// proj/src/engine.cpp:30-41 -> proj/src/assign.cpp:8-38
+// proj/src/engine.cpp:30-41 -> proj/src/assign.cpp:8-38; then the GPU rank
+// (owner % world) and its next pool index.
 void Engine::assign_owner(int slot) {
     SlotInfo& t = slots_[slot];
     std::vector<int> owners;
@@ -725,6 +738,11 @@ void Engine::assign_owner(int slot) {
     ++per_dev_[chosen];
     t.owner = chosen;
     log_[t.log_index].owner = chosen;
+    t.rank = chosen % world_;
+    t.local = next_local_[t.rank]++;
+    if (t.local >= lcap_) throw std::runtime_error("local block pool exhausted");
+    h_lidx_[slot] = t.rank == rank_ ? t.local : -1;
+    if (t.rank == rank_) local_cells_ += uint64_t(t.fluid);
 }
 
 // Ghost routing (proj/src/engine.cpp:266-296): a face ghost reads the face
@@ -756,7 +774,7 @@ void Engine::recompute_step_bytes() {
     // Closed form of record_exchange over one step: P2 and P4 each record one
     // transfer per (tile, face) with an existing neighbour (engine.cpp:305-309).
     step_bytes_[0] = step_bytes_[1] = step_bytes_[2] = 0;
-    for (int s : active_) {
+    for (int s : all_active_) {
         for (int f = 0; f < 6; ++f) {
             Coord n;
             if (!neighbor_coords(slots_[s].c, f, n)) continue;
@@ -767,11 +785,43 @@ void Engine::recompute_step_bytes() {
     }
 }
 
+// Per-slot device pointers: own slots and the ambient slot into this rank's
+// pool, remote slots into the owner rank's pool (IPC-mapped peer memory).
+void Engine::upload_pointers() {
+    const size_t nslot = size_t(cap_ + 1);
+    std::vector<double*> f[2], pf[2];
+    for (int b = 0; b < 2; ++b) {
+        f[b].assign(nslot, nullptr);
+        pf[b].assign(nslot, nullptr);
+    }
+    auto fill = [&](int s, int r, int local) {
+        for (int b = 0; b < 2; ++b) {
+            if (!peer_f_[r]) continue;
+            f[b][s] = peer_f_[r] + (size_t(b) * (lcap_ + 1) + local) * per_slot_;
+            pf[b][s] = peer_pf_[r] + (size_t(b) * (lcap_ + 1) + local) * per_pf_;
+        }
+    };
+    for (int s : all_active_) fill(s, slots_[s].rank, slots_[s].local);
+    fill(amb_, rank_, lcap_);
+    for (int b = 0; b < 2; ++b) {
+        CK(cudaMemcpyAsync(d_slot_f_[b], f[b].data(), nslot * sizeof(double*), cudaMemcpyHostToDevice,
+                           stream_));
+        CK(cudaMemcpyAsync(d_slot_pf_[b], pf[b].data(), nslot * sizeof(double*), cudaMemcpyHostToDevice,
+                           stream_));
+    }
+    stats_.h2d_bytes += 4 * nslot * sizeof(double*);
+    CK(cudaStreamSynchronize(stream_));  // host vectors die here
+}
+
 void Engine::upload_map(const std::vector<int>& new_slots, bool initial) {
-    // active list in coordinate order
+    // active lists in coordinate order (all tiles / this rank's tiles)
+    all_active_.clear();
     active_.clear();
     for (size_t k = 0; k < grid_slot_.size(); ++k)
-        if (grid_slot_[k] >= 0) active_.push_back(grid_slot_[k]);
+        if (grid_slot_[k] >= 0) {
+            all_active_.push_back(grid_slot_[k]);
+            if (slots_[grid_slot_[k]].rank == rank_) active_.push_back(grid_slot_[k]);
+        }
     const size_t nslot = size_t(cap_ + 1);
     CK(cudaMemcpyAsync(d_active_, active_.data(), active_.size() * sizeof(int),
                        cudaMemcpyHostToDevice, stream_));
@@ -779,25 +829,25 @@ void Engine::upload_map(const std::vector<int>& new_slots, bool initial) {
                        stream_));
     CK(cudaMemcpyAsync(d_has_solid_, h_has_solid_.data(), nslot, cudaMemcpyHostToDevice, stream_));
     CK(cudaMemcpyAsync(d_mode_, h_mode_.data(), nslot, cudaMemcpyHostToDevice, stream_));
+    CK(cudaMemcpyAsync(d_lidx_, h_lidx_.data(), nslot * sizeof(int), cudaMemcpyHostToDevice, stream_));
+    std::vector<int> mine;
     for (int s : new_slots) {
+        if (slots_[s].rank != rank_) continue;
+        mine.push_back(s);
         if (h_has_solid_[s])
             CK(cudaMemcpyAsync(d_solid_ + size_t(s) * solid_words_, &h_solid_[size_t(s) * solid_words_],
                                solid_words_ * sizeof(uint32_t), cudaMemcpyHostToDevice, stream_));
         if (d_capture_)
-            CK(cudaMemsetAsync(d_capture_ + size_t(s) * C_ * 4 * E3_, 0,
+            CK(cudaMemsetAsync(d_capture_ + size_t(slots_[s].local) * C_ * 4 * E3_, 0,
                                size_t(C_) * 4 * E3_ * sizeof(double), stream_));
     }
-    // newborn faces hold psi of the fresh ambient cell (initial tiles get
-    // theirs from k_face over the generated state)
-    if (!initial && !new_slots.empty()) {
-        CK(cudaMemcpyAsync(d_scratch_slots_, new_slots.data(), new_slots.size() * sizeof(int),
-                           cudaMemcpyHostToDevice, stream_));
-        K_.face_amb(d_, d_scratch_slots_, int(new_slots.size()), stream_);
-        ++stats_.kernels_launched;
-    }
+    if (peers_ready()) upload_pointers();
+    // newborns' psi faces need no write: readers see the GEN_AMBIENT mode and
+    // use psi of a fresh ambient cell (kernels.cuh psi_ghost); initial tiles
+    // get theirs from k_face over the generated state (prepare())
     // routes: pull table = map of the step that just ran, psi table = new map
     std::vector<int> routes(nslot * 18, amb_);
-    for (int s : active_) compute_routes(s, &routes[size_t(s) * 18]);
+    for (int s : all_active_) compute_routes(s, &routes[size_t(s) * 18]);
     if (!initial)
         CK(cudaMemcpyAsync(d_route_[ROUTE_PULL], d_route_[ROUTE_PSI], routes.size() * sizeof(int),
                            cudaMemcpyDeviceToDevice, stream_));
@@ -808,9 +858,9 @@ void Engine::upload_map(const std::vector<int>& new_slots, bool initial) {
                        cudaMemcpyHostToDevice, stream_));
     routes_differ_ = !initial;
     any_gen_ = true;
-    stats_.h2d_bytes += active_.size() * sizeof(int) + nslot * (3 * sizeof(int) + 2) +
+    stats_.h2d_bytes += active_.size() * sizeof(int) + nslot * (4 * sizeof(int) + 2) +
                         routes.size() * sizeof(int) * (initial ? 2 : 1);
-    for (int s : new_slots)
+    for (int s : mine)
         if (h_has_solid_[s]) stats_.h2d_bytes += solid_words_ * sizeof(uint32_t);
     recompute_step_bytes();
     // the host vectors must outlive the async copies
@@ -821,8 +871,7 @@ void Engine::launch_face(int src, int flags, long iter) {
     if (active_.empty()) return;
     EvPair* ev = profiling_ ? &next_event(1, 0) : nullptr;
     if (ev) CK(cudaEventRecord(ev->a, stream_));
-    const unsigned nch = unsigned((E2_ + K_.nt - 1) / K_.nt);
-    K_.face(d_, d_active_, src, flags, iter, dim3(unsigned(active_.size() * 6) * nch), stream_);
+    K_.face(d_, d_active_, src, flags, iter, unsigned(active_.size()), stream_);
     CK(cudaGetLastError());
     ++stats_.kernels_launched;
     if (ev) CK(cudaEventRecord(ev->b, stream_));
@@ -830,20 +879,11 @@ void Engine::launch_face(int src, int flags, long iter) {
 
 void Engine::launch_main(long iter) {
     if (active_.empty()) return;
-    const dim3 grid(unsigned(active_.size() * (E_ / K_.bz)));
-    EvPair* ev = profiling_ ? &next_event(0, active_cells_) : nullptr;
+    EvPair* ev = profiling_ ? &next_event(0, local_cells_) : nullptr;
     if (ev) CK(cudaEventRecord(ev->a, stream_));
     const int wu = mode_ == PLBM_MODE_PROGRESSIVE ? 1 : 0;
-    if (K_.main_tm2 && variant_ == 0)
-        K_.main_tm2(d_, d_active_, cur_, wu, iter, unsigned(active_.size()), stream_);
-    else if (K_.main_tm4 && variant_ == 4)
-        K_.main_tm4(d_, d_active_, cur_, wu, iter, unsigned(active_.size()), stream_);
-    else if (K_.main_tm3 && variant_ == 3)
-        K_.main_tm3(d_, d_active_, cur_, wu, iter, unsigned(active_.size()), stream_);
-    else if (K_.main_tm && variant_ <= 1)
-        K_.main_tm(d_, d_active_, cur_, wu, iter, unsigned(active_.size()), stream_);
-    else
-        K_.main(d_, d_active_, cur_, wu, iter, grid, dim3(K_.nt), K_.smem, stream_);
+    const MainFn fn = (K_.main_tm && variant_ == 0) ? K_.main_tm : K_.main_plain;
+    fn(d_, d_active_, cur_, wu, iter, unsigned(active_.size()), stream_);
     CK(cudaGetLastError());
     ++stats_.kernels_launched;
     if (ev) CK(cudaEventRecord(ev->b, stream_));
@@ -956,57 +996,125 @@ void Engine::expand(const std::vector<std::pair<Coord, int>>& triggers, long ite
               [&](int a, int b) { return slots_[a].c < slots_[b].c; });
 }
 
-int Engine::step(int n, plbm_error* err) {
-    const bool progressive = mode_ == PLBM_MODE_PROGRESSIVE;
-    // Static meshes never change: the whole batch is queued without a host
-    // round trip and the error flag (earliest iteration wins) is read once.
-    // Progressive meshes synchronise once per step to expand on the mirror.
-    const long it0 = iteration_;
-    for (int k = 0; k < n; ++k) {
-        const long it = iteration_ + 1;
-        launch_main(it);
-        cur_ ^= 1;
-        if (any_gen_) {
-            CK(cudaMemsetAsync(d_mode_, MODE_PULL, size_t(cap_ + 1), stream_));
-            std::fill(h_mode_.begin(), h_mode_.end(), uint8_t(MODE_PULL));
-            any_gen_ = false;
+// Engine::step() in three parts so ranks can synchronise between them:
+//   step_main  the fused kernel of this rank's tiles (reads peers' f_post^(k-1)
+//              and psi faces of step k, all complete before the previous
+//              step's trigger all-reduce)
+//   -- cross-rank barrier: k_face pulls peers' f_post^(k) --
+//   step_face  face pre-pass: psi faces for k+1, criterion, local trigger bits
+//   -- trigger all-reduce --
+//   step_end   expansion on the merged bits (touches nothing peers read)
+int Engine::step_main(plbm_error* err) {
+    if (!prepared_) {
+        if (err) {
+            std::memset(err, 0, sizeof *err);
+            err->code = 2;
+            std::snprintf(err->message, sizeof err->message,
+                          "engine not prepared (attach peers, then plbm_gpu_prepare on every rank)");
         }
-        if (routes_differ_) {
-            CK(cudaMemcpyAsync(d_route_[ROUTE_PULL], d_route_[ROUTE_PSI],
-                               size_t(cap_ + 1) * 18 * sizeof(int), cudaMemcpyDeviceToDevice, stream_));
-            routes_differ_ = false;
+        return 2;
+    }
+    if (phase_ != 0) return 0;
+    const long it = iteration_ + 1;
+    launch_main(it);
+    cur_ ^= 1;
+    if (any_gen_) {
+        CK(cudaMemsetAsync(d_mode_, MODE_PULL, size_t(cap_ + 1), stream_));
+        std::fill(h_mode_.begin(), h_mode_.end(), uint8_t(MODE_PULL));
+        any_gen_ = false;
+    }
+    if (routes_differ_) {
+        CK(cudaMemcpyAsync(d_route_[ROUTE_PULL], d_route_[ROUTE_PSI], size_t(cap_ + 1) * 18 * sizeof(int),
+                           cudaMemcpyDeviceToDevice, stream_));
+        routes_differ_ = false;
+    }
+    phase_ = 1;
+    return 0;
+}
+
+int Engine::step_face() {
+    if (phase_ != 1) return 0;
+    launch_face(cur_, mode_ == PLBM_MODE_PROGRESSIVE ? 3 : 2, iteration_ + 1);
+    phase_ = 2;
+    return 0;
+}
+
+int Engine::step_begin(plbm_error* err) {
+    const int rc = step_main(err);
+    if (rc) return rc;
+    return step_face();
+}
+
+// Second half: error check, then (progressive) expansion on the merged
+// trigger bits of all ranks.  `merged` = host copy of the all-reduced trigger
+// array, or NULL to read it from this engine's device array (single rank, or a
+// caller that all-reduced d_trig_ in place).
+int Engine::step_end(const uint8_t* merged, plbm_error* err) {
+    if (phase_ != 2) return 0;
+    phase_ = 0;
+    const long it = iteration_ + 1;
+    bool failed = false;
+    check_error(err, failed);
+    if (failed) return 1;
+    const uint64_t updates = active_cells_;
+    for (int a = 0; a < 3; ++a) bytes_[a] += step_bytes_[a];
+    if (mode_ == PLBM_MODE_PROGRESSIVE) {
+        std::vector<uint8_t> trig;
+        if (!merged) {
+            trig.resize(trig_bytes_);
+            CK(cudaMemcpyAsync(trig.data(), d_trig_, trig_bytes_, cudaMemcpyDeviceToHost, stream_));
+            stats_.d2h_bytes += trig_bytes_;
+            CK(cudaStreamSynchronize(stream_));
+            merged = trig.data();
         }
-        launch_face(cur_, progressive ? 3 : 2, it);
-        if (!progressive) {
-            for (int a = 0; a < 3; ++a) bytes_[a] += step_bytes_[a];
-            ++iteration_;
-            cell_updates_ += active_cells_;
-            continue;
-        }
-        bool failed = false;
-        check_error(err, failed);
-        if (failed) return 1;
-        std::vector<uint8_t> trig(size_t(cap_ + 1));
-        CK(cudaMemcpyAsync(trig.data(), d_trig_, trig.size(), cudaMemcpyDeviceToHost, stream_));
-        stats_.d2h_bytes += trig.size();
-        CK(cudaStreamSynchronize(stream_));
-        const uint64_t updates = active_cells_;
-        for (int a = 0; a < 3; ++a) bytes_[a] += step_bytes_[a];
         std::vector<std::pair<Coord, int>> triggers;
-        for (int s : active_)
+        for (int s : all_active_)
             for (int f = 0; f < 6; ++f)
-                if (trig[s] & (1u << f)) triggers.push_back({slots_[s].c, f});
+                if (merged[s] & (1u << f)) triggers.push_back({slots_[s].c, f});
+        CK(cudaMemsetAsync(d_trig_, 0, trig_bytes_, stream_));
         if (!triggers.empty()) {
-            CK(cudaMemsetAsync(d_trig_, 0, (size_t(cap_ + 1) + 3) / 4 * 4, stream_));
             std::vector<int> created;
             expand(triggers, it, created);
             for (int s : created) assign_owner(s);
             if (!created.empty()) upload_map(created, false);
         }
-        ++iteration_;
-        cell_updates_ += updates;
     }
-    if (!progressive && n > 0) {
+    ++iteration_;
+    cell_updates_ += updates;
+    return 0;
+}
+
+int Engine::step(int n, plbm_error* err) {
+    if (world_ != 1) {
+        if (err) {
+            std::memset(err, 0, sizeof *err);
+            err->code = 2;
+            std::snprintf(err->message, sizeof err->message,
+                          "multi-rank engines step with step_begin / all-reduce / step_end");
+        }
+        return 2;
+    }
+    if (mode_ == PLBM_MODE_PROGRESSIVE) {
+        for (int k = 0; k < n; ++k) {
+            int rc = step_begin(err);
+            if (rc) return rc;
+            rc = step_end(nullptr, err);
+            if (rc) return rc;
+        }
+        return 0;
+    }
+    // Static meshes never change: the whole batch is queued without a host
+    // round trip and the error flag (earliest iteration wins) is read once.
+    const long it0 = iteration_;
+    for (int k = 0; k < n; ++k) {
+        const int rc = step_begin(err);
+        if (rc) return rc;
+        phase_ = 0;
+        for (int a = 0; a < 3; ++a) bytes_[a] += step_bytes_[a];
+        ++iteration_;
+        cell_updates_ += active_cells_;
+    }
+    if (n > 0) {
         bool failed = false;
         check_error(err, failed);
         if (failed) {
@@ -1022,6 +1130,53 @@ int Engine::step(int n, plbm_error* err) {
     return 0;
 }
 
+int Engine::local_triggers(uint8_t* out, int n) {
+    if (n < int(trig_bytes_)) return -1;
+    CK(cudaMemcpyAsync(out, d_trig_, trig_bytes_, cudaMemcpyDeviceToHost, stream_));
+    stats_.d2h_bytes += trig_bytes_;
+    CK(cudaStreamSynchronize(stream_));
+    return int(trig_bytes_);
+}
+
+int Engine::ipc_handles(void* out) const {
+    cudaIpcMemHandle_t h[2];
+    CK(cudaIpcGetMemHandle(&h[0], d_pool_f_));
+    CK(cudaIpcGetMemHandle(&h[1], d_pool_pf_));
+    std::memcpy(out, h, sizeof h);
+    return int(sizeof h);
+}
+
+int Engine::open_peer(int rank, const void* handles) {
+    if (rank < 0 || rank >= world_ || rank == rank_) return -1;
+    cudaIpcMemHandle_t h[2];
+    std::memcpy(h, handles, sizeof h);
+    void* f = nullptr;
+    void* pf = nullptr;
+    CK(cudaIpcOpenMemHandle(&f, h[0], cudaIpcMemLazyEnablePeerAccess));
+    CK(cudaIpcOpenMemHandle(&pf, h[1], cudaIpcMemLazyEnablePeerAccess));
+    peer_f_[rank] = static_cast<double*>(f);
+    peer_pf_[rank] = static_cast<double*>(pf);
+    peer_opened_[rank] = true;
+    if (peers_ready()) upload_pointers();
+    return 0;
+}
+
+int Engine::set_peer(int rank, void* pool_f, void* pool_pf) {
+    if (rank < 0 || rank >= world_ || rank == rank_) return -1;
+    peer_f_[rank] = static_cast<double*>(pool_f);
+    peer_pf_[rank] = static_cast<double*>(pool_pf);
+    if (peers_ready()) upload_pointers();
+    return 0;
+}
+
+int Engine::rank_of(const int32_t* cc) const {
+    const Coord c{cc[0], cc[1], cc[2]};
+    if (c.x < 0 || c.y < 0 || c.z < 0 || c.x >= grid_[0] || c.y >= grid_[1] || c.z >= grid_[2])
+        return -1;
+    const int s = slot_at(c);
+    return s < 0 ? -1 : slots_[s].rank;
+}
+
 void Engine::counters(plbm_counters* out) {
     std::memset(out, 0, sizeof *out);
     unsigned long long c[CNT_N] = {};
@@ -1030,12 +1185,12 @@ void Engine::counters(plbm_counters* out) {
     stats_.d2h_bytes += sizeof c;
     out->iteration = iteration_;
     out->cell_updates = cell_updates_;
-    out->negative_populations = c[CNT_NEG];
+    out->negative_populations = c[CNT_NEG];  // this rank's tiles
     out->psi_clamps = c[CNT_CLAMP];
     out->zero_rho_forcings = c[CNT_ZERO_RHO];
     out->suppressed_expansions = suppressed_;
     for (int a = 0; a < 3; ++a) out->bytes[a] = bytes_[a];
-    out->tiles = active_.size();
+    out->tiles = all_active_.size();
     out->active_cells = active_cells_;
     const uint64_t g = uint64_t(E_ + 2) * (E_ + 2) * (E_ + 2);
     out->bytes_resident = out->tiles * g * (uint64_t(C_) * (2 * Q + 8) * 8 + 1);  // tile.cpp:7-13
@@ -1043,7 +1198,7 @@ void Engine::counters(plbm_counters* out) {
 
 int Engine::tiles(int32_t* coords, int32_t* owners, int64_t* births, int max) const {
     int k = 0;
-    for (int s : active_) {
+    for (int s : all_active_) {
         if (k < max) {
             if (coords) {
                 coords[3 * k] = slots_[s].c.x;
@@ -1066,10 +1221,13 @@ int Engine::read_tile(const int32_t* cc, int comp, int field, double* out) {
     if (s < 0) return -1;
     if (comp < 0 || comp >= C_) return -2;
     if (field < 0 || field > PLBM_FIELD_PSI) return -3;
+    if (slots_[s].rank != rank_) return -7;  // fields live on the owner rank
+    if (!peers_ready()) return -8;
     if (field == PLBM_FIELD_PSI || field >= PLBM_FIELD_PUX) {
         if (!d_capture_) return -4;
         const int which = field == PLBM_FIELD_PSI ? 0 : 1 + (field - PLBM_FIELD_PUX);
-        CK(cudaMemcpyAsync(out, d_capture_ + (size_t(s) * C_ + comp) * 4 * E3_ + size_t(which) * E3_,
+        CK(cudaMemcpyAsync(out,
+                           d_capture_ + (size_t(slots_[s].local) * C_ + comp) * 4 * E3_ + size_t(which) * E3_,
                            size_t(E3_) * sizeof(double), cudaMemcpyDeviceToHost, stream_));
         CK(cudaStreamSynchronize(stream_));
         return 0;
@@ -1104,7 +1262,7 @@ int Engine::creation_log(plbm_creation_event* out, int max) const {
 
 int Engine::set_capture(bool on) {
     if (on && !d_capture_) {
-        const size_t n = size_t(cap_ + 1) * C_ * 4 * E3_;
+        const size_t n = size_t(lcap_ + 1) * C_ * 4 * E3_;
         d_capture_ = dmalloc<double>(n);
         CK(cudaMemsetAsync(d_capture_, 0, n * sizeof(double), stream_));
         CK(cudaStreamSynchronize(stream_));
@@ -1118,7 +1276,7 @@ int Engine::set_capture(bool on) {
 }
 
 int Engine::poke_f(const int32_t*, int, int, const int32_t*, double) {
-    return -5;  // not supported yet on the device pool
+    return -5;  // not supported on the device pool
 }
 
 }  // namespace plbm
@@ -1133,14 +1291,16 @@ void fill_err(plbm_error* e, int code, const char* msg) {
     e->code = code;
     std::snprintf(e->message, sizeof e->message, "%s", msg);
 }
+plbm::Engine* EG(void* h) { return static_cast<plbm::Engine*>(h); }
 }  // namespace
 
 extern "C" {
 
-void* plbm_gpu_create(const plbm_scenario_desc* desc, int device, plbm_error* err) {
+void* plbm_gpu_create_dist(const plbm_scenario_desc* desc, int device, int rank, int world,
+                           plbm_error* err) {
     fill_err(err, 0, "");
     try {
-        return new plbm::Engine(*desc, device);
+        return new plbm::Engine(*desc, device, rank, world);
     } catch (const plbm::CudaError& e) {
         fill_err(err, 3, e.what());
     } catch (const std::exception& e) {
@@ -1149,60 +1309,157 @@ void* plbm_gpu_create(const plbm_scenario_desc* desc, int device, plbm_error* er
     return nullptr;
 }
 
+void* plbm_gpu_create(const plbm_scenario_desc* desc, int device, plbm_error* err) {
+    return plbm_gpu_create_dist(desc, device, 0, 1, err);
+}
+
+int plbm_gpu_prepare(void* h) {
+    try {
+        return EG(h)->prepare();
+    } catch (const std::exception&) {
+        return -6;
+    }
+}
+
 int plbm_gpu_step(void* h, int n, plbm_error* err) {
     fill_err(err, 0, "");
     try {
-        return static_cast<plbm::Engine*>(h)->step(n, err);
+        return EG(h)->step(n, err);
     } catch (const std::exception& e) {
         fill_err(err, 3, e.what());
         return 3;
     }
 }
 
+int plbm_gpu_step_begin(void* h, plbm_error* err) {
+    fill_err(err, 0, "");
+    try {
+        return EG(h)->step_begin(err);
+    } catch (const std::exception& e) {
+        fill_err(err, 3, e.what());
+        return 3;
+    }
+}
+
+int plbm_gpu_step_main(void* h, plbm_error* err) {
+    fill_err(err, 0, "");
+    try {
+        return EG(h)->step_main(err);
+    } catch (const std::exception& e) {
+        fill_err(err, 3, e.what());
+        return 3;
+    }
+}
+
+int plbm_gpu_step_face(void* h) {
+    try {
+        return EG(h)->step_face();
+    } catch (const std::exception&) {
+        return 3;
+    }
+}
+
+int plbm_gpu_step_end(void* h, const uint8_t* merged, plbm_error* err) {
+    fill_err(err, 0, "");
+    try {
+        return EG(h)->step_end(merged, err);
+    } catch (const std::exception& e) {
+        fill_err(err, 3, e.what());
+        return 3;
+    }
+}
+
+int plbm_gpu_trigger_bytes(void* h) { return EG(h)->trig_bytes(); }
+void* plbm_gpu_triggers_device(void* h) { return EG(h)->trig_device(); }
+
+int plbm_gpu_local_triggers(void* h, uint8_t* out, int n) {
+    try {
+        return EG(h)->local_triggers(out, n);
+    } catch (const std::exception&) {
+        return -6;
+    }
+}
+
+int plbm_gpu_ipc_handles(void* h, void* out) {
+    try {
+        return EG(h)->ipc_handles(out);
+    } catch (const std::exception&) {
+        return -6;
+    }
+}
+
+int plbm_gpu_open_peer(void* h, int rank, const void* handles) {
+    try {
+        return EG(h)->open_peer(rank, handles);
+    } catch (const std::exception&) {
+        return -6;
+    }
+}
+
+int plbm_gpu_set_peer_pools(void* h, int rank, void* pool_f, void* pool_pf) {
+    try {
+        return EG(h)->set_peer(rank, pool_f, pool_pf);
+    } catch (const std::exception&) {
+        return -6;
+    }
+}
+
+void plbm_gpu_pool_pointers(void* h, void** pool_f, void** pool_pf) { EG(h)->pool_pointers(pool_f, pool_pf); }
+
+int plbm_gpu_tile_rank(void* h, const int32_t* coords) { return EG(h)->rank_of(coords); }
+
+int plbm_gpu_sync(void* h) {
+    try {
+        return EG(h)->sync();
+    } catch (const std::exception&) {
+        return -6;
+    }
+}
+
 void plbm_gpu_counters(void* h, plbm_counters* out) {
     try {
-        static_cast<plbm::Engine*>(h)->counters(out);
+        EG(h)->counters(out);
     } catch (const std::exception&) {
         std::memset(out, 0, sizeof *out);
     }
 }
 
 int plbm_gpu_tiles(void* h, int32_t* coords, int32_t* owners, int64_t* births, int max) {
-    return static_cast<plbm::Engine*>(h)->tiles(coords, owners, births, max);
+    return EG(h)->tiles(coords, owners, births, max);
 }
 
 int plbm_gpu_read_tile(void* h, const int32_t* coords, int comp, int field, double* out) {
     try {
-        return static_cast<plbm::Engine*>(h)->read_tile(coords, comp, field, out);
+        return EG(h)->read_tile(coords, comp, field, out);
     } catch (const std::exception&) {
         return -6;
     }
 }
 
 int plbm_gpu_creation_log(void* h, plbm_creation_event* out, int max) {
-    return static_cast<plbm::Engine*>(h)->creation_log(out, max);
+    return EG(h)->creation_log(out, max);
 }
 
 int plbm_gpu_poke_f(void* h, const int32_t* coords, int comp, int i, const int32_t* local, double v) {
-    return static_cast<plbm::Engine*>(h)->poke_f(coords, comp, i, local, v);
+    return EG(h)->poke_f(coords, comp, i, local, v);
 }
 
 int plbm_gpu_set_capture(void* h, int on) {
     try {
-        return static_cast<plbm::Engine*>(h)->set_capture(on != 0);
+        return EG(h)->set_capture(on != 0);
     } catch (const std::exception&) {
         return -6;
     }
 }
 
 int plbm_gpu_set_profiling(void* h, int on) {
-    static_cast<plbm::Engine*>(h)->set_profiling(on != 0);
+    EG(h)->set_profiling(on != 0);
     return 0;
 }
 
 void plbm_gpu_kernel_stats(void* h, plbm_kernel_stats* out) {
     try {
-        *out = static_cast<plbm::Engine*>(h)->stats();
+        *out = EG(h)->stats();
     } catch (const std::exception&) {
         std::memset(out, 0, sizeof *out);
     }
@@ -1210,18 +1467,18 @@ void plbm_gpu_kernel_stats(void* h, plbm_kernel_stats* out) {
 
 void plbm_gpu_reset_kernel_stats(void* h) {
     try {
-        static_cast<plbm::Engine*>(h)->reset_stats();
+        EG(h)->reset_stats();
     } catch (const std::exception&) {
     }
 }
 
-void* plbm_gpu_stream(void* h) { return static_cast<plbm::Engine*>(h)->stream(); }
+void* plbm_gpu_stream(void* h) { return EG(h)->stream(); }
 
 int plbm_gpu_set_kernel_variant(void* h, int variant) {
-    static_cast<plbm::Engine*>(h)->set_variant(variant);
+    EG(h)->set_variant(variant);
     return 0;
 }
 
-void plbm_gpu_destroy(void* h) { delete static_cast<plbm::Engine*>(h); }
+void plbm_gpu_destroy(void* h) { delete EG(h); }
 
 }  // extern "C"

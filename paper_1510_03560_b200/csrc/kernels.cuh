@@ -1,28 +1,33 @@
 // kernels.cuh — the B200 step-loop kernels (sm_100a, FP64, no tensor cores).
 //
-// Storage (HBM block pool, SoA):
-//   f[b]      : [slot][comp][19][E^3] doubles, b in {0,1} (A-B buffers).  The
-//               stored state is the POST-COLLISION population of the last step
-//               (f_post^(k)); the reference's post-stream f_read is produced on
-//               the fly by pulling (stream fused into the next step's load).
-//   slot AMB  : one extra pool slot holding feq_amb in both buffers; every route
-//               to an absent tile points at it, so frontier pulls need no branch.
-//   route[r]  : [slot][18] source slot for the 6 face and 12 edge ghost classes,
-//               resolved with the reference's ghost-routing rule (hop along the
-//               higher axis first; proj/src/engine.cpp:266-296).  Two tables:
-//               ROUTE_PULL = map of the previous step (P4 of the last step ran on
-//               it), ROUTE_PSI = map of this step (P2 runs on it).
-//   psi_face  : [slot][comp][6][E^2] face-layer pseudo-potential of the step
-//               about to run (written by k_face, read by neighbours in k_main).
-//   u_face    : [slot][comp][6][3][E^2] velocity used by the last collision on
-//               frontier faces (u_prev of the activation criterion).
+// Storage (HBM block pool, SoA), addressed through per-slot pointer tables so
+// that a slot may live on this GPU or on a peer GPU (read over NVLink):
+//   slot_f[b][s]  : -> [comp][19][E^3] doubles of slot s in buffer b (A-B).
+//                   The stored state is the POST-COLLISION population of the
+//                   last step (f_post^(k)); the reference's post-stream f_read
+//                   is produced on the fly by pulling (stream fused into the
+//                   next step's load).
+//   slot_pf[p][s] : -> [comp][6][E^2] face-layer psi of slot s for the step of
+//                   parity p (written by k_face at the end of the previous step,
+//                   read by neighbours in k_main; double-buffered so a peer can
+//                   still read step k's faces while this GPU writes step k+1's).
+//   AMB slot      : one extra slot (global id = capacity) holding feq_amb in both
+//                   buffers and psi_amb on its faces; every route to an absent
+//                   tile points at it, so frontier pulls need no branch.
+//   route[r]      : [slot][18] source slot for the 6 face and 12 edge ghost
+//                   classes, resolved with the reference's ghost-routing rule
+//                   (hop along the higher axis first; proj/src/engine.cpp:266-296).
+//                   ROUTE_PULL = map of the previous step (P4 of the last step ran
+//                   on it), ROUTE_PSI = map of this step (P2 runs on it).
+//   u_face        : [local][comp][6][3][E^2] velocity used by the last collision
+//                   on frontier faces (u_prev of the activation criterion).
 //
 // Per step k:
-//   k_main  : pull f_in^(k) from f_post^(k-1) (or generate it for seeded /
+//   k_main* : pull f_in^(k) from f_post^(k-1) (or generate it for seeded /
 //             newborn tiles), rho/psi planes in shared memory marching in z,
 //             Shan-Chen forces, BGK + velocity-shift forcing, store f_post^(k).
 //             = reference P1 + P2 + P3 + P4 + (P5 moments of the previous step).
-//   k_face  : moments of f_in^(k+1) on the 6 face layers: psi_face for step
+//   k_face  : moments of f_in^(k+1) on the 6 face layers: psi faces for step
 //             k+1 and the activation criterion of step k (P5 + evaluate_criterion).
 #pragma once
 
@@ -58,18 +63,19 @@ struct Params {
 };
 
 struct Dev {
-    double* f[2];
-    const int* route[2];       // [slot][18]
-    const uint32_t* solid;     // [slot][solid_words]
-    const uint8_t* has_solid;  // [slot]
-    const uint8_t* mode;       // [slot]
-    const int* coords;         // [slot][3]
-    double* psi_face;          // [slot][C][6][E2]
-    double* u_face;            // [slot][C][6][3][E2]
-    uint8_t* trig;             // [slot]
-    double* capture;           // [slot][C][4][E3] or nullptr
-    unsigned long long* cnt;   // CNT_N
-    unsigned long long* err;   // packed (tile_lin << 8 | code), atomicMin
+    double* const* slot_f[2];   // [slot] -> f block in buffer b (local or peer)
+    double* const* slot_pf[2];  // [slot] -> psi faces for step parity p
+    const int* route[2];        // [slot][18]
+    const int* lidx;            // [slot] -> local index (u_face / capture), -1 remote
+    const uint32_t* solid;      // [slot][solid_words]
+    const uint8_t* has_solid;   // [slot]
+    const uint8_t* mode;        // [slot]
+    const int* coords;          // [slot][3]
+    double* u_face;             // [local][C][6][3][E2]
+    uint8_t* trig;              // [slot]
+    double* capture;            // [local][C][4][E3] or nullptr
+    unsigned long long* cnt;    // CNT_N
+    unsigned long long* err;    // packed (iter, tile_lin, code), atomicMin
     int solid_words;
 };
 
@@ -107,11 +113,6 @@ __device__ __forceinline__ void atomic_err(unsigned long long* err, long iter, i
                                            int code) {
     atomicMin(err, ((unsigned long long)iter << 36) | ((unsigned long long)(unsigned)tile_lin << 4) |
                        (unsigned)code);
-}
-
-__device__ __forceinline__ void warp_count(unsigned long long* c, bool pred) {
-    const unsigned m = __ballot_sync(0xffffffffu, pred);
-    if ((threadIdx.x & 31) == 0 && m) atomicAdd(c, (unsigned long long)__popc(m));
 }
 
 // Extended-grid solid bit of the tile (local coords in [-1, E]).
@@ -164,43 +165,52 @@ __device__ __forceinline__ void gen_fin(int mode, int c, const int* tc, int x, i
     }
 }
 
-// Per-CTA routing table: slot for each out pattern (ox+1)+3(oy+1)+9(oz+1).
+// Per-CTA routing table for each out pattern (ox+1)+3(oy+1)+9(oz+1): the
+// source slot and the base pointer of that slot's block (buffer or psi faces).
+// `nb` flags tiles born at the end of the previous step (GEN_AMBIENT): their
+// psi faces are those of a fresh ambient cell, taken from the constants, so a
+// peer rank never has to wait for a newborn's face buffer to be written.
 struct RouteTab {
     int s[27];
+    const double* p[27];
+    uint8_t nb[27];
 };
-__device__ __forceinline__ void load_routes(RouteTab& rt, const int* routes, int self, int amb) {
+__device__ __forceinline__ void load_routes(RouteTab& rt, const int* routes, int self, int amb,
+                                            double* const* bases, const uint8_t* mode = nullptr) {
     for (int k = threadIdx.x; k < 27; k += blockDim.x) {
         const int ox = k % 3 - 1, oy = (k / 3) % 3 - 1, oz = k / 9 - 1;
         const int cls = ghost_class(ox, oy, oz);
-        rt.s[k] = (ox == 0 && oy == 0 && oz == 0) ? self : (cls < 0 ? amb : routes[cls]);
+        const int s = (ox == 0 && oy == 0 && oz == 0) ? self : (cls < 0 ? amb : routes[cls]);
+        rt.s[k] = s;
+        rt.p[k] = bases[s];
+        rt.nb[k] = mode ? uint8_t(mode[s] == MODE_GEN_AMBIENT) : uint8_t(0);
     }
 }
 
 // Pull of one cell's 19 populations of component c from f_post (the
 // reference's P4a ghost fill + stream_pull, proj/src/kernels.cpp:5-30):
 //   f_in[i](x) = solid(x - e_i) ? f_post(x)[opp i] : f_post(route(x - e_i))[i]
-template <int E>
-__device__ __forceinline__ void pull_cell(const double* __restrict__ fp, const RouteTab& rt,
-                                          int self, int c, bool hs, const uint32_t* sb, int x,
-                                          int y, int z, double* f) {
+// `op(i, ptr)` receives each population's source address.
+template <int E, class Op>
+__device__ __forceinline__ void pull_addr(const RouteTab& rt, int c, bool hs, const uint32_t* sb,
+                                          int x, int y, int z, Op&& op) {
     constexpr int E3 = E * E * E;
     const size_t cs = size_t(Q) * E3;
-    const int C = P.C;
 #pragma unroll
     for (int i = 0; i < Q; ++i) {
         const int sx = x - ex_(i), sy = y - ey_(i), sz = z - ez_(i);
         const int ox = sx < 0 ? -1 : (sx >= E ? 1 : 0);
         const int oy = sy < 0 ? -1 : (sy >= E ? 1 : 0);
         const int oz = sz < 0 ? -1 : (sz >= E ? 1 : 0);
-        int slot = rt.s[(ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)];
+        const double* base = rt.p[(ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)];
         int cell = ((sz & (E - 1)) * E + (sy & (E - 1))) * E + (sx & (E - 1));
         int dir = i;
         if (hs && solid_at<E>(sb, sx, sy, sz)) {
-            slot = self;
+            base = rt.p[13];
             cell = (z * E + y) * E + x;
             dir = opp_(i);
         }
-        f[i] = __ldg(fp + (size_t(slot) * C + c) * cs + size_t(dir) * E3 + cell);
+        op(i, base + c * cs + size_t(dir) * E3 + cell);
     }
 }
 
@@ -209,65 +219,18 @@ __device__ __forceinline__ void pull_cell(const double* __restrict__ fp, const R
 // Only the x shift can leave the tile; that lane-dependent choice collapses to
 // two base pointers, and every population is a load at a compile-time
 // immediate offset from one of three bases.
-template <int E>
-__device__ __forceinline__ void pull_cell_fast(const double* __restrict__ fp, const RouteTab& rt,
-                                               int self, int c, int x, int y, int z, double* f) {
+template <int E, class Op>
+__device__ __forceinline__ void pull_addr_fast(const RouteTab& rt, int c, int x, int y, int z,
+                                               Op&& op) {
     constexpr int E2 = E * E;
     constexpr int E3 = E * E * E;
     const size_t cs = size_t(Q) * E3;
-    const int C = P.C;
     const int row = (z * E + y) * E;
-    const double* own = fp + (size_t(self) * C + c) * cs + row + x;
+    const double* own = rt.p[13] + c * cs + row + x;
     // ex = +1 pulls from x-1: the -x neighbour's column E-1 on lane x == 0
-    const double* bp = x == 0 ? fp + (size_t(rt.s[12]) * C + c) * cs + row + (E - 1) : own - 1;
+    const double* bp = x == 0 ? rt.p[12] + c * cs + row + (E - 1) : own - 1;
     // ex = -1 pulls from x+1: the +x neighbour's column 0 on lane x == E-1
-    const double* bm = x == E - 1 ? fp + (size_t(rt.s[14]) * C + c) * cs + row : own + 1;
-#pragma unroll
-    for (int i = 0; i < Q; ++i) {
-        const int off = i * E3 - ey_(i) * E - ez_(i) * E2;
-        const double* b = ex_(i) > 0 ? bp : (ex_(i) < 0 ? bm : own);
-        f[i] = __ldg(b + off);
-    }
-}
-
-// Address-only variants of the two pulls (same routing/bounce-back), handing
-// each population's source pointer to `op(i, ptr)` — used to issue cp.async.
-template <int E, class Op>
-__device__ __forceinline__ void pull_addr(const double* __restrict__ fp, const RouteTab& rt, int self,
-                                          int c, bool hs, const uint32_t* sb, int x, int y, int z,
-                                          Op&& op) {
-    constexpr int E3 = E * E * E;
-    const size_t cs = size_t(Q) * E3;
-    const int C = P.C;
-#pragma unroll
-    for (int i = 0; i < Q; ++i) {
-        const int sx = x - ex_(i), sy = y - ey_(i), sz = z - ez_(i);
-        const int ox = sx < 0 ? -1 : (sx >= E ? 1 : 0);
-        const int oy = sy < 0 ? -1 : (sy >= E ? 1 : 0);
-        const int oz = sz < 0 ? -1 : (sz >= E ? 1 : 0);
-        int slot = rt.s[(ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)];
-        int cell = ((sz & (E - 1)) * E + (sy & (E - 1))) * E + (sx & (E - 1));
-        int dir = i;
-        if (hs && solid_at<E>(sb, sx, sy, sz)) {
-            slot = self;
-            cell = (z * E + y) * E + x;
-            dir = opp_(i);
-        }
-        op(i, fp + (size_t(slot) * C + c) * cs + size_t(dir) * E3 + cell);
-    }
-}
-
-template <int E, class Op>
-__device__ __forceinline__ void pull_addr_fast(const double* __restrict__ fp, const RouteTab& rt,
-                                               int self, int c, int x, int y, int z, Op&& op) {
-    constexpr int E2 = E * E;
-    constexpr int E3 = E * E * E;
-    const size_t cs = size_t(Q) * E3;
-    const int C = P.C;
-    const int row = (z * E + y) * E;
-    const double* own = fp + (size_t(self) * C + c) * cs + row + x;
-    const double* bp = x == 0 ? fp + (size_t(rt.s[12]) * C + c) * cs + row + (E - 1) : own - 1;
-    const double* bm = x == E - 1 ? fp + (size_t(rt.s[14]) * C + c) * cs + row : own + 1;
+    const double* bm = x == E - 1 ? rt.p[14] + c * cs + row : own + 1;
 #pragma unroll
     for (int i = 0; i < Q; ++i) {
         const int off = i * E3 - ey_(i) * E - ez_(i) * E2;
@@ -276,29 +239,24 @@ __device__ __forceinline__ void pull_addr_fast(const double* __restrict__ fp, co
     }
 }
 
-__device__ __forceinline__ void cp_async8(double* dst_smem, const double* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
-                     static_cast<uint32_t>(__cvta_generic_to_shared(dst_smem))),
-                 "l"(src)
-                 : "memory");
+template <int E>
+__device__ __forceinline__ void pull_cell(const RouteTab& rt, int c, bool hs, const uint32_t* sb,
+                                          int x, int y, int z, double* f) {
+    pull_addr<E>(rt, c, hs, sb, x, y, z, [&](int i, const double* p) { f[i] = __ldg(p); });
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+template <int E>
+__device__ __forceinline__ void pull_cell_fast(const RouteTab& rt, int c, int x, int y, int z,
+                                               double* f) {
+    pull_addr_fast<E>(rt, c, x, y, z, [&](int i, const double* p) { f[i] = __ldg(p); });
 }
 
 // f_in for any mode (u is only meaningful for GEN modes).
 template <int E>
-__device__ __forceinline__ void fin_cell(const Dev& d, const double* fp, const RouteTab& rt,
-                                         int self, int mode, const int* tc, int c, bool hs,
-                                         const uint32_t* sb, int x, int y, int z, double* f,
-                                         double& u0, double& u1, double& u2) {
-    if (mode == MODE_PULL) {
-        pull_cell<E>(fp, rt, self, c, hs, sb, x, y, z, f);
-    } else {
-        gen_fin<E>(mode, c, tc, x, y, z, f, u0, u1, u2);
-    }
+__device__ __forceinline__ void fin_cell(const RouteTab& rt, int mode, const int* tc, int c,
+                                         bool hs, const uint32_t* sb, int x, int y, int z,
+                                         double* f, double& u0, double& u1, double& u2) {
+    if (mode == MODE_PULL) pull_cell<E>(rt, c, hs, sb, x, y, z, f);
+    else gen_fin<E>(mode, c, tc, x, y, z, f, u0, u1, u2);
 }
 
 // Face-layer index helpers: face f = 2*axis + (dir > 0); the in-face index
@@ -311,14 +269,17 @@ __device__ __forceinline__ int face_index(int face, int x, int y, int z) {
 
 // psi at an out-of-tile cell (local coords with 1 or 2 axes outside) from the
 // routed tile's face buffer (P2 ghost fill, proj/src/engine.cpp:317-352).
+// rt.p holds the psi-face bases of the ROUTE_PSI table.
 template <int E>
-__device__ __forceinline__ double psi_ghost(const Dev& d, const RouteTab& rt, int c, bool hs,
-                                            const uint32_t* sb, int x, int y, int z) {
+__device__ __forceinline__ double psi_ghost(const RouteTab& rt, int c, bool hs, const uint32_t* sb,
+                                            int x, int y, int z) {
     if (hs && solid_at<E>(sb, x, y, z)) return 0.0;
     const int ox = x < 0 ? -1 : (x >= E ? 1 : 0);
     const int oy = y < 0 ? -1 : (y >= E ? 1 : 0);
     const int oz = z < 0 ? -1 : (z >= E ? 1 : 0);
-    const int slot = rt.s[(ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)];
+    const int pat = (ox + 1) + 3 * (oy + 1) + 9 * (oz + 1);
+    if (rt.nb[pat]) return P.comp[c].psi_nb;
+    const double* base = rt.p[pat];
     // the cell lies on the routed tile's face opposite our first out axis
     int face;
     if (ox) face = ox > 0 ? 0 : 1;
@@ -326,13 +287,15 @@ __device__ __forceinline__ double psi_ghost(const Dev& d, const RouteTab& rt, in
     else face = oz > 0 ? 4 : 5;
     const int lx = x & (E - 1), ly = y & (E - 1), lz = z & (E - 1);
     constexpr int E2 = E * E;
-    return d.psi_face[((size_t(slot) * P.C + c) * 6 + face) * E2 + face_index<E>(face, lx, ly, lz)];
+    return base[(size_t(c) * 6 + face) * E2 + face_index<E>(face, lx, ly, lz)];
 }
 
 // ---------------------------------------------------------------------------
-// k_main: one CTA = one tile x one z-chunk of BZ planes.
-// NOPSI: every component is psi-free and uncoupled (e.g. single-component
-// ideal gas) so no pseudo-potential stencil is needed at all.
+// k_main: the plain fused kernel (variant 1).  One CTA = one tile x one z-chunk
+// of BZ planes; psi planes (with halo planes recomputed) in a shared ring, and
+// every population pulled twice (psi pass + collide).  Used for E = 8 and for
+// psi-free scenarios (NOPSI: no pseudo-potential stencil at all — a single
+// pull-collide pass per cell).
 template <int E, int C, int BZ, int NT, bool NOPSI>
 __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ active, int src_buf,
                                              int write_uface, long iter) {
@@ -353,10 +316,11 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
     const uint8_t mode = d.mode[slot];
     const bool hs = d.has_solid[slot] != 0;
     const int amb = P.amb_slot;
-    const double* __restrict__ fp = d.f[src_buf];
-    double* __restrict__ fo = d.f[src_buf ^ 1];
-    load_routes(rt_pull, d.route[ROUTE_PULL] + size_t(slot) * 18, slot, amb);
-    load_routes(rt_psi, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, amb);
+    const int par = int(iter & 1);
+    double* __restrict__ fo = d.slot_f[src_buf ^ 1][slot];
+    const int li = d.lidx[slot];
+    load_routes(rt_pull, d.route[ROUTE_PULL] + size_t(slot) * 18, slot, amb, d.slot_f[src_buf]);
+    load_routes(rt_psi, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, amb, d.slot_pf[par], d.mode);
     if (threadIdx.x < 3) s_tc[threadIdx.x] = d.coords[slot * 3 + threadIdx.x];
     if (hs)
         for (int k = threadIdx.x; k < d.solid_words; k += NT)
@@ -379,11 +343,10 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
             for (int c = 0; c < C; ++c) {
                 double v = 0.0;
                 if (!inside) {
-                    v = psi_ghost<E>(d, rt_psi, c, hs, s_solid, x, y, pz);
+                    v = psi_ghost<E>(rt_psi, c, hs, s_solid, x, y, pz);
                 } else if (!(hs && solid_at<E>(s_solid, x, y, pz))) {
                     double f[Q], u0, u1, u2;
-                    fin_cell<E>(d, fp, rt_pull, slot, mode, s_tc, c, hs, s_solid, x, y, pz, f,
-                                u0, u1, u2);
+                    fin_cell<E>(rt_pull, mode, s_tc, c, hs, s_solid, x, y, pz, f, u0, u1, u2);
                     double rho = 0.0;
 #pragma unroll
                     for (int i = 0; i < Q; ++i) {
@@ -418,7 +381,7 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
 #pragma unroll
             for (int c = 0; c < C; ++c)
                 psi[(r * C + c) * GG + (x + 1) + G * (y + 1)] =
-                    corner3 ? 0.0 : psi_ghost<E>(d, rt_psi, c, hs, s_solid, x, y, pz);
+                    corner3 ? 0.0 : psi_ghost<E>(rt_psi, c, hs, s_solid, x, y, pz);
         }
         if (owned) {
             const unsigned m1 = __reduce_add_sync(0xffffffffu, (unsigned)negs);
@@ -447,8 +410,7 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
             for (int c = 0; c < C; ++c) {
                 double f[Q];
                 double u0 = 0.0, u1 = 0.0, u2 = 0.0, rho;
-                fin_cell<E>(d, fp, rt_pull, slot, mode, s_tc, c, hs, s_solid, x, y, z, f, u0, u1,
-                            u2);
+                fin_cell<E>(rt_pull, mode, s_tc, c, hs, s_solid, x, y, z, f, u0, u1, u2);
                 if (mode == MODE_PULL) {
                     moments(f, rho, u0, u1, u2);
                 } else {
@@ -475,23 +437,19 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
                     const double* p0 = psi + (rc * C + c) * GG + pc;
                     const double* pp = psi + (rp * C + c) * GG + pc;
                     double s10 = 0.0, s11 = 0.0, s12 = 0.0, s20 = 0.0, s21 = 0.0, s22 = 0.0;
-                    auto nb = [&](int i) -> double {
-                        const int dx = ex_(i), dy = ey_(i), dz = ez_(i);
-                        const double* pl = dz < 0 ? pm : (dz > 0 ? pp : p0);
-                        return pl[dx + G * dy];
-                    };
 #pragma unroll
                     for (int i = 1; i < Q; ++i) {
-                        const double pn = nb(i);
-                        const double w = w_(i);
-                        const double a1 = w * pn;
+                        const int dx = ex_(i), dy = ey_(i), dz = ez_(i);
+                        const double* pl = dz < 0 ? pm : (dz > 0 ? pp : p0);
+                        const double pn = pl[dx + G * dy];
+                        const double a1 = w_(i) * pn;
                         const double a2 = a1 * pn;
-                        if (ex_(i) > 0) { s10 += a1; s20 += a2; }
-                        if (ex_(i) < 0) { s10 -= a1; s20 -= a2; }
-                        if (ey_(i) > 0) { s11 += a1; s21 += a2; }
-                        if (ey_(i) < 0) { s11 -= a1; s21 -= a2; }
-                        if (ez_(i) > 0) { s12 += a1; s22 += a2; }
-                        if (ez_(i) < 0) { s12 -= a1; s22 -= a2; }
+                        if (dx > 0) { s10 += a1; s20 += a2; }
+                        if (dx < 0) { s10 -= a1; s20 -= a2; }
+                        if (dy > 0) { s11 += a1; s21 += a2; }
+                        if (dy < 0) { s11 -= a1; s21 -= a2; }
+                        if (dz > 0) { s12 += a1; s22 += a2; }
+                        if (dz < 0) { s12 -= a1; s22 -= a2; }
                     }
                     const double c1 = kc.c1f * p0[0];
                     const double c2 = kc.c2;
@@ -538,7 +496,7 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
                         const int axis = face >> 1;
                         const int coord = axis == 0 ? x : (axis == 1 ? y : z);
                         if (coord == ((face & 1) ? E - 1 : 0) && rt_psi.s[face_pattern(face)] == amb) {
-                            double* uf = d.u_face + ((size_t(slot) * C + c) * 6 + face) * 3 * E2;
+                            double* uf = d.u_face + ((size_t(li) * C + c) * 6 + face) * 3 * E2;
                             const int fi = face_index<E>(face, x, y, z);
                             uf[fi] = u0;
                             uf[E2 + fi] = u1;
@@ -547,7 +505,7 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
                     }
                 }
                 if (d.capture) {
-                    double* cp = d.capture + (size_t(slot) * C + c) * 4 * E3;
+                    double* cp = d.capture + (size_t(li) * C + c) * 4 * E3;
                     // psi-free: radicand 2(+0)/(cs2 g) is a signed zero, sqrt keeps it
                     cp[cell] = NOPSI ? (kc.cs2_g < 0.0 ? -0.0 : 0.0) : psi[(rc * C + c) * GG + pc];
                     cp[E3 + cell] = u0;
@@ -556,7 +514,7 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
                 }
                 // ---- collision (engine.cpp:450-475)
                 const double om = kc.omega;
-                double* out = fo + (size_t(slot) * C + c) * size_t(Q) * E3 + cell;
+                double* out = fo + c * size_t(Q) * E3 + cell;
                 const double uu = u0 * u0 + u1 * u1 + u2 * u2;
                 const double t3 = (0.5 * uu) * 3.0;
                 const double wr0 = PLBM_W0 * rho, wr1 = PLBM_W1 * rho, wr2 = PLBM_W2 * rho;
@@ -625,8 +583,9 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
 
 // ---------------------------------------------------------------------------
 // k_face: moments of f_in^(k+1) on the six face layers of every active tile.
-// Writes psi_face for the next step and evaluates the activation criterion
-// (proj/src/tilemap.cpp:182-218) plus the P5 NaN check (engine.cpp:509-512).
+// Writes the psi faces for the next step (parity of iter + 1) and evaluates
+// the activation criterion (proj/src/tilemap.cpp:182-218) plus the P5 NaN
+// check (engine.cpp:509-512).  One cell per thread.
 template <int E, int C, int NT>
 __global__ void __launch_bounds__(NT) k_face(Dev d, const int* __restrict__ active, int src_buf,
                                              int flags, long iter) {
@@ -634,19 +593,20 @@ __global__ void __launch_bounds__(NT) k_face(Dev d, const int* __restrict__ acti
     const bool nan_check = flags & 2;  // P5 NaN check of the moments
     constexpr int E2 = E * E;
     constexpr int G = E + 2;
+    constexpr int NCH = (E2 + NT - 1) / NT;  // blocks per face
     __shared__ RouteTab rt;
     __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
     __shared__ int s_tc[3];
     __shared__ int s_fired;
-    constexpr int NCH = (E2 + NT - 1) / NT;  // blocks per face (one cell per thread)
     const int slot = active[blockIdx.x / (6 * NCH)];
     const int face = (blockIdx.x / NCH) % 6;
     const int chunk = blockIdx.x % NCH;
     const uint8_t mode = d.mode[slot];
     const bool hs = d.has_solid[slot] != 0;
     const int amb = P.amb_slot;
+    const int li = d.lidx[slot];
     // after k_main every tile pulls with the map it just stepped on (ROUTE_PSI)
-    load_routes(rt, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, amb);
+    load_routes(rt, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, amb, d.slot_f[src_buf]);
     if (threadIdx.x < 3) s_tc[threadIdx.x] = d.coords[slot * 3 + threadIdx.x];
     if (threadIdx.x == 0) s_fired = 0;
     if (hs)
@@ -655,7 +615,7 @@ __global__ void __launch_bounds__(NT) k_face(Dev d, const int* __restrict__ acti
     __syncthreads();
     const int tile_lin = (s_tc[0] * P.grid[1] + s_tc[1]) * P.grid[2] + s_tc[2];
     const bool frontier = criterion && (d.route[ROUTE_PSI][size_t(slot) * 18 + face] == amb);
-    const double* __restrict__ fp = d.f[src_buf];
+    double* pf = d.slot_pf[int((iter + 1) & 1)][slot];
     const int axis = face >> 1;
     const int fixed = (face & 1) ? E - 1 : 0;
     bool fired = false;
@@ -670,13 +630,13 @@ __global__ void __launch_bounds__(NT) k_face(Dev d, const int* __restrict__ acti
             double v = 0.0;
             if (!sol) {
                 double f[Q], u0 = 0.0, u1 = 0.0, u2 = 0.0, rho;
-                fin_cell<E>(d, fp, rt, slot, mode, s_tc, c, hs, s_solid, x, y, z, f, u0, u1, u2);
+                fin_cell<E>(rt, mode, s_tc, c, hs, s_solid, x, y, z, f, u0, u1, u2);
                 if (mode == MODE_PULL) moments(f, rho, u0, u1, u2);
                 else rho = sum19(f);
                 if (nan_check && (!isfinite(rho) || !isfinite(u0) || !isfinite(u1) || !isfinite(u2)))
                     atomic_err(d.err, iter, tile_lin, ERR_P5_NAN);
                 if (frontier && !fired) {
-                    const double* uf = d.u_face + ((size_t(slot) * C + c) * 6 + face) * 3 * E2;
+                    const double* uf = d.u_face + ((size_t(li) * C + c) * 6 + face) * 3 * E2;
                     const double dx = u0 - uf[idx], dy = u1 - uf[E2 + idx], dz = u2 - uf[2 * E2 + idx];
                     if (dx * dx + dy * dy + dz * dz > P.s2) fired = true;
                 }
@@ -687,7 +647,7 @@ __global__ void __launch_bounds__(NT) k_face(Dev d, const int* __restrict__ acti
                     v = pseudo_potential(rho, press, kc, cl);
                 }
             }
-            d.psi_face[((size_t(slot) * C + c) * 6 + face) * E2 + idx] = v;
+            pf[(size_t(c) * 6 + face) * E2 + idx] = v;
         }
     }
     if (__any_sync(0xffffffffu, fired) && (threadIdx.x & 31) == 0) s_fired = 1;
@@ -695,22 +655,10 @@ __global__ void __launch_bounds__(NT) k_face(Dev d, const int* __restrict__ acti
     if (threadIdx.x == 0 && s_fired) atomicOr((unsigned*)(d.trig) + slot / 4, 1u << (8 * (slot % 4) + face));
 }
 
-// Newborn / ambient face buffers: psi of the ambient-equilibrium cell.
-template <int E>
-__global__ void k_face_ambient(Dev d, const int* __restrict__ slots, int n) {
-    constexpr int E2 = E * E;
-    const int k = blockIdx.x;
-    if (k >= n) return;
-    const int slot = slots[k];
-    for (int idx = threadIdx.x; idx < 6 * E2; idx += blockDim.x)
-        for (int c = 0; c < P.C; ++c)
-            d.psi_face[(size_t(slot) * P.C + c) * 6 * E2 + idx] = P.comp[c].psi_nb;
-}
-
 // Reference-view read-back of one tile (f_read, rho, u) into out:
 // [19*E3 f][E3 rho][E3 ux][E3 uy][E3 uz]
 template <int E>
-__global__ void k_readback(Dev d, int slot, int c, int src_buf, int fresh_birth, double* out) {
+__global__ void k_readback(Dev d, int slot, int c, int src_buf, double* out) {
     constexpr int E3 = E * E * E;
     constexpr int G = E + 2;
     __shared__ RouteTab rt;
@@ -718,13 +666,12 @@ __global__ void k_readback(Dev d, int slot, int c, int src_buf, int fresh_birth,
     __shared__ int s_tc[3];
     const uint8_t mode = d.mode[slot];
     const bool hs = d.has_solid[slot] != 0;
-    load_routes(rt, d.route[ROUTE_PULL] + size_t(slot) * 18, slot, P.amb_slot);
+    load_routes(rt, d.route[ROUTE_PULL] + size_t(slot) * 18, slot, P.amb_slot, d.slot_f[src_buf]);
     if (threadIdx.x < 3) s_tc[threadIdx.x] = d.coords[slot * 3 + threadIdx.x];
     if (hs)
         for (int k = threadIdx.x; k < d.solid_words; k += blockDim.x)
             s_solid[k] = d.solid[size_t(slot) * d.solid_words + k];
     __syncthreads();
-    const double* fp = d.f[src_buf];
     for (int cell = blockIdx.x * blockDim.x + threadIdx.x; cell < E3; cell += gridDim.x * blockDim.x) {
         const int x = cell % E, y = (cell / E) % E, z = cell / (E * E);
         double f[Q], u0 = 0.0, u1 = 0.0, u2 = 0.0, rho = 0.0;
@@ -732,7 +679,7 @@ __global__ void k_readback(Dev d, int slot, int c, int src_buf, int fresh_birth,
         if (sol) {
             for (int i = 0; i < Q; ++i) f[i] = P.comp[c].feq_amb[i];
         } else if (mode == MODE_PULL) {
-            pull_cell<E>(fp, rt, slot, c, hs, s_solid, x, y, z, f);
+            pull_cell<E>(rt, c, hs, s_solid, x, y, z, f);
             moments(f, rho, u0, u1, u2);
         } else {
             gen_fin<E>(mode, c, s_tc, x, y, z, f, u0, u1, u2);
@@ -746,7 +693,6 @@ __global__ void k_readback(Dev d, int slot, int c, int src_buf, int fresh_birth,
         out[size_t(21) * E3 + cell] = u1;
         out[size_t(22) * E3 + cell] = u2;
     }
-    (void)fresh_birth;
 }
 
 }  // namespace plbm

@@ -1,35 +1,32 @@
-// kernels_tm.cuh — k_main_tm: the fused step kernel with a TMEM stash.
+// kernels_tm.cuh — k_main_tm: the default fused step kernel (sm_100a).
 //
-// Why: the Shan-Chen force needs psi of all 18 neighbours, and psi needs the
-// density of the POST-STREAM populations, so every cell's pulled f_in is used
-// twice — once for rho -> psi (one plane ahead), once for the collision.  The
-// plain kernel (k_main) pulls twice; the second pull misses L2 (reuse
-// distance ~90 MB chip-wide) and DRAM reads run at 2.4x the algorithmic
-// bytes.  Here the first pull is the only one: its 19*C doubles per cell go to
-// Tensor Memory (tcgen05.st, 32x32b, one TMEM lane per thread) and come back
-// for the collision two planes later (tcgen05.ld).  TMEM is 256 KB per SM that
-// this FP64 stencil otherwise never uses.
+// Why not a plain stencil: the Shan-Chen force needs psi of all 18
+// neighbours, and psi needs the density of the POST-STREAM populations, so
+// each cell's pulled f_in is used twice — once for rho -> psi (one plane
+// ahead), once for the collision.  Pulling twice misses L2 (reuse distance
+// ~90 MB chip-wide; ncu: DRAM reads 2.4x the algorithmic bytes), so the first
+// pull is the only one and its 19*C doubles stay on chip until the collide:
+//   * even planes in Tensor Memory (tcgen05.st / tcgen05.ld, 32x32b shape,
+//     one TMEM lane per thread) — 256 KB per SM this FP64 stencil otherwise
+//     never uses;
+//   * odd planes in shared memory;
+// which lets two CTAs (16 warps) share an SM at <= 128 registers per thread.
 //
 // Decomposition: one CTA = a 32 x 8 (x, y) column block of one 32^3 tile,
-// marching z over the whole tile; the four blocks of a tile form a thread-block
-// cluster and exchange their psi boundary rows through distributed shared
-// memory (no halo recompute).  Halo planes/rows outside the tile come from the
-// neighbours' face buffers (psi_face, k_face) through the ghost routing table.
+// marching z over the whole tile; the four blocks of a tile form a thread-
+// block cluster.  Block rows 0 and BY-1 push their psi values straight into
+// the neighbouring block's shared ring with st.async, completing transactions
+// on the receiver's mbarrier — no per-plane cluster barrier, no GPU-scope
+// fence.  Halo planes / rows outside the tile come from the neighbours' psi
+// faces (k_face) through the ghost routing table.
 //
-// Pipeline per plane z (all on-chip except the f loads / stores):
-//   issue the pull loads of plane z+2           (in flight during the collide)
-//   collide plane z  : f(z) <- TMEM slot z&1, psi planes z-1..z+1 from smem
-//   rho/psi of plane z+2 -> smem ring slot (z+2)&3; f(z+2) -> TMEM slot z&1
-//   cluster barrier; copy the neighbour blocks' boundary rows of psi(z+2)
+// Per plane z:  psi pass of plane z+1 (pull, rho, psi, stash, push rows)
+//               | CTA barrier | edge rows wait on the mbarrier | collide z.
 #pragma once
-
-#include <cooperative_groups.h>
 
 #include "kernels.cuh"
 
 namespace plbm {
-
-namespace cg = cooperative_groups;
 
 template <int E, int C>
 struct TmCfg {
@@ -37,18 +34,16 @@ struct TmCfg {
     static constexpr int BY = NT / E;            // rows per CTA
     static constexpr int NB = E / BY;            // CTAs per tile = cluster size
     static constexpr int CB = 40;                // TMEM columns per component (38 used)
-    static constexpr int SCOLS = CB * C;         // TMEM columns per stash slot
-    static constexpr int WCOLS = 2 * SCOLS;      // two slots per thread
-    static constexpr int NCOLS = (2 * WCOLS <= 256) ? 256 : 512;  // 2 warps per lane quarter
-    static constexpr int HALF = NCOLS / 2;
+    static constexpr int NCOLS = 256;            // per CTA; two CTAs per SM
+    static constexpr int HALF = NCOLS / 2;       // per warp (two warps per lane quarter)
     static constexpr int PW = E + 2;             // psi plane row pitch (x + ring)
     static constexpr int PH = BY + 2;
     static constexpr int PP = PW * PH;
     static constexpr int PSI_BYTES = 4 * C * PP * 8;
-    // >= 116 KB of dynamic shared memory pins one CTA per SM, so a CTA that
-    // waits in tcgen05.alloc can never block a co-resident cluster peer.
-    static constexpr int SMEM = PSI_BYTES > 118 * 1024 ? PSI_BYTES : 118 * 1024;
-    static_assert(WCOLS <= HALF, "TMEM stash does not fit");
+    static constexpr int STAGE_BYTES = Q * C * NT * 8;
+    static constexpr int SMEM = PSI_BYTES + STAGE_BYTES;
+    static_assert(CB * C <= HALF, "TMEM slot does not fit");
+    static_assert(2 * (SMEM + 6 * 1024) <= 228 * 1024, "two CTAs per SM must fit");
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -103,15 +98,14 @@ __device__ __forceinline__ void tm_load19(uint32_t taddr, double* f) {
 }
 
 // One component's collision at one cell (engine.cpp:420-476): gravity +
-// intra + inter force, then BGK with the velocity-shift forcing.  psi is a
-// [C] array of plane pointers at the cell centre for planes z-1, z, z+1.
+// intra + inter force, then BGK with the velocity-shift forcing.  pm0/p00/pp0
+// point at this cell's psi in planes z-1, z, z+1 for component 0; component k
+// is CP doubles further.
 template <int C, int PW, int CP>
 __device__ __forceinline__ void collide_comp(const double* f, double rho, double u0, double u1,
                                              double u2, int c, const double* pm0,
                                              const double* p00, const double* pp0,
                                              double* out, size_t dstride, int& zero_rho) {
-    // pm0/p00/pp0: psi at this cell in planes z-1, z, z+1 for component 0;
-    // component k is CP doubles further.
     const double* pm_c = pm0 + c * CP;
     const double* p0_c = p00 + c * CP;
     const double* pp_c = pp0 + c * CP;
@@ -227,562 +221,17 @@ __device__ __forceinline__ void gen_u(int mode, int c, const int* tc, int x, int
 }
 
 template <int E, int C>
-__global__ void __launch_bounds__(256, 1) k_main_tm(Dev d, const int* __restrict__ active,
+__global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict__ active,
                                                     int src_buf, int write_uface, long iter) {
     using T = TmCfg<E, C>;
     constexpr int NT = T::NT, BY = T::BY, NB = T::NB, PW = T::PW, PH = T::PH, PP = T::PP;
     constexpr int G = E + 2;
     constexpr int E2 = E * E;
     constexpr int E3 = E * E * E;
+    static_assert(NB == 1 || BY * E == NT, "one warp per block row");
     extern __shared__ __align__(16) double smem[];
-    double* psi = smem;  // [4 ring slots][C][PH][PW]
-    __shared__ RouteTab rt_pull, rt_psi;
-    __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
-    __shared__ int s_tc[3];
-    __shared__ uint32_t s_tmem;
-
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5;
-    const int tile_i = blockIdx.x / NB;
-    const int yb = blockIdx.x % NB;
-    const int y0 = yb * BY;
-    const int slot = active[tile_i];
-    const uint8_t mode = d.mode[slot];
-    const bool hs = d.has_solid[slot] != 0;
-    const int amb = P.amb_slot;
-    const double* __restrict__ fp = d.f[src_buf];
-    double* __restrict__ fo = d.f[src_buf ^ 1];
-
-    // ---- TMEM: one warp allocates, everyone reads the base after the fence
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                         smem_u32(&s_tmem)),
-                     "n"(T::NCOLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-    }
-    load_routes(rt_pull, d.route[ROUTE_PULL] + size_t(slot) * 18, slot, amb);
-    load_routes(rt_psi, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, amb);
-    if (tid < 3) s_tc[tid] = d.coords[slot * 3 + tid];
-    if (hs)
-        for (int k = tid; k < d.solid_words; k += NT) s_solid[k] = d.solid[size_t(slot) * d.solid_words + k];
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    const uint32_t tbase = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * T::HALF);
-    const int tile_lin = (s_tc[0] * P.grid[1] + s_tc[1]) * P.grid[2] + s_tc[2];
-
-    const int x = tid % E;
-    const int yl = tid / E;
-    const int y = y0 + yl;
-    const bool sol_xy_any = hs;  // per-plane solidity is looked up per z
-    auto pidx = [&](int ring, int c, int xx, int yy_local) {
-        return ((ring * C + c) * PH + (yy_local + 1)) * PW + (xx + 1);
-    };
-
-    // ---- psi of out-of-block positions -------------------------------------
-    // whole plane outside the tile in z (pz = -1 or E)
-    auto fill_zghost = [&](int pz) {
-        const int ring = pz & 3;
-        for (int k = tid; k < PP; k += NT) {
-            const int xx = k % PW - 1, yy = k / PW - 1 + y0;
-            const bool xo = xx < 0 || xx >= E, yo = yy < 0 || yy >= E;
-#pragma unroll
-            for (int c = 0; c < C; ++c)
-                psi[pidx(ring, c, xx, yy - y0)] =
-                    (xo && yo) ? 0.0 : psi_ghost<E>(d, rt_psi, c, hs, s_solid, xx, yy, pz);
-        }
-    };
-    // x ring (both sides, rows -1..BY) and y rows that lie outside the tile
-    auto fill_ring = [&](int pz) {
-        const int ring = pz & 3;
-        for (int k = tid; k < 2 * PH + 2 * E; k += NT) {
-            int xx, yyl;
-            if (k < 2 * PH) {
-                xx = (k & 1) ? E : -1;
-                yyl = (k >> 1) - 1;
-            } else {
-                const int q = k - 2 * PH;
-                xx = q % E;
-                yyl = (q / E) ? BY : -1;
-                const int yy = y0 + yyl;
-                if (yy >= 0 && yy < E) continue;  // in-tile row: cluster neighbour's
-            }
-#pragma unroll
-            for (int c = 0; c < C; ++c)
-                psi[pidx(ring, c, xx, yyl)] = psi_ghost<E>(d, rt_psi, c, hs, s_solid, xx, y0 + yyl, pz);
-        }
-    };
-    // in-tile boundary rows from the cluster neighbours (DSMEM)
-    auto copy_rows = [&](int pz) {
-        if constexpr (NB > 1) {
-            cg::cluster_group cl = cg::this_cluster();
-            const int ring = pz & 3;
-            for (int k = tid; k < 2 * E * C; k += NT) {
-                const int side = k / (E * C);  // 0: row -1 from yb-1, 1: row BY from yb+1
-                const int c = (k / E) % C;
-                const int xx = k % E;
-                const int nb = yb + (side ? 1 : -1);
-                if (nb < 0 || nb >= NB) continue;
-                const double* peer = cl.map_shared_rank(psi, nb);
-                const int src_row = side ? 0 : BY - 1;
-                psi[pidx(ring, c, xx, side ? BY : -1)] = peer[pidx(ring, c, xx, src_row)];
-            }
-        }
-    };
-    auto cluster_sync = [&]() {
-        if constexpr (NB > 1) {
-            asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-            asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-        } else {
-            __syncthreads();
-        }
-    };
-
-    // ---- f_in of this thread's cell in plane pz (pull or generated) ---------
-    double R[C][Q];
-    auto load_plane = [&](int pz) {
-        const bool sol = sol_xy_any && solid_at<E>(s_solid, x, y, pz);
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-            if (sol) {
-#pragma unroll
-                for (int i = 0; i < Q; ++i) R[c][i] = 0.0;
-            } else if (mode == MODE_PULL) {
-                pull_cell<E>(fp, rt_pull, slot, c, hs, s_solid, x, y, pz, R[c]);
-            } else {
-                double a0, a1, a2;
-                gen_fin<E>(mode, c, s_tc, x, y, pz, R[c], a0, a1, a2);
-            }
-        }
-    };
-    // rho -> psi of the loaded plane (P1: engine.cpp:221-264) and TMEM stash
-    auto finish_plane = [&](int pz, int tslot) {
-        const int ring = pz & 3;
-        const bool sol = sol_xy_any && solid_at<E>(s_solid, x, y, pz);
-        int negs = 0, clamps = 0;
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-            double v = 0.0;
-            if (!sol) {
-                double rho = 0.0;
-#pragma unroll
-                for (int i = 0; i < Q; ++i) {
-                    rho += R[c][i];
-                    negs += R[c][i] < 0.0;
-                }
-                if (!isfinite(rho)) {
-                    atomic_err(d.err, iter, tile_lin, ERR_P1_NAN);
-                } else {
-                    double press;
-                    if (!pr_pressure(rho, P.comp[c], press)) {
-                        atomic_err(d.err, iter, tile_lin, ERR_P1_POLE);
-                    } else {
-                        bool cl;
-                        v = pseudo_potential(rho, press, P.comp[c], cl);
-                        clamps += cl;
-                    }
-                }
-            }
-            psi[pidx(ring, c, x, yl)] = v;
-            tm_store19(tbase + uint32_t(tslot * T::SCOLS + c * T::CB), R[c]);
-        }
-        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-        const unsigned m1 = __reduce_add_sync(0xffffffffu, (unsigned)negs);
-        const unsigned m2 = __reduce_add_sync(0xffffffffu, (unsigned)clamps);
-        if ((tid & 31) == 0) {
-            if (m1) atomicAdd(&d.cnt[CNT_NEG], (unsigned long long)m1);
-            if (m2) atomicAdd(&d.cnt[CNT_CLAMP], (unsigned long long)m2);
-        }
-    };
-
-    // ---- collide plane z from the TMEM stash --------------------------------
-    auto collide_plane = [&](int z) {
-        const bool sol = sol_xy_any && solid_at<E>(s_solid, x, y, z);
-        const int cell = (z * E + y) * E + x;
-        const double* pm = psi + pidx((z - 1) & 3, 0, x, yl);
-        const double* p0 = psi + pidx(z & 3, 0, x, yl);
-        const double* ppl = psi + pidx((z + 1) & 3, 0, x, yl);
-        // frontier faces this cell lies on (u_prev of the activation criterion)
-        unsigned fmask = 0;
-        if (write_uface) {
-#pragma unroll
-            for (int face = 0; face < 6; ++face) {
-                const int axis = face >> 1;
-                const int coord = axis == 0 ? x : (axis == 1 ? y : z);
-                if (coord == ((face & 1) ? E - 1 : 0) && rt_psi.s[face_pattern(face)] == amb)
-                    fmask |= 1u << face;
-            }
-        }
-        int zero_rho = 0;
-#pragma unroll 1
-        for (int c = 0; c < C; ++c) {
-            double f[Q];
-            tm_load19(tbase + uint32_t((z & 1) * T::SCOLS + c * T::CB), f);  // warp-convergent
-            if (sol) continue;
-            double rho, u0 = 0.0, u1 = 0.0, u2 = 0.0;
-            if (mode == MODE_PULL) {
-                moments(f, rho, u0, u1, u2);
-            } else {
-                rho = sum19(f);
-                gen_u<E>(mode, c, s_tc, x, y, z, u0, u1, u2);
-            }
-            if (fmask) {
-#pragma unroll 1
-                for (int face = 0; face < 6; ++face) {
-                    if (!(fmask & (1u << face))) continue;
-                    double* uf = d.u_face + ((size_t(slot) * C + c) * 6 + face) * 3 * E2;
-                    const int fi = face_index<E>(face, x, y, z);
-                    uf[fi] = u0;
-                    uf[E2 + fi] = u1;
-                    uf[2 * E2 + fi] = u2;
-                }
-            }
-            if (d.capture) {
-                double* cp = d.capture + (size_t(slot) * C + c) * 4 * E3;
-                cp[cell] = p0[c * PP];
-                cp[E3 + cell] = u0;
-                cp[2 * E3 + cell] = u1;
-                cp[3 * E3 + cell] = u2;
-            }
-            double* out = fo + (size_t(slot) * C + c) * size_t(Q) * E3 + cell;
-            collide_comp<C, PW, PP>(f, rho, u0, u1, u2, c, pm, p0, ppl, out, size_t(E3), zero_rho);
-        }
-        const unsigned zr = __reduce_add_sync(0xffffffffu, (unsigned)zero_rho);
-        if ((tid & 31) == 0 && zr) atomicAdd(&d.cnt[CNT_ZERO_RHO], (unsigned long long)zr);
-    };
-
-    // ---- prologue: psi planes -1, 0, 1; f(0), f(1) stashed -------------------
-    fill_zghost(-1);
-    load_plane(0);
-    finish_plane(0, 0);
-    fill_ring(0);
-    load_plane(1);
-    finish_plane(1, 1);
-    fill_ring(1);
-    cluster_sync();
-    copy_rows(0);
-    copy_rows(1);
-    __syncthreads();
-
-#pragma unroll 1
-    for (int z = 0; z < E; ++z) {
-        const bool ahead = z + 2 < E;
-        if (ahead) load_plane(z + 2);  // in flight during the collide
-        collide_plane(z);
-        if (ahead) {
-            finish_plane(z + 2, z & 1);
-            fill_ring(z + 2);
-        } else if (z + 2 == E) {
-            fill_zghost(E);
-        }
-        cluster_sync();
-        if (ahead) copy_rows(z + 2);
-        __syncthreads();
-    }
-
-    // ---- teardown
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    cluster_sync();
-    if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(s_tmem),
-                     "n"(T::NCOLS));
-}
-
-
-// ---------------------------------------------------------------------------
-// k_main_tm2: two CTAs (16 warps) per SM for latency hiding.  The stash of
-// plane p lives in TMEM when p is even and in shared memory when p is odd, so
-// one TMEM slot (<= 80 columns per lane, 256 columns per CTA) and one smem
-// slot (19*C*256 doubles) suffice and nothing is held in registers across the
-// collide; registers are capped at 128 per thread.  Each thread only ever
-// touches its own TMEM lane and its own smem column, so the only block-wide
-// synchronisation per plane is the psi exchange.
-//
-// Per plane z:  psi pass of plane z+1 (pull, rho, psi, stash)  | cluster barrier
-//               + neighbour psi rows  |  collide plane z from its stash.
-template <int E, int C>
-struct Tm2Cfg {
-    static constexpr int NT = 256;
-    static constexpr int BY = NT / E;
-    static constexpr int NB = E / BY;
-    static constexpr int CB = 40;
-    static constexpr int NCOLS = 256;            // per CTA; 2 CTAs per SM
-    static constexpr int HALF = NCOLS / 2;       // per warp (two warps per lane quarter)
-    static constexpr int PW = E + 2;
-    static constexpr int PH = BY + 2;
-    static constexpr int PP = PW * PH;
-    static constexpr int PSI_BYTES = 4 * C * PP * 8;
-    static constexpr int STAGE_BYTES = Q * C * NT * 8;
-    static constexpr int SMEM = PSI_BYTES + STAGE_BYTES;
-    static_assert(CB * C <= HALF, "TMEM slot does not fit");
-    static_assert(2 * (SMEM + 6 * 1024) <= 228 * 1024, "two CTAs per SM must fit");
-};
-
-template <int E, int C>
-__global__ void __launch_bounds__(256, 2) k_main_tm2(Dev d, const int* __restrict__ active,
-                                                     int src_buf, int write_uface, long iter) {
-    using T = Tm2Cfg<E, C>;
-    constexpr int NT = T::NT, BY = T::BY, NB = T::NB, PW = T::PW, PH = T::PH, PP = T::PP;
-    constexpr int G = E + 2;
-    constexpr int E2 = E * E;
-    constexpr int E3 = E * E * E;
-    extern __shared__ __align__(16) double smem[];
-    double* psi = smem;                        // [4][C][PH][PW]
-    double* stage = smem + 4 * C * PP;         // [C][Q][NT]
-    __shared__ RouteTab rt_pull, rt_psi;
-    __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
-    __shared__ int s_tc[3];
-    __shared__ uint32_t s_tmem;
-
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5;
-    const int tile_i = blockIdx.x / NB;
-    const int yb = blockIdx.x % NB;
-    const int y0 = yb * BY;
-    const int slot = active[tile_i];
-    const uint8_t mode = d.mode[slot];
-    const bool hs = d.has_solid[slot] != 0;
-    const int amb = P.amb_slot;
-    const double* __restrict__ fp = d.f[src_buf];
-    double* __restrict__ fo = d.f[src_buf ^ 1];
-
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                         smem_u32(&s_tmem)),
-                     "n"(T::NCOLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-    }
-    load_routes(rt_pull, d.route[ROUTE_PULL] + size_t(slot) * 18, slot, amb);
-    load_routes(rt_psi, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, amb);
-    if (tid < 3) s_tc[tid] = d.coords[slot * 3 + tid];
-    if (hs)
-        for (int k = tid; k < d.solid_words; k += NT) s_solid[k] = d.solid[size_t(slot) * d.solid_words + k];
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    const uint32_t tbase = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * T::HALF);
-    const int tile_lin = (s_tc[0] * P.grid[1] + s_tc[1]) * P.grid[2] + s_tc[2];
-
-    const int x = tid % E;
-    const int yl = tid / E;
-    const int y = y0 + yl;
-    // fast pull applies to this warp's row(s): no solids, y+-1 inside the tile
-    // (E = 32: one warp is one row, so the test is warp-uniform)
-    const bool fast_rows = mode == MODE_PULL && !hs && y >= 1 && y <= E - 2;
-    auto pidx = [&](int ring, int c, int xx, int yy_local) {
-        return ((ring * C + c) * PH + (yy_local + 1)) * PW + (xx + 1);
-    };
-    auto fill_zghost = [&](int pz) {
-        const int ring = pz & 3;
-        for (int k = tid; k < PP; k += NT) {
-            const int xx = k % PW - 1, yy = k / PW - 1 + y0;
-            const bool xo = xx < 0 || xx >= E, yo = yy < 0 || yy >= E;
-#pragma unroll 1
-            for (int c = 0; c < C; ++c)
-                psi[pidx(ring, c, xx, yy - y0)] =
-                    (xo && yo) ? 0.0 : psi_ghost<E>(d, rt_psi, c, hs, s_solid, xx, yy, pz);
-        }
-    };
-    auto fill_ring = [&](int pz) {
-        const int ring = pz & 3;
-        for (int k = tid; k < 2 * PH + 2 * E; k += NT) {
-            int xx, yyl;
-            if (k < 2 * PH) {
-                xx = (k & 1) ? E : -1;
-                yyl = (k >> 1) - 1;
-            } else {
-                const int q = k - 2 * PH;
-                xx = q % E;
-                yyl = (q / E) ? BY : -1;
-                const int yy = y0 + yyl;
-                if (yy >= 0 && yy < E) continue;
-            }
-#pragma unroll 1
-            for (int c = 0; c < C; ++c)
-                psi[pidx(ring, c, xx, yyl)] = psi_ghost<E>(d, rt_psi, c, hs, s_solid, xx, y0 + yyl, pz);
-        }
-    };
-    auto copy_rows = [&](int pz) {
-        if constexpr (NB > 1) {
-            cg::cluster_group cl = cg::this_cluster();
-            const int ring = pz & 3;
-            for (int k = tid; k < 2 * E * C; k += NT) {
-                const int side = k / (E * C);
-                const int c = (k / E) % C;
-                const int xx = k % E;
-                const int nb = yb + (side ? 1 : -1);
-                if (nb < 0 || nb >= NB) continue;
-                const double* peer = cl.map_shared_rank(psi, nb);
-                psi[pidx(ring, c, xx, side ? BY : -1)] = peer[pidx(ring, c, xx, side ? 0 : BY - 1)];
-            }
-        }
-    };
-    auto cluster_sync = [&]() {
-        if constexpr (NB > 1) {
-            asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-            asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-        } else {
-            __syncthreads();
-        }
-    };
-
-    // psi pass of plane pz: pull (or generate) f_in, rho -> psi, stash f_in
-    auto psi_pass = [&](int pz) {
-        const int ring = pz & 3;
-        const bool sol = hs && solid_at<E>(s_solid, x, y, pz);
-        int negs = 0, clamps = 0;
-#pragma unroll 1
-        for (int c = 0; c < C; ++c) {
-            double f[Q];
-            double v = 0.0;
-            if (sol) {
-#pragma unroll
-                for (int i = 0; i < Q; ++i) f[i] = 0.0;
-            } else {
-                if (fast_rows && pz >= 1 && pz <= E - 2) {
-                    pull_cell_fast<E>(fp, rt_pull, slot, c, x, y, pz, f);
-                } else if (mode == MODE_PULL) {
-                    pull_cell<E>(fp, rt_pull, slot, c, hs, s_solid, x, y, pz, f);
-                } else {
-                    double a0, a1, a2;
-                    gen_fin<E>(mode, c, s_tc, x, y, pz, f, a0, a1, a2);
-                }
-                double rho = 0.0;
-#pragma unroll
-                for (int i = 0; i < Q; ++i) {
-                    rho += f[i];
-                    negs += f[i] < 0.0;
-                }
-                if (!isfinite(rho)) {
-                    atomic_err(d.err, iter, tile_lin, ERR_P1_NAN);
-                } else {
-                    double press;
-                    if (!pr_pressure(rho, P.comp[c], press)) {
-                        atomic_err(d.err, iter, tile_lin, ERR_P1_POLE);
-                    } else {
-                        bool cl;
-                        v = pseudo_potential(rho, press, P.comp[c], cl);
-                        clamps += cl;
-                    }
-                }
-            }
-            psi[pidx(ring, c, x, yl)] = v;
-            if ((pz & 1) == 0) {
-                tm_store19(tbase + uint32_t(c * T::CB), f);
-            } else {
-                double* st = stage + size_t(c) * Q * NT + tid;
-#pragma unroll
-                for (int i = 0; i < Q; ++i) st[i * NT] = f[i];
-            }
-        }
-        if ((pz & 1) == 0) asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-        const unsigned m1 = __reduce_add_sync(0xffffffffu, (unsigned)negs);
-        const unsigned m2 = __reduce_add_sync(0xffffffffu, (unsigned)clamps);
-        if ((tid & 31) == 0) {
-            if (m1) atomicAdd(&d.cnt[CNT_NEG], (unsigned long long)m1);
-            if (m2) atomicAdd(&d.cnt[CNT_CLAMP], (unsigned long long)m2);
-        }
-    };
-
-    auto collide_plane = [&](int z) {
-        const bool sol = hs && solid_at<E>(s_solid, x, y, z);
-        const int cell = (z * E + y) * E + x;
-        const double* pm = psi + pidx((z - 1) & 3, 0, x, yl);
-        const double* p0 = psi + pidx(z & 3, 0, x, yl);
-        const double* ppl = psi + pidx((z + 1) & 3, 0, x, yl);
-        // frontier faces this cell lies on (u_prev of the activation criterion)
-        unsigned fmask = 0;
-        if (write_uface) {
-#pragma unroll
-            for (int face = 0; face < 6; ++face) {
-                const int axis = face >> 1;
-                const int coord = axis == 0 ? x : (axis == 1 ? y : z);
-                if (coord == ((face & 1) ? E - 1 : 0) && rt_psi.s[face_pattern(face)] == amb)
-                    fmask |= 1u << face;
-            }
-        }
-        int zero_rho = 0;
-#pragma unroll 1
-        for (int c = 0; c < C; ++c) {
-            double f[Q];
-            if ((z & 1) == 0) {
-                tm_load19(tbase + uint32_t(c * T::CB), f);  // warp-convergent
-            } else {
-                const double* st = stage + size_t(c) * Q * NT + tid;
-#pragma unroll
-                for (int i = 0; i < Q; ++i) f[i] = st[i * NT];
-            }
-            if (sol) continue;
-            double rho, u0 = 0.0, u1 = 0.0, u2 = 0.0;
-            if (mode == MODE_PULL) {
-                moments(f, rho, u0, u1, u2);
-            } else {
-                rho = sum19(f);
-                gen_u<E>(mode, c, s_tc, x, y, z, u0, u1, u2);
-            }
-            if (fmask) {
-#pragma unroll 1
-                for (int face = 0; face < 6; ++face) {
-                    if (!(fmask & (1u << face))) continue;
-                    double* uf = d.u_face + ((size_t(slot) * C + c) * 6 + face) * 3 * E2;
-                    const int fi = face_index<E>(face, x, y, z);
-                    uf[fi] = u0;
-                    uf[E2 + fi] = u1;
-                    uf[2 * E2 + fi] = u2;
-                }
-            }
-            if (d.capture) {
-                double* cp = d.capture + (size_t(slot) * C + c) * 4 * E3;
-                cp[cell] = p0[c * PP];
-                cp[E3 + cell] = u0;
-                cp[2 * E3 + cell] = u1;
-                cp[3 * E3 + cell] = u2;
-            }
-            double* out = fo + (size_t(slot) * C + c) * size_t(Q) * E3 + cell;
-            collide_comp<C, PW, PP>(f, rho, u0, u1, u2, c, pm, p0, ppl, out, size_t(E3), zero_rho);
-        }
-        const unsigned zr = __reduce_add_sync(0xffffffffu, (unsigned)zero_rho);
-        if ((tid & 31) == 0 && zr) atomicAdd(&d.cnt[CNT_ZERO_RHO], (unsigned long long)zr);
-    };
-
-    fill_zghost(-1);
-    psi_pass(0);
-    fill_ring(0);
-    cluster_sync();
-    copy_rows(0);
-    __syncthreads();
-#pragma unroll 1
-    for (int z = 0; z < E; ++z) {
-        if (z + 1 < E) {
-            psi_pass(z + 1);
-            fill_ring(z + 1);
-        } else {
-            fill_zghost(E);
-        }
-        cluster_sync();
-        if (z + 1 < E) copy_rows(z + 1);
-        __syncthreads();
-        collide_plane(z);
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    cluster_sync();
-    if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(s_tmem),
-                     "n"(T::NCOLS));
-}
-
-
-template <int E, int C>
-__global__ void __launch_bounds__(256, 2) k_main_tm4(Dev d, const int* __restrict__ active,
-                                                     int src_buf, int write_uface, long iter) {
-    using T = Tm2Cfg<E, C>;  // same footprint + 2 mbarriers
-    constexpr int NT = T::NT, BY = T::BY, NB = T::NB, PW = T::PW, PH = T::PH, PP = T::PP;
-    constexpr int G = E + 2;
-    constexpr int E2 = E * E;
-    constexpr int E3 = E * E * E;
-    extern __shared__ __align__(16) double smem[];
-    double* psi = smem;                        // [4][C][PH][PW]
-    double* stage = smem + 4 * C * PP;         // [C][Q][NT]
+    double* psi = smem;                 // [4][C][PH][PW] ring of psi planes
+    double* stage = smem + 4 * C * PP;  // [C][Q][NT] odd-plane stash
     __shared__ RouteTab rt_pull, rt_psi;
     __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
     __shared__ int s_tc[3];
@@ -798,8 +247,9 @@ __global__ void __launch_bounds__(256, 2) k_main_tm4(Dev d, const int* __restric
     const uint8_t mode = d.mode[slot];
     const bool hs = d.has_solid[slot] != 0;
     const int amb = P.amb_slot;
-    const double* __restrict__ fp = d.f[src_buf];
-    double* __restrict__ fo = d.f[src_buf ^ 1];
+    const int par = int(iter & 1);
+    double* __restrict__ fo = d.slot_f[src_buf ^ 1][slot];
+    const int li = d.lidx[slot];
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
@@ -807,8 +257,8 @@ __global__ void __launch_bounds__(256, 2) k_main_tm4(Dev d, const int* __restric
                      "n"(T::NCOLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
-    load_routes(rt_pull, d.route[ROUTE_PULL] + size_t(slot) * 18, slot, amb);
-    load_routes(rt_psi, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, amb);
+    load_routes(rt_pull, d.route[ROUTE_PULL] + size_t(slot) * 18, slot, amb, d.slot_f[src_buf]);
+    load_routes(rt_psi, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, amb, d.slot_pf[par], d.mode);
     if (tid < 3) s_tc[tid] = d.coords[slot * 3 + tid];
     if (hs)
         for (int k = tid; k < d.solid_words; k += NT) s_solid[k] = d.solid[size_t(slot) * d.solid_words + k];
@@ -837,17 +287,17 @@ __global__ void __launch_bounds__(256, 2) k_main_tm4(Dev d, const int* __restric
     auto pidx = [&](int ring, int c, int xx, int yy_local) {
         return ((ring * C + c) * PH + (yy_local + 1)) * PW + (xx + 1);
     };
-    // ---- push-based psi row exchange (no per-plane cluster barrier) ---------
+
+    // ---- push-based psi row exchange --------------------------------------
     // Block row 0 feeds the -y neighbour's ring row BY, block row BY-1 feeds
-    // the +y neighbour's ring row -1: each value goes out as an 8-byte
-    // st.async that completes a transaction on the receiver's mbarrier.
+    // the +y neighbour's ring row -1: each value goes out as an 8-byte st.async
+    // that completes a transaction on the receiver's mbarrier.
     const bool push_lo = NB > 1 && yl == 0 && yb > 0;
     const bool push_hi = NB > 1 && yl == BY - 1 && yb < NB - 1;
-    const uint32_t psi_sh = smem_u32(psi);
     uint32_t peer_psi = 0, peer_mbar = 0;
     if (push_lo || push_hi) {
         const uint32_t nb = uint32_t(yb + (push_lo ? -1 : 1));
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(peer_psi) : "r"(psi_sh), "r"(nb));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(peer_psi) : "r"(smem_u32(psi)), "r"(nb));
         asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n"
                      : "=r"(peer_mbar)
                      : "r"(smem_u32(&s_mbar[0])), "r"(nb));
@@ -884,7 +334,9 @@ __global__ void __launch_bounds__(256, 2) k_main_tm4(Dev d, const int* __restric
                 : "r"(bar), "r"(parity)
                 : "memory");
     };
-    auto fill_zghost = [&](int pz) {
+
+    // ---- psi of out-of-block positions (face buffers of neighbour tiles) ----
+    auto fill_zghost = [&](int pz) {  // whole plane outside the tile in z
         const int ring = pz & 3;
         for (int k = tid; k < PP; k += NT) {
             const int xx = k % PW - 1, yy = k / PW - 1 + y0;
@@ -892,10 +344,10 @@ __global__ void __launch_bounds__(256, 2) k_main_tm4(Dev d, const int* __restric
 #pragma unroll 1
             for (int c = 0; c < C; ++c)
                 psi[pidx(ring, c, xx, yy - y0)] =
-                    (xo && yo) ? 0.0 : psi_ghost<E>(d, rt_psi, c, hs, s_solid, xx, yy, pz);
+                    (xo && yo) ? 0.0 : psi_ghost<E>(rt_psi, c, hs, s_solid, xx, yy, pz);
         }
     };
-    auto fill_ring = [&](int pz) {
+    auto fill_ring = [&](int pz) {  // x ring + y rows that lie outside the tile
         const int ring = pz & 3;
         for (int k = tid; k < 2 * PH + 2 * E; k += NT) {
             int xx, yyl;
@@ -907,38 +359,15 @@ __global__ void __launch_bounds__(256, 2) k_main_tm4(Dev d, const int* __restric
                 xx = q % E;
                 yyl = (q / E) ? BY : -1;
                 const int yy = y0 + yyl;
-                if (yy >= 0 && yy < E) continue;
+                if (yy >= 0 && yy < E) continue;  // pushed by the cluster neighbour
             }
 #pragma unroll 1
             for (int c = 0; c < C; ++c)
-                psi[pidx(ring, c, xx, yyl)] = psi_ghost<E>(d, rt_psi, c, hs, s_solid, xx, y0 + yyl, pz);
-        }
-    };
-    auto copy_rows = [&](int pz) {
-        if constexpr (NB > 1) {
-            cg::cluster_group cl = cg::this_cluster();
-            const int ring = pz & 3;
-            for (int k = tid; k < 2 * E * C; k += NT) {
-                const int side = k / (E * C);
-                const int c = (k / E) % C;
-                const int xx = k % E;
-                const int nb = yb + (side ? 1 : -1);
-                if (nb < 0 || nb >= NB) continue;
-                const double* peer = cl.map_shared_rank(psi, nb);
-                psi[pidx(ring, c, xx, side ? BY : -1)] = peer[pidx(ring, c, xx, side ? 0 : BY - 1)];
-            }
-        }
-    };
-    auto cluster_sync = [&]() {
-        if constexpr (NB > 1) {
-            asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-            asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-        } else {
-            __syncthreads();
+                psi[pidx(ring, c, xx, yyl)] = psi_ghost<E>(rt_psi, c, hs, s_solid, xx, y0 + yyl, pz);
         }
     };
 
-    // psi pass of plane pz: pull (or generate) f_in, rho -> psi, stash f_in
+    // ---- psi pass of plane pz: pull f_in, rho -> psi (P1), stash -------------
     auto psi_pass = [&](int pz) {
         const int ring = pz & 3;
         const bool sol = hs && solid_at<E>(s_solid, x, y, pz);
@@ -952,9 +381,9 @@ __global__ void __launch_bounds__(256, 2) k_main_tm4(Dev d, const int* __restric
                 for (int i = 0; i < Q; ++i) f[i] = 0.0;
             } else {
                 if (fast_rows && pz >= 1 && pz <= E - 2) {
-                    pull_cell_fast<E>(fp, rt_pull, slot, c, x, y, pz, f);
+                    pull_cell_fast<E>(rt_pull, c, x, y, pz, f);
                 } else if (mode == MODE_PULL) {
-                    pull_cell<E>(fp, rt_pull, slot, c, hs, s_solid, x, y, pz, f);
+                    pull_cell<E>(rt_pull, c, hs, s_solid, x, y, pz, f);
                 } else {
                     double a0, a1, a2;
                     gen_fin<E>(mode, c, s_tc, x, y, pz, f, a0, a1, a2);
@@ -997,14 +426,14 @@ __global__ void __launch_bounds__(256, 2) k_main_tm4(Dev d, const int* __restric
         }
     };
 
+    // ---- collide plane z from its stash ---------------------------------------
     auto collide_plane = [&](int z) {
         const bool sol = hs && solid_at<E>(s_solid, x, y, z);
         const int cell = (z * E + y) * E + x;
         const double* pm = psi + pidx((z - 1) & 3, 0, x, yl);
         const double* p0 = psi + pidx(z & 3, 0, x, yl);
         const double* ppl = psi + pidx((z + 1) & 3, 0, x, yl);
-        // frontier faces this cell lies on (u_prev of the activation criterion)
-        unsigned fmask = 0;
+        unsigned fmask = 0;  // frontier faces this cell lies on (criterion u_prev)
         if (write_uface) {
 #pragma unroll
             for (int face = 0; face < 6; ++face) {
@@ -1037,7 +466,7 @@ __global__ void __launch_bounds__(256, 2) k_main_tm4(Dev d, const int* __restric
 #pragma unroll 1
                 for (int face = 0; face < 6; ++face) {
                     if (!(fmask & (1u << face))) continue;
-                    double* uf = d.u_face + ((size_t(slot) * C + c) * 6 + face) * 3 * E2;
+                    double* uf = d.u_face + ((size_t(li) * C + c) * 6 + face) * 3 * E2;
                     const int fi = face_index<E>(face, x, y, z);
                     uf[fi] = u0;
                     uf[E2 + fi] = u1;
@@ -1045,13 +474,13 @@ __global__ void __launch_bounds__(256, 2) k_main_tm4(Dev d, const int* __restric
                 }
             }
             if (d.capture) {
-                double* cp = d.capture + (size_t(slot) * C + c) * 4 * E3;
+                double* cp = d.capture + (size_t(li) * C + c) * 4 * E3;
                 cp[cell] = p0[c * PP];
                 cp[E3 + cell] = u0;
                 cp[2 * E3 + cell] = u1;
                 cp[3 * E3 + cell] = u2;
             }
-            double* out = fo + (size_t(slot) * C + c) * size_t(Q) * E3 + cell;
+            double* out = fo + c * size_t(Q) * E3 + cell;
             collide_comp<C, PW, PP>(f, rho, u0, u1, u2, c, pm, p0, ppl, out, size_t(E3), zero_rho);
         }
         const unsigned zr = __reduce_add_sync(0xffffffffu, (unsigned)zero_rho);
@@ -1078,298 +507,11 @@ __global__ void __launch_bounds__(256, 2) k_main_tm4(Dev d, const int* __restric
         collide_plane(z);
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    cluster_sync();
-    if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(s_tmem),
-                     "n"(T::NCOLS));
-}
-
-
-// ---------------------------------------------------------------------------
-// k_main_tm3: one CTA (8 warps) per SM, memory latency hidden by cp.async.
-// The pulls of plane z+2 are issued as 8-byte cp.async copies (no registers
-// held) into a shared-memory landing buffer while plane z+1's psi pass and
-// plane z's collide run; the psi pass reads the landed plane, stashes it in
-// TMEM (two slots), and the collide reads TMEM.
-template <int E, int C>
-struct Tm3Cfg {
-    static constexpr int NT = 256;
-    static constexpr int BY = NT / E;
-    static constexpr int NB = E / BY;
-    static constexpr int CB = 40;
-    static constexpr int SCOLS = CB * C;
-    static constexpr int NCOLS = (4 * SCOLS <= 256) ? 256 : 512;
-    static constexpr int HALF = NCOLS / 2;
-    static constexpr int PW = E + 2;
-    static constexpr int PH = BY + 2;
-    static constexpr int PP = PW * PH;
-    static constexpr int PSI_BYTES = 4 * C * PP * 8;
-    static constexpr int LAND_BYTES = 2 * Q * C * NT * 8;
-    static constexpr int RAW = PSI_BYTES + LAND_BYTES;
-    static constexpr int SMEM = RAW > 118 * 1024 ? RAW : 118 * 1024;  // one CTA per SM
-    static_assert(2 * SCOLS <= HALF, "TMEM stash does not fit");
-    static_assert(RAW + 8 * 1024 <= 227 * 1024, "shared memory");
-};
-
-template <int E, int C>
-__global__ void __launch_bounds__(256, 1) k_main_tm3(Dev d, const int* __restrict__ active,
-                                                     int src_buf, int write_uface, long iter) {
-    using T = Tm3Cfg<E, C>;
-    constexpr int NT = T::NT, BY = T::BY, NB = T::NB, PW = T::PW, PH = T::PH, PP = T::PP;
-    constexpr int G = E + 2;
-    constexpr int E2 = E * E;
-    constexpr int E3 = E * E * E;
-    extern __shared__ __align__(16) double smem[];
-    double* psi = smem;                   // [4][C][PH][PW]
-    double* land = smem + 4 * C * PP;     // [2][C][Q][NT]
-    __shared__ RouteTab rt_pull, rt_psi;
-    __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
-    __shared__ int s_tc[3];
-    __shared__ uint32_t s_tmem;
-
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5;
-    const int tile_i = blockIdx.x / NB;
-    const int yb = blockIdx.x % NB;
-    const int y0 = yb * BY;
-    const int slot = active[tile_i];
-    const uint8_t mode = d.mode[slot];
-    const bool hs = d.has_solid[slot] != 0;
-    const int amb = P.amb_slot;
-    const double* __restrict__ fp = d.f[src_buf];
-    double* __restrict__ fo = d.f[src_buf ^ 1];
-
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                         smem_u32(&s_tmem)),
-                     "n"(T::NCOLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-    }
-    load_routes(rt_pull, d.route[ROUTE_PULL] + size_t(slot) * 18, slot, amb);
-    load_routes(rt_psi, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, amb);
-    if (tid < 3) s_tc[tid] = d.coords[slot * 3 + tid];
-    if (hs)
-        for (int k = tid; k < d.solid_words; k += NT) s_solid[k] = d.solid[size_t(slot) * d.solid_words + k];
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    const uint32_t tbase = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * T::HALF);
-    const int tile_lin = (s_tc[0] * P.grid[1] + s_tc[1]) * P.grid[2] + s_tc[2];
-
-    const int x = tid % E;
-    const int yl = tid / E;
-    const int y = y0 + yl;
-    const bool fast_rows = mode == MODE_PULL && !hs && y >= 1 && y <= E - 2;
-    auto pidx = [&](int ring, int c, int xx, int yy_local) {
-        return ((ring * C + c) * PH + (yy_local + 1)) * PW + (xx + 1);
-    };
-    auto lidx = [&](int buf, int c, int i) { return ((buf * C + c) * Q + i) * NT + tid; };
-    auto fill_zghost = [&](int pz) {
-        const int ring = pz & 3;
-        for (int k = tid; k < PP; k += NT) {
-            const int xx = k % PW - 1, yy = k / PW - 1 + y0;
-            const bool xo = xx < 0 || xx >= E, yo = yy < 0 || yy >= E;
-#pragma unroll 1
-            for (int c = 0; c < C; ++c)
-                psi[pidx(ring, c, xx, yy - y0)] =
-                    (xo && yo) ? 0.0 : psi_ghost<E>(d, rt_psi, c, hs, s_solid, xx, yy, pz);
-        }
-    };
-    auto fill_ring = [&](int pz) {
-        const int ring = pz & 3;
-        for (int k = tid; k < 2 * PH + 2 * E; k += NT) {
-            int xx, yyl;
-            if (k < 2 * PH) {
-                xx = (k & 1) ? E : -1;
-                yyl = (k >> 1) - 1;
-            } else {
-                const int q = k - 2 * PH;
-                xx = q % E;
-                yyl = (q / E) ? BY : -1;
-                const int yy = y0 + yyl;
-                if (yy >= 0 && yy < E) continue;
-            }
-#pragma unroll 1
-            for (int c = 0; c < C; ++c)
-                psi[pidx(ring, c, xx, yyl)] = psi_ghost<E>(d, rt_psi, c, hs, s_solid, xx, y0 + yyl, pz);
-        }
-    };
-    auto copy_rows = [&](int pz) {
-        if constexpr (NB > 1) {
-            cg::cluster_group cl = cg::this_cluster();
-            const int ring = pz & 3;
-            for (int k = tid; k < 2 * E * C; k += NT) {
-                const int side = k / (E * C);
-                const int c = (k / E) % C;
-                const int xx = k % E;
-                const int nb = yb + (side ? 1 : -1);
-                if (nb < 0 || nb >= NB) continue;
-                const double* peer = cl.map_shared_rank(psi, nb);
-                psi[pidx(ring, c, xx, side ? BY : -1)] = peer[pidx(ring, c, xx, side ? 0 : BY - 1)];
-            }
-        }
-    };
-    auto cluster_sync = [&]() {
-        if constexpr (NB > 1) {
-            asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-            asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-        } else {
-            __syncthreads();
-        }
-    };
-
-    // issue the pulls of plane pz into landing buffer pz & 1
-    auto issue = [&](int pz) {
-        const int buf = pz & 1;
-        const bool sol = hs && solid_at<E>(s_solid, x, y, pz);
-#pragma unroll 1
-        for (int c = 0; c < C; ++c) {
-            if (sol) continue;
-            if (fast_rows && pz >= 1 && pz <= E - 2) {
-                pull_addr_fast<E>(fp, rt_pull, slot, c, x, y, pz,
-                                  [&](int i, const double* p) { cp_async8(&land[lidx(buf, c, i)], p); });
-            } else if (mode == MODE_PULL) {
-                pull_addr<E>(fp, rt_pull, slot, c, hs, s_solid, x, y, pz,
-                             [&](int i, const double* p) { cp_async8(&land[lidx(buf, c, i)], p); });
-            } else {
-                double f[Q], a0, a1, a2;
-                gen_fin<E>(mode, c, s_tc, x, y, pz, f, a0, a1, a2);
-#pragma unroll
-                for (int i = 0; i < Q; ++i) land[lidx(buf, c, i)] = f[i];
-            }
-        }
-        cp_async_commit();
-    };
-
-    // psi pass of a landed plane + TMEM stash (slot pz & 1)
-    auto psi_pass = [&](int pz) {
-        const int ring = pz & 3;
-        const int buf = pz & 1;
-        const bool sol = hs && solid_at<E>(s_solid, x, y, pz);
-        int negs = 0, clamps = 0;
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-            double f[Q];
-            double v = 0.0;
-            if (sol) {
-#pragma unroll
-                for (int i = 0; i < Q; ++i) f[i] = 0.0;
-            } else {
-#pragma unroll
-                for (int i = 0; i < Q; ++i) f[i] = land[lidx(buf, c, i)];
-                double rho = 0.0;
-#pragma unroll
-                for (int i = 0; i < Q; ++i) {
-                    rho += f[i];
-                    negs += f[i] < 0.0;
-                }
-                if (!isfinite(rho)) {
-                    atomic_err(d.err, iter, tile_lin, ERR_P1_NAN);
-                } else {
-                    double press;
-                    if (!pr_pressure(rho, P.comp[c], press)) {
-                        atomic_err(d.err, iter, tile_lin, ERR_P1_POLE);
-                    } else {
-                        bool cl;
-                        v = pseudo_potential(rho, press, P.comp[c], cl);
-                        clamps += cl;
-                    }
-                }
-            }
-            psi[pidx(ring, c, x, yl)] = v;
-            tm_store19(tbase + uint32_t((pz & 1) * T::SCOLS + c * T::CB), f);
-        }
-        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-        const unsigned m1 = __reduce_add_sync(0xffffffffu, (unsigned)negs);
-        const unsigned m2 = __reduce_add_sync(0xffffffffu, (unsigned)clamps);
-        if ((tid & 31) == 0) {
-            if (m1) atomicAdd(&d.cnt[CNT_NEG], (unsigned long long)m1);
-            if (m2) atomicAdd(&d.cnt[CNT_CLAMP], (unsigned long long)m2);
-        }
-    };
-
-    auto collide_plane = [&](int z) {
-        const bool sol = hs && solid_at<E>(s_solid, x, y, z);
-        const int cell = (z * E + y) * E + x;
-        const double* pm = psi + pidx((z - 1) & 3, 0, x, yl);
-        const double* p0 = psi + pidx(z & 3, 0, x, yl);
-        const double* ppl = psi + pidx((z + 1) & 3, 0, x, yl);
-        unsigned fmask = 0;
-        if (write_uface) {
-#pragma unroll
-            for (int face = 0; face < 6; ++face) {
-                const int axis = face >> 1;
-                const int coord = axis == 0 ? x : (axis == 1 ? y : z);
-                if (coord == ((face & 1) ? E - 1 : 0) && rt_psi.s[face_pattern(face)] == amb)
-                    fmask |= 1u << face;
-            }
-        }
-        int zero_rho = 0;
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-            double f[Q];
-            tm_load19(tbase + uint32_t((z & 1) * T::SCOLS + c * T::CB), f);  // warp-convergent
-            if (sol) continue;
-            double rho, u0 = 0.0, u1 = 0.0, u2 = 0.0;
-            if (mode == MODE_PULL) {
-                moments(f, rho, u0, u1, u2);
-            } else {
-                rho = sum19(f);
-                gen_u<E>(mode, c, s_tc, x, y, z, u0, u1, u2);
-            }
-            if (fmask) {
-#pragma unroll 1
-                for (int face = 0; face < 6; ++face) {
-                    if (!(fmask & (1u << face))) continue;
-                    double* uf = d.u_face + ((size_t(slot) * C + c) * 6 + face) * 3 * E2;
-                    const int fi = face_index<E>(face, x, y, z);
-                    uf[fi] = u0;
-                    uf[E2 + fi] = u1;
-                    uf[2 * E2 + fi] = u2;
-                }
-            }
-            if (d.capture) {
-                double* cp = d.capture + (size_t(slot) * C + c) * 4 * E3;
-                cp[cell] = p0[c * PP];
-                cp[E3 + cell] = u0;
-                cp[2 * E3 + cell] = u1;
-                cp[3 * E3 + cell] = u2;
-            }
-            double* out = fo + (size_t(slot) * C + c) * size_t(Q) * E3 + cell;
-            collide_comp<C, PW, PP>(f, rho, u0, u1, u2, c, pm, p0, ppl, out, size_t(E3), zero_rho);
-        }
-        const unsigned zr = __reduce_add_sync(0xffffffffu, (unsigned)zero_rho);
-        if ((tid & 31) == 0 && zr) atomicAdd(&d.cnt[CNT_ZERO_RHO], (unsigned long long)zr);
-    };
-
-    issue(0);
-    issue(1);
-    fill_zghost(-1);
-    cp_async_wait<1>();
-    psi_pass(0);
-    fill_ring(0);
-    cluster_sync();
-    copy_rows(0);
-    __syncthreads();
-#pragma unroll 1
-    for (int z = 0; z < E; ++z) {
-        if (z + 2 < E) issue(z + 2);
-        else cp_async_commit();  // keep one group per iteration
-        cp_async_wait<1>();
-        if (z + 1 < E) {
-            psi_pass(z + 1);
-            fill_ring(z + 1);
-        } else {
-            fill_zghost(E);
-        }
-        cluster_sync();
-        if (z + 1 < E) copy_rows(z + 1);
-        __syncthreads();
-        collide_plane(z);
+    if constexpr (NB > 1) {  // all pushes into peers have landed before anyone exits
+        asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
     }
-    cp_async_wait<0>();
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    cluster_sync();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(s_tmem),
                      "n"(T::NCOLS));

@@ -286,3 +286,19 @@ def mpmc_release(n: int = 256, extent: int = 32, mode: int = MODE_PROGRESSIVE,
     return Scenario(domain=dom, tile_extent=extent, mode=mode, threshold=threshold,
                     devices=devices, components=comps, coupling=g, seeds=seeds,
                     name="mpmc_release")
+
+
+def mpmc_release_weak(n_blocks: int, n: int = 256, extent: int = 32, threshold: float = 1e-9) -> Scenario:
+    """Weak-scaling form of C2 for N GPUs: N 256^3 blocks side by side along x,
+    each with its own ramped liquid sphere (the single-GPU case is exactly
+    mpmc_release(256)); owners = GPUs (devices = N)."""
+    sc = mpmc_release(n=n, extent=extent, threshold=threshold, devices=n_blocks,
+                      domain=(n * n_blocks, n, n))
+    heavy = sc.components[0]
+    seeds = []
+    for b in range(n_blocks):
+        seeds += ramped_sphere_seeds((n * b + n / 2.0, n / 2.0, n / 2.0), n / 8.0, 6.5,
+                                     heavy.rho_ambient, 6, 0)
+    sc.seeds = seeds
+    sc.name = f"mpmc_release_weak_x{n_blocks}"
+    return sc
