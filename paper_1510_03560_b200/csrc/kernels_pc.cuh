@@ -1,0 +1,367 @@
+// kernels_pc.cuh — k_main_pc: one CTA per (column block, component), with the
+// pulls staged asynchronously.
+//
+// Measured constraints that shape it (profiles/, tools/bwtest.cu):
+//   * the 38 shifted SoA streams of a column block stream at the flat-copy
+//     rate when enough bytes are in flight — the access pattern is not the
+//     limit, memory-level parallelism is;
+//   * the FP64 work needs ~16 warps per SM to hide its dependency chains
+//     (k_main_as at 8 warps/SM was latency-bound on arithmetic);
+//   * at 16 warps/SM and two components per thread there is no room on chip
+//     for a landing buffer next to the two-plane stash.
+// Splitting the components over the two CTAs of a cluster pair halves the
+// per-CTA population state, which buys both: at 16 warps per SM each thread
+// holds one cell of one component, its next plane lands in shared memory by
+// cp.async while the current plane collides, and the stash of two planes
+// lives in Tensor Memory (2 x 40 columns).  psi values cross to the partner
+// component's CTA (whole plane) and to the y-neighbour blocks (edge rows, both
+// components) through distributed shared memory with st.async, completing
+// transactions on the receiver's per-plane mbarrier.
+//
+// Cluster = NB y-blocks x C components of one tile (E = 32: 4 x 2 = 8 CTAs).
+// Per plane z:  wait landing(z+1) | psi pass z+1 -> TMEM, push psi | issue
+//               pulls(z+2) | CTA barrier | issue ghosts(z+2) | wait pushes(z+1)
+//               | collide z from TMEM.
+#pragma once
+
+#include "kernels_as.cuh"
+
+namespace plbm {
+
+template <int E, int C>
+struct PcCfg {
+    static constexpr int NT = 256;
+    static constexpr int BY = NT / E;   // rows per CTA
+    static constexpr int NB = E / BY;   // y-blocks per tile
+    static constexpr int CL = NB * C;   // cluster size
+    static constexpr int CB = 40;       // TMEM columns per plane slot (19 f + rho)
+    static constexpr int NCOLS = 256;   // two warps per lane quarter x 128 columns
+    static constexpr int PW = E + 2;
+    static constexpr int PH = BY + 2;
+    static constexpr int PP = PW * PH;
+    static constexpr int RING = 4;
+    static constexpr int PSI_BYTES = RING * C * PP * 8;
+    static constexpr int LAND_BYTES = Q * NT * 8;
+    static constexpr int SMEM = PSI_BYTES + LAND_BYTES;
+    static_assert(CL <= 8, "portable cluster size");
+    static_assert(2 * CB <= NCOLS / 2, "TMEM plane slots do not fit");
+    static_assert(2 * (SMEM + 8 * 1024) <= 228 * 1024, "two CTAs per SM must fit");
+};
+
+template <int E, int C>
+__global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict__ active,
+                                                    int src_buf, int write_uface, long iter) {
+    using T = PcCfg<E, C>;
+    constexpr int NT = T::NT, BY = T::BY, NB = T::NB, PW = T::PW, PH = T::PH, PP = T::PP;
+    constexpr int R = T::RING;
+    constexpr int G = E + 2;
+    constexpr int E2 = E * E;
+    constexpr int E3 = E * E * E;
+    extern __shared__ __align__(16) double smem[];
+    double* psi = smem;                // [R][C][PH][PW] ring of psi planes, all components
+    double* land = smem + R * C * PP;  // [Q][NT] landed populations of the next plane
+    __shared__ RouteTab rt_pull, rt_psi;
+    __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
+    __shared__ int s_tc[3];
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(8) uint64_t s_mbar[2];  // pushed psi of plane p, by parity
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int rank = int(blockIdx.x % T::CL);  // = cluster CTA rank (1-D clusters)
+    const int tile_i = int(blockIdx.x / T::CL);
+    const int c = rank / NB;                   // this CTA's component
+    const int yb = rank % NB;
+    const int y0 = yb * BY;
+    const int slot = active[tile_i];
+    const uint8_t mode = d.mode[slot];
+    const bool hs = d.has_solid[slot] != 0;
+    const int amb = P.amb_slot;
+    const int par = int(iter & 1);
+    double* __restrict__ fo = d.slot_f[src_buf ^ 1][slot] + size_t(c) * Q * E3;
+    const int li = d.lidx[slot];
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                         smem_u32(&s_tmem)),
+                     "n"(T::NCOLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    load_routes(rt_pull, d.route[ROUTE_PULL] + size_t(slot) * 18, slot, amb, d.slot_f[src_buf]);
+    load_routes(rt_psi, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, amb, d.slot_pf[par], d.mode);
+    if (tid < 3) s_tc[tid] = d.coords[slot * 3 + tid];
+    if (hs)
+        for (int k = tid; k < d.solid_words; k += NT) s_solid[k] = d.solid[size_t(slot) * d.solid_words + k];
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&s_mbar[0])), "r"(1));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&s_mbar[1])), "r"(1));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    if constexpr (T::CL > 1) {  // peers see our initialised mbarriers before pushing
+        asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    }
+    // 8 warps: warps w and w+4 share TMEM lanes 32(w%4).., split by columns
+    const uint32_t tbase = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * (T::NCOLS / 2));
+    const int tile_lin = (s_tc[0] * P.grid[1] + s_tc[1]) * P.grid[2] + s_tc[2];
+
+    const int x = tid % E;
+    const int yl = tid / E;
+    const int y = y0 + yl;
+    const bool fast_rows = mode == MODE_PULL && !hs && y >= 1 && y <= E - 2;
+    auto pidx = [&](int pz, int cc, int xx, int yy_local) {
+        return (((pz & (R - 1)) * C + cc) * PH + (yy_local + 1)) * PW + (xx + 1);
+    };
+    const uint32_t land_u32 = smem_u32(land);
+
+    // ---- psi pushes: whole plane to the other components' CTAs of this block,
+    // edge rows to every component's CTA of the adjacent y-blocks ------------
+    const uint32_t psi_u32 = smem_u32(psi);
+    const uint32_t mbar_u32 = smem_u32(&s_mbar[0]);
+    auto push = [&](int dst_rank, int pz, int yy_local, double v) {
+        uint32_t ra, rb;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(psi_u32), "r"(dst_rank));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rb) : "r"(mbar_u32), "r"(dst_rank));
+        asm volatile(
+            "st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n" ::"r"(
+                ra + uint32_t(pidx(pz, c, x, yy_local)) * 8u),
+            "l"(__double_as_longlong(v)), "r"(rb + uint32_t((pz & 1) * 8))
+            : "memory");
+    };
+    auto push_all = [&](int pz, double v) {
+#pragma unroll
+        for (int c2 = 0; c2 < C; ++c2) {
+            if (c2 != c) push(c2 * NB + yb, pz, yl, v);
+            if (yl == 0 && yb > 0) push(c2 * NB + yb - 1, pz, BY, v);
+            if (yl == BY - 1 && yb < NB - 1) push(c2 * NB + yb + 1, pz, -1, v);
+        }
+    };
+    constexpr uint32_t PLANE_BYTES = uint32_t((C - 1) * BY * E * 8);
+    const uint32_t expect_bytes =
+        PLANE_BYTES + uint32_t(((yb > 0) + (yb < NB - 1)) * C * E * 8);
+    auto expect = [&](int pz) {
+        if (T::CL > 1 && tid == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                             mbar_u32 + uint32_t((pz & 1) * 8)),
+                         "r"(expect_bytes)
+                         : "memory");
+    };
+    auto wait_pushed = [&](int pz) {
+        if (T::CL == 1) return;
+        const uint32_t bar = mbar_u32 + uint32_t((pz & 1) * 8);
+        const uint32_t parity = uint32_t((pz >> 1) & 1);
+        uint32_t ok = 0;
+        while (!ok)
+            asm volatile(
+                "{\n .reg .pred q;\n mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n"
+                " selp.u32 %0, 1, 0, q;\n}\n"
+                : "=r"(ok)
+                : "r"(bar), "r"(parity)
+                : "memory");
+    };
+
+    // ---- psi ghost entries (both components) ---------------------------------
+    auto fill_zghost = [&](int pz) {
+        for (int k = tid; k < PP; k += NT) {
+            const int xx = k % PW - 1, yy = k / PW - 1 + y0;
+            const bool xo = xx < 0 || xx >= E, yo = yy < 0 || yy >= E;
+#pragma unroll 1
+            for (int cc = 0; cc < C; ++cc)
+                psi[pidx(pz, cc, xx, yy - y0)] =
+                    (xo && yo) ? 0.0 : psi_ghost<E>(rt_psi, cc, hs, s_solid, xx, yy, pz);
+        }
+    };
+    auto issue_ring = [&](int pz) {  // x ring + tile-edge halo rows, asynchronously
+        if (pz >= E) return;
+        for (int k = tid; k < 2 * PH + 2 * E; k += NT) {
+            int xx, yyl;
+            if (k < 2 * PH) {
+                xx = (k & 1) ? E : -1;
+                yyl = (k >> 1) - 1;
+            } else {
+                const int q = k - 2 * PH;
+                xx = q % E;
+                yyl = (q / E) ? BY : -1;
+                const int yy = y0 + yyl;
+                if (yy >= 0 && yy < E) continue;  // pushed by the adjacent y-block
+            }
+#pragma unroll 1
+            for (int cc = 0; cc < C; ++cc) {
+                double v;
+                const double* src = psi_ghost_src<E>(rt_psi, cc, hs, s_solid, xx, y0 + yyl, pz, v);
+                const int idx = pidx(pz, cc, xx, yyl);
+                if (src) cp_async8(smem_u32(psi + idx), src);
+                else psi[idx] = v;
+            }
+        }
+    };
+    auto issue_pulls = [&](int pz) {
+        if (pz >= E || mode != MODE_PULL || (hs && solid_at<E>(s_solid, x, y, pz))) return;
+        auto op = [&](int i, const double* p) { cp_async8(land_u32 + uint32_t(i * NT + tid) * 8u, p); };
+        if (fast_rows && pz >= 1 && pz <= E - 2) pull_addr_fast<E>(rt_pull, c, x, y, pz, op);
+        else pull_addr<E>(rt_pull, c, hs, s_solid, x, y, pz, op);
+    };
+
+    // ---- psi pass of plane pz ---------------------------------------------------
+    auto psi_pass = [&](int pz) {
+        const bool sol = hs && solid_at<E>(s_solid, x, y, pz);
+        double f[Q];
+        double v = 0.0, rho = 0.0;
+        int negs = 0, clamps = 0;
+        if (sol) {
+#pragma unroll
+            for (int i = 0; i < Q; ++i) f[i] = 0.0;
+        } else {
+            if (mode == MODE_PULL) {
+#pragma unroll
+                for (int i = 0; i < Q; ++i) f[i] = land[i * NT + tid];
+            } else {
+                double a0, a1, a2;
+                gen_fin<E>(mode, c, s_tc, x, y, pz, f, a0, a1, a2);
+            }
+#pragma unroll
+            for (int i = 0; i < Q; ++i) {
+                rho += f[i];
+                negs += f[i] < 0.0;
+            }
+            if (!isfinite(rho)) {
+                atomic_err(d.err, iter, tile_lin, ERR_P1_NAN);
+            } else {
+                double press;
+                if (!pr_pressure(rho, P.comp[c], press)) {
+                    atomic_err(d.err, iter, tile_lin, ERR_P1_POLE);
+                } else {
+                    bool cl;
+                    v = pseudo_potential(rho, press, P.comp[c], cl);
+                    clamps += cl;
+                }
+            }
+        }
+        psi[pidx(pz, c, x, yl)] = v;
+        push_all(pz, v);
+        tm_store20(tbase + uint32_t((pz & 1) * T::CB), f, rho);
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        const unsigned m1 = __reduce_add_sync(0xffffffffu, (unsigned)negs);
+        const unsigned m2 = __reduce_add_sync(0xffffffffu, (unsigned)clamps);
+        if ((tid & 31) == 0) {
+            if (m1) atomicAdd(&d.cnt[CNT_NEG], (unsigned long long)m1);
+            if (m2) atomicAdd(&d.cnt[CNT_CLAMP], (unsigned long long)m2);
+        }
+    };
+
+    // ---- collide plane z (this CTA's component) ------------------------------
+    auto collide_plane = [&](int z) {
+        const bool sol = hs && solid_at<E>(s_solid, x, y, z);
+        const int cell = (z * E + y) * E + x;
+        const double* pm = psi + pidx(z - 1, 0, x, yl);
+        const double* p0 = psi + pidx(z, 0, x, yl);
+        const double* ppl = psi + pidx(z + 1, 0, x, yl);
+        constexpr int CP = PP;
+        double f[Q], rho;
+        tm_load20(tbase + uint32_t((z & 1) * T::CB), f, rho);  // warp-convergent
+        int zero_rho = 0;
+        if (!sol) {
+            // forces (engine.cpp:420-449): intra of c, inter from the other
+            // component's s1 (the same sum as its intra s1)
+            double s1[3], s2[3];
+            sc_sums<PW, true>(pm + c * CP, p0 + c * CP, ppl + c * CP, s1, s2);
+            const CompConst& kc = P.comp[c];
+            const double c1 = kc.c1f * p0[c * CP];
+            double F0 = 0.0, F1 = 0.0, F2 = 0.0;
+            double u0 = 0.0, u1 = 0.0, u2 = 0.0;
+            if (mode == MODE_PULL) velocity(f, rho, u0, u1, u2);
+            else gen_u<E>(mode, c, s_tc, x, y, z, u0, u1, u2);
+            if (kc.has_gravity) {
+                F0 = rho * kc.gravity[0];
+                F1 = rho * kc.gravity[1];
+                F2 = rho * kc.gravity[2];
+            }
+            F0 += c1 * s1[0] + kc.c2 * s2[0];
+            F1 += c1 * s1[1] + kc.c2 * s2[1];
+            F2 += c1 * s1[2] + kc.c2 * s2[2];
+#pragma unroll
+            for (int c2 = 0; c2 < C; ++c2) {  // inter_force in c2 order (C <= 2: one term)
+                if (c2 == c) continue;
+                const double g = P.coupling[c * C + c2];
+                if (g == 0.0) continue;
+                double t[3];
+                sc_sums<PW, false>(pm + c2 * CP, p0 + c2 * CP, ppl + c2 * CP, t, nullptr);
+                const double cc = (-g) * p0[c * CP];
+                F0 += cc * t[0];
+                F1 += cc * t[1];
+                F2 += cc * t[2];
+            }
+            if (write_uface) {
+#pragma unroll 1
+                for (int face = 0; face < 6; ++face) {
+                    const int axis = face >> 1;
+                    const int coord = axis == 0 ? x : (axis == 1 ? y : z);
+                    if (coord != ((face & 1) ? E - 1 : 0) || rt_psi.s[face_pattern(face)] != amb) continue;
+                    double* uf = d.u_face + ((size_t(li) * C + c) * 6 + face) * 3 * E2;
+                    const int fi = face_index<E>(face, x, y, z);
+                    uf[fi] = u0;
+                    uf[E2 + fi] = u1;
+                    uf[2 * E2 + fi] = u2;
+                }
+            }
+            if (d.capture) {
+                double* cp = d.capture + (size_t(li) * C + c) * 4 * E3;
+                cp[cell] = p0[c * CP];
+                cp[E3 + cell] = u0;
+                cp[2 * E3 + cell] = u1;
+                cp[3 * E3 + cell] = u2;
+            }
+            collide_bgk(f, rho, u0, u1, u2, F0, F1, F2, kc.omega, fo + cell, size_t(E3), zero_rho);
+        }
+        const unsigned zr = __reduce_add_sync(0xffffffffu, (unsigned)zero_rho);
+        if ((tid & 31) == 0 && zr) atomicAdd(&d.cnt[CNT_ZERO_RHO], (unsigned long long)zr);
+    };
+
+    // ---- pipeline -------------------------------------------------------------
+    issue_pulls(0);
+    issue_ring(0);
+    cp_async_commit();
+    fill_zghost(-1);
+    expect(0);
+    cp_async_wait<0>();
+    __syncthreads();
+    psi_pass(0);
+    issue_pulls(1);
+    cp_async_commit();
+    __syncthreads();
+    issue_ring(1);
+    cp_async_commit();
+    wait_pushed(0);
+#pragma unroll 1
+    for (int z = 0; z < E; ++z) {
+        if (z + 1 < E) {
+            expect(z + 1);
+            cp_async_wait<0>();  // pulls and ghost ring of plane z+1 have landed
+            psi_pass(z + 1);
+            issue_pulls(z + 2);  // this thread's landing slots were just read
+            cp_async_commit();
+        } else {
+            fill_zghost(E);
+        }
+        __syncthreads();  // psi plane z+1 visible; every warp is past collide(z-1)
+        issue_ring(z + 2);  // ring slot of plane z-2 is free now
+        cp_async_commit();
+        if (z + 1 < E) wait_pushed(z + 1);
+        collide_plane(z);
+    }
+    cp_async_wait<0>();
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if constexpr (T::CL > 1) {  // every push into a peer has landed before anyone exits
+        asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    }
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(s_tmem),
+                     "n"(T::NCOLS));
+}
+
+}  // namespace plbm

@@ -33,14 +33,14 @@ struct TmCfg {
     static constexpr int NT = 256;
     static constexpr int BY = NT / E;            // rows per CTA
     static constexpr int NB = E / BY;            // CTAs per tile = cluster size
-    static constexpr int CB = 40;                // TMEM columns per component (38 used)
+    static constexpr int CB = 40;                // TMEM columns per component: 19 f + rho
     static constexpr int NCOLS = 256;            // per CTA; two CTAs per SM
     static constexpr int HALF = NCOLS / 2;       // per warp (two warps per lane quarter)
     static constexpr int PW = E + 2;             // psi plane row pitch (x + ring)
     static constexpr int PH = BY + 2;
     static constexpr int PP = PW * PH;
     static constexpr int PSI_BYTES = 4 * C * PP * 8;
-    static constexpr int STAGE_BYTES = Q * C * NT * 8;
+    static constexpr int STAGE_BYTES = (Q + 1) * C * NT * 8;  // 19 f + rho
     static constexpr int SMEM = PSI_BYTES + STAGE_BYTES;
     static_assert(CB * C <= HALF, "TMEM slot does not fit");
     static_assert(2 * (SMEM + 6 * 1024) <= 228 * 1024, "two CTAs per SM must fit");
@@ -50,119 +50,132 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// 19 doubles = 38 TMEM columns of this thread's lane, written as 32x32b
-// x8,x8,x8,x8,x4,x2 chunks at offsets aligned to the chunk width (each
-// component block starts on an 8-column boundary: CB = 40 columns).
-#define PLBM_TM_ST8(A, R, o)                                                                     \
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" \
-                 ::"r"(A), "r"(R[o]), "r"(R[o + 1]), "r"(R[o + 2]), "r"(R[o + 3]), "r"(R[o + 4]), \
-                 "r"(R[o + 5]), "r"(R[o + 6]), "r"(R[o + 7]))
-#define PLBM_TM_LD8(A, R, o)                                                                     \
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n" \
-                 : "=r"(R[o]), "=r"(R[o + 1]), "=r"(R[o + 2]), "=r"(R[o + 3]), "=r"(R[o + 4]),    \
-                   "=r"(R[o + 5]), "=r"(R[o + 6]), "=r"(R[o + 7])                                 \
-                 : "r"(A))
-
-__device__ __forceinline__ void tm_store19(uint32_t taddr, const double* f) {
-    uint32_t r[38];
+// 19 populations + rho = 40 TMEM columns of this thread's lane, written as
+// one 32x32b.x32 and one .x8 chunk (each component block starts on an
+// 8-column boundary: CB = 40 columns).
+__device__ __forceinline__ void tm_store20(uint32_t taddr, const double* f, double rho) {
+    uint32_t r[40];
 #pragma unroll
     for (int i = 0; i < 19; ++i) {
         r[2 * i] = uint32_t(__double2loint(f[i]));
         r[2 * i + 1] = uint32_t(__double2hiint(f[i]));
     }
-    PLBM_TM_ST8(taddr, r, 0);
-    PLBM_TM_ST8(taddr + 8, r, 8);
-    PLBM_TM_ST8(taddr + 16, r, 16);
-    PLBM_TM_ST8(taddr + 24, r, 24);
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(taddr + 32),
-                 "r"(r[32]), "r"(r[33]), "r"(r[34]), "r"(r[35]));
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(taddr + 36),
-                 "r"(r[36]), "r"(r[37]));
+    r[38] = uint32_t(__double2loint(rho));
+    r[39] = uint32_t(__double2hiint(rho));
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
+        "%29, %30, %31, %32};\n" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+        "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]),
+        "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(
+                     taddr + 32),
+                 "r"(r[32]), "r"(r[33]), "r"(r[34]), "r"(r[35]), "r"(r[36]), "r"(r[37]), "r"(r[38]),
+                 "r"(r[39]));
 }
 
-__device__ __forceinline__ void tm_load19(uint32_t taddr, double* f) {
-    uint32_t r[38];
-    PLBM_TM_LD8(taddr, r, 0);
-    PLBM_TM_LD8(taddr + 8, r, 8);
-    PLBM_TM_LD8(taddr + 16, r, 16);
-    PLBM_TM_LD8(taddr + 24, r, 24);
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
-                 : "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35])
+__device__ __forceinline__ void tm_load20(uint32_t taddr, double* f, double& rho) {
+    uint32_t r[40];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+        "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+        "%30, %31}, [%32];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+          "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+          "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                 : "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]),
+                   "=r"(r[38]), "=r"(r[39])
                  : "r"(taddr + 32));
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];\n"
-                 : "=r"(r[36]), "=r"(r[37])
-                 : "r"(taddr + 36));
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 19; ++i) f[i] = __hiloint2double(int(r[2 * i + 1]), int(r[2 * i]));
+    rho = __hiloint2double(int(r[39]), int(r[38]));
 }
 
-// One component's collision at one cell (engine.cpp:420-476): gravity +
-// intra + inter force, then BGK with the velocity-shift forcing.  pm0/p00/pp0
-// point at this cell's psi in planes z-1, z, z+1 for component 0; component k
-// is CP doubles further.
+// Shan-Chen sums of component k over the 18 neighbours (physics.cpp:44-78):
+// s1 = sum (w psi_n) e_i, s2 = sum ((w psi_n) psi_n) e_i, in i order with the
+// zero-e terms folded.  inter_force's sum for (c <- k) is the same expression
+// in the same order as intra_force's s1 of k, so it is computed once per k and
+// shared (bit-identical).  pl[dz+1] points at this cell's psi of component k
+// in planes z-1, z, z+1.
+template <int PW, bool S2>
+__device__ __forceinline__ void sc_sums(const double* pm, const double* p0, const double* pp,
+                                        double* s1, double* s2) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0;
+#pragma unroll
+    for (int i = 1; i < Q; ++i) {
+        const int dx = ex_(i), dy = ey_(i), dz = ez_(i);
+        const double* pl = dz < 0 ? pm : (dz > 0 ? pp : p0);
+        const double pn = pl[dx + PW * dy];
+        const double t1 = w_(i) * pn;
+        if (dx > 0) a0 += t1;
+        if (dx < 0) a0 -= t1;
+        if (dy > 0) a1 += t1;
+        if (dy < 0) a1 -= t1;
+        if (dz > 0) a2 += t1;
+        if (dz < 0) a2 -= t1;
+        if constexpr (S2) {
+            const double t2 = t1 * pn;
+            if (dx > 0) b0 += t2;
+            if (dx < 0) b0 -= t2;
+            if (dy > 0) b1 += t2;
+            if (dy < 0) b1 -= t2;
+            if (dz > 0) b2 += t2;
+            if (dz < 0) b2 -= t2;
+        }
+    }
+    s1[0] = a0; s1[1] = a1; s1[2] = a2;
+    if constexpr (S2) { s2[0] = b0; s2[1] = b1; s2[2] = b2; }
+}
+
+// Force of every component at one cell, without gravity (engine.cpp:420-449):
+// Fi[c] = intra_force, Fx[c] = the inter_force term (C <= 2: at most one).  Gravity
+// (the first term of the reference's sum) is added by the caller, so the
+// accumulation order stays ((rho g + Fi) + Fx_c2...).
 template <int C, int PW, int CP>
-__device__ __forceinline__ void collide_comp(const double* f, double rho, double u0, double u1,
-                                             double u2, int c, const double* pm0,
-                                             const double* p00, const double* pp0,
-                                             double* out, size_t dstride, int& zero_rho) {
-    const double* pm_c = pm0 + c * CP;
-    const double* p0_c = p00 + c * CP;
-    const double* pp_c = pp0 + c * CP;
-    const CompConst& kc = P.comp[c];
-    double F0 = 0.0, F1 = 0.0, F2 = 0.0;
-    if (kc.has_gravity) {
-        F0 = rho * kc.gravity[0];
-        F1 = rho * kc.gravity[1];
-        F2 = rho * kc.gravity[2];
-    }
-    {  // intra_force, proj/src/physics.cpp:44-63
-        double s10 = 0.0, s11 = 0.0, s12 = 0.0, s20 = 0.0, s21 = 0.0, s22 = 0.0;
+__device__ __forceinline__ void forces_all(const double* pm0, const double* p00, const double* pp0,
+                                           double (&Fi)[C][3], double (&Fx)[C][3], bool (&has_x)[C]) {
+    static_assert(C <= 2, "k_main_tm handles one or two components");
+    double s1[C][3];
 #pragma unroll
-        for (int i = 1; i < Q; ++i) {
-            const int dx = ex_(i), dy = ey_(i), dz = ez_(i);
-            const double* pl = dz < 0 ? pm_c : (dz > 0 ? pp_c : p0_c);
-            const double pn = pl[dx + PW * dy];
-            const double a1 = w_(i) * pn;
-            const double a2 = a1 * pn;
-            if (dx > 0) { s10 += a1; s20 += a2; }
-            if (dx < 0) { s10 -= a1; s20 -= a2; }
-            if (dy > 0) { s11 += a1; s21 += a2; }
-            if (dy < 0) { s11 -= a1; s21 -= a2; }
-            if (dz > 0) { s12 += a1; s22 += a2; }
-            if (dz < 0) { s12 -= a1; s22 -= a2; }
+    for (int k = 0; k < C; ++k) {
+        double s2[3];
+        sc_sums<PW, true>(pm0 + k * CP, p00 + k * CP, pp0 + k * CP, s1[k], s2);
+        const double c1 = P.comp[k].c1f * p00[k * CP];
+        const double c2 = P.comp[k].c2;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) Fi[k][a] = c1 * s1[k][a] + c2 * s2[a];
+    }
+    // C <= 2: at most one coupling term per component
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        has_x[c] = false;
+        Fx[c][0] = Fx[c][1] = Fx[c][2] = 0.0;
+        if constexpr (C == 2) {
+            const int k = 1 - c;
+            const double g = P.coupling[c * C + k];
+            if (g != 0.0) {
+                const double cc = (-g) * p00[c * CP];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) Fx[c][a] = cc * s1[k][a];
+                has_x[c] = true;
+            }
         }
-        const double c1 = kc.c1f * p0_c[0];
-        const double c2 = kc.c2;
-        F0 += c1 * s10 + c2 * s20;
-        F1 += c1 * s11 + c2 * s21;
-        F2 += c1 * s12 + c2 * s22;
     }
-#pragma unroll
-    for (int c2i = 0; c2i < C; ++c2i) {  // inter_force, proj/src/physics.cpp:65-78
-        if (c2i == c) continue;
-        const double g = P.coupling[c * C + c2i];
-        if (g == 0.0) continue;
-        double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-#pragma unroll
-        for (int i = 1; i < Q; ++i) {
-            const int dx = ex_(i), dy = ey_(i), dz = ez_(i);
-            const double* pl = (dz < 0 ? pm0 : (dz > 0 ? pp0 : p00)) + c2i * CP;
-            const double a1 = w_(i) * pl[dx + PW * dy];
-            if (dx > 0) t0 += a1;
-            if (dx < 0) t0 -= a1;
-            if (dy > 0) t1 += a1;
-            if (dy < 0) t1 -= a1;
-            if (dz > 0) t2 += a1;
-            if (dz < 0) t2 -= a1;
-        }
-        const double cc = (-g) * p0_c[0];
-        F0 += cc * t0;
-        F1 += cc * t1;
-        F2 += cc * t2;
-    }
-    // ---- collision (engine.cpp:450-475)
-    const double om = kc.omega;
+}
+
+// One component's BGK collision with the velocity-shift forcing
+// (engine.cpp:450-475) given the total force F.
+__device__ __forceinline__ void collide_bgk(const double* f, double rho, double u0, double u1,
+                                            double u2, double F0, double F1, double F2,
+                                            double om, double* out, size_t dstride,
+                                            int& zero_rho) {
     const double uu = u0 * u0 + u1 * u1 + u2 * u2;
     const double t3 = (0.5 * uu) * 3.0;
     const double wr0 = PLBM_W0 * rho, wr1 = PLBM_W1 * rho, wr2 = PLBM_W2 * rho;
@@ -205,6 +218,28 @@ __device__ __forceinline__ void collide_comp(const double* f, double rho, double
     }
 }
 
+// Momentum by sequential sums (kernels.hpp:31-48) and u = m / rho, with rho
+// the P1 density of the same populations (same sum, same order).
+__device__ __forceinline__ void velocity(const double* f, double r, double& u0, double& u1,
+                                         double& u2) {
+    double m0 = 0.0;
+    m0 += f[1]; m0 -= f[2]; m0 += f[7]; m0 -= f[8]; m0 += f[9]; m0 -= f[10];
+    m0 += f[11]; m0 -= f[12]; m0 += f[13]; m0 -= f[14];
+    double m1 = 0.0;
+    m1 += f[3]; m1 -= f[4]; m1 += f[7]; m1 -= f[8]; m1 -= f[9]; m1 += f[10];
+    m1 += f[15]; m1 -= f[16]; m1 += f[17]; m1 -= f[18];
+    double m2 = 0.0;
+    m2 += f[5]; m2 -= f[6]; m2 += f[11]; m2 -= f[12]; m2 -= f[13]; m2 += f[14];
+    m2 += f[15]; m2 -= f[16]; m2 -= f[17]; m2 += f[18];
+    if (r != 0.0) {
+        u0 = m0 / r;
+        u1 = m1 / r;
+        u2 = m2 / r;
+    } else {
+        u0 = u1 = u2 = 0.0;
+    }
+}
+
 // Seed / ambient velocity of a GEN-mode cell (the u the reference holds
 // before a tile's first collision).
 template <int E>
@@ -220,7 +255,14 @@ __device__ __forceinline__ void gen_u(int mode, int c, const int* tc, int x, int
     }
 }
 
-template <int E, int C>
+// OPT bits (A/B variants, all bit-identical)
+constexpr int TM_ILV = 1;  // psi pass: all components' loads in flight together
+constexpr int TM_PF = 2;   // bulk L2 prefetch of the next psi pass's source rows
+constexpr int TM_WSYNC = 4; // per-warp neighbour sync (mbarriers) instead of a CTA barrier per plane
+constexpr int TM_MEMONLY = 8; // measurement only (NOT the physics): same loads, stash and stores, no FP64 work
+constexpr int TM_DEFAULT_OPT = 0;
+
+template <int E, int C, int OPT>
 __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict__ active,
                                                     int src_buf, int write_uface, long iter) {
     using T = TmCfg<E, C>;
@@ -231,12 +273,15 @@ __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict
     static_assert(NB == 1 || BY * E == NT, "one warp per block row");
     extern __shared__ __align__(16) double smem[];
     double* psi = smem;                 // [4][C][PH][PW] ring of psi planes
-    double* stage = smem + 4 * C * PP;  // [C][Q][NT] odd-plane stash
+    double* stage = smem + 4 * C * PP;  // [C][Q+1][NT] odd-plane stash (19 f + rho)
     __shared__ RouteTab rt_pull, rt_psi;
     __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
     __shared__ int s_tc[3];
     __shared__ uint32_t s_tmem;
-    __shared__ __align__(8) uint64_t s_mbar[2];  // psi-row arrival, by plane parity
+    // pushed psi rows by plane parity: [0..1] row -1 (from the -y peer, read by
+    // block row 0), [2..3] row BY (from the +y peer, read by block row BY-1)
+    __shared__ __align__(8) uint64_t s_mbar[4];
+    __shared__ __align__(8) uint64_t s_wbar[2][NT / 32];  // TM_WSYNC: warp w's plane is ready
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -263,8 +308,11 @@ __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict
     if (hs)
         for (int k = tid; k < d.solid_words; k += NT) s_solid[k] = d.solid[size_t(slot) * d.solid_words + k];
     if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&s_mbar[0])), "r"(1));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&s_mbar[1])), "r"(1));
+        for (int k = 0; k < 4; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&s_mbar[k])), "r"(1));
+        for (int k = 0; k < 2 * (NT / 32); ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&s_wbar[0][0] + k)),
+                         "r"(32));
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -291,7 +339,8 @@ __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict
     // ---- push-based psi row exchange --------------------------------------
     // Block row 0 feeds the -y neighbour's ring row BY, block row BY-1 feeds
     // the +y neighbour's ring row -1: each value goes out as an 8-byte st.async
-    // that completes a transaction on the receiver's mbarrier.
+    // that completes a transaction on the receiver's mbarrier for that row.
+    // The warp that reads a pushed row also arms (expect_tx) its barrier.
     const bool push_lo = NB > 1 && yl == 0 && yb > 0;
     const bool push_hi = NB > 1 && yl == BY - 1 && yb < NB - 1;
     uint32_t peer_psi = 0, peer_mbar = 0;
@@ -300,9 +349,9 @@ __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict
         asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(peer_psi) : "r"(smem_u32(psi)), "r"(nb));
         asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n"
                      : "=r"(peer_mbar)
-                     : "r"(smem_u32(&s_mbar[0])), "r"(nb));
+                     : "r"(smem_u32(&s_mbar[push_lo ? 2 : 0])), "r"(nb));
     }
-    const uint32_t rows_bytes = uint32_t(((yb > 0) + (yb < NB - 1)) * E * C * 8);
+    constexpr uint32_t ROW_BYTES = uint32_t(E * C * 8);
     auto push_row = [&](int pz, int c, double v) {
         if (!(push_lo || push_hi)) return;
         const int idx = pidx(pz & 3, c, x, push_lo ? BY : -1);
@@ -312,18 +361,20 @@ __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict
             "l"(__double_as_longlong(v)), "r"(peer_mbar + uint32_t((pz & 1) * 8))
             : "memory");
     };
+    // only the rows that read a pushed ring row arm and wait for it (E = 32:
+    // one warp per row, so this is warp-uniform)
+    const bool needs_rows = NB > 1 && ((yl == 0 && yb > 0) || (yl == BY - 1 && yb < NB - 1));
+    const uint32_t my_mbar = smem_u32(&s_mbar[yl == 0 ? 0 : 2]);
     auto expect_rows = [&](int pz) {
-        if (NB > 1 && tid == 0)
+        if (needs_rows && (tid & 31) == 0)
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
-                             smem_u32(&s_mbar[pz & 1])),
-                         "r"(rows_bytes)
+                             my_mbar + uint32_t((pz & 1) * 8)),
+                         "r"(ROW_BYTES)
                          : "memory");
     };
-    // only the rows that read a pushed ring row wait for it
-    const bool needs_rows = NB > 1 && ((yl == 0 && yb > 0) || (yl == BY - 1 && yb < NB - 1));
     auto wait_rows = [&](int pz) {
         if (!needs_rows) return;
-        const uint32_t bar = smem_u32(&s_mbar[pz & 1]);
+        const uint32_t bar = my_mbar + uint32_t((pz & 1) * 8);
         const uint32_t parity = uint32_t((pz >> 1) & 1);
         uint32_t ok = 0;
         while (!ok)
@@ -367,34 +418,80 @@ __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict
         }
     };
 
+    // TM_WSYNC: the x-ring entries of this warp's rows, and the halo row next
+    // to a block edge (whole row at a tile edge, else only its two x-ring
+    // corners: the rest is pushed by the cluster neighbour).  Everything warp
+    // w's collide reads is then produced by warps w-1, w, w+1 (or pushed).
+    constexpr int RPW = 32 / E > 0 ? 32 / E : 1;  // block rows per warp
+    auto fill_ring_w = [&](int pz) {
+        const int ring = pz & 3;
+        const int lane = tid & 31;
+        const int r0 = warp * RPW;
+        const bool lo = r0 == 0, hi = r0 + RPW == BY;
+        const bool lo_full = lo && y0 == 0, hi_full = hi && y0 + BY == E;
+        const int nlo = lo ? (lo_full ? E + 2 : 2) : 0;
+        const int nhi = hi ? (hi_full ? E + 2 : 2) : 0;
+        for (int k = lane; k < 2 * RPW + nlo + nhi; k += 32) {
+            int xx, yyl;
+            if (k < 2 * RPW) {
+                yyl = r0 + (k >> 1);
+                xx = (k & 1) ? E : -1;
+            } else if (k < 2 * RPW + nlo) {
+                const int q = k - 2 * RPW;
+                yyl = -1;
+                xx = lo_full ? q - 1 : ((q & 1) ? E : -1);
+            } else {
+                const int q = k - 2 * RPW - nlo;
+                yyl = BY;
+                xx = hi_full ? q - 1 : ((q & 1) ? E : -1);
+            }
+#pragma unroll 1
+            for (int c = 0; c < C; ++c)
+                psi[pidx(ring, c, xx, yyl)] = psi_ghost<E>(rt_psi, c, hs, s_solid, xx, y0 + yyl, pz);
+        }
+    };
+    auto wbar_wait = [&](int w, int z) {
+        const uint32_t bar = smem_u32(&s_wbar[z & 1][w]);
+        const uint32_t parity = uint32_t((z >> 1) & 1);
+        uint32_t ok = 0;
+        while (!ok)
+            asm volatile(
+                "{\n .reg .pred q;\n mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n"
+                " selp.u32 %0, 1, 0, q;\n}\n"
+                : "=r"(ok)
+                : "r"(bar), "r"(parity)
+                : "memory");
+    };
+
     // ---- psi pass of plane pz: pull f_in, rho -> psi (P1), stash -------------
     auto psi_pass = [&](int pz) {
         const int ring = pz & 3;
         const bool sol = hs && solid_at<E>(s_solid, x, y, pz);
         int negs = 0, clamps = 0;
-#pragma unroll 1
-        for (int c = 0; c < C; ++c) {
-            double f[Q];
-            double v = 0.0;
+        auto load = [&](int c, double* f) {
             if (sol) {
 #pragma unroll
                 for (int i = 0; i < Q; ++i) f[i] = 0.0;
+            } else if (fast_rows && pz >= 1 && pz <= E - 2) {
+                pull_cell_fast<E>(rt_pull, c, x, y, pz, f);
+            } else if (mode == MODE_PULL) {
+                pull_cell<E>(rt_pull, c, hs, s_solid, x, y, pz, f);
             } else {
-                if (fast_rows && pz >= 1 && pz <= E - 2) {
-                    pull_cell_fast<E>(rt_pull, c, x, y, pz, f);
-                } else if (mode == MODE_PULL) {
-                    pull_cell<E>(rt_pull, c, hs, s_solid, x, y, pz, f);
-                } else {
-                    double a0, a1, a2;
-                    gen_fin<E>(mode, c, s_tc, x, y, pz, f, a0, a1, a2);
-                }
-                double rho = 0.0;
+                double a0, a1, a2;
+                gen_fin<E>(mode, c, s_tc, x, y, pz, f, a0, a1, a2);
+            }
+        };
+        auto finish = [&](int c, const double* f) {
+            double v = 0.0, rho = 0.0;
+            if (!sol) {
 #pragma unroll
                 for (int i = 0; i < Q; ++i) {
                     rho += f[i];
                     negs += f[i] < 0.0;
                 }
-                if (!isfinite(rho)) {
+                if constexpr ((OPT & TM_MEMONLY) != 0) {
+                    v = rho;
+                } else if (!isfinite(rho)) {
                     atomic_err(d.err, iter, tile_lin, ERR_P1_NAN);
                 } else {
                     double press;
@@ -409,12 +506,30 @@ __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict
             }
             psi[pidx(ring, c, x, yl)] = v;
             push_row(pz, c, v);
+            // the P1 density is the P5 density of the same populations (same
+            // sum, same order): stashed with them for the collision
             if ((pz & 1) == 0) {
-                tm_store19(tbase + uint32_t(c * T::CB), f);
+                tm_store20(tbase + uint32_t(c * T::CB), f, rho);
             } else {
-                double* st = stage + size_t(c) * Q * NT + tid;
+                double* st = stage + size_t(c) * (Q + 1) * NT + tid;
 #pragma unroll
                 for (int i = 0; i < Q; ++i) st[i * NT] = f[i];
+                st[Q * NT] = rho;
+            }
+        };
+        if constexpr (OPT & TM_ILV) {
+            // every component's 19 loads in flight before the first sum
+            double f[C][Q];
+#pragma unroll
+            for (int c = 0; c < C; ++c) load(c, f[c]);
+#pragma unroll
+            for (int c = 0; c < C; ++c) finish(c, f[c]);
+        } else {
+#pragma unroll 1
+            for (int c = 0; c < C; ++c) {
+                double f[Q];
+                load(c, f);
+                finish(c, f);
             }
         }
         if ((pz & 1) == 0) asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
@@ -444,24 +559,33 @@ __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict
             }
         }
         int zero_rho = 0;
-#pragma unroll 1
+        double Fi[C][3], Fx[C][3];
+        bool has_x[C];
+        if constexpr ((OPT & TM_MEMONLY) == 0) {
+            if (!sol) forces_all<C, PW, PP>(pm, p0, ppl, Fi, Fx, has_x);
+        }
+#pragma unroll
         for (int c = 0; c < C; ++c) {
-            double f[Q];
+            double f[Q], rho;
             if ((z & 1) == 0) {
-                tm_load19(tbase + uint32_t(c * T::CB), f);  // warp-convergent
+                tm_load20(tbase + uint32_t(c * T::CB), f, rho);  // warp-convergent
             } else {
-                const double* st = stage + size_t(c) * Q * NT + tid;
+                const double* st = stage + size_t(c) * (Q + 1) * NT + tid;
 #pragma unroll
                 for (int i = 0; i < Q; ++i) f[i] = st[i * NT];
+                rho = st[Q * NT];
             }
             if (sol) continue;
-            double rho, u0 = 0.0, u1 = 0.0, u2 = 0.0;
-            if (mode == MODE_PULL) {
-                moments(f, rho, u0, u1, u2);
-            } else {
-                rho = sum19(f);
-                gen_u<E>(mode, c, s_tc, x, y, z, u0, u1, u2);
+            if constexpr ((OPT & TM_MEMONLY) != 0) {
+                double* out = fo + c * size_t(Q) * E3 + cell;
+                const double ps = p0[c * PP] + pm[c * PP] + ppl[c * PP];
+#pragma unroll
+                for (int i = 0; i < Q; ++i) out[size_t(i) * E3] = f[i] + ps;
+                continue;
             }
+            double u0 = 0.0, u1 = 0.0, u2 = 0.0;
+            if (mode == MODE_PULL) velocity(f, rho, u0, u1, u2);
+            else gen_u<E>(mode, c, s_tc, x, y, z, u0, u1, u2);
             if (fmask) {
 #pragma unroll 1
                 for (int face = 0; face < 6; ++face) {
@@ -480,30 +604,89 @@ __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict
                 cp[2 * E3 + cell] = u1;
                 cp[3 * E3 + cell] = u2;
             }
+            // total force in the reference's order: gravity, intra, inter
+            const CompConst& kc = P.comp[c];
+            double F0 = 0.0, F1 = 0.0, F2 = 0.0;
+            if (kc.has_gravity) {
+                F0 = rho * kc.gravity[0];
+                F1 = rho * kc.gravity[1];
+                F2 = rho * kc.gravity[2];
+            }
+            F0 += Fi[c][0];
+            F1 += Fi[c][1];
+            F2 += Fi[c][2];
+            if (has_x[c]) {
+                F0 += Fx[c][0];
+                F1 += Fx[c][1];
+                F2 += Fx[c][2];
+            }
             double* out = fo + c * size_t(Q) * E3 + cell;
-            collide_comp<C, PW, PP>(f, rho, u0, u1, u2, c, pm, p0, ppl, out, size_t(E3), zero_rho);
+            collide_bgk(f, rho, u0, u1, u2, F0, F1, F2, kc.omega, out, size_t(E3), zero_rho);
         }
         const unsigned zr = __reduce_add_sync(0xffffffffu, (unsigned)zero_rho);
         if ((tid & 31) == 0 && zr) atomicAdd(&d.cnt[CNT_ZERO_RHO], (unsigned long long)zr);
     };
 
+    // ---- L2 prefetch of the rows the psi pass of plane pz pulls from --------
+    // One bulk prefetch per (component, direction): the source plane pz - ez_i,
+    // rows y0-1 .. y0+BY of this tile's f_post block (contiguous in SoA), so the
+    // psi pass one iteration later reads from L2 instead of waiting on DRAM.
+    auto prefetch_plane = [&](int pz) {
+        if constexpr (OPT & TM_PF) {
+            if (mode != MODE_PULL || pz >= E || tid >= C * Q) return;
+            const int c = tid / Q, i = tid - c * Q;
+            int ez = 0;
+#pragma unroll
+            for (int j = 0; j < Q; ++j)
+                if (j == i) ez = ez_(j);
+            const int sz = pz - ez;
+            if (sz < 0 || sz >= E) return;
+            const int ylo = y0 > 0 ? y0 - 1 : 0;
+            const int yhi = y0 + BY < E ? y0 + BY : E - 1;
+            const double* src = rt_pull.p[13] + (size_t(c) * Q + i) * E3 + size_t(sz * E + ylo) * E;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src),
+                         "r"(uint32_t((yhi - ylo + 1) * E * 8))
+                         : "memory");
+        }
+    };
+
+    prefetch_plane(1);
+    constexpr bool WS = (OPT & TM_WSYNC) != 0;
     fill_zghost(-1);
     expect_rows(0);
     psi_pass(0);
-    fill_ring(0);
+    if (WS) fill_ring_w(0);
+    else fill_ring(0);
     __syncthreads();
     wait_rows(0);
 #pragma unroll 1
     for (int z = 0; z < E; ++z) {
+        prefetch_plane(z + 2);
         if (z + 1 < E) {
             expect_rows(z + 1);
             psi_pass(z + 1);
-            fill_ring(z + 1);
+            if constexpr (WS) {
+                // plane z+1 of this warp's rows is in the ring: publish it, then
+                // wait only for the two neighbouring warps (no CTA barrier)
+                fill_ring_w(z + 1);
+                __syncwarp();
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(
+                                 smem_u32(&s_wbar[z & 1][warp]))
+                             : "memory");
+                if (warp > 0) wbar_wait(warp - 1, z);
+                if (warp + 1 < NT / 32) wbar_wait(warp + 1, z);
+            } else {
+                fill_ring(z + 1);
+                __syncthreads();
+            }
+            wait_rows(z + 1);
         } else {
+            // fill_zghost(E) overwrites the ring slot of plane E-4 for every row:
+            // all warps must be past collide(E-3) first
+            if constexpr (WS) __syncthreads();
             fill_zghost(E);
+            __syncthreads();
         }
-        __syncthreads();
-        if (z + 1 < E) wait_rows(z + 1);
         collide_plane(z);
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
