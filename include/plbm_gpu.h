@@ -78,12 +78,18 @@ typedef struct plbm_kernel_stats {
 void plbm_gpu_kernel_stats(void* h, plbm_kernel_stats* out);
 void plbm_gpu_reset_kernel_stats(void* h);
 
-/* Fused-kernel variant (A/B measurement; both are bit-identical):
- *   0 = TMEM + smem alternating stash, 4-CTA cluster, psi rows pushed with
- *       st.async + mbarrier (default where it applies: E in {16,32}, C <= 2,
- *       a psi stencil)
- *   1 = plain kernel that pulls every population twice (always used for
- *       E = 8 and psi-free scenarios)                                        */
+/* Fused-kernel variant (A/B measurement; all are bit-identical):
+ *   0  = default: k_main_pc where it applies (E in {16,32}, C <= 2, a psi
+ *        stencil), else k_main_tm, else the plain kernel
+ *   1  = plain kernel that pulls every population twice (always used for
+ *        E = 8, C = 3 and psi-free scenarios)
+ *   2  = k_main_tm: both components per thread, TMEM + smem two-plane stash,
+ *        synchronous pulls (the previous default)
+ *   10 = k_main_tm memory-only probe: same loads/stash/stores, no physics
+ *        (measurement only; NOT a valid step)
+ *   21 = k_main_pc: one CTA per (y-block, component) in a cluster, pulls
+ *        staged by cp.async one plane ahead, TMEM two-plane stash
+ *   22 = k_main_pc with psi computed two planes ahead (three TMEM slots)     */
 int plbm_gpu_set_kernel_variant(void* h, int variant);
 
 /* The engine's CUDA stream (cudaStream_t) for callers that time with events. */

@@ -100,8 +100,8 @@ struct Kernels {
     MainFn main_plain;  // variant 1 (and the only kernel for E = 8 / psi-free)
     MainFn main_tm;     // variant 0: TMEM/smem stash, 4-CTA cluster (default OPT)
     MainFn main_tm_opt[16]; // variant 2 + OPT: the same kernel with OPT bits (A/B)
-    MainFn main_as;     // variant 20: cp.async-staged pulls + TMEM two-plane stash
     MainFn main_pc;     // variant 21: one CTA per (block, component), cp.async staged
+    MainFn main_pc2;    // variant 22: as 21 with psi computed two planes ahead
     void (*face)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
     void (*readback)(Dev, int, int, int, double*, cudaStream_t);
     int nt;
@@ -125,27 +125,9 @@ void launch_tm(Dev d, const int* act, int src, int wu, long it, unsigned ntiles,
     cudaLaunchKernelEx(&cfg, k_main_tm<E, C, OPT>, d, act, src, wu, it);
 }
 
-template <int E, int C>
-void launch_as(Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
-    using T = AsCfg<E, C>;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ntiles * T::NB);
-    cfg.blockDim = dim3(T::NT);
-    cfg.dynamicSmemBytes = T::SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = T::NB;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_main_as<E, C>, d, act, src, wu, it);
-}
-
-template <int E, int C>
+template <int E, int C, int LAG>
 void launch_pc(Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
-    using T = PcCfg<E, C>;
+    using T = PcCfg<E, C, LAG>;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ntiles * T::CL);
     cfg.blockDim = dim3(T::NT);
@@ -158,7 +140,7 @@ void launch_pc(Dev d, const int* act, int src, int wu, long it, unsigned ntiles,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_main_pc<E, C>, d, act, src, wu, it);
+    cudaLaunchKernelEx(&cfg, k_main_pc<E, C, LAG>, d, act, src, wu, it);
 }
 
 template <int E, int C, int OPT>
@@ -182,22 +164,19 @@ Kernels make_kernels() {
         k_main<E, C, BZ, NT, NOPSI><<<ntiles * (E / BZ), NT, SMEM_PLAIN, s>>>(d, act, src, wu, it);
     };
     k.main_tm = nullptr;
-    k.main_as = k.main_pc = nullptr;
+    k.main_pc = k.main_pc2 = nullptr;
     for (auto& f : k.main_tm_opt) f = nullptr;  // OPT values not instantiated fall back
     if constexpr (!NOPSI && (E == 16 || E == 32) && C <= 2) {
         constexpr int S = TmCfg<E, C>::SMEM;
         reg_tm<E, C, 0>(k.main_tm_opt, S);
-        reg_tm<E, C, 1>(k.main_tm_opt, S);
-        reg_tm<E, C, 2>(k.main_tm_opt, S);
-        reg_tm<E, C, 4>(k.main_tm_opt, S);
         reg_tm<E, C, TM_MEMONLY>(k.main_tm_opt, S);
-        reg_tm<E, C, TM_MEMONLY | TM_ILV>(k.main_tm_opt, S);
-        reg_tm<E, C, TM_MEMONLY | TM_PF>(k.main_tm_opt, S);
         k.main_tm = k.main_tm_opt[TM_DEFAULT_OPT];
-        cudaFuncSetAttribute(k_main_as<E, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, AsCfg<E, C>::SMEM);
-        k.main_as = launch_as<E, C>;
-        cudaFuncSetAttribute(k_main_pc<E, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, PcCfg<E, C>::SMEM);
-        k.main_pc = launch_pc<E, C>;
+        cudaFuncSetAttribute(k_main_pc<E, C, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             PcCfg<E, C, 1>::SMEM);
+        cudaFuncSetAttribute(k_main_pc<E, C, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             PcCfg<E, C, 2>::SMEM);
+        k.main_pc = launch_pc<E, C, 1>;
+        k.main_pc2 = launch_pc<E, C, 2>;
     }
     k.face = [](Dev d, const int* act, int src, int flags, long it, unsigned ntiles, cudaStream_t s) {
         constexpr unsigned NCH = (E * E + NT - 1) / NT;
@@ -940,11 +919,11 @@ void Engine::launch_main(long iter) {
     if (ev) CK(cudaEventRecord(ev->a, stream_));
     const int wu = mode_ == PLBM_MODE_PROGRESSIVE ? 1 : 0;
     MainFn fn = K_.main_plain;
-    if (K_.main_tm && variant_ == 0) fn = K_.main_tm;
+    if (variant_ == 0) fn = K_.main_pc ? K_.main_pc : (K_.main_tm ? K_.main_tm : K_.main_plain);
     if (K_.main_tm && variant_ >= 2 && variant_ < 18 && K_.main_tm_opt[variant_ - 2])
         fn = K_.main_tm_opt[variant_ - 2];
-    if (K_.main_as && variant_ == 20) fn = K_.main_as;
     if (K_.main_pc && variant_ == 21) fn = K_.main_pc;
+    if (K_.main_pc2 && variant_ == 22) fn = K_.main_pc2;
     fn(d_, d_active_, cur_, wu, iter, unsigned(active_.size()), stream_);
     CK(cudaGetLastError());
     ++stats_.kernels_launched;

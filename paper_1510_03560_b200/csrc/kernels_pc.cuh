@@ -5,8 +5,9 @@
 //   * the 38 shifted SoA streams of a column block stream at the flat-copy
 //     rate when enough bytes are in flight — the access pattern is not the
 //     limit, memory-level parallelism is;
-//   * the FP64 work needs ~16 warps per SM to hide its dependency chains
-//     (k_main_as at 8 warps/SM was latency-bound on arithmetic);
+//   * the FP64 work needs ~16 warps per SM to hide its dependency chains (a
+//     cp.async-staged two-components-per-thread variant at 8 warps/SM was
+//     latency-bound on arithmetic: 4.9 ms vs 3.6 ms for k_main_tm);
 //   * at 16 warps/SM and two components per thread there is no room on chip
 //     for a landing buffer next to the two-plane stash.
 // Splitting the components over the two CTAs of a cluster pair halves the
@@ -24,11 +25,47 @@
 //               | collide z from TMEM.
 #pragma once
 
-#include "kernels_as.cuh"
+#include "kernels_tm.cuh"
 
 namespace plbm {
 
-template <int E, int C>
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// psi_ghost (kernels.cuh) split into "load this address" or "use this value".
+template <int E>
+__device__ __forceinline__ const double* psi_ghost_src(const RouteTab& rt, int c, bool hs,
+                                                       const uint32_t* sb, int x, int y, int z,
+                                                       double& val) {
+    if (hs && solid_at<E>(sb, x, y, z)) {
+        val = 0.0;
+        return nullptr;
+    }
+    const int ox = x < 0 ? -1 : (x >= E ? 1 : 0);
+    const int oy = y < 0 ? -1 : (y >= E ? 1 : 0);
+    const int oz = z < 0 ? -1 : (z >= E ? 1 : 0);
+    const int pat = (ox + 1) + 3 * (oy + 1) + 9 * (oz + 1);
+    if (rt.nb[pat]) {
+        val = P.comp[c].psi_nb;
+        return nullptr;
+    }
+    int face;
+    if (ox) face = ox > 0 ? 0 : 1;
+    else if (oy) face = oy > 0 ? 2 : 3;
+    else face = oz > 0 ? 4 : 5;
+    const int lx = x & (E - 1), ly = y & (E - 1), lz = z & (E - 1);
+    constexpr int E2 = E * E;
+    return rt.p[pat] + (size_t(c) * 6 + face) * E2 + face_index<E>(face, lx, ly, lz);
+}
+
+
+template <int E, int C, int LAG = 1>
 struct PcCfg {
     static constexpr int NT = 256;
     static constexpr int BY = NT / E;   // rows per CTA
@@ -39,19 +76,25 @@ struct PcCfg {
     static constexpr int PW = E + 2;
     static constexpr int PH = BY + 2;
     static constexpr int PP = PW * PH;
-    static constexpr int RING = 4;
+    static constexpr int RING = LAG == 1 ? 4 : 8;  // psi planes z-2 .. z+LAG+1 live
+    static constexpr int NMB = 2 * LAG;             // pushed-plane mbarriers
+    static constexpr int TSLOTS = LAG + 1;          // TMEM plane slots
     static constexpr int PSI_BYTES = RING * C * PP * 8;
     static constexpr int LAND_BYTES = Q * NT * 8;
     static constexpr int SMEM = PSI_BYTES + LAND_BYTES;
     static_assert(CL <= 8, "portable cluster size");
-    static_assert(2 * CB <= NCOLS / 2, "TMEM plane slots do not fit");
+    static_assert(TSLOTS * CB <= NCOLS / 2, "TMEM plane slots do not fit");
     static_assert(2 * (SMEM + 8 * 1024) <= 228 * 1024, "two CTAs per SM must fit");
 };
 
-template <int E, int C>
+// LAG = planes between a plane's psi pass and its collision: 1 (psi of z+1
+// is computed and pushed in the iteration that collides z) or 2 (pushed one
+// iteration before it is needed, three TMEM plane slots).
+template <int E, int C, int LAG>
 __global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict__ active,
                                                     int src_buf, int write_uface, long iter) {
-    using T = PcCfg<E, C>;
+    using T = PcCfg<E, C, LAG>;
+    constexpr int NMB = T::NMB;
     constexpr int NT = T::NT, BY = T::BY, NB = T::NB, PW = T::PW, PH = T::PH, PP = T::PP;
     constexpr int R = T::RING;
     constexpr int G = E + 2;
@@ -64,7 +107,7 @@ __global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict
     __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
     __shared__ int s_tc[3];
     __shared__ uint32_t s_tmem;
-    __shared__ __align__(8) uint64_t s_mbar[2];  // pushed psi of plane p, by parity
+    __shared__ __align__(8) uint64_t s_mbar[T::NMB];  // pushed psi of plane p: slot p % NMB
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -93,8 +136,8 @@ __global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict
     if (hs)
         for (int k = tid; k < d.solid_words; k += NT) s_solid[k] = d.solid[size_t(slot) * d.solid_words + k];
     if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&s_mbar[0])), "r"(1));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&s_mbar[1])), "r"(1));
+        for (int k = 0; k < NMB; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&s_mbar[k])), "r"(1));
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -116,6 +159,17 @@ __global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict
         return (((pz & (R - 1)) * C + cc) * PH + (yy_local + 1)) * PW + (xx + 1);
     };
     const uint32_t land_u32 = smem_u32(land);
+    // frontier faces this cell's column lies on (criterion u_prev, u_face):
+    // x/y faces are fixed per thread, z faces apply to the first/last plane
+    unsigned xy_fmask = 0, z_fmask = 0;
+    if (write_uface) {
+        if (x == 0 && rt_psi.s[face_pattern(0)] == amb) xy_fmask |= 1u;
+        if (x == E - 1 && rt_psi.s[face_pattern(1)] == amb) xy_fmask |= 2u;
+        if (y == 0 && rt_psi.s[face_pattern(2)] == amb) xy_fmask |= 4u;
+        if (y == E - 1 && rt_psi.s[face_pattern(3)] == amb) xy_fmask |= 8u;
+        if (rt_psi.s[face_pattern(4)] == amb) z_fmask |= 16u;
+        if (rt_psi.s[face_pattern(5)] == amb) z_fmask |= 32u;
+    }
 
     // ---- psi pushes: whole plane to the other components' CTAs of this block,
     // edge rows to every component's CTA of the adjacent y-blocks ------------
@@ -128,7 +182,7 @@ __global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict
         asm volatile(
             "st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n" ::"r"(
                 ra + uint32_t(pidx(pz, c, x, yy_local)) * 8u),
-            "l"(__double_as_longlong(v)), "r"(rb + uint32_t((pz & 1) * 8))
+            "l"(__double_as_longlong(v)), "r"(rb + uint32_t((pz & (NMB - 1)) * 8))
             : "memory");
     };
     auto push_all = [&](int pz, double v) {
@@ -145,14 +199,14 @@ __global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict
     auto expect = [&](int pz) {
         if (T::CL > 1 && tid == 0)
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
-                             mbar_u32 + uint32_t((pz & 1) * 8)),
+                             mbar_u32 + uint32_t((pz & (NMB - 1)) * 8)),
                          "r"(expect_bytes)
                          : "memory");
     };
     auto wait_pushed = [&](int pz) {
         if (T::CL == 1) return;
-        const uint32_t bar = mbar_u32 + uint32_t((pz & 1) * 8);
-        const uint32_t parity = uint32_t((pz >> 1) & 1);
+        const uint32_t bar = mbar_u32 + uint32_t((pz & (NMB - 1)) * 8);
+        const uint32_t parity = uint32_t((pz / NMB) & 1);
         uint32_t ok = 0;
         while (!ok)
             asm volatile(
@@ -242,7 +296,7 @@ __global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict
         }
         psi[pidx(pz, c, x, yl)] = v;
         push_all(pz, v);
-        tm_store20(tbase + uint32_t((pz & 1) * T::CB), f, rho);
+        tm_store20(tbase + uint32_t((pz % T::TSLOTS) * T::CB), f, rho);
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         const unsigned m1 = __reduce_add_sync(0xffffffffu, (unsigned)negs);
         const unsigned m2 = __reduce_add_sync(0xffffffffu, (unsigned)clamps);
@@ -261,7 +315,7 @@ __global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict
         const double* ppl = psi + pidx(z + 1, 0, x, yl);
         constexpr int CP = PP;
         double f[Q], rho;
-        tm_load20(tbase + uint32_t((z & 1) * T::CB), f, rho);  // warp-convergent
+        tm_load20(tbase + uint32_t((z % T::TSLOTS) * T::CB), f, rho);  // warp-convergent
         int zero_rho = 0;
         if (!sol) {
             // forces (engine.cpp:420-449): intra of c, inter from the other
@@ -294,12 +348,11 @@ __global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict
                 F1 += cc * t[1];
                 F2 += cc * t[2];
             }
-            if (write_uface) {
+            const unsigned fmask = xy_fmask | (z == 0 ? z_fmask & 16u : 0u) | (z == E - 1 ? z_fmask & 32u : 0u);
+            if (fmask) {
 #pragma unroll 1
                 for (int face = 0; face < 6; ++face) {
-                    const int axis = face >> 1;
-                    const int coord = axis == 0 ? x : (axis == 1 ? y : z);
-                    if (coord != ((face & 1) ? E - 1 : 0) || rt_psi.s[face_pattern(face)] != amb) continue;
+                    if (!(fmask & (1u << face))) continue;
                     double* uf = d.u_face + ((size_t(li) * C + c) * 6 + face) * 3 * E2;
                     const int fi = face_index<E>(face, x, y, z);
                     uf[fi] = u0;
@@ -321,35 +374,40 @@ __global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict
     };
 
     // ---- pipeline -------------------------------------------------------------
-    issue_pulls(0);
-    issue_ring(0);
-    cp_async_commit();
     fill_zghost(-1);
-    expect(0);
-    cp_async_wait<0>();
-    __syncthreads();
-    psi_pass(0);
-    issue_pulls(1);
+#pragma unroll 1
+    for (int p = 0; p < LAG; ++p) {
+        issue_pulls(p);
+        issue_ring(p);
+        cp_async_commit();
+        expect(p);
+        cp_async_wait<0>();
+        __syncthreads();
+        psi_pass(p);
+    }
+    issue_pulls(LAG);
     cp_async_commit();
     __syncthreads();
-    issue_ring(1);
+    issue_ring(LAG);
     cp_async_commit();
-    wait_pushed(0);
+#pragma unroll 1
+    for (int p = 0; p < LAG; ++p) wait_pushed(p);
 #pragma unroll 1
     for (int z = 0; z < E; ++z) {
-        if (z + 1 < E) {
-            expect(z + 1);
-            cp_async_wait<0>();  // pulls and ghost ring of plane z+1 have landed
-            psi_pass(z + 1);
-            issue_pulls(z + 2);  // this thread's landing slots were just read
+        const int pn = z + LAG;
+        if (pn < E) {
+            expect(pn);
+            cp_async_wait<0>();  // pulls and ghost ring of plane pn have landed
+            psi_pass(pn);
+            issue_pulls(pn + 1);  // this thread's landing slots were just read
             cp_async_commit();
-        } else {
+        } else if (pn == E) {
             fill_zghost(E);
         }
-        __syncthreads();  // psi plane z+1 visible; every warp is past collide(z-1)
-        issue_ring(z + 2);  // ring slot of plane z-2 is free now
+        __syncthreads();  // psi plane pn visible; every warp is past collide(z-1)
+        issue_ring(pn + 1);  // its ring slot is no longer read by anyone
         cp_async_commit();
-        if (z + 1 < E) wait_pushed(z + 1);
+        if (z + 1 < E && z + 1 >= LAG) wait_pushed(z + 1);
         collide_plane(z);
     }
     cp_async_wait<0>();

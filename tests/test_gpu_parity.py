@@ -11,7 +11,7 @@ from tests.compare import assert_same_state
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("variant", [0, 1, 21], ids=["tmem", "plain", "percomp"])
+@pytest.mark.parametrize("variant", [0, 1, 2, 22], ids=["default_percomp", "plain", "tmem_both_comps", "percomp_lag2"])
 @pytest.mark.parametrize("name", sorted(scenarios.ALL))
 def test_gpu_matches_oracle(built, name, variant):
     make, steps = scenarios.ALL[name]
