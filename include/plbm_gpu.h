@@ -89,7 +89,11 @@ void plbm_gpu_reset_kernel_stats(void* h);
  *        (measurement only; NOT a valid step)
  *   21 = k_main_pc: one CTA per (y-block, component) in a cluster, pulls
  *        staged by cp.async one plane ahead, TMEM two-plane stash
- *   22 = k_main_pc with psi computed two planes ahead (three TMEM slots)     */
+ *   22 = k_main_pc with psi computed two planes ahead (three TMEM slots)
+ * Modifiers (added to the variant): +100 = run the face pass in the k_main_pc
+ * tail ("last arriver" dependency counting, single rank) instead of a k_face
+ * launch; +200 = face pass reads the x faces from the SoA block instead of the
+ * xcol side buffers.                                                          */
 int plbm_gpu_set_kernel_variant(void* h, int variant);
 
 /* The engine's CUDA stream (cudaStream_t) for callers that time with events. */

@@ -179,8 +179,7 @@ Kernels make_kernels() {
         k.main_pc2 = launch_pc<E, C, 2>;
     }
     k.face = [](Dev d, const int* act, int src, int flags, long it, unsigned ntiles, cudaStream_t s) {
-        constexpr unsigned NCH = (E * E + NT - 1) / NT;
-        k_face<E, C, NT><<<ntiles * 6 * NCH, NT, 0, s>>>(d, act, src, flags, it);
+        k_face<E, C, NT><<<ntiles * 6, NT, 0, s>>>(d, act, src, flags, it);
     };
     k.readback = [](Dev d, int slot, int c, int src, double* out, cudaStream_t s) {
         k_readback<E><<<(E * E * E + 255) / 256, 256, 0, s>>>(d, slot, c, src, out);
@@ -258,7 +257,11 @@ class Engine {
     int set_capture(bool on);
     int poke_f(const int32_t* coords, int comp, int i, const int32_t* local, double v);
     void set_profiling(bool on) { profiling_ = on; }
-    void set_variant(int v) { variant_ = v; }
+    void set_variant(int v) {
+        variant_ = v % 100;
+        fuse_ = (v / 100) & 1;     // +100: face pass in the fused kernel's tail (A/B)
+        no_xcol_ = (v / 200) & 1;  // +200: face pass reads x faces from the SoA block
+    }
     plbm_kernel_stats stats();
     void reset_stats() {
         resolve_events();
@@ -342,6 +345,10 @@ class Engine {
     int* d_coords_ = nullptr;
     double* d_u_face_ = nullptr;
     uint8_t* d_trig_ = nullptr;
+    int* d_dep_cnt_ = nullptr;   // fused face pass: per-slot completion counts
+    int* d_dep_need_ = nullptr;  // 1 + active geometric neighbours
+    int* d_geo_ = nullptr;       // [slot][18] active geometric neighbour or -1
+    bool face_fused_ = false;    // the last k_main ran the face pass itself
     double* d_capture_ = nullptr;
     unsigned long long* d_cnt_ = nullptr;
     unsigned long long* d_err_ = nullptr;
@@ -352,6 +359,7 @@ class Engine {
     int solid_words_ = 0;
     bool profiling_ = false;
     int variant_ = 0;
+    bool fuse_ = false, no_xcol_ = false;
     plbm_kernel_stats stats_{};
     struct EvPair {
         cudaEvent_t a = nullptr, b = nullptr;
@@ -501,7 +509,7 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
         lcap_ = std::min(int(n_tiles), owners_per_rank * tiles_per_owner);
         if (world_ == 1) lcap_ = int(n_tiles);
     }
-    per_slot_ = size_t(C_) * Q * E3_;
+    per_slot_ = size_t(C_) * Q * E3_ + size_t(C_) * XN * E2_;  // f block + xcol side buffer
     per_pf_ = size_t(C_) * 6 * E2_;
     const int nslot = cap_ + 1;
     const int G = E_ + 2;
@@ -526,6 +534,10 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     d_coords_ = dmalloc<int>(size_t(nslot) * 3);
     d_u_face_ = dmalloc<double>(size_t(lcap_ + 1) * C_ * 6 * 3 * E2_);
     d_trig_ = dmalloc<uint8_t>(trig_bytes_);
+    d_dep_cnt_ = dmalloc<int>(nslot);
+    d_dep_need_ = dmalloc<int>(nslot);
+    d_geo_ = dmalloc<int>(size_t(nslot) * 18);
+    CK(cudaMemsetAsync(d_dep_cnt_, 0, nslot * sizeof(int), stream_));
     d_cnt_ = dmalloc<unsigned long long>(CNT_N);
     d_err_ = dmalloc<unsigned long long>(1);
     d_active_ = dmalloc<int>(nslot);
@@ -541,8 +553,13 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     {
         std::vector<double> amb(per_slot_);
         for (int c = 0; c < C_; ++c)
-            for (int i = 0; i < Q; ++i)
+            for (int i = 0; i < Q; ++i) {
                 std::fill_n(amb.begin() + (size_t(c) * Q + i) * E3_, E3_, p.comp[c].feq_amb[i]);
+                for (int cls = 0; cls < 4; ++cls)
+                    if (xslot_(cls, i) >= 0)
+                        std::fill_n(amb.begin() + size_t(C_) * Q * E3_ + (size_t(c) * XN + xslot_(cls, i)) * E2_,
+                                    E2_, p.comp[c].feq_amb[i]);
+            }
         std::vector<double> pf(per_pf_);
         for (int c = 0; c < C_; ++c)
             std::fill_n(pf.begin() + size_t(c) * 6 * E2_, 6 * E2_, p.comp[c].psi_amb);
@@ -575,6 +592,11 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     d_.cnt = d_cnt_;
     d_.err = d_err_;
     d_.solid_words = solid_words_;
+    d_.dep_cnt = d_dep_cnt_;
+    d_.dep_need = d_dep_need_;
+    d_.geo = d_geo_;
+    d_.face_flags = 0;
+    d_.xcol_ok = 0;
 
     // ---- host mirror + initial tiles (make_state, engine.cpp:134-159)
     grid_slot_.assign(n_tiles, -1);
@@ -663,7 +685,7 @@ void Engine::release() {
     void* ptrs[] = {d_pool_f_, d_pool_pf_, d_slot_f_[0], d_slot_f_[1], d_slot_pf_[0], d_slot_pf_[1],
                     d_route_[0], d_route_[1], d_lidx_, d_solid_, d_has_solid_, d_mode_, d_coords_,
                     d_u_face_, d_trig_, d_capture_, d_cnt_, d_err_, d_active_, d_scratch_slots_,
-                    d_readback_};
+                    d_readback_, d_dep_cnt_, d_dep_need_, d_geo_};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     for (auto& e : ev_pool_) {
@@ -882,6 +904,38 @@ void Engine::upload_map(const std::vector<int>& new_slots, bool initial) {
     // use psi of a fresh ambient cell (kernels.cuh psi_ghost); initial tiles
     // get theirs from k_face over the generated state (prepare())
     // routes: pull table = map of the step that just ran, psi table = new map
+    // geometric neighbour table + dependency counts of the fused face pass
+    {
+        static const int off[18][3] = {{-1, 0, 0}, {1, 0, 0},  {0, -1, 0},  {0, 1, 0},  {0, 0, -1},
+                                       {0, 0, 1},  {-1, -1, 0}, {1, -1, 0}, {-1, 1, 0},  {1, 1, 0},
+                                       {-1, 0, -1}, {1, 0, -1}, {-1, 0, 1}, {1, 0, 1},  {0, -1, -1},
+                                       {0, 1, -1}, {0, -1, 1}, {0, 1, 1}};
+        std::vector<int> geo(nslot * 18, -1), need(nslot, 0);
+        for (int s : all_active_) {
+            int n = 1;
+            for (int k = 0; k < 18; ++k) {
+                int q[3];
+                bool ok = true;
+                for (int a = 0; a < 3; ++a) {
+                    q[a] = (a == 0 ? slots_[s].c.x : a == 1 ? slots_[s].c.y : slots_[s].c.z) + off[k][a];
+                    if (q[a] < 0 || q[a] >= grid_[a]) {
+                        if (!periodic_[a]) ok = false;
+                        q[a] = (q[a] + grid_[a]) % grid_[a];
+                    }
+                }
+                if (!ok) continue;
+                const int m = grid_slot_[(size_t(q[0]) * grid_[1] + q[1]) * grid_[2] + q[2]];
+                if (m < 0) continue;
+                geo[size_t(s) * 18 + k] = m;
+                ++n;
+            }
+            need[s] = n;
+        }
+        CK(cudaMemcpyAsync(d_geo_, geo.data(), geo.size() * sizeof(int), cudaMemcpyHostToDevice, stream_));
+        CK(cudaMemcpyAsync(d_dep_need_, need.data(), need.size() * sizeof(int), cudaMemcpyHostToDevice,
+                           stream_));
+        stats_.h2d_bytes += (geo.size() + need.size()) * sizeof(int);
+    }
     std::vector<int> routes(nslot * 18, amb_);
     for (int s : all_active_) compute_routes(s, &routes[size_t(s) * 18]);
     if (!initial)
@@ -919,11 +973,18 @@ void Engine::launch_main(long iter) {
     if (ev) CK(cudaEventRecord(ev->a, stream_));
     const int wu = mode_ == PLBM_MODE_PROGRESSIVE ? 1 : 0;
     MainFn fn = K_.main_plain;
+    // single rank: the pc kernels run the face pass themselves (no k_face)
+    const auto fusable = [&](MainFn f) { return world_ == 1 && f && (f == K_.main_pc || f == K_.main_pc2); };
     if (variant_ == 0) fn = K_.main_pc ? K_.main_pc : (K_.main_tm ? K_.main_tm : K_.main_plain);
     if (K_.main_tm && variant_ >= 2 && variant_ < 18 && K_.main_tm_opt[variant_ - 2])
         fn = K_.main_tm_opt[variant_ - 2];
     if (K_.main_pc && variant_ == 21) fn = K_.main_pc;
     if (K_.main_pc2 && variant_ == 22) fn = K_.main_pc2;
+    face_fused_ = fusable(fn) && fuse_;
+    // the pc kernels write the xcol side buffers the face pass reads
+    d_.xcol_ok = (fn == K_.main_pc || fn == K_.main_pc2) && !no_xcol_;
+    d_.face_flags = face_fused_ ? (FACE_FUSED | FACE_NAN | (mode_ == PLBM_MODE_PROGRESSIVE ? FACE_CRITERION : 0))
+                                : 0;
     fn(d_, d_active_, cur_, wu, iter, unsigned(active_.size()), stream_);
     CK(cudaGetLastError());
     ++stats_.kernels_launched;
@@ -1075,7 +1136,7 @@ int Engine::step_main(plbm_error* err) {
 
 int Engine::step_face() {
     if (phase_ != 1) return 0;
-    launch_face(cur_, mode_ == PLBM_MODE_PROGRESSIVE ? 3 : 2, iteration_ + 1);
+    if (!face_fused_) launch_face(cur_, mode_ == PLBM_MODE_PROGRESSIVE ? 3 : 2, iteration_ + 1);
     phase_ = 2;
     return 0;
 }

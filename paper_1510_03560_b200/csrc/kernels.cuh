@@ -77,7 +77,15 @@ struct Dev {
     unsigned long long* cnt;    // CNT_N
     unsigned long long* err;    // packed (iter, tile_lin, code), atomicMin
     int solid_words;
+    // fused face pass (single rank): the cluster that completes the last of a
+    // tile's 19 dependencies (itself + geometric neighbours) runs its face pass
+    int* dep_cnt;               // [slot] completions this step (self-resetting)
+    const int* dep_need;        // [slot] 1 + active geometric neighbours
+    const int* geo;             // [slot][18] active geometric neighbour or -1
+    int face_flags;             // FACE_* bits
+    int xcol_ok;                // the last fused kernel wrote the xcol side buffers
 };
+enum { FACE_CRITERION = 1, FACE_NAN = 2, FACE_FUSED = 4 };
 
 __constant__ Params P;
 
@@ -582,77 +590,211 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
 }
 
 // ---------------------------------------------------------------------------
-// k_face: moments of f_in^(k+1) on the six face layers of every active tile.
-// Writes the psi faces for the next step (parity of iter + 1) and evaluates
-// the activation criterion (proj/src/tilemap.cpp:182-218) plus the P5 NaN
-// check (engine.cpp:509-512).  One cell per thread.
+// Face pass (P5 moments of f_in^(k+1) on the six face layers): per face cell
+// and component, pull f_in^(k+1), psi for the next step's ghost faces, the P5
+// NaN check (engine.cpp:509-512) and, on a frontier face, the activation
+// criterion (tilemap.cpp:182-218).  Work items are (face cell, component)
+// pairs; each thread prefetches its next item's 19 populations before it
+// finishes the current one, so two items' loads are in flight per thread.
+template <int E>
+__device__ __forceinline__ void face_xyz(int face, int idx, int& x, int& y, int& z) {
+    const int axis = face >> 1;
+    const int fixed = (face & 1) ? E - 1 : 0;
+    const int a = idx % E, b = idx / E;
+    x = axis == 0 ? fixed : a;
+    y = axis == 0 ? a : (axis == 1 ? fixed : b);
+    z = axis == 2 ? fixed : b;
+}
+
+// COH: read f_post through L2 (written by other CTAs of the same launch in
+// the fused path).
+template <int E, bool COH>
+__device__ __forceinline__ void face_load(const RouteTab& rt, int mode, const int* tc, int c, bool hs,
+                                          const uint32_t* sb, int face, int idx, double* f,
+                                          bool xcol = false) {
+    int x, y, z;
+    face_xyz<E>(face, idx, x, y, z);
+    if (hs && solid_at<E>(sb, x, y, z)) return;
+    if (xcol && face < 2 && !hs && mode == MODE_PULL) {
+        // x faces from the routed tiles' xcol buffers (lattice.cuh): the
+        // source column x - e_x is 0 / 1 / E-2 / E-1 of the own tile or x = E-1
+        // / 0 of the -x / +x neighbour; consecutive threads read consecutive y
+        constexpr int E2 = E * E;
+        constexpr int E3 = E * E * E;
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+            const int sx = x - ex_(i), sy = y - ey_(i), sz = z - ez_(i);
+            const int ox = sx < 0 ? -1 : (sx >= E ? 1 : 0);
+            const int oy = sy < 0 ? -1 : (sy >= E ? 1 : 0);
+            const int oz = sz < 0 ? -1 : (sz >= E ? 1 : 0);
+            const int lx = sx & (E - 1);
+            const int cls = lx == 0 ? 0 : lx == 1 ? 1 : lx == E - 2 ? 2 : 3;
+            const double* p = rt.p[(ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)] + size_t(P.C) * Q * E3 +
+                              (size_t(c) * XN + xslot_sel(cls, i)) * E2 + (sz & (E - 1)) * E + (sy & (E - 1));
+            f[i] = COH ? __ldcg(p) : __ldg(p);
+        }
+        return;
+    }
+    if (mode == MODE_PULL) {
+        if (COH) pull_addr<E>(rt, c, hs, sb, x, y, z, [&](int i, const double* p) { f[i] = __ldcg(p); });
+        else pull_addr<E>(rt, c, hs, sb, x, y, z, [&](int i, const double* p) { f[i] = __ldg(p); });
+    } else {
+        double a0, a1, a2;
+        gen_fin<E>(mode, c, tc, x, y, z, f, a0, a1, a2);
+    }
+}
+
+// Returns true when the criterion fires at this cell.
+template <int E>
+__device__ __forceinline__ bool face_finish(const Dev& d, int mode, int c, bool hs, const uint32_t* sb,
+                                            int face, int idx, const double* f, bool frontier,
+                                            bool nan_check, int li, double* pf, long iter, int tile_lin) {
+    constexpr int E2 = E * E;
+    int x, y, z;
+    face_xyz<E>(face, idx, x, y, z);
+    bool fired = false;
+    double v = 0.0;
+    if (!(hs && solid_at<E>(sb, x, y, z))) {
+        double rho = 0.0;
+#pragma unroll
+        for (int i = 0; i < Q; ++i) rho += f[i];
+        if (mode == MODE_PULL && (frontier || nan_check)) {
+            // u = m / rho (kernels.hpp:31-48) is needed for the criterion; for
+            // the NaN check alone it is provably finite when |m| <= 2^100 and
+            // |rho| >= 2^-900, so the divisions are skipped then
+            double m0 = 0.0, m1 = 0.0, m2 = 0.0;
+            m0 += f[1]; m0 -= f[2]; m0 += f[7]; m0 -= f[8]; m0 += f[9]; m0 -= f[10];
+            m0 += f[11]; m0 -= f[12]; m0 += f[13]; m0 -= f[14];
+            m1 += f[3]; m1 -= f[4]; m1 += f[7]; m1 -= f[8]; m1 -= f[9]; m1 += f[10];
+            m1 += f[15]; m1 -= f[16]; m1 += f[17]; m1 -= f[18];
+            m2 += f[5]; m2 -= f[6]; m2 += f[11]; m2 -= f[12]; m2 -= f[13]; m2 += f[14];
+            m2 += f[15]; m2 -= f[16]; m2 -= f[17]; m2 += f[18];
+            const bool safe = fabs(rho) >= 0x1p-900 && fabs(m0) <= 0x1p100 && fabs(m1) <= 0x1p100 &&
+                              fabs(m2) <= 0x1p100;
+            double u0 = 0.0, u1 = 0.0, u2 = 0.0;
+            if ((frontier || !safe) && rho != 0.0) {
+                u0 = m0 / rho;
+                u1 = m1 / rho;
+                u2 = m2 / rho;
+            }
+            if (nan_check && (!isfinite(rho) ||
+                              (!safe && (!isfinite(u0) || !isfinite(u1) || !isfinite(u2)))))
+                atomic_err(d.err, iter, tile_lin, ERR_P5_NAN);
+            if (frontier) {
+                const double* uf = d.u_face + ((size_t(li) * P.C + c) * 6 + face) * 3 * E2;
+                const double dx = u0 - __ldcg(uf + idx), dy = u1 - __ldcg(uf + E2 + idx),
+                             dz = u2 - __ldcg(uf + 2 * E2 + idx);
+                if (dx * dx + dy * dy + dz * dz > P.s2) fired = true;
+            }
+        } else if (nan_check && !isfinite(rho)) {
+            atomic_err(d.err, iter, tile_lin, ERR_P5_NAN);
+        }
+        double press;
+        if (isfinite(rho) && pr_pressure(rho, P.comp[c], press)) {
+            bool cl;
+            v = pseudo_potential(rho, press, P.comp[c], cl);
+        }
+    }
+    pf[(size_t(c) * 6 + face) * E2 + idx] = v;
+    return fired;
+}
+
+// Items t = 0, 1, ... of this thread: cell k = k0 + tid + (t / nc) * NT of
+// the 6 E^2 face cells (k < k1), component c0 + t % nc.  Returns the bitmask
+// of faces whose criterion fired (OR over the warp, set by lane 0 only).
+template <int E, int NT, bool COH>
+__device__ unsigned face_run(const Dev& d, const RouteTab& rt, int mode, const int* tc, bool hs,
+                             const uint32_t* sb, int c0, int nc, int k0, int k1, const int* routes,
+                             bool criterion, bool nan_check, int li, double* pf, long iter,
+                             int tile_lin) {
+    constexpr int E2 = E * E;
+    unsigned fired = 0;
+    auto item = [&](int t, int& face, int& idx, int& c) {
+        const int k = k0 + int(threadIdx.x) + (t / nc) * NT;
+        if (k >= k1) return false;
+        face = k / E2;
+        idx = k - face * E2;
+        c = c0 + t % nc;
+        return true;
+    };
+    const bool xcol = d.xcol_ok != 0;
+    auto load = [&](int t, double* f) {
+        int face, idx, c;
+        if (item(t, face, idx, c)) face_load<E, COH>(rt, mode, tc, c, hs, sb, face, idx, f, xcol);
+    };
+    auto finish = [&](int t, const double* f) {
+        int face, idx, c;
+        if (!item(t, face, idx, c)) return false;
+        const bool frontier = criterion && routes[face] == P.amb_slot && !(fired & (1u << face));
+        if (face_finish<E>(d, mode, c, hs, sb, face, idx, f, frontier, nan_check, li, pf, iter, tile_lin))
+            fired |= 1u << face;
+        return true;
+    };
+    double fa[Q], fb[Q];
+    load(0, fa);
+#pragma unroll 1
+    for (int t = 0;; t += 2) {
+        load(t + 1, fb);
+        if (!finish(t, fa)) break;
+        load(t + 2, fa);
+        if (!finish(t + 1, fb)) break;
+    }
+    return __reduce_or_sync(0xffffffffu, fired);
+}
+
+__device__ __forceinline__ void set_triggers(const Dev& d, int slot, unsigned faces) {
+    if (faces && (threadIdx.x & 31) == 0)
+        atomicOr((unsigned*)(d.trig) + slot / 4, faces << (8 * (slot % 4)));
+}
+
+// The face pass of tile `slot`, components [c0, c0 + nc), face cells [k0, k1),
+// run by one CTA inside the fused kernel once the tile's dependencies are
+// complete.  rt / sb / tc are the CTA's shared scratch.
+template <int E, int NT>
+__device__ void face_pass_part(const Dev& d, int slot, int c0, int nc, int k0, int k1, int post_buf,
+                               long iter, RouteTab& rt, uint32_t* sb, int* tc) {
+    __syncthreads();  // the shared scratch is free
+    load_routes(rt, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, P.amb_slot, d.slot_f[post_buf]);
+    const bool hs = d.has_solid[slot] != 0;
+    if (hs)
+        for (int k = threadIdx.x; k < d.solid_words; k += NT) sb[k] = d.solid[size_t(slot) * d.solid_words + k];
+    if (threadIdx.x < 3) tc[threadIdx.x] = d.coords[slot * 3 + threadIdx.x];
+    __syncthreads();
+    const int tile_lin = (tc[0] * P.grid[1] + tc[1]) * P.grid[2] + tc[2];
+    const unsigned f = face_run<E, NT, true>(
+        d, rt, MODE_PULL, tc, hs, sb, c0, nc, k0, k1, d.route[ROUTE_PSI] + size_t(slot) * 18,
+        (d.face_flags & FACE_CRITERION) != 0, (d.face_flags & FACE_NAN) != 0, d.lidx[slot],
+        d.slot_pf[int((iter + 1) & 1)][slot], iter, tile_lin);
+    set_triggers(d, slot, f);
+}
+
+// k_face: the face pass as its own launch (multi-rank runs, the non-fused
+// kernels, and the initial psi faces).  One CTA per (tile, face).
 template <int E, int C, int NT>
 __global__ void __launch_bounds__(NT) k_face(Dev d, const int* __restrict__ active, int src_buf,
                                              int flags, long iter) {
-    const bool criterion = flags & 1;  // evaluate the activation criterion
-    const bool nan_check = flags & 2;  // P5 NaN check of the moments
     constexpr int E2 = E * E;
     constexpr int G = E + 2;
-    constexpr int NCH = (E2 + NT - 1) / NT;  // blocks per face
     __shared__ RouteTab rt;
     __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
     __shared__ int s_tc[3];
-    __shared__ int s_fired;
-    const int slot = active[blockIdx.x / (6 * NCH)];
-    const int face = (blockIdx.x / NCH) % 6;
-    const int chunk = blockIdx.x % NCH;
+    const int slot = active[blockIdx.x / 6];
+    const int face = blockIdx.x % 6;
     const uint8_t mode = d.mode[slot];
     const bool hs = d.has_solid[slot] != 0;
-    const int amb = P.amb_slot;
-    const int li = d.lidx[slot];
     // after k_main every tile pulls with the map it just stepped on (ROUTE_PSI)
-    load_routes(rt, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, amb, d.slot_f[src_buf]);
+    load_routes(rt, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, P.amb_slot, d.slot_f[src_buf]);
     if (threadIdx.x < 3) s_tc[threadIdx.x] = d.coords[slot * 3 + threadIdx.x];
-    if (threadIdx.x == 0) s_fired = 0;
     if (hs)
         for (int k = threadIdx.x; k < d.solid_words; k += NT)
             s_solid[k] = d.solid[size_t(slot) * d.solid_words + k];
     __syncthreads();
     const int tile_lin = (s_tc[0] * P.grid[1] + s_tc[1]) * P.grid[2] + s_tc[2];
-    const bool frontier = criterion && (d.route[ROUTE_PSI][size_t(slot) * 18 + face] == amb);
-    double* pf = d.slot_pf[int((iter + 1) & 1)][slot];
-    const int axis = face >> 1;
-    const int fixed = (face & 1) ? E - 1 : 0;
-    bool fired = false;
-    for (int idx = chunk * NT + threadIdx.x; idx < E2 && idx < (chunk + 1) * NT; idx += NT) {
-        const int a = idx % E, b = idx / E;
-        const int x = axis == 0 ? fixed : a;
-        const int y = axis == 0 ? a : (axis == 1 ? fixed : b);
-        const int z = axis == 2 ? fixed : b;
-        const bool sol = hs && solid_at<E>(s_solid, x, y, z);
-#pragma unroll 1
-        for (int c = 0; c < C; ++c) {
-            double v = 0.0;
-            if (!sol) {
-                double f[Q], u0 = 0.0, u1 = 0.0, u2 = 0.0, rho;
-                fin_cell<E>(rt, mode, s_tc, c, hs, s_solid, x, y, z, f, u0, u1, u2);
-                if (mode == MODE_PULL) moments(f, rho, u0, u1, u2);
-                else rho = sum19(f);
-                if (nan_check && (!isfinite(rho) || !isfinite(u0) || !isfinite(u1) || !isfinite(u2)))
-                    atomic_err(d.err, iter, tile_lin, ERR_P5_NAN);
-                if (frontier && !fired) {
-                    const double* uf = d.u_face + ((size_t(li) * C + c) * 6 + face) * 3 * E2;
-                    const double dx = u0 - uf[idx], dy = u1 - uf[E2 + idx], dz = u2 - uf[2 * E2 + idx];
-                    if (dx * dx + dy * dy + dz * dz > P.s2) fired = true;
-                }
-                const CompConst& kc = P.comp[c];
-                double press;
-                if (isfinite(rho) && pr_pressure(rho, kc, press)) {
-                    bool cl;
-                    v = pseudo_potential(rho, press, kc, cl);
-                }
-            }
-            pf[(size_t(c) * 6 + face) * E2 + idx] = v;
-        }
-    }
-    if (__any_sync(0xffffffffu, fired) && (threadIdx.x & 31) == 0) s_fired = 1;
-    __syncthreads();
-    if (threadIdx.x == 0 && s_fired) atomicOr((unsigned*)(d.trig) + slot / 4, 1u << (8 * (slot % 4) + face));
+    const unsigned f = face_run<E, NT, false>(d, rt, mode, s_tc, hs, s_solid, 0, C, face * E2,
+                                              (face + 1) * E2, d.route[ROUTE_PSI] + size_t(slot) * 18,
+                                              (flags & 1) != 0, (flags & 2) != 0, d.lidx[slot],
+                                              d.slot_pf[int((iter + 1) & 1)][slot], iter, tile_lin);
+    set_triggers(d, slot, f);
 }
 
 // Reference-view read-back of one tile (f_read, rho, u) into out:

@@ -29,6 +29,9 @@
 
 namespace plbm {
 
+__constant__ unsigned char c_xdir[XN] = {0, 2, 3, 4, 5, 6, 8, 10, 12, 14, 15, 16, 17, 18, 2, 8, 10, 12, 14,
+                                         1, 7, 9, 11, 13, 0, 1, 3, 4, 5, 6, 7, 9, 11, 13, 15, 16, 17, 18};
+
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
 }
@@ -81,7 +84,8 @@ struct PcCfg {
     static constexpr int TSLOTS = LAG + 1;          // TMEM plane slots
     static constexpr int PSI_BYTES = RING * C * PP * 8;
     static constexpr int LAND_BYTES = Q * NT * 8;
-    static constexpr int SMEM = PSI_BYTES + LAND_BYTES;
+    static constexpr int XST_BYTES = 2 * 4 * Q * BY * 8;  // x-column staging, two planes
+    static constexpr int SMEM = PSI_BYTES + LAND_BYTES + XST_BYTES;
     static_assert(CL <= 8, "portable cluster size");
     static_assert(TSLOTS * CB <= NCOLS / 2, "TMEM plane slots do not fit");
     static_assert(2 * (SMEM + 8 * 1024) <= 228 * 1024, "two CTAs per SM must fit");
@@ -103,11 +107,13 @@ __global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict
     extern __shared__ __align__(16) double smem[];
     double* psi = smem;                // [R][C][PH][PW] ring of psi planes, all components
     double* land = smem + R * C * PP;  // [Q][NT] landed populations of the next plane
+    double* xst = land + Q * NT;       // [2][4][Q][BY] x-column values of the block's rows, by plane parity
     __shared__ RouteTab rt_pull, rt_psi;
     __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
     __shared__ int s_tc[3];
     __shared__ uint32_t s_tmem;
     __shared__ __align__(8) uint64_t s_mbar[T::NMB];  // pushed psi of plane p: slot p % NMB
+    __shared__ int s_ready[20], s_nready;              // fused face pass: tiles this cluster runs
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -154,6 +160,20 @@ __global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict
     const int x = tid % E;
     const int yl = tid / E;
     const int y = y0 + yl;
+    const int xcls = x == 0 ? 0 : x == 1 ? 1 : x == E - 2 ? 2 : x == E - 1 ? 3 : -1;  // xcol lanes
+    double* const xcol = d.slot_f[src_buf ^ 1][slot] + size_t(C) * Q * E3 + size_t(c) * XN * E2;
+    const bool wx = d.xcol_ok != 0;
+    // xcol: the x-column lanes stage their values in shared memory during the
+    // collision; after the next CTA barrier the block writes them out as
+    // 8-row (64-byte) segments of xcol[c][slot][z][y]
+    auto flush_xcol = [&](int pz) {
+        if (!wx || pz < 0) return;
+        const double* src = xst + (pz & 1) * 4 * Q * BY;
+        for (int k = tid; k < XN * BY; k += NT) {
+            const int s = k / BY, r = k - s * BY;
+            xcol[size_t(s) * E2 + pz * E + y0 + r] = src[(xslot_cls(s) * Q + c_xdir[s]) * BY + r];
+        }
+    };
     const bool fast_rows = mode == MODE_PULL && !hs && y >= 1 && y <= E - 2;
     auto pidx = [&](int pz, int cc, int xx, int yy_local) {
         return (((pz & (R - 1)) * C + cc) * PH + (yy_local + 1)) * PW + (xx + 1);
@@ -367,7 +387,8 @@ __global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict
                 cp[2 * E3 + cell] = u1;
                 cp[3 * E3 + cell] = u2;
             }
-            collide_bgk(f, rho, u0, u1, u2, F0, F1, F2, kc.omega, fo + cell, size_t(E3), zero_rho);
+            collide_bgk(f, rho, u0, u1, u2, F0, F1, F2, kc.omega, fo + cell, size_t(E3), zero_rho,
+                        (xcls >= 0 && wx) ? xst + ((z & 1) * 4 + xcls) * Q * BY + yl : nullptr, BY);
         }
         const unsigned zr = __reduce_add_sync(0xffffffffu, (unsigned)zero_rho);
         if ((tid & 31) == 0 && zr) atomicAdd(&d.cnt[CNT_ZERO_RHO], (unsigned long long)zr);
@@ -405,6 +426,7 @@ __global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict
             fill_zghost(E);
         }
         __syncthreads();  // psi plane pn visible; every warp is past collide(z-1)
+        flush_xcol(z - 1);
         issue_ring(pn + 1);  // its ring slot is no longer read by anyone
         cp_async_commit();
         if (z + 1 < E && z + 1 >= LAG) wait_pushed(z + 1);
@@ -412,14 +434,62 @@ __global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict
     }
     cp_async_wait<0>();
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    const bool fused = (d.face_flags & FACE_FUSED) != 0;
     __syncthreads();
-    if constexpr (T::CL > 1) {  // every push into a peer has landed before anyone exits
-        asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-        asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-    }
+    flush_xcol(E - 1);
+    if (fused) __threadfence();  // this thread's f_post / u_face / xcol stores, GPU-wide
+    __syncthreads();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(s_tmem),
                      "n"(T::NCOLS));
+    auto cluster_sync = [&] {
+        if constexpr (T::CL > 1) {
+            asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+            asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+        } else {
+            __syncthreads();
+        }
+    };
+    cluster_sync();  // every push into a peer has landed; the whole tile is written
+    if (!fused) return;
+
+    // ---- fused face pass ---------------------------------------------------------
+    // This tile is complete: count it towards itself and its active geometric
+    // neighbours.  Whoever brings a tile's count to dep_need (all of the tiles
+    // its face cells pull from are written) runs that tile's face pass: psi
+    // faces for the next step, criterion, P5 NaN check.  Nobody waits.
+    if (rank == 0 && tid == 0) {
+        int n = 0;
+        auto count = [&](int m) {
+            if (atomicAdd(&d.dep_cnt[m], 1) == d.dep_need[m] - 1) {
+                d.dep_cnt[m] = 0;  // every count of this step is in: reset for the next
+                s_ready[n++] = m;
+            }
+        };
+        count(slot);
+        for (int k = 0; k < 18; ++k) {
+            const int m = d.geo[size_t(slot) * 18 + k];
+            if (m >= 0) count(m);
+        }
+        s_nready = n;
+        __threadfence();  // acquire side of the counts: the other tiles' stores
+    }
+    cluster_sync();
+    int ready[20];
+    int nready;
+    {
+        uint32_t a0;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(a0) : "r"(smem_u32(&s_nready)));
+        asm volatile("ld.shared::cluster.u32 %0, [%1];\n" : "=r"(nready) : "r"(a0) : "memory");
+        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(a0) : "r"(smem_u32(&s_ready[0])));
+        for (int j = 0; j < nready; ++j)
+            asm volatile("ld.shared::cluster.u32 %0, [%1];\n" : "=r"(ready[j]) : "r"(a0 + 4u * j) : "memory");
+    }
+    cluster_sync();  // rank 0 may exit once everyone has the list
+    constexpr int PER = 6 * E2 / NB;
+    for (int j = 0; j < nready; ++j)
+        face_pass_part<E, NT>(d, ready[j], c, 1, yb * PER, (yb + 1) * PER, src_buf ^ 1, iter, rt_pull,
+                              s_solid, s_tc);
 }
 
 }  // namespace plbm

@@ -171,11 +171,14 @@ __device__ __forceinline__ void forces_all(const double* pm0, const double* p00,
 }
 
 // One component's BGK collision with the velocity-shift forcing
-// (engine.cpp:450-475) given the total force F.
-__device__ __forceinline__ void collide_bgk(const double* f, double rho, double u0, double u1,
+// (engine.cpp:450-475) given the total force F.  f is overwritten with the
+// post-collision populations; xc (x-column lanes only, else nullptr) receives
+// a copy of all 19 at stride xstride.
+__device__ __forceinline__ void collide_bgk(double* f, double rho, double u0, double u1,
                                             double u2, double F0, double F1, double F2,
                                             double om, double* out, size_t dstride,
-                                            int& zero_rho) {
+                                            int& zero_rho, double* xc = nullptr, int xstride = 0) {
+
     const double uu = u0 * u0 + u1 * u1 + u2 * u2;
     const double t3 = (0.5 * uu) * 3.0;
     const double wr0 = PLBM_W0 * rho, wr1 = PLBM_W1 * rho, wr2 = PLBM_W2 * rho;
@@ -188,7 +191,8 @@ __device__ __forceinline__ void collide_bgk(const double* f, double rho, double 
         const double wr = (I == 0) ? wr0 : ((I <= 6) ? wr1 : wr2);                            \
         const double eu = (I == 0) ? 0.0 : eu_pair<IP>(u0, u1, u2);                           \
         const double e0 = feq_dir<I>(wr, eu, t3);                                             \
-        out[size_t(I) * dstride] = f[I] + om * (e0 - f[I]);                                   \
+        f[I] = f[I] + om * (e0 - f[I]);                                                       \
+        out[size_t(I) * dstride] = f[I];                                                      \
     }
         PLBM_TM_RELAX(0) PLBM_TM_RELAX(1) PLBM_TM_RELAX(2) PLBM_TM_RELAX(3) PLBM_TM_RELAX(4)
         PLBM_TM_RELAX(5) PLBM_TM_RELAX(6) PLBM_TM_RELAX(7) PLBM_TM_RELAX(8) PLBM_TM_RELAX(9)
@@ -207,7 +211,8 @@ __device__ __forceinline__ void collide_bgk(const double* f, double rho, double 
         const double ev = (I == 0) ? 0.0 : eu_pair<IP>(v0, v1, v2);                           \
         const double e0 = feq_dir<I>(wr, eu, t3);                                             \
         const double e1 = feq_dir<I>(wr, ev, s3);                                             \
-        out[size_t(I) * dstride] = f[I] + ((om * (e0 - f[I]) + e1) - e0);                     \
+        f[I] = f[I] + ((om * (e0 - f[I]) + e1) - e0);                                         \
+        out[size_t(I) * dstride] = f[I];                                                      \
     }
         PLBM_TM_FORCED(0) PLBM_TM_FORCED(1) PLBM_TM_FORCED(2) PLBM_TM_FORCED(3)
         PLBM_TM_FORCED(4) PLBM_TM_FORCED(5) PLBM_TM_FORCED(6) PLBM_TM_FORCED(7)
@@ -215,6 +220,11 @@ __device__ __forceinline__ void collide_bgk(const double* f, double rho, double 
         PLBM_TM_FORCED(12) PLBM_TM_FORCED(13) PLBM_TM_FORCED(14) PLBM_TM_FORCED(15)
         PLBM_TM_FORCED(16) PLBM_TM_FORCED(17) PLBM_TM_FORCED(18)
 #undef PLBM_TM_FORCED
+    }
+    // x-column lanes: all 19 post-collision values to the staging area
+    if (xc) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) xc[i * xstride] = f[i];
     }
 }
 

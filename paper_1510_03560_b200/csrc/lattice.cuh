@@ -38,6 +38,36 @@ __host__ __device__ constexpr int opp_(int i) {
     constexpr int t[Q] = {0, 2, 1, 4, 3, 6, 5, 8, 7, 10, 9, 12, 11, 14, 13, 16, 15, 18, 17};
     return t[i];
 }
+// x-column side buffer ("xcol"): the fused kernel also stores the post-
+// collision populations of the four x-boundary columns (x = 0, 1, E-2, E-1)
+// that the x faces' pulls need, y-contiguous, so the face pass reads them
+// coalesced instead of one 8-byte element per 32-byte sector of the SoA block.
+//   class 0 (x = 0):   e_x in {0, -1} (own x = 0 face, -x neighbour's x = E-1 face)
+//   class 1 (x = 1):   e_x = -1       (own x = 0 face)
+//   class 2 (x = E-2): e_x = +1       (own x = E-1 face)
+//   class 3 (x = E-1): e_x in {0, +1} (own x = E-1 face, +x neighbour's x = 0 face)
+constexpr int XN = 38;  // (class, direction) pairs per component
+__host__ __device__ constexpr int xslot_(int cls, int i) {
+    constexpr int t[4][Q] = {
+        {0, -1, 1, 2, 3, 4, 5, -1, 6, -1, 7, -1, 8, -1, 9, 10, 11, 12, 13},
+        {-1, -1, 14, -1, -1, -1, -1, -1, 15, -1, 16, -1, 17, -1, 18, -1, -1, -1, -1},
+        {-1, 19, -1, -1, -1, -1, -1, 20, -1, 21, -1, 22, -1, 23, -1, -1, -1, -1, -1},
+        {24, 25, -1, 26, 27, 28, 29, 30, -1, 31, -1, 32, -1, 33, -1, 34, 35, 36, 37}};
+    return t[cls][i];
+}
+// inverse map: xcol slot -> (class, direction)
+__host__ __device__ constexpr int xslot_cls(int s) { return s < 14 ? 0 : s < 19 ? 1 : s < 24 ? 2 : 3; }
+__host__ __device__ constexpr int xslot_dir(int s) {
+    constexpr int t[XN] = {0, 2, 3, 4, 5, 6, 8, 10, 12, 14, 15, 16, 17, 18, 2, 8, 10, 12, 14,
+                           1, 7, 9, 11, 13, 0, 1, 3, 4, 5, 6, 7, 9, 11, 13, 15, 16, 17, 18};
+    return t[s];
+}
+// xslot_ with a compile-time direction and a runtime class, without a table
+// in local memory
+__host__ __device__ __forceinline__ constexpr int xslot_sel(int cls, int i) {
+    return cls == 0 ? xslot_(0, i) : cls == 1 ? xslot_(1, i) : cls == 2 ? xslot_(2, i) : xslot_(3, i);
+}
+
 // weight class: 0 -> 1/3, 1 -> 1/18, 2 -> 1/36
 __host__ __device__ constexpr int wclass_(int i) { return i == 0 ? 0 : (i <= 6 ? 1 : 2); }
 
