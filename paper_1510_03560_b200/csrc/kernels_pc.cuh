@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict
         uint32_t ok = 0;
         while (!ok)
             asm volatile(
-                "{\n .reg .pred q;\n mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n"
+                "{\n .reg .pred q;\n mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2, 1000000;\n"
                 " selp.u32 %0, 1, 0, q;\n}\n"
                 : "=r"(ok)
                 : "r"(bar), "r"(parity)

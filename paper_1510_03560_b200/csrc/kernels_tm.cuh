@@ -200,7 +200,15 @@ __device__ __forceinline__ void collide_bgk(double* f, double rho, double u0, do
         PLBM_TM_RELAX(15) PLBM_TM_RELAX(16) PLBM_TM_RELAX(17) PLBM_TM_RELAX(18)
 #undef PLBM_TM_RELAX
     } else {
-        const double v0 = u0 + F0 / rho, v1 = u1 + F1 / rho, v2 = u2 + F2 / rho;
+        bool ok = true;
+        const double rr = rcp_nv(rho);
+        double q0 = div_nv(F0, rho, rr, ok), q1 = div_nv(F1, rho, rr, ok), q2 = div_nv(F2, rho, rr, ok);
+        if (!ok) {
+            q0 = F0 / rho;
+            q1 = F1 / rho;
+            q2 = F2 / rho;
+        }
+        const double v0 = u0 + q0, v1 = u1 + q1, v2 = u2 + q2;
         const double vv = v0 * v0 + v1 * v1 + v2 * v2;
         const double s3 = (0.5 * vv) * 3.0;
 #define PLBM_TM_FORCED(I)                                                                     \
@@ -242,9 +250,16 @@ __device__ __forceinline__ void velocity(const double* f, double r, double& u0, 
     m2 += f[5]; m2 -= f[6]; m2 += f[11]; m2 -= f[12]; m2 -= f[13]; m2 += f[14];
     m2 += f[15]; m2 -= f[16]; m2 -= f[17]; m2 += f[18];
     if (r != 0.0) {
-        u0 = m0 / r;
-        u1 = m1 / r;
-        u2 = m2 / r;
+        bool ok = true;
+        const double rr = rcp_nv(r);
+        u0 = div_nv(m0, r, rr, ok);
+        u1 = div_nv(m1, r, rr, ok);
+        u2 = div_nv(m2, r, rr, ok);
+        if (!ok) {
+            u0 = m0 / r;
+            u1 = m1 / r;
+            u2 = m2 / r;
+        }
     } else {
         u0 = u1 = u2 = 0.0;
     }
@@ -389,7 +404,7 @@ __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict
         uint32_t ok = 0;
         while (!ok)
             asm volatile(
-                "{\n .reg .pred q;\n mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n"
+                "{\n .reg .pred q;\n mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2, 1000000;\n"
                 " selp.u32 %0, 1, 0, q;\n}\n"
                 : "=r"(ok)
                 : "r"(bar), "r"(parity)
@@ -466,7 +481,7 @@ __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict
         uint32_t ok = 0;
         while (!ok)
             asm volatile(
-                "{\n .reg .pred q;\n mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n"
+                "{\n .reg .pred q;\n mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2, 1000000;\n"
                 " selp.u32 %0, 1, 0, q;\n}\n"
                 : "=r"(ok)
                 : "r"(bar), "r"(parity)

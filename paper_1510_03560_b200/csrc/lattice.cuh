@@ -16,6 +16,8 @@
 
 #include <cstdint>
 
+#include "ieee_div.cuh"
+
 namespace plbm {
 
 constexpr int Q = 19;
@@ -187,8 +189,16 @@ __device__ __forceinline__ bool pr_pressure(double rho, const CompConst& k, doub
         return true;
     }
     if (k.b * rho >= 1.0) return false;
-    const double ideal = ((rho * k.R) * k.T) / (1.0 - k.b * rho);
-    const double attr = ((k.a_theta * rho) * rho) / ((1.0 + k.two_b * rho) - (k.b_b * rho) * rho);
+    // ideal = ((rho R) T) / (1 - b rho); attr = ((a theta rho) rho) / ((1 + 2b rho) - (b^2 rho) rho)
+    const double n1 = (rho * k.R) * k.T, d1 = 1.0 - k.b * rho;
+    const double n2 = (k.a_theta * rho) * rho, d2 = (1.0 + k.two_b * rho) - (k.b_b * rho) * rho;
+    bool ok = true;
+    double ideal = div_nv(n1, d1, rcp_nv(d1), ok);
+    double attr = div_nv(n2, d2, rcp_nv(d2), ok);
+    if (!ok) {
+        ideal = n1 / d1;
+        attr = n2 / d2;
+    }
     p = ideal - attr;
     return true;
 }
@@ -196,7 +206,10 @@ __device__ __forceinline__ bool pr_pressure(double rho, const CompConst& k, doub
 // proj/src/physics.cpp:34-42; *clamped set on a negative radicand.
 __device__ __forceinline__ double pseudo_potential(double rho, double press, const CompConst& k,
                                                    bool& clamped) {
-    const double radicand = (2.0 * (press - PLBM_CS2 * rho)) / k.cs2_g;
+    const double num = 2.0 * (press - PLBM_CS2 * rho);
+    bool ok = true;
+    double radicand = div_nv(num, k.cs2_g, rcp_nv(k.cs2_g), ok);
+    if (!ok) radicand = num / k.cs2_g;
     if (radicand < 0.0) {
         clamped = true;
         return 0.0;
