@@ -79,8 +79,9 @@ void plbm_gpu_kernel_stats(void* h, plbm_kernel_stats* out);
 void plbm_gpu_reset_kernel_stats(void* h);
 
 /* Fused-kernel variant (A/B measurement; all are bit-identical):
- *   0  = default: k_main_pc where it applies (E in {16,32}, C <= 2, a psi
- *        stencil), else k_main_tm, else the plain kernel
+ *   0  = default: k_main_pc where it applies (E in {16,32}, a psi stencil;
+ *        C = 3 at E = 32 uses a 12-CTA non-portable cluster), else the plain
+ *        kernel
  *   1  = plain kernel that pulls every population twice (always used for
  *        E = 8, C = 3 and psi-free scenarios)
  *   2  = k_main_tm: both components per thread, TMEM + smem two-plane stash,
@@ -136,6 +137,19 @@ int plbm_gpu_set_peer_pools(void* h, int rank, void* pool_f, void* pool_pf);
 void plbm_gpu_pool_pointers(void* h, void** pool_f, void** pool_pf);
 int plbm_gpu_tile_rank(void* h, const int32_t* coords);      /* -1 if absent */
 int plbm_gpu_sync(void* h);
+
+/* ---- output path -----------------------------------------
+ * iobench::gather_field (dump.cpp:21-57): one field ("rho", "u_magnitude",
+ * "psi") of one component over the whole domain, x fastest, absent cells at
+ * the ambient fill, values as the reference holds them between steps ("psi"
+ * needs plbm_gpu_set_capture(h, 1) before the step).  grid holds
+ * domain[0]*domain[1]*domain[2] doubles.  0 ok, -2 bad component, -3 bad
+ * field, -4 not captured, -7 multi-rank handle.                              */
+int plbm_gpu_gather_field(void* h, const char* field, int comp, double* grid);
+/* iobench::dump_field (dump.cpp:59-125): <base>.raw / .meta / .pgm, byte for
+ * byte the reference's files.  -5 on a file error.                           */
+int plbm_gpu_dump_field(void* h, const char* field, int comp, int64_t iteration, const char* base_path,
+                        int with_pgm);
 
 /* Engine::~Engine + SimulationState release.                                 */
 void plbm_gpu_destroy(void* h);

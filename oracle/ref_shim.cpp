@@ -13,6 +13,7 @@
 //   plbm_ref_step    -> Engine::step() n times (proj/src/engine.cpp:537-563)
 //   plbm_ref_read_tile / counters / creation_log -> the state callers read
 //                       between steps (SURVEY §8b "State read by callers").
+#include "plbm/dump.hpp"
 #include "plbm/engine.hpp"
 #include "plbm/kernels.hpp"
 #include "plbm/physics.hpp"
@@ -21,6 +22,7 @@
 
 #include "plbm_scenario.h"
 
+#include <array>
 #include <cstdio>
 #include <cstring>
 #include <filesystem>
@@ -37,6 +39,7 @@ struct RefHandle {
     std::unique_ptr<engine::SimulationState> st;
     std::unique_ptr<engine::Engine> eng;
     std::string tmpdir;
+    std::array<int, 3> domain{};
 };
 
 void set_err(plbm_error* e, int code, const std::string& msg) {
@@ -141,6 +144,7 @@ void* plbm_ref_create(const plbm_scenario_desc* d, int workers,
     h->tmpdir = dir;
     try {
         const auto cfg = to_config(d, h->tmpdir);
+        h->domain = cfg.domain;
         h->st = engine::make_state(cfg);
         h->eng = std::make_unique<engine::Engine>(*h->st, workers);
     } catch (const std::exception& e) {
@@ -348,6 +352,57 @@ void plbm_ref_kat_stencil(int* e, double* w, int* opp) {
         w[i] = s.w[i];
         opp[i] = s.opp[i];
     }
+}
+
+// iobench::dump_field on the reference state (proj/src/dump.cpp:59-125).
+int plbm_ref_dump_field(void* hp, const char* field, int comp, long iteration,
+                        const char* base_path, int with_pgm) {
+    auto* h = static_cast<RefHandle*>(hp);
+    try {
+        iobench::dump_field(h->st->map, h->domain, field, comp, iteration,
+                            base_path, with_pgm != 0);
+    } catch (const std::exception&) {
+        return -5;
+    }
+    return 0;
+}
+
+// The reference driver itself, engine::run_scenario (proj/src/engine.cpp:
+// 580-704): time_series.csv, creation_log.csv, summary.json and snapshots
+// under output_dir.  fields: comma-separated snapshot field names.
+int plbm_ref_run_scenario(const plbm_scenario_desc* d, int workers,
+                          long iterations, int report_interval,
+                          int snapshot_interval, const char* fields,
+                          int with_pgm, const char* name,
+                          const char* output_dir) {
+    char tmpl[] = "/tmp/plbm_refrun_XXXXXX";
+    const char* dir = mkdtemp(tmpl);
+    if (!dir) return -3;
+    int rc = 0;
+    try {
+        auto cfg = to_config(d, dir);
+        cfg.name = name;
+        cfg.workers = workers;
+        cfg.iterations = iterations;
+        cfg.report_interval = report_interval;
+        cfg.snapshot_interval = snapshot_interval;
+        cfg.snapshot_pgm = with_pgm != 0;
+        cfg.output_dir = output_dir;
+        cfg.snapshot_fields.clear();
+        std::string f = fields ? fields : "";
+        size_t p = 0;
+        while (p < f.size()) {
+            const size_t q = f.find(',', p);
+            cfg.snapshot_fields.push_back(f.substr(p, q == std::string::npos ? std::string::npos : q - p));
+            if (q == std::string::npos) break;
+            p = q + 1;
+        }
+        engine::run_scenario(cfg);
+    } catch (const std::exception&) {
+        rc = -2;
+    }
+    std::filesystem::remove_all(dir);
+    return rc;
 }
 
 } // extern "C"

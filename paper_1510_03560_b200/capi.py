@@ -129,6 +129,16 @@ class StepEngine:
         if self._fn("poke_f")(self._h, cc, comp, i, ll, value) != 0:
             raise KeyError("poke_f: no such tile")
 
+    def dump_field(self, field: str, comp: int, iteration: int, base_path: str,
+                   with_pgm: bool = False) -> None:
+        """iobench::dump_field (proj/src/dump.cpp:59-125): <base>.raw/.meta[/.pgm]."""
+        fn = self._fn("dump_field")
+        fn.restype = C.c_int
+        fn.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_long, C.c_char_p, C.c_int]
+        rc = fn(self._h, field.encode(), comp, iteration, base_path.encode(), int(with_pgm))
+        if rc != 0:
+            raise RuntimeError(f"{self.prefix}_dump_field({field}, {comp}) failed: rc={rc}")
+
     def close(self) -> None:
         if self._h:
             self._fn("destroy")(self._h)
@@ -149,6 +159,23 @@ class StepEngine:
 
 def ref_engine(sc: Scenario, workers: int = 1) -> StepEngine:
     return StepEngine(sc, REF_LIB, "plbm_ref", workers)
+
+
+def ref_run_scenario(sc: Scenario, output_dir: str, iterations: int, report_interval: int = 10,
+                     snapshot_interval: int = 0, fields=("rho",), with_pgm: bool = False,
+                     name: str = "shim", workers: int = 1) -> None:
+    """The reference driver itself (engine::run_scenario, proj/src/engine.cpp:
+    580-704), through the test shim: writes the reference's output files."""
+    lib = load(REF_LIB, "plbm_ref")
+    fn = lib.plbm_ref_run_scenario
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_void_p, C.c_int, C.c_long, C.c_int, C.c_int, C.c_char_p, C.c_int,
+                   C.c_char_p, C.c_char_p]
+    cs = sc.to_c()
+    rc = fn(C.cast(cs.ptr(), C.c_void_p), workers, iterations, report_interval, snapshot_interval,
+            ",".join(fields).encode(), int(with_pgm), name.encode(), output_dir.encode())
+    if rc != 0:
+        raise RuntimeError(f"plbm_ref_run_scenario failed: rc={rc}")
 
 
 def oracle_engine(sc: Scenario) -> StepEngine:
@@ -291,6 +318,19 @@ class GpuEngine(StepEngine):
 
     def sync(self) -> None:
         self.lib.plbm_gpu_sync(self._h)
+
+    def gather_field(self, field: str, comp: int) -> np.ndarray:
+        """iobench::gather_field (proj/src/dump.cpp:21-57): the domain grid,
+        indexed [z, y, x]."""
+        d = self.scenario.domain
+        out = np.empty(d[0] * d[1] * d[2], np.float64)
+        fn = self.lib.plbm_gpu_gather_field
+        fn.restype = C.c_int
+        fn.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_void_p]
+        rc = fn(self._h, field.encode(), comp, out.ctypes.data_as(C.c_void_p))
+        if rc != 0:
+            raise RuntimeError(f"plbm_gpu_gather_field({field}, {comp}) failed: rc={rc}")
+        return out.reshape(d[2], d[1], d[0])
 
     def set_kernel_variant(self, variant: int) -> None:
         """0 = TMEM/smem-stash cluster kernel where it applies, 1 = plain kernel."""

@@ -104,6 +104,7 @@ struct Kernels {
     MainFn main_pc2;    // variant 22: as 21 with psi computed two planes ahead
     void (*face)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
     void (*readback)(Dev, int, int, int, double*, cudaStream_t);
+    void (*gather)(Dev, const int*, int, int, int, int, double*, int, int, cudaStream_t);
     int nt;
 };
 
@@ -171,18 +172,28 @@ Kernels make_kernels() {
         reg_tm<E, C, 0>(k.main_tm_opt, S);
         reg_tm<E, C, TM_MEMONLY>(k.main_tm_opt, S);
         k.main_tm = k.main_tm_opt[TM_DEFAULT_OPT];
-        cudaFuncSetAttribute(k_main_pc<E, C, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             PcCfg<E, C, 1>::SMEM);
-        cudaFuncSetAttribute(k_main_pc<E, C, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             PcCfg<E, C, 2>::SMEM);
+    }
+    if constexpr (!NOPSI && (E == 16 || E == 32)) {
+        auto setup = [](auto fn, int smem, int cl) {
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (cl > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        };
+        setup(k_main_pc<E, C, 1>, PcCfg<E, C, 1>::SMEM, PcCfg<E, C, 1>::CL);
         k.main_pc = launch_pc<E, C, 1>;
-        k.main_pc2 = launch_pc<E, C, 2>;
+        if constexpr (C <= 2) {
+            setup(k_main_pc<E, C, 2>, PcCfg<E, C, 2>::SMEM, PcCfg<E, C, 2>::CL);
+            k.main_pc2 = launch_pc<E, C, 2>;
+        }
     }
     k.face = [](Dev d, const int* act, int src, int flags, long it, unsigned ntiles, cudaStream_t s) {
         k_face<E, C, NT><<<ntiles * 6, NT, 0, s>>>(d, act, src, flags, it);
     };
     k.readback = [](Dev d, int slot, int c, int src, double* out, cudaStream_t s) {
         k_readback<E><<<(E * E * E + 255) / 256, 256, 0, s>>>(d, slot, c, src, out);
+    };
+    k.gather = [](Dev d, const int* act, int ntiles, int kind, int c, int src, double* grid, int D0, int D1,
+                  cudaStream_t s) {
+        k_gather<E><<<dim3((E * E * E + 255) / 256, ntiles), 256, 0, s>>>(d, act, kind, c, src, grid, D0, D1);
     };
     return k;
 }
@@ -253,6 +264,8 @@ class Engine {
     void counters(plbm_counters* out);
     int tiles(int32_t* coords, int32_t* owners, int64_t* births, int max) const;
     int read_tile(const int32_t* coords, int comp, int field, double* out);
+    int gather_field(const char* field, int comp, double* grid);
+    int dump_field(const char* field, int comp, long iteration, const char* base, int with_pgm);
     int creation_log(plbm_creation_event* out, int max) const;
     int set_capture(bool on);
     int poke_f(const int32_t* coords, int comp, int i, const int32_t* local, double v);
@@ -1349,6 +1362,83 @@ int Engine::read_tile(const int32_t* cc, int comp, int field, double* out) {
     return 0;
 }
 
+// gather_field (dump.cpp:21-57): the whole domain, x fastest, ambient fill.
+int Engine::gather_field(const char* field, int comp, double* grid) {
+    const std::string f = field ? field : "";
+    const int kind = f == "rho" ? 0 : f == "u_magnitude" ? 1 : f == "psi" ? 2 : -1;
+    if (kind < 0) return -3;
+    if (comp < 0 || comp >= C_) return -2;
+    if (world_ != 1) return -7;
+    if (kind == 2 && !d_capture_) return -4;
+    // dump.cpp:15-20 ambient_fill: rho_ambient / psi_ambient / 0
+    const double fill = kind == 0 ? params_.comp[comp].rho_amb : kind == 2 ? params_.comp[comp].psi_amb : 0.0;
+    const size_t n = size_t(dom_[0]) * dom_[1] * dom_[2];
+    double* d_grid = nullptr;
+    CK(cudaMallocAsync(&d_grid, n * sizeof(double), stream_));
+    k_fill<<<148 * 8, 256, 0, stream_>>>(d_grid, n, fill);
+    if (!active_.empty())
+        K_.gather(d_, d_active_, int(active_.size()), kind, comp, cur_, d_grid, dom_[0], dom_[1], stream_);
+    CK(cudaGetLastError());
+    stats_.kernels_launched += 2;
+    CK(cudaMemcpyAsync(grid, d_grid, n * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    CK(cudaFreeAsync(d_grid, stream_));
+    CK(cudaStreamSynchronize(stream_));
+    stats_.d2h_bytes += n * sizeof(double);
+    return 0;
+}
+
+// dump_field (dump.cpp:59-125): <base>.raw (float64 grid), <base>.meta and,
+// with_pgm, <base>.pgm (mid-z slice, min-max normalised to 8 bits), byte for
+// byte the files the reference writes.
+int Engine::dump_field(const char* field, int comp, long iteration, const char* base, int with_pgm) {
+    std::vector<double> grid(size_t(dom_[0]) * dom_[1] * dom_[2]);
+    const int rc = gather_field(field, comp, grid.data());
+    if (rc) return rc;
+    const std::string b = base;
+    {
+        FILE* fp = std::fopen((b + ".raw").c_str(), "wb");
+        if (!fp) return -5;
+        const size_t w = std::fwrite(grid.data(), sizeof(double), grid.size(), fp);
+        std::fclose(fp);
+        if (w != grid.size()) return -5;
+    }
+    double lo = grid[0], hi = grid[0];
+    if (with_pgm)
+        for (double v : grid) {
+            lo = std::min(lo, v);
+            hi = std::max(hi, v);
+        }
+    const std::string fs = field;
+    const double fill = fs == "rho" ? params_.comp[comp].rho_amb : fs == "psi" ? params_.comp[comp].psi_amb : 0.0;
+    {
+        FILE* fp = std::fopen((b + ".meta").c_str(), "w");
+        if (!fp) return -5;
+        // std::ostream with precision(17), default float field == %.17g
+        std::fprintf(fp, "dims %d %d %d\nfield %s\ncomponent %d\niteration %ld\nfill %.17g\n"
+                         "layout x-fastest float64 little-endian\n",
+                     dom_[0], dom_[1], dom_[2], field, comp, iteration, fill);
+        if (with_pgm) std::fprintf(fp, "pgm_min %.17g\npgm_max %.17g\n", lo, hi);
+        std::fclose(fp);
+    }
+    if (with_pgm) {
+        FILE* fp = std::fopen((b + ".pgm").c_str(), "wb");
+        if (!fp) return -5;
+        std::fprintf(fp, "P5\n%d %d\n255\n", dom_[0], dom_[1]);
+        const size_t z = size_t(dom_[2] / 2);
+        const double scale = hi > lo ? 255.0 / (hi - lo) : 0.0;
+        std::vector<uint8_t> row(static_cast<size_t>(dom_[0]));
+        for (int y = 0; y < dom_[1]; ++y) {
+            for (int x = 0; x < dom_[0]; ++x) {
+                const double v = grid[size_t(x) + size_t(dom_[0]) * (size_t(y) + size_t(dom_[1]) * z)];
+                row[size_t(x)] = uint8_t(std::lround((v - lo) * scale));
+            }
+            std::fwrite(row.data(), 1, row.size(), fp);
+        }
+        std::fclose(fp);
+    }
+    return 0;
+}
+
 int Engine::creation_log(plbm_creation_event* out, int max) const {
     for (size_t k = 0; k < log_.size() && int(k) < max; ++k) {
         out[k].iteration = log_[k].iteration;
@@ -1507,6 +1597,23 @@ int plbm_gpu_set_peer_pools(void* h, int rank, void* pool_f, void* pool_pf) {
 }
 
 void plbm_gpu_pool_pointers(void* h, void** pool_f, void** pool_pf) { EG(h)->pool_pointers(pool_f, pool_pf); }
+
+int plbm_gpu_gather_field(void* h, const char* field, int comp, double* grid) {
+    try {
+        return EG(h)->gather_field(field, comp, grid);
+    } catch (const std::exception&) {
+        return -6;
+    }
+}
+
+int plbm_gpu_dump_field(void* h, const char* field, int comp, int64_t iteration, const char* base_path,
+                        int with_pgm) {
+    try {
+        return EG(h)->dump_field(field, comp, iteration, base_path, with_pgm);
+    } catch (const std::exception&) {
+        return -6;
+    }
+}
 
 int plbm_gpu_tile_rank(void* h, const int32_t* coords) { return EG(h)->rank_of(coords); }
 

@@ -837,4 +837,56 @@ __global__ void k_readback(Dev d, int slot, int c, int src_buf, double* out) {
     }
 }
 
+// Snapshot gather (dump.cpp:21-57, gather_field): one field of one component
+// of every active tile into the domain grid (x fastest), as the reference
+// holds it between steps.  kind 0 = rho (0 on solid cells), 1 = |u| =
+// sqrt((ux ux + uy uy) + uz uz), 2 = psi (from the capture buffer: psi of the
+// step's P1).  grid is pre-filled with the ambient value; grid.y = tile.
+template <int E>
+__global__ void k_gather(Dev d, const int* __restrict__ active, int kind, int c, int src_buf,
+                         double* grid, int D0, int D1) {
+    constexpr int E3 = E * E * E;
+    constexpr int G = E + 2;
+    __shared__ RouteTab rt;
+    __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
+    __shared__ int s_tc[3];
+    const int slot = active[blockIdx.y];
+    const uint8_t mode = d.mode[slot];
+    const bool hs = d.has_solid[slot] != 0;
+    load_routes(rt, d.route[ROUTE_PULL] + size_t(slot) * 18, slot, P.amb_slot, d.slot_f[src_buf]);
+    if (threadIdx.x < 3) s_tc[threadIdx.x] = d.coords[slot * 3 + threadIdx.x];
+    if (hs)
+        for (int k = threadIdx.x; k < d.solid_words; k += blockDim.x)
+            s_solid[k] = d.solid[size_t(slot) * d.solid_words + k];
+    __syncthreads();
+    const int li = d.lidx[slot];
+    for (int cell = blockIdx.x * blockDim.x + threadIdx.x; cell < E3; cell += gridDim.x * blockDim.x) {
+        const int x = cell % E, y = (cell / E) % E, z = cell / (E * E);
+        const bool sol = hs && solid_at<E>(s_solid, x, y, z);
+        double v = 0.0;
+        if (kind == 2) {
+            v = d.capture[(size_t(li) * P.C + c) * 4 * E3 + cell];
+        } else if (!sol || kind == 1) {
+            double f[Q], u0 = 0.0, u1 = 0.0, u2 = 0.0, rho = 0.0;
+            if (sol) {
+                // u of a solid cell is never written by the reference: 0
+            } else if (mode == MODE_PULL) {
+                pull_cell<E>(rt, c, hs, s_solid, x, y, z, f);
+                moments(f, rho, u0, u1, u2);
+            } else {
+                gen_fin<E>(mode, c, s_tc, x, y, z, f, u0, u1, u2);
+                const int s = mode == MODE_GEN_SEEDED ? seed_for<E>(c, s_tc, x, y, z) : -1;
+                rho = s >= 0 ? P.seeds[s].rho : P.comp[c].rho_amb;
+            }
+            v = kind == 0 ? rho : sqrt(u0 * u0 + u1 * u1 + u2 * u2);
+        }
+        grid[size_t(s_tc[0] * E + x) + size_t(D0) * (size_t(s_tc[1] * E + y) + size_t(D1) * size_t(s_tc[2] * E + z))] = v;
+    }
+}
+
+__global__ void k_fill(double* p, size_t n, double v) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+
 }  // namespace plbm

@@ -19,7 +19,8 @@
 // components) through distributed shared memory with st.async, completing
 // transactions on the receiver's per-plane mbarrier.
 //
-// Cluster = NB y-blocks x C components of one tile (E = 32: 4 x 2 = 8 CTAs).
+// Cluster = NB y-blocks x C components of one tile (E = 32: 4 x 2 = 8 CTAs;
+// 4 x 3 = 12 at C = 3, a non-portable cluster size B200 supports).
 // Per plane z:  wait landing(z+1) | psi pass z+1 -> TMEM, push psi | issue
 //               pulls(z+2) | CTA barrier | issue ghosts(z+2) | wait pushes(z+1)
 //               | collide z from TMEM.
@@ -86,7 +87,7 @@ struct PcCfg {
     static constexpr int LAND_BYTES = Q * NT * 8;
     static constexpr int XST_BYTES = 2 * 4 * Q * BY * 8;  // x-column staging, two planes
     static constexpr int SMEM = PSI_BYTES + LAND_BYTES + XST_BYTES;
-    static_assert(CL <= 8, "portable cluster size");
+    static_assert(CL <= 16, "cluster size (> 8 needs the non-portable opt-in)");
     static_assert(TSLOTS * CB <= NCOLS / 2, "TMEM plane slots do not fit");
     static_assert(2 * (SMEM + 8 * 1024) <= 228 * 1024, "two CTAs per SM must fit");
 };

@@ -273,6 +273,8 @@ def mpmc_release(n: int = 256, extent: int = 32, mode: int = MODE_PROGRESSIVE,
     coupled to both (C5)."""
     dom = tuple(domain) if domain is not None else (n, n, n)
     comps = [pr_heavy(), ideal_light()]
+    if n_components == 1:  # single-component multiphase (PR liquid/vapour only)
+        comps = [pr_heavy()]
     if n_components == 3:
         comps.append(Component(tau=1.0, T=2.0 / 3.0, g_self=1.0, rho_ambient=0.3))
     nc = len(comps)

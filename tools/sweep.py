@@ -1,0 +1,104 @@
+#!/usr/bin/env python
+"""Measurement sweeps on one B200 (results -> JSON lines on stdout).
+
+    python tools/sweep.py c5 [--n 256] [--steps 20]
+        BASELINE configs[4] on one GPU: tile extent E in {16, 32} x components
+        C in {1, 2, 3}, static full-domain MPMC (all tiles active), MLUPS per
+        component of the whole step and of the fused kernel.
+    python tools/sweep.py c3 [--n 512] [--steps 300]
+        BASELINE configs[2], the paper's comparison: the same MPMC release run
+        on the progressive mesh and on the static full-domain mesh for the
+        same number of steps; wall time on the device, tiles over time.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+
+from paper_1510_03560_b200 import capi  # noqa: E402
+from paper_1510_03560_b200 import scenario as S  # noqa: E402
+
+BYTES = 304
+
+
+def timed(eng, steps, chunk=1):
+    import torch
+    stream = torch.cuda.ExternalStream(eng.stream())
+    eng.reset_kernel_stats()
+    eng.set_profiling(True)
+    c0 = eng.counters()["cell_updates"]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    done = 0
+    while done < steps:
+        k = min(chunk, steps - done)
+        eng.step(k)
+        done += k
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ks = eng.kernel_stats()
+    eng.set_profiling(False)
+    return e0.elapsed_time(e1), eng.counters()["cell_updates"] - c0, ks
+
+
+def c5(a):
+    for E in (16, 32):
+        for C in (1, 2, 3):
+            sc = S.mpmc_release(n=a.n, extent=E, mode=S.MODE_STATIC, n_components=C)
+            eng = capi.gpu_engine(sc)
+            eng.step(a.warmup)
+            ms, cells, ks = timed(eng, a.steps, chunk=a.steps)
+            main = ks["main_cell_updates"] * C * BYTES / (ks["main_ms"] / 1e3) / 1e9
+            print(json.dumps({
+                "sweep": "c5", "E": E, "C": C, "domain": a.n, "tiles": eng.counters()["tiles"],
+                "steps": a.steps, "ms_per_step": round(ms / a.steps, 4),
+                "mlups_per_comp": round(cells * C / (ms / 1e3) / 1e6, 1),
+                "k_main_ms": round(ks["main_ms"] / max(ks["main_launches"], 1), 4),
+                "k_face_ms": round(ks["face_ms"] / max(ks["face_launches"], 1), 4),
+                "k_main_algorithmic_GBs": round(main, 1)}), flush=True)
+            eng.close()
+
+
+def c3(a):
+    out = {}
+    for mode, name in ((S.MODE_PROGRESSIVE, "progressive"), (S.MODE_STATIC, "static")):
+        sc = S.mpmc_release(n=a.n, extent=32, mode=mode, threshold=1e-9)
+        eng = capi.gpu_engine(sc)
+        series = []
+        total_ms = 0.0
+        for k0 in range(0, a.steps, a.every):
+            ms, cells, _ = timed(eng, min(a.every, a.steps - k0), chunk=1 if mode == S.MODE_PROGRESSIVE else a.every)
+            total_ms += ms
+            series.append({"step": k0 + a.every, "tiles": eng.counters()["tiles"], "ms": round(ms, 3)})
+        out[name] = {"total_ms": round(total_ms, 2), "final_tiles": eng.counters()["tiles"],
+                     "cell_updates": eng.counters()["cell_updates"], "series": series}
+        eng.close()
+    out["speedup_progressive_vs_static"] = round(out["static"]["total_ms"] / out["progressive"]["total_ms"], 3)
+    print(json.dumps({"sweep": "c3", "domain": a.n, "steps": a.steps, **out}), flush=True)
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("what", choices=["c5", "c3"])
+    p.add_argument("--n", type=int, default=None)
+    p.add_argument("--steps", type=int, default=None)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--every", type=int, default=25)
+    a = p.parse_args()
+    if a.what == "c5":
+        a.n = a.n or 256
+        a.steps = a.steps or 20
+        c5(a)
+    else:
+        a.n = a.n or 512
+        a.steps = a.steps or 300
+        c3(a)
+
+
+if __name__ == "__main__":
+    main()
