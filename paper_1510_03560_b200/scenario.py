@@ -304,3 +304,91 @@ def mpmc_release_weak(n_blocks: int, n: int = 256, extent: int = 32, threshold: 
     sc.seeds = seeds
     sc.name = f"mpmc_release_weak_x{n_blocks}"
     return sc
+
+
+# ---- 3-D channel network --------------------------
+def channel_network(nx: int = 1024, ny: int = 512, nz: int = 512, seed: int = 1510,
+                    radius: Optional[float] = None) -> np.ndarray:
+    """Deterministic 3-D channel network in solid rock, uint8 [nz, ny, nx]
+    (x fastest, 1 = solid), the geometry of BASELINE config 4.
+
+    An inlet channel runs along +x from x = 0 on the domain axis; at a quarter
+    of the length it splits into four branches that wander (seeded random
+    turns) towards the far end, each splitting once more.  Channels are
+    capsules (cylinders with round ends) of radius r (r/2 for the last
+    level).  Every dimension scales with the domain, so a 64 x 32 x 32 copy
+    is the parity-test version of the same network (three branching levels,
+    radius r, 0.8 r, 0.65 r, 0.5 r; r = ny / 14 by default)."""
+    rng = np.random.default_rng(seed)
+    r0 = radius if radius is not None else max(2.0, ny / 14.0)
+    g = np.ones((nz, ny, nx), np.uint8)
+    zz, yy, xx = (np.arange(n, dtype=np.float64) + 0.5 for n in (nz, ny, nx))
+
+    def capsule(p, q, r):
+        p, q = np.asarray(p, float), np.asarray(q, float)
+        lo = np.maximum(np.floor(np.minimum(p, q) - r - 1).astype(int), 0)
+        hi = np.minimum(np.ceil(np.maximum(p, q) + r + 1).astype(int), (nx, ny, nz))
+        if np.any(hi <= lo):
+            return
+        X = xx[lo[0]:hi[0]][None, None, :]
+        Y = yy[lo[1]:hi[1]][None, :, None]
+        Z = zz[lo[2]:hi[2]][:, None, None]
+        d = q - p
+        L2 = float(d @ d) or 1.0
+        t = np.clip(((X - p[0]) * d[0] + (Y - p[1]) * d[1] + (Z - p[2]) * d[2]) / L2, 0.0, 1.0)
+        dist2 = (X - p[0] - t * d[0]) ** 2 + (Y - p[1] - t * d[1]) ** 2 + (Z - p[2] - t * d[2]) ** 2
+        sub = g[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]]
+        sub[dist2 <= r * r] = 0
+
+    def wander(p, direction, length, r, steps):
+        pts = [np.asarray(p, float)]
+        d = np.asarray(direction, float)
+        d /= np.linalg.norm(d)
+        for _ in range(steps):
+            turn = rng.normal(0.0, 0.35, 3)
+            turn[0] = abs(turn[0]) * 0.2  # keep heading downstream
+            d = d + turn
+            d[0] = max(d[0], 0.35)
+            d /= np.linalg.norm(d)
+            q = pts[-1] + d * (length / steps)
+            q = np.clip(q, [0, r + 1, r + 1], [nx - 1, ny - r - 1, nz - r - 1])
+            capsule(pts[-1], q, r)
+            pts.append(q)
+        return pts[-1], d
+
+    inlet = np.array([0.0, ny / 2.0, nz / 2.0])
+    junction = np.array([nx / 4.0, ny / 2.0, nz / 2.0])
+    capsule(inlet, junction, r0)
+    for dy, dz in ((1, 1), (1, -1), (-1, 1), (-1, -1)):
+        end, d = wander(junction, (1.0, 0.6 * dy, 0.6 * dz), nx * 0.3, r0 * 0.8, 6)
+        for s in (1, -1):
+            end2, d2 = wander(end, (1.0, d[1] + 0.5 * s, d[2] - 0.5 * s), nx * 0.25, r0 * 0.65, 5)
+            for t in (1, -1):
+                wander(end2, (1.0, d2[1] - 0.5 * t, d2[2] + 0.5 * t), nx * 0.25, r0 * 0.5, 5)
+    return g
+
+
+def mpmc_channel(nx: int = 1024, ny: int = 512, nz: int = 512, extent: int = 32,
+                 threshold: float = 1e-9, mode: int = MODE_PROGRESSIVE, devices: int = 1,
+                 seed: int = 1510) -> Scenario:
+    """C4: C2's two-component MPMC with the ramped liquid sphere wholly inside
+    the inlet channel of the 3-D channel network."""
+    geo = channel_network(nx, ny, nz, seed)
+    comps = [pr_heavy(), ideal_light()]
+    g = np.full((2, 2), 0.08)
+    np.fill_diagonal(g, 0.0)
+    r0 = max(2.0, ny / 14.0)
+    core = r0 * 0.5
+    center = (nx / 8.0, ny / 2.0, nz / 2.0)
+    seeds = ramped_sphere_seeds(center, core, 6.5, comps[0].rho_ambient, max(1, int(r0 * 0.4)), 0)
+    return Scenario(domain=(nx, ny, nz), tile_extent=extent, mode=mode, threshold=threshold,
+                    devices=devices, components=comps, coupling=g, seeds=seeds, geometry=geo,
+                    name="mpmc_channel")
+
+
+def save_lbmgeo(mask: np.ndarray, path: str) -> None:
+    """LBMGEO v1 (proj/src/geometry.cpp:64-75): 'LBMGEO v1 nx ny nz\\n' + bytes."""
+    nz, ny, nx = mask.shape
+    with open(path, "wb") as fh:
+        fh.write(f"LBMGEO v1 {nx} {ny} {nz}\n".encode())
+        fh.write(np.ascontiguousarray(mask, np.uint8).tobytes())

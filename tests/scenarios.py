@@ -109,7 +109,14 @@ def mpmc_e16_solid(n=32):
     return sc
 
 
+def mpmc_channel_e16():
+    """C4 geometry at test scale: the 3-D channel network, liquid sphere in the
+    inlet channel, progressive."""
+    return S.mpmc_channel(nx=128, ny=64, nz=64, extent=16, threshold=1e-10)
+
+
 ALL.update({
+    "mpmc_channel_e16": (mpmc_channel_e16, 16),
     "mpmc_e32": (mpmc_e32, 8),
     "mpmc_e32_solid_periodic": (mpmc_e32_solid_periodic, 6),
     "mpmc3_e32": (mpmc3_e32, 6),

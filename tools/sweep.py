@@ -5,6 +5,9 @@
         BASELINE configs[4] on one GPU: tile extent E in {16, 32} x components
         C in {1, 2, 3}, static full-domain MPMC (all tiles active), MLUPS per
         component of the whole step and of the fused kernel.
+    python tools/sweep.py c4 [--steps 400]
+        BASELINE configs[3] on one GPU: MPMC release in the 3-D channel
+        network (scenario.channel_network) at 1024x512x512, progressive.
     python tools/sweep.py c3 [--n 512] [--steps 300]
         BASELINE configs[2], the paper's comparison: the same MPMC release run
         on the progressive mesh and on the static full-domain mesh for the
@@ -82,9 +85,31 @@ def c3(a):
     print(json.dumps({"sweep": "c3", "domain": a.n, "steps": a.steps, **out}), flush=True)
 
 
+def c4(a):
+    """BASELINE configs[3] on one GPU: the 3-D channel network at full size,
+    progressive mesh (the static full domain, 8192 tiles, does not fit one
+    GPU's HBM with two population buffers)."""
+    t0 = time.time()
+    sc = S.mpmc_channel(nx=1024, ny=512, nz=512, extent=32, threshold=1e-9)
+    eng = capi.gpu_engine(sc)
+    setup_s = time.time() - t0
+    series, total_ms, cells = [], 0.0, 0
+    for k0 in range(0, a.steps, a.every):
+        ms, c, ks = timed(eng, min(a.every, a.steps - k0))
+        total_ms += ms
+        cells += c
+        series.append({"step": k0 + a.every, "tiles": eng.counters()["tiles"], "ms": round(ms, 3),
+                       "mlups_per_comp": round(c * 2 / (ms / 1e3) / 1e6, 1)})
+    print(json.dumps({"sweep": "c4", "domain": list(sc.domain), "fluid_fraction": round(1 - float(sc.geometry.mean()), 4),
+                      "setup_s": round(setup_s, 2), "steps": a.steps, "total_ms": round(total_ms, 2),
+                      "final_tiles": eng.counters()["tiles"], "tiles_total": 8192,
+                      "mlups_per_comp": round(cells * 2 / (total_ms / 1e3) / 1e6, 1), "series": series}), flush=True)
+    eng.close()
+
+
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("what", choices=["c5", "c3"])
+    p.add_argument("what", choices=["c5", "c3", "c4"])
     p.add_argument("--n", type=int, default=None)
     p.add_argument("--steps", type=int, default=None)
     p.add_argument("--warmup", type=int, default=3)
@@ -94,6 +119,10 @@ def main():
         a.n = a.n or 256
         a.steps = a.steps or 20
         c5(a)
+    elif a.what == "c4":
+        a.steps = a.steps or 400
+        a.every = 50
+        c4(a)
     else:
         a.n = a.n or 512
         a.steps = a.steps or 300
