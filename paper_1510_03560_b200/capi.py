@@ -22,7 +22,7 @@ from .scenario import (Counters, CreationEvent, EngineError, Error, FACE_NAMES,
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(_HERE)
-GPU_LIB = os.path.join(_HERE, "libplbm_gpu.so")
+GPU_LIB = os.environ.get("PLBM_GPU_LIB", os.path.join(_HERE, "libplbm_gpu.so"))
 ORACLE_LIB = os.path.join(REPO, "oracle", "_build", "libplbm_oracle.so")
 REF_LIB = os.path.join(REPO, "oracle", "_ref", "libplbm_ref.so")
 

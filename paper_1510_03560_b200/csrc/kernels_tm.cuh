@@ -281,9 +281,9 @@ __device__ __forceinline__ void gen_u(int mode, int c, const int* tc, int x, int
 }
 
 // OPT bits (A/B variants, all bit-identical)
-constexpr int TM_ILV = 1;  // psi pass: all components' loads in flight together
-constexpr int TM_PF = 2;   // bulk L2 prefetch of the next psi pass's source rows
-constexpr int TM_WSYNC = 4; // per-warp neighbour sync (mbarriers) instead of a CTA barrier per plane
+// (Measured and removed: both components' loads in flight together, an L2
+// bulk prefetch of the next plane, per-warp mbarrier sync instead of the CTA
+// barrier — none faster.)
 constexpr int TM_MEMONLY = 8; // measurement only (NOT the physics): same loads, stash and stores, no FP64 work
 constexpr int TM_DEFAULT_OPT = 0;
 
@@ -306,7 +306,6 @@ __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict
     // pushed psi rows by plane parity: [0..1] row -1 (from the -y peer, read by
     // block row 0), [2..3] row BY (from the +y peer, read by block row BY-1)
     __shared__ __align__(8) uint64_t s_mbar[4];
-    __shared__ __align__(8) uint64_t s_wbar[2][NT / 32];  // TM_WSYNC: warp w's plane is ready
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -335,9 +334,6 @@ __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict
     if (tid == 0) {
         for (int k = 0; k < 4; ++k)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&s_mbar[k])), "r"(1));
-        for (int k = 0; k < 2 * (NT / 32); ++k)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&s_wbar[0][0] + k)),
-                         "r"(32));
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -443,51 +439,6 @@ __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict
         }
     };
 
-    // TM_WSYNC: the x-ring entries of this warp's rows, and the halo row next
-    // to a block edge (whole row at a tile edge, else only its two x-ring
-    // corners: the rest is pushed by the cluster neighbour).  Everything warp
-    // w's collide reads is then produced by warps w-1, w, w+1 (or pushed).
-    constexpr int RPW = 32 / E > 0 ? 32 / E : 1;  // block rows per warp
-    auto fill_ring_w = [&](int pz) {
-        const int ring = pz & 3;
-        const int lane = tid & 31;
-        const int r0 = warp * RPW;
-        const bool lo = r0 == 0, hi = r0 + RPW == BY;
-        const bool lo_full = lo && y0 == 0, hi_full = hi && y0 + BY == E;
-        const int nlo = lo ? (lo_full ? E + 2 : 2) : 0;
-        const int nhi = hi ? (hi_full ? E + 2 : 2) : 0;
-        for (int k = lane; k < 2 * RPW + nlo + nhi; k += 32) {
-            int xx, yyl;
-            if (k < 2 * RPW) {
-                yyl = r0 + (k >> 1);
-                xx = (k & 1) ? E : -1;
-            } else if (k < 2 * RPW + nlo) {
-                const int q = k - 2 * RPW;
-                yyl = -1;
-                xx = lo_full ? q - 1 : ((q & 1) ? E : -1);
-            } else {
-                const int q = k - 2 * RPW - nlo;
-                yyl = BY;
-                xx = hi_full ? q - 1 : ((q & 1) ? E : -1);
-            }
-#pragma unroll 1
-            for (int c = 0; c < C; ++c)
-                psi[pidx(ring, c, xx, yyl)] = psi_ghost<E>(rt_psi, c, hs, s_solid, xx, y0 + yyl, pz);
-        }
-    };
-    auto wbar_wait = [&](int w, int z) {
-        const uint32_t bar = smem_u32(&s_wbar[z & 1][w]);
-        const uint32_t parity = uint32_t((z >> 1) & 1);
-        uint32_t ok = 0;
-        while (!ok)
-            asm volatile(
-                "{\n .reg .pred q;\n mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2, 1000000;\n"
-                " selp.u32 %0, 1, 0, q;\n}\n"
-                : "=r"(ok)
-                : "r"(bar), "r"(parity)
-                : "memory");
-    };
-
     // ---- psi pass of plane pz: pull f_in, rho -> psi (P1), stash -------------
     auto psi_pass = [&](int pz) {
         const int ring = pz & 3;
@@ -542,20 +493,11 @@ __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict
                 st[Q * NT] = rho;
             }
         };
-        if constexpr (OPT & TM_ILV) {
-            // every component's 19 loads in flight before the first sum
-            double f[C][Q];
-#pragma unroll
-            for (int c = 0; c < C; ++c) load(c, f[c]);
-#pragma unroll
-            for (int c = 0; c < C; ++c) finish(c, f[c]);
-        } else {
 #pragma unroll 1
-            for (int c = 0; c < C; ++c) {
-                double f[Q];
-                load(c, f);
-                finish(c, f);
-            }
+        for (int c = 0; c < C; ++c) {
+            double f[Q];
+            load(c, f);
+            finish(c, f);
         }
         if ((pz & 1) == 0) asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         const unsigned m1 = __reduce_add_sync(0xffffffffu, (unsigned)negs);
@@ -652,63 +594,21 @@ __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict
         if ((tid & 31) == 0 && zr) atomicAdd(&d.cnt[CNT_ZERO_RHO], (unsigned long long)zr);
     };
 
-    // ---- L2 prefetch of the rows the psi pass of plane pz pulls from --------
-    // One bulk prefetch per (component, direction): the source plane pz - ez_i,
-    // rows y0-1 .. y0+BY of this tile's f_post block (contiguous in SoA), so the
-    // psi pass one iteration later reads from L2 instead of waiting on DRAM.
-    auto prefetch_plane = [&](int pz) {
-        if constexpr (OPT & TM_PF) {
-            if (mode != MODE_PULL || pz >= E || tid >= C * Q) return;
-            const int c = tid / Q, i = tid - c * Q;
-            int ez = 0;
-#pragma unroll
-            for (int j = 0; j < Q; ++j)
-                if (j == i) ez = ez_(j);
-            const int sz = pz - ez;
-            if (sz < 0 || sz >= E) return;
-            const int ylo = y0 > 0 ? y0 - 1 : 0;
-            const int yhi = y0 + BY < E ? y0 + BY : E - 1;
-            const double* src = rt_pull.p[13] + (size_t(c) * Q + i) * E3 + size_t(sz * E + ylo) * E;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src),
-                         "r"(uint32_t((yhi - ylo + 1) * E * 8))
-                         : "memory");
-        }
-    };
-
-    prefetch_plane(1);
-    constexpr bool WS = (OPT & TM_WSYNC) != 0;
     fill_zghost(-1);
     expect_rows(0);
     psi_pass(0);
-    if (WS) fill_ring_w(0);
-    else fill_ring(0);
+    fill_ring(0);
     __syncthreads();
     wait_rows(0);
 #pragma unroll 1
     for (int z = 0; z < E; ++z) {
-        prefetch_plane(z + 2);
         if (z + 1 < E) {
             expect_rows(z + 1);
             psi_pass(z + 1);
-            if constexpr (WS) {
-                // plane z+1 of this warp's rows is in the ring: publish it, then
-                // wait only for the two neighbouring warps (no CTA barrier)
-                fill_ring_w(z + 1);
-                __syncwarp();
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(
-                                 smem_u32(&s_wbar[z & 1][warp]))
-                             : "memory");
-                if (warp > 0) wbar_wait(warp - 1, z);
-                if (warp + 1 < NT / 32) wbar_wait(warp + 1, z);
-            } else {
-                fill_ring(z + 1);
-                __syncthreads();
-            }
+            fill_ring(z + 1);
+            __syncthreads();
             wait_rows(z + 1);
         } else {
-            // fill_zghost(E) overwrites the ring slot of plane E-4 for every row:
-            // all warps must be past collide(E-3) first
-            if constexpr (WS) __syncthreads();
             fill_zghost(E);
             __syncthreads();
         }
