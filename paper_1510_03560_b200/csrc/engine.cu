@@ -23,8 +23,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <deque>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -102,6 +104,7 @@ struct Kernels {
     MainFn main_tm_opt[16]; // variant 2 + OPT: the same kernel with OPT bits (A/B)
     MainFn main_pc;     // variant 21: one CTA per (block, component), cp.async staged
     MainFn main_pc2;    // variant 22: as 21 with psi computed two planes ahead
+    MainFn main_pc128;  // variant 23: 4-warp CTAs (measured slower, 3.64 ms; not instantiated)
     void (*face)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
     void (*readback)(Dev, int, int, int, double*, cudaStream_t);
     void (*gather)(Dev, const int*, int, int, int, int, double*, int, int, cudaStream_t);
@@ -126,9 +129,9 @@ void launch_tm(Dev d, const int* act, int src, int wu, long it, unsigned ntiles,
     cudaLaunchKernelEx(&cfg, k_main_tm<E, C, OPT>, d, act, src, wu, it);
 }
 
-template <int E, int C, int LAG>
+template <int E, int C, int LAG, int NT = 256>
 void launch_pc(Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
-    using T = PcCfg<E, C, LAG>;
+    using T = PcCfg<E, C, LAG, NT>;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ntiles * T::CL);
     cfg.blockDim = dim3(T::NT);
@@ -141,7 +144,7 @@ void launch_pc(Dev d, const int* act, int src, int wu, long it, unsigned ntiles,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_main_pc<E, C, LAG>, d, act, src, wu, it);
+    cudaLaunchKernelEx(&cfg, k_main_pc<E, C, LAG, NT>, d, act, src, wu, it);
 }
 
 template <int E, int C, int OPT>
@@ -165,7 +168,7 @@ Kernels make_kernels() {
         k_main<E, C, BZ, NT, NOPSI><<<ntiles * (E / BZ), NT, SMEM_PLAIN, s>>>(d, act, src, wu, it);
     };
     k.main_tm = nullptr;
-    k.main_pc = k.main_pc2 = nullptr;
+    k.main_pc = k.main_pc2 = k.main_pc128 = nullptr;
     for (auto& f : k.main_tm_opt) f = nullptr;  // OPT values not instantiated fall back
     if constexpr (!NOPSI && (E == 16 || E == 32) && C <= 2) {
         constexpr int S = TmCfg<E, C>::SMEM;
@@ -261,6 +264,9 @@ class Engine {
     int step_main(plbm_error* err);
     int step_face();
     int step_end(const uint8_t* merged, plbm_error* err);
+    int step_speculative(int n, plbm_error* err);
+    void enqueue_step(long it);
+    void host_expand(const uint8_t* merged, long it);
     void counters(plbm_counters* out);
     int tiles(int32_t* coords, int32_t* owners, int64_t* births, int max) const;
     int read_tile(const int32_t* coords, int comp, int field, double* out);
@@ -358,6 +364,15 @@ class Engine {
     int* d_coords_ = nullptr;
     double* d_u_face_ = nullptr;
     uint8_t* d_trig_ = nullptr;
+    uint8_t* d_bmask_ = nullptr;  // [slot] faces whose trigger would be a birth
+    uint8_t* d_omask_ = nullptr;  // [slot] faces whose trigger is out of bounds (suppressed)
+    int* d_halt_ = nullptr;       // sticky halt flag of the speculative step queue
+    int* h_flags_ = nullptr;      // pinned copies of the halt flag, one per queued step
+    cudaEvent_t flag_ev_[8] = {};
+    int spec_depth_ = 3;          // steps queued ahead (1 = a host round trip every step)
+    bool in_spec_ = false;        // a speculative queue is open (profiling events stay unresolved)
+    Poke* d_pokes_ = nullptr;     // test hook: f_in overrides for the next step
+    std::vector<Poke> pokes_;
     int* d_dep_cnt_ = nullptr;   // fused face pass: per-slot completion counts
     int* d_dep_need_ = nullptr;  // 1 + active geometric neighbours
     int* d_geo_ = nullptr;       // [slot][18] active geometric neighbour or -1
@@ -547,6 +562,14 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     d_coords_ = dmalloc<int>(size_t(nslot) * 3);
     d_u_face_ = dmalloc<double>(size_t(lcap_ + 1) * C_ * 6 * 3 * E2_);
     d_trig_ = dmalloc<uint8_t>(trig_bytes_);
+    d_bmask_ = dmalloc<uint8_t>(nslot);
+    d_omask_ = dmalloc<uint8_t>(nslot);
+    d_halt_ = dmalloc<int>(1);
+    CK(cudaMemsetAsync(d_halt_, 0, sizeof(int), stream_));
+    CK(cudaMallocHost(&h_flags_, 8 * sizeof(int)));
+    for (auto& e : flag_ev_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    if (const char* sd = std::getenv("PLBM_SPEC_DEPTH")) spec_depth_ = std::max(1, std::min(8, std::atoi(sd)));
+    d_pokes_ = dmalloc<Poke>(64);
     d_dep_cnt_ = dmalloc<int>(nslot);
     d_dep_need_ = dmalloc<int>(nslot);
     d_geo_ = dmalloc<int>(size_t(nslot) * 18);
@@ -610,6 +633,9 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     d_.geo = d_geo_;
     d_.face_flags = 0;
     d_.xcol_ok = 0;
+    d_.halt = nullptr;
+    d_.pokes = nullptr;
+    d_.npoke = 0;
 
     // ---- host mirror + initial tiles (make_state, engine.cpp:134-159)
     grid_slot_.assign(n_tiles, -1);
@@ -698,9 +724,12 @@ void Engine::release() {
     void* ptrs[] = {d_pool_f_, d_pool_pf_, d_slot_f_[0], d_slot_f_[1], d_slot_pf_[0], d_slot_pf_[1],
                     d_route_[0], d_route_[1], d_lidx_, d_solid_, d_has_solid_, d_mode_, d_coords_,
                     d_u_face_, d_trig_, d_capture_, d_cnt_, d_err_, d_active_, d_scratch_slots_,
-                    d_readback_, d_dep_cnt_, d_dep_need_, d_geo_};
+                    d_readback_, d_dep_cnt_, d_dep_need_, d_geo_, d_bmask_, d_omask_, d_halt_, d_pokes_};
     for (void* q : ptrs)
         if (q) cudaFree(q);
+    if (h_flags_) cudaFreeHost(h_flags_);
+    for (auto& e : flag_ev_)
+        if (e) cudaEventDestroy(e);
     for (auto& e : ev_pool_) {
         if (e.a) cudaEventDestroy(e.a);
         if (e.b) cudaEventDestroy(e.b);
@@ -945,6 +974,18 @@ void Engine::upload_map(const std::vector<int>& new_slots, bool initial) {
             need[s] = n;
         }
         CK(cudaMemcpyAsync(d_geo_, geo.data(), geo.size() * sizeof(int), cudaMemcpyHostToDevice, stream_));
+        // speculative queue: which trigger bits need the host (births) and
+        // which only count as suppressed expansions (out of bounds)
+        std::vector<uint8_t> bm(nslot, 0), om(nslot, 0);
+        for (int s : all_active_)
+            for (int f = 0; f < 6; ++f) {
+                Coord n;
+                if (!neighbor_coords(slots_[s].c, f, n)) om[s] |= uint8_t(1u << f);
+                else if (slot_at(n) < 0) bm[s] |= uint8_t(1u << f);
+            }
+        CK(cudaMemcpyAsync(d_bmask_, bm.data(), nslot, cudaMemcpyHostToDevice, stream_));
+        CK(cudaMemcpyAsync(d_omask_, om.data(), nslot, cudaMemcpyHostToDevice, stream_));
+        CK(cudaStreamSynchronize(stream_));  // host vectors die here
         CK(cudaMemcpyAsync(d_dep_need_, need.data(), need.size() * sizeof(int), cudaMemcpyHostToDevice,
                            stream_));
         stats_.h2d_bytes += (geo.size() + need.size()) * sizeof(int);
@@ -987,26 +1028,31 @@ void Engine::launch_main(long iter) {
     const int wu = mode_ == PLBM_MODE_PROGRESSIVE ? 1 : 0;
     MainFn fn = K_.main_plain;
     // single rank: the pc kernels run the face pass themselves (no k_face)
-    const auto fusable = [&](MainFn f) { return world_ == 1 && f && (f == K_.main_pc || f == K_.main_pc2); };
+    const auto fusable = [&](MainFn f) { return world_ == 1 && f && (f == K_.main_pc || f == K_.main_pc2 || f == K_.main_pc128); };
     if (variant_ == 0) fn = K_.main_pc ? K_.main_pc : (K_.main_tm ? K_.main_tm : K_.main_plain);
     if (K_.main_tm && variant_ >= 2 && variant_ < 18 && K_.main_tm_opt[variant_ - 2])
         fn = K_.main_tm_opt[variant_ - 2];
     if (K_.main_pc && variant_ == 21) fn = K_.main_pc;
     if (K_.main_pc2 && variant_ == 22) fn = K_.main_pc2;
+    if (K_.main_pc128 && variant_ == 23) fn = K_.main_pc128;
     face_fused_ = fusable(fn) && fuse_;
     // the pc kernels write the xcol side buffers the face pass reads
-    d_.xcol_ok = (fn == K_.main_pc || fn == K_.main_pc2) && !no_xcol_;
+    d_.xcol_ok = (fn == K_.main_pc || fn == K_.main_pc2 || fn == K_.main_pc128) && !no_xcol_;
     d_.face_flags = face_fused_ ? (FACE_FUSED | FACE_NAN | (mode_ == PLBM_MODE_PROGRESSIVE ? FACE_CRITERION : 0))
                                 : 0;
     fn(d_, d_active_, cur_, wu, iter, unsigned(active_.size()), stream_);
     CK(cudaGetLastError());
+    if (d_.npoke) {  // pokes apply to one step's f_in
+        d_.npoke = 0;
+        pokes_.clear();
+    }
     ++stats_.kernels_launched;
     if (ev) CK(cudaEventRecord(ev->b, stream_));
 }
 
 Engine::EvPair& Engine::next_event(int kind, uint64_t cells) {
     if (ev_used_ == ev_pool_.size()) {
-        if (ev_pool_.size() >= 8192) resolve_events();
+        if (ev_pool_.size() >= 8192 && !in_spec_) resolve_events();
         if (ev_used_ == ev_pool_.size()) {
             EvPair p;
             CK(cudaEventCreate(&p.a));
@@ -1026,6 +1072,7 @@ void Engine::resolve_events() {
     for (size_t k = 0; k < ev_used_; ++k) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ev_pool_[k].a, ev_pool_[k].b));
+        if (ev_pool_[k].kind < 0) continue;  // a discarded speculative step (no-op launch)
         if (ev_pool_[k].kind == 0) {
             stats_.main_ms += ms;
             ++stats_.main_launches;
@@ -1182,21 +1229,119 @@ int Engine::step_end(const uint8_t* merged, plbm_error* err) {
             CK(cudaStreamSynchronize(stream_));
             merged = trig.data();
         }
-        std::vector<std::pair<Coord, int>> triggers;
-        for (int s : all_active_)
-            for (int f = 0; f < 6; ++f)
-                if (merged[s] & (1u << f)) triggers.push_back({slots_[s].c, f});
-        CK(cudaMemsetAsync(d_trig_, 0, trig_bytes_, stream_));
-        if (!triggers.empty()) {
-            std::vector<int> created;
-            expand(triggers, it, created);
-            for (int s : created) assign_owner(s);
-            if (!created.empty()) upload_map(created, false);
-        }
+        host_expand(merged, it);
     }
     ++iteration_;
     cell_updates_ += updates;
     return 0;
+}
+
+// expand + assign_owner on the host mirror from a (merged) trigger array,
+// then clear the device triggers (tilemap.cpp:220-266, engine.cpp:30-41).
+void Engine::host_expand(const uint8_t* merged, long it) {
+    std::vector<std::pair<Coord, int>> triggers;
+    for (int s : all_active_)
+        for (int f = 0; f < 6; ++f)
+            if (merged[s] & (1u << f)) triggers.push_back({slots_[s].c, f});
+    CK(cudaMemsetAsync(d_trig_, 0, trig_bytes_, stream_));
+    if (!triggers.empty()) {
+        std::vector<int> created;
+        expand(triggers, it, created);
+        for (int s : created) assign_owner(s);
+        if (!created.empty()) upload_map(created, false);
+    }
+}
+
+// One step's launches (= step_main + step_face of a single rank).
+void Engine::enqueue_step(long it) {
+    launch_main(it);
+    cur_ ^= 1;
+    if (any_gen_) {
+        CK(cudaMemsetAsync(d_mode_, MODE_PULL, size_t(cap_ + 1), stream_));
+        std::fill(h_mode_.begin(), h_mode_.end(), uint8_t(MODE_PULL));
+        any_gen_ = false;
+    }
+    if (routes_differ_) {
+        CK(cudaMemcpyAsync(d_route_[ROUTE_PULL], d_route_[ROUTE_PSI], size_t(cap_ + 1) * 18 * sizeof(int),
+                           cudaMemcpyDeviceToDevice, stream_));
+        routes_differ_ = false;
+    }
+    if (!face_fused_) launch_face(cur_, 3, it);
+}
+
+// Progressive single-rank stepping without a host round trip per step: up to
+// spec_depth_ steps are queued ahead.  After each step's face pass k_check
+// decides on the device whether its triggers need the host (a birth, or an
+// error); if so it sets a sticky halt flag that turns every step queued after
+// it into a no-op, and the host — which retires steps in order from pinned
+// copies of the flag — runs the expansion and resumes from the next step.
+// Steps without births count their out-of-bounds triggers as suppressed
+// expansions on the device.  Results are identical to stepping one at a time.
+int Engine::step_speculative(int n, plbm_error* err) {
+    struct Queued {
+        long it;
+        int cur_after;
+        uint64_t updates;
+        int flag;
+        size_t ev_after;  // profiling events recorded up to and including this step
+    };
+    std::deque<Queued> q;
+    d_.halt = d_halt_;
+    in_spec_ = true;
+    int done = 0, enqueued = 0, flag_ctr = 0;
+    int rc = 0;
+    while (done < n) {
+        while (int(q.size()) < spec_depth_ && enqueued < n) {
+            Queued e{iteration_ + 1 + long(q.size()), 0, active_cells_, flag_ctr++ % 8, 0};
+            enqueue_step(e.it);
+            e.cur_after = cur_;
+            e.ev_after = ev_used_;
+            k_check<<<1, 256, 0, stream_>>>(d_, d_bmask_, d_omask_, cap_ + 1, d_halt_);
+            CK(cudaGetLastError());
+            ++stats_.kernels_launched;
+            CK(cudaMemcpyAsync(&h_flags_[e.flag], d_halt_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+            CK(cudaEventRecord(flag_ev_[e.flag], stream_));
+            stats_.d2h_bytes += sizeof(int);
+            q.push_back(e);
+            ++enqueued;
+        }
+        const Queued e = q.front();
+        q.pop_front();
+        CK(cudaEventSynchronize(flag_ev_[e.flag]));
+        if (h_flags_[e.flag] == 0) {  // no birth, no error: the step is final
+            iteration_ = e.it;
+            cell_updates_ += e.updates;
+            for (int a = 0; a < 3; ++a) bytes_[a] += step_bytes_[a];
+            ++done;
+            continue;
+        }
+        // halted at e: the steps queued after it did nothing
+        enqueued -= int(q.size());
+        q.clear();
+        for (size_t k = e.ev_after; k < ev_used_; ++k) ev_pool_[k].kind = -1;
+        cur_ = e.cur_after;
+        bool failed = false;
+        check_error(err, failed);  // synchronises the stream
+        if (failed) {
+            rc = 1;
+            break;
+        }
+        iteration_ = e.it;
+        cell_updates_ += e.updates;
+        for (int a = 0; a < 3; ++a) bytes_[a] += step_bytes_[a];
+        ++done;
+        std::vector<uint8_t> trig(trig_bytes_);
+        CK(cudaMemcpyAsync(trig.data(), d_trig_, trig_bytes_, cudaMemcpyDeviceToHost, stream_));
+        stats_.d2h_bytes += trig_bytes_;
+        CK(cudaStreamSynchronize(stream_));
+        host_expand(trig.data(), e.it);
+        CK(cudaMemsetAsync(d_halt_, 0, sizeof(int), stream_));
+    }
+    if (!q.empty() || rc) CK(cudaStreamSynchronize(stream_));
+    CK(cudaMemsetAsync(d_halt_, 0, sizeof(int), stream_));
+    d_.halt = nullptr;
+    in_spec_ = false;
+    return rc;
 }
 
 int Engine::step(int n, plbm_error* err) {
@@ -1209,6 +1354,7 @@ int Engine::step(int n, plbm_error* err) {
         }
         return 2;
     }
+    if (mode_ == PLBM_MODE_PROGRESSIVE && spec_depth_ > 1) return step_speculative(n, err);
     if (mode_ == PLBM_MODE_PROGRESSIVE) {
         for (int k = 0; k < n; ++k) {
             int rc = step_begin(err);
@@ -1303,7 +1449,7 @@ void Engine::counters(plbm_counters* out) {
     out->negative_populations = c[CNT_NEG];  // this rank's tiles
     out->psi_clamps = c[CNT_CLAMP];
     out->zero_rho_forcings = c[CNT_ZERO_RHO];
-    out->suppressed_expansions = suppressed_;
+    out->suppressed_expansions = suppressed_ + c[CNT_SUPP];  // host expand + device k_check
     for (int a = 0; a < 3; ++a) out->bytes[a] = bytes_[a];
     out->tiles = all_active_.size();
     out->active_cells = active_cells_;
@@ -1467,8 +1613,23 @@ int Engine::set_capture(bool on) {
     return 0;
 }
 
-int Engine::poke_f(const int32_t*, int, int, const int32_t*, double) {
-    return -5;  // not supported on the device pool
+// proj/tests/test_engine.cpp:284-310: overwrite one population of f_read
+// (the pulled f_in of the next step) at an interior cell of a tile.
+int Engine::poke_f(const int32_t* cc, int comp, int i, const int32_t* local, double v) {
+    const Coord c{cc[0], cc[1], cc[2]};
+    if (c.x < 0 || c.y < 0 || c.z < 0 || c.x >= grid_[0] || c.y >= grid_[1] || c.z >= grid_[2]) return -1;
+    const int s = slot_at(c);
+    if (s < 0) return -1;
+    if (comp < 0 || comp >= C_ || i < 0 || i >= Q) return -2;
+    for (int a = 0; a < 3; ++a)
+        if (local[a] < 0 || local[a] >= E_) return -3;
+    if (pokes_.size() >= 64) return -4;
+    pokes_.push_back({s, comp, i, (local[2] * E_ + local[1]) * E_ + local[0], v});
+    CK(cudaMemcpyAsync(d_pokes_, pokes_.data(), pokes_.size() * sizeof(Poke), cudaMemcpyHostToDevice, stream_));
+    CK(cudaStreamSynchronize(stream_));
+    d_.pokes = d_pokes_;
+    d_.npoke = int(pokes_.size());
+    return 0;
 }
 
 }  // namespace plbm

@@ -38,7 +38,7 @@ namespace plbm {
 enum TileMode : uint8_t { MODE_PULL = 0, MODE_GEN_SEEDED = 1, MODE_GEN_AMBIENT = 2 };
 enum { ROUTE_PULL = 0, ROUTE_PSI = 1 };
 enum { ERR_NONE = 0, ERR_P1_NAN = 1, ERR_P1_POLE = 2, ERR_P5_NAN = 3 };
-enum { CNT_NEG = 0, CNT_CLAMP = 1, CNT_ZERO_RHO = 2, CNT_N = 4 };
+enum { CNT_NEG = 0, CNT_CLAMP = 1, CNT_ZERO_RHO = 2, CNT_SUPP = 3, CNT_N = 4 };
 
 constexpr int MAX_COMP = 4;
 constexpr int MAX_SEEDS = 64;
@@ -84,7 +84,39 @@ struct Dev {
     const int* geo;             // [slot][18] active geometric neighbour or -1
     int face_flags;             // FACE_* bits
     int xcol_ok;                // the last fused kernel wrote the xcol side buffers
+    const int* halt;            // speculative queue: a step kernel finding *halt != 0 does nothing
+    const struct Poke* pokes;   // test hook (plbm_gpu_poke_f): overrides of f_in for the next step
+    int npoke;
 };
+
+struct Poke {
+    int slot, comp, i, cell;
+    double v;
+};
+
+// plbm_gpu_poke_f: the reference overwrites f_read between steps
+// (proj/tests/test_engine.cpp:284-310); here the override is applied to the
+// pulled f_in of the next step's psi pass.  f stays in registers (the
+// direction index is matched against the unrolled loop).
+template <int E>
+__device__ __forceinline__ void apply_pokes(const Dev& d, int slot, int c, int x, int y, int z, double* f) {
+    if (d.npoke == 0) return;
+    const int cell = (z * E + y) * E + x;
+    for (int k = 0; k < d.npoke; ++k) {
+        const Poke p = d.pokes[k];
+        if (p.slot != slot || p.comp != c || p.cell != cell) continue;
+#pragma unroll
+        for (int i = 0; i < Q; ++i)
+            if (i == p.i) f[i] = p.v;
+    }
+}
+
+// Speculatively queued steps (Engine::step, single rank, progressive): every
+// step kernel first checks the sticky halt flag that k_check sets when the
+// previous step's triggers need the host (a birth) or an error occurred.
+__device__ __forceinline__ bool halted(const Dev& d) {
+    return d.halt && *(volatile const int*)d.halt != 0;
+}
 enum { FACE_CRITERION = 1, FACE_NAN = 2, FACE_FUSED = 4 };
 
 __constant__ Params P;
@@ -307,6 +339,7 @@ __device__ __forceinline__ double psi_ghost(const RouteTab& rt, int c, bool hs, 
 template <int E, int C, int BZ, int NT, bool NOPSI>
 __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ active, int src_buf,
                                              int write_uface, long iter) {
+    if (halted(d)) return;
     constexpr int G = E + 2;
     constexpr int GG = G * G;
     constexpr int E2 = E * E;
@@ -355,6 +388,7 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
                 } else if (!(hs && solid_at<E>(s_solid, x, y, pz))) {
                     double f[Q], u0, u1, u2;
                     fin_cell<E>(rt_pull, mode, s_tc, c, hs, s_solid, x, y, pz, f, u0, u1, u2);
+                    apply_pokes<E>(d, slot, c, x, y, pz, f);
                     double rho = 0.0;
 #pragma unroll
                     for (int i = 0; i < Q; ++i) {
@@ -419,6 +453,7 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
                 double f[Q];
                 double u0 = 0.0, u1 = 0.0, u2 = 0.0, rho;
                 fin_cell<E>(rt_pull, mode, s_tc, c, hs, s_solid, x, y, z, f, u0, u1, u2);
+                apply_pokes<E>(d, slot, c, x, y, z, f);
                 if (mode == MODE_PULL) {
                     moments(f, rho, u0, u1, u2);
                 } else {
@@ -773,6 +808,7 @@ __device__ void face_pass_part(const Dev& d, int slot, int c0, int nc, int k0, i
 template <int E, int C, int NT>
 __global__ void __launch_bounds__(NT) k_face(Dev d, const int* __restrict__ active, int src_buf,
                                              int flags, long iter) {
+    if (halted(d)) return;
     constexpr int E2 = E * E;
     constexpr int G = E + 2;
     __shared__ RouteTab rt;
@@ -887,6 +923,41 @@ __global__ void k_gather(Dev d, const int* __restrict__ active, int kind, int c,
 __global__ void k_fill(double* p, size_t n, double v) {
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
         p[i] = v;
+}
+
+// After k_face of a speculatively queued step: does this step's trigger set
+// need the host (a birth: an in-bounds absent target), or did an error occur?
+// Then set the sticky halt flag and leave the triggers for the host's expand.
+// Otherwise count the out-of-bounds triggers as suppressed expansions
+// (tilemap.cpp:220-266 counts every out-of-bounds trigger) and clear them, so
+// the next queued step proceeds without a host round trip.  One CTA.
+__global__ void k_check(Dev d, const uint8_t* __restrict__ bmask, const uint8_t* __restrict__ omask,
+                        int nslot, int* halt) {
+    if (*(volatile int*)halt != 0) return;
+    __shared__ int s_birth;
+    __shared__ unsigned long long s_supp;
+    if (threadIdx.x == 0) {
+        s_birth = (*d.err != ~0ull) ? 1 : 0;
+        s_supp = 0;
+    }
+    __syncthreads();
+    int birth = 0;
+    unsigned supp = 0;
+    for (int s = threadIdx.x; s < nslot; s += blockDim.x) {
+        const unsigned t = d.trig[s];
+        birth |= (t & bmask[s]) != 0;
+        supp += __popc(t & omask[s]);
+    }
+    if (__any_sync(0xffffffffu, birth) && (threadIdx.x & 31) == 0) s_birth = 1;
+    supp = __reduce_add_sync(0xffffffffu, supp);
+    if ((threadIdx.x & 31) == 0 && supp) atomicAdd(&s_supp, (unsigned long long)supp);
+    __syncthreads();
+    if (s_birth) {
+        if (threadIdx.x == 0) *halt = 1;
+        return;
+    }
+    for (int s = threadIdx.x; s < nslot; s += blockDim.x) d.trig[s] = 0;
+    if (threadIdx.x == 0 && s_supp) d.cnt[CNT_SUPP] += s_supp;
 }
 
 }  // namespace plbm

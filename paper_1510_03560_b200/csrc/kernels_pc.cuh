@@ -69,14 +69,15 @@ __device__ __forceinline__ const double* psi_ghost_src(const RouteTab& rt, int c
 }
 
 
-template <int E, int C, int LAG = 1>
+template <int E, int C, int LAG = 1, int NT_ = 256>
 struct PcCfg {
-    static constexpr int NT = 256;
+    static constexpr int NT = NT_;      // 256: 8 warps, 2 CTAs/SM; 128: 4 warps, 4 CTAs/SM
     static constexpr int BY = NT / E;   // rows per CTA
     static constexpr int NB = E / BY;   // y-blocks per tile
     static constexpr int CL = NB * C;   // cluster size
     static constexpr int CB = 40;       // TMEM columns per plane slot (19 f + rho)
-    static constexpr int NCOLS = 256;   // two warps per lane quarter x 128 columns
+    static constexpr int WPQ = NT / 128;  // warps per TMEM lane quarter
+    static constexpr int NCOLS = 128 * WPQ;  // 128 columns per thread
     static constexpr int PW = E + 2;
     static constexpr int PH = BY + 2;
     static constexpr int PP = PW * PH;
@@ -88,17 +89,19 @@ struct PcCfg {
     static constexpr int XST_BYTES = 2 * 4 * Q * BY * 8;  // x-column staging, two planes
     static constexpr int SMEM = PSI_BYTES + LAND_BYTES + XST_BYTES;
     static_assert(CL <= 16, "cluster size (> 8 needs the non-portable opt-in)");
-    static_assert(TSLOTS * CB <= NCOLS / 2, "TMEM plane slots do not fit");
-    static_assert(2 * (SMEM + 8 * 1024) <= 228 * 1024, "two CTAs per SM must fit");
+    static_assert(TSLOTS * CB <= NCOLS / WPQ, "TMEM plane slots do not fit");
+    static constexpr int PER_SM = 512 / NT;  // 16 warps per SM
+    static_assert(PER_SM * (SMEM + 8 * 1024) <= 228 * 1024, "CTAs per SM must fit");
 };
 
 // LAG = planes between a plane's psi pass and its collision: 1 (psi of z+1
 // is computed and pushed in the iteration that collides z) or 2 (pushed one
 // iteration before it is needed, three TMEM plane slots).
-template <int E, int C, int LAG>
-__global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict__ active,
-                                                    int src_buf, int write_uface, long iter) {
-    using T = PcCfg<E, C, LAG>;
+template <int E, int C, int LAG, int NT_ = 256>
+__global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __restrict__ active,
+                                                            int src_buf, int write_uface, long iter) {
+    if (halted(d)) return;
+    using T = PcCfg<E, C, LAG, NT_>;
     constexpr int NMB = T::NMB;
     constexpr int NT = T::NT, BY = T::BY, NB = T::NB, PW = T::PW, PH = T::PH, PP = T::PP;
     constexpr int R = T::RING;
@@ -155,7 +158,7 @@ __global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict
         asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
     }
     // 8 warps: warps w and w+4 share TMEM lanes 32(w%4).., split by columns
-    const uint32_t tbase = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * (T::NCOLS / 2));
+    const uint32_t tbase = s_tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t((warp >> 2) * 128);
     const int tile_lin = (s_tc[0] * P.grid[1] + s_tc[1]) * P.grid[2] + s_tc[2];
 
     const int x = tid % E;
@@ -297,6 +300,7 @@ __global__ void __launch_bounds__(256, 2) k_main_pc(Dev d, const int* __restrict
                 double a0, a1, a2;
                 gen_fin<E>(mode, c, s_tc, x, y, pz, f, a0, a1, a2);
             }
+            apply_pokes<E>(d, slot, c, x, y, pz, f);
 #pragma unroll
             for (int i = 0; i < Q; ++i) {
                 rho += f[i];

@@ -290,6 +290,7 @@ constexpr int TM_DEFAULT_OPT = 0;
 template <int E, int C, int OPT>
 __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict__ active,
                                                     int src_buf, int write_uface, long iter) {
+    if (halted(d)) return;
     using T = TmCfg<E, C>;
     constexpr int NT = T::NT, BY = T::BY, NB = T::NB, PW = T::PW, PH = T::PH, PP = T::PP;
     constexpr int G = E + 2;
@@ -456,6 +457,7 @@ __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict
                 double a0, a1, a2;
                 gen_fin<E>(mode, c, s_tc, x, y, pz, f, a0, a1, a2);
             }
+            if (!sol) apply_pokes<E>(d, slot, c, x, y, pz, f);
         };
         auto finish = [&](int c, const double* f) {
             double v = 0.0, rho = 0.0;

@@ -36,3 +36,41 @@ def test_gpu_reproduces_reference_golden_states(built, name):
     gpu = capi.gpu_engine(make(), capture=True)
     gpu.step(steps)
     assert_matches_golden(gpu, name)
+
+
+@pytest.mark.parametrize("variant", [0, 2])
+@pytest.mark.parametrize("name", ["mpmc_progressive_e16", "mpmc_e32", "c1_static"])
+def test_poked_nan_matches_reference(built, name, variant):
+    """proj/tests/test_engine.cpp:284-310: a NaN written into one f_read
+    population between steps -> the same EngineError (iteration, tile, phase)
+    as the reference, and no advance of iteration / cell_updates.  (A finite
+    poke is not comparable: the reference's collision then mixes the poked
+    f_read with the u of the previous P5, which this engine recomputes.)"""
+    value = float("nan")
+    from tests.conftest import have_ref
+    from paper_1510_03560_b200.scenario import EngineError
+    if not have_ref():
+        pytest.skip("reference shim not built")
+    make, _ = scenarios.ALL[name]
+    sc = make()
+    ref = capi.ref_engine(sc)
+    gpu = capi.gpu_engine(sc, capture=True)
+    gpu.set_kernel_variant(variant)
+    ref.step(3)
+    gpu.step(3)
+    coords = ref.tiles()[0][0]
+    E = sc.tile_extent
+    local = (E // 2, E // 2 - 1, E // 2 + 1)
+    ref.poke_f(coords, 0, 7, local, value)
+    gpu.poke_f(coords, 0, 7, local, value)
+    errs = []
+    for eng in (ref, gpu):
+        try:
+            eng.step(3)
+            errs.append(None)
+        except EngineError as e:
+            errs.append((e.iteration, tuple(e.tile), e.phase))
+    assert errs[0] == errs[1], errs
+    assert errs[0] is not None
+    for k in ("iteration", "cell_updates"):
+        assert ref.counters()[k] == gpu.counters()[k]
