@@ -101,3 +101,72 @@ def test_ranks_in_one_process_match_single_engine(built, name, world):
                 b = engs[r].read_tile(coords, comp, f)
                 assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), (coords, comp, f)
     assert len(owners) == world  # the run really was split across ranks
+
+
+def _proc_rank(rank, world, port, name, steps, q):
+    """One rank of a real multi-process run (gloo plumbing, CUDA IPC pools) on
+    GPU 0, checked against a single-engine run of the same scenario."""
+    try:
+        import torch
+        import torch.distributed as td
+        from tests.compare import FIELDS
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        td.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        make, _ = scenarios.ALL[name]
+        sc = make()
+        sc.devices = max(sc.devices, world)
+        eng = capi.gpu_engine(sc, capture=True, rank=rank, world=world)
+        stepper = dist.DistStepper(eng, td, 0)
+        stepper.step(steps)
+        eng.sync()
+        single = capi.gpu_engine(sc, capture=True)
+        single.step(steps)
+        bad = []
+        for k in ("iteration", "cell_updates", "suppressed_expansions", "tiles", "active_cells", "bytes"):
+            if eng.counters()[k] != single.counters()[k]:
+                bad.append(k)
+        if eng.creation_log() != single.creation_log():
+            bad.append("creation_log")
+        mine = 0
+        for coords, _, _ in single.tiles():
+            if eng.tile_rank(coords) != rank:
+                continue
+            mine += 1
+            for comp in range(sc.n_components):
+                for f in FIELDS:
+                    a = single.read_tile(coords, comp, f)
+                    b = eng.read_tile(coords, comp, f)
+                    if not np.array_equal(a.view(np.uint64), b.view(np.uint64)):
+                        bad.append((coords, comp, f))
+        td.barrier()
+        td.destroy_process_group()
+        q.put((rank, mine, bad[:5]))
+    except Exception as ex:  # report instead of hanging the parent
+        q.put((rank, -1, [repr(ex)]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["mpmc_progressive_e16", "mpmc_e32"])
+def test_two_processes_one_gpu_match_single_engine(built, name):
+    """The DistStepper protocol across real processes (IPC-mapped peer pools,
+    torch.distributed collectives): bit-identical to one engine."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    _, steps = scenarios.ALL[name]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_proc_rank, args=(r, 2, port, name, steps, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r, (m, b)) for r, m, b in (q.get(timeout=600) for _ in procs))
+    for p in procs:
+        p.join(120)
+    for r in range(2):
+        mine, bad = res[r]
+        assert mine > 0 and not bad, (r, mine, bad)
