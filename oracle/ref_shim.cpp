@@ -15,6 +15,7 @@
 //                       between steps (SURVEY §8b "State read by callers").
 #include "plbm/dump.hpp"
 #include "plbm/engine.hpp"
+#include "plbm/scenario.hpp"
 #include "plbm/kernels.hpp"
 #include "plbm/physics.hpp"
 #include "plbm/geometry.hpp"
@@ -403,6 +404,20 @@ int plbm_ref_run_scenario(const plbm_scenario_desc* d, int workers,
     }
     std::filesystem::remove_all(dir);
     return rc;
+}
+
+// The reference's CLI `run` path without CLI11: iobench::load_config on a
+// scenario TOML, the output directory overridden, engine::run_scenario.
+int plbm_ref_run_toml(const char* path, const char* output_dir) {
+    try {
+        auto cfg = iobench::load_config(path);
+        cfg.output_dir = output_dir;
+        engine::run_scenario(cfg);
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "plbm_ref_run_toml: %s\n", e.what());
+        return -2;
+    }
+    return 0;
 }
 
 } // extern "C"

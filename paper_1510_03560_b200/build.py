@@ -67,7 +67,15 @@ def build_oracle() -> None:
         subprocess.run(["make", "-s", "-j8", "-C", odir, "ref"], check=True)
 
 
+def build_integration() -> None:
+    """The reference's driver linked against libplbm_gpu.so
+    (integration/plbm_gpu_run.cpp), where /root/reference exists."""
+    if os.path.isdir("/root/reference/proj/src"):
+        subprocess.run(["make", "-s", "-C", os.path.join(REPO, "integration")], check=True)
+
+
 if __name__ == "__main__":
     build_gpu(force="--force" in sys.argv, verbose=True)
     build_oracle()
+    build_integration()
     print(LIB)

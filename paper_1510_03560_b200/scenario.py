@@ -9,6 +9,7 @@ proj/include/plbm/physics.hpp:14-30).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import math
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
@@ -153,6 +154,56 @@ class Scenario:
 
     def to_c(self) -> "CScenario":
         return CScenario(self)
+
+    def to_toml(self, path: str, iterations: int = 10, report_interval: int = 10,
+                snapshot_interval: int = 0, snapshot_fields=("rho",), snapshot_pgm: bool = False,
+                output: str = "out", workers: int = 0) -> None:
+        """The reference's scenario file (proj/src/scenario.cpp:185-290, read by
+        iobench::load_config); a geometry is written next to it as LBMGEO v1."""
+        def num(v):
+            return repr(float(v))
+
+        def arr(vs, f=num):
+            return "[" + ", ".join(f(v) for v in vs) + "]"
+        lines = [f'name = "{self.name}"', 'stencil = "D3Q19"',
+                 f"domain = {arr(self.domain, str)}", f"tile_extent = {self.tile_extent}",
+                 f'mode = "{"static" if self.mode == MODE_STATIC else "progressive"}"',
+                 f"iterations = {iterations}", f"report_interval = {report_interval}",
+                 f"snapshot_interval = {snapshot_interval}", f"threshold = {num(self.threshold)}",
+                 f"devices = {self.devices}",
+                 f'policy = "{"simple" if self.policy == POLICY_SIMPLE else "optimized"}"',
+                 f"weight_p2p = {num(self.weight_p2p)}", f"weight_staged = {num(self.weight_staged)}",
+                 f'output = "{output}"',
+                 "snapshot_fields = [" + ", ".join(f'"{f}"' for f in snapshot_fields) + "]",
+                 f"snapshot_pgm = {'true' if snapshot_pgm else 'false'}", f"workers = {workers}",
+                 "boundary = [" + ", ".join('"periodic"' if p else '"ambient"' for p in self.periodic) + "]"]
+        if self.p2p is not None:
+            raise ValueError("to_toml: a custom P2P topology is not written")
+        if self.geometry is not None:
+            geo = os.path.splitext(path)[0] + ".lbmgeo"
+            save_lbmgeo(self.geometry, geo)
+            lines.append(f'geometry = "{os.path.basename(geo)}"')
+        for c in self.components:
+            lines += ["", "[[component]]", f"tau = {num(c.tau)}", f"rho_ambient = {num(c.rho_ambient)}",
+                      f"g_self = {num(c.g_self)}", f"beta = {num(c.beta)}", f"gravity = {arr(c.gravity)}",
+                      f"a = {num(c.a)}", f"b = {num(c.b)}", f"R = {num(c.R)}", f"T = {num(c.T)}",
+                      f"Tc = {num(c.Tc)}", f"omega = {num(c.omega)}"]
+        n = len(self.components)
+        if self.coupling is not None:
+            g = np.asarray(self.coupling, float)
+            for a in range(n):
+                for b in range(a + 1, n):
+                    if g[a, b] != 0.0:
+                        lines += ["", "[[coupling]]", f"pair = [{a}, {b}]", f"g = {num(g[a, b])}"]
+        for sd in self.seeds:
+            lines += ["", "[[seed]]"]
+            if sd.shape == SEED_SPHERE:
+                lines += ['shape = "sphere"', f"center = {arr(sd.center)}", f"radius = {num(sd.radius)}"]
+            else:
+                lines += ['shape = "box"', f"min = {arr(sd.box_min)}", f"max = {arr(sd.box_max)}"]
+            lines += [f"component = {sd.component}", f"rho = {num(sd.rho)}", f"velocity = {arr(sd.velocity)}"]
+        with open(path, "w") as fh:
+            fh.write("\n".join(lines) + "\n")
 
 
 class CScenario:
