@@ -254,6 +254,10 @@ def main():
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max, e_dt_max = float(t[0]), float(t[1])
+    xb = torch.tensor([float(eng.exchange_bytes()["bytes_per_step"])], dtype=torch.float64, device=tdev)
+    if dist is not None:
+        dist.all_reduce(xb)  # job total per step
+    nvlink_bytes = int(xb[0])
     cells_all, e_cells_all = float(cells), float(e_cells)
     if rank != 0:
         if dist is not None:
@@ -300,6 +304,14 @@ def main():
                      "face_ms_avg": round(ks["face_ms"] / max(ks["face_launches"], 1), 4)},
         "clocks": clk.summary(),
     }
+    if world > 1:
+        # real cross-GPU volume per step (routing tables) next to the
+        # reference's modeled classes (record_exchange), SURVEY §8(f)4
+        c = eng.counters()
+        line["exchange"] = {"nvlink_read_bytes_per_step": nvlink_bytes,
+                            "nvlink_GBs": round(nvlink_bytes / (ms_max / a.steps / 1e3) / 1e9, 1),
+                            "modeled_bytes_total": {"intra": c["bytes"][0], "p2p": c["bytes"][1],
+                                                    "staged": c["bytes"][2]}}
     if not a.no_cpu_baseline and world == 1:
         try:
             v, cores, sample, _, _ = run_reference_cpu(a.cpu_seconds)

@@ -137,6 +137,11 @@ int plbm_gpu_set_peer_pools(void* h, int rank, void* pool_f, void* pool_pf);
 void plbm_gpu_pool_pointers(void* h, void** pool_f, void** pool_pf);
 int plbm_gpu_tile_rank(void* h, const int32_t* coords);      /* -1 if absent */
 int plbm_gpu_sync(void* h);
+/* Real byte accounting: bytes this rank's kernels read from
+ * peer pools per step on the current map (NVLink traffic), next to the
+ * reference's modeled record_exchange classes (plbm_counters.bytes).
+ * out[0] = bytes, out[1] = remote face routes, out[2] = remote edge routes. */
+void plbm_gpu_exchange_bytes(void* h, uint64_t* out);
 
 /* ---- output path -----------------------------------------
  * iobench::gather_field (dump.cpp:21-57): one field ("rho", "u_magnitude",

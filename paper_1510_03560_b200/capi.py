@@ -319,6 +319,14 @@ class GpuEngine(StepEngine):
     def sync(self) -> None:
         self.lib.plbm_gpu_sync(self._h)
 
+    def exchange_bytes(self) -> dict:
+        """Bytes this rank reads from peer pools per step (NVLink), from the
+        routing tables (plbm_gpu_exchange_bytes)."""
+        out = (C.c_uint64 * 3)()
+        self.lib.plbm_gpu_exchange_bytes.argtypes = [C.c_void_p, C.c_void_p]
+        self.lib.plbm_gpu_exchange_bytes(self._h, out)
+        return {"bytes_per_step": out[0], "remote_face_routes": out[1], "remote_edge_routes": out[2]}
+
     def gather_field(self, field: str, comp: int) -> np.ndarray:
         """iobench::gather_field (proj/src/dump.cpp:21-57): the domain grid,
         indexed [z, y, x]."""

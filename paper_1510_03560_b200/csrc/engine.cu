@@ -298,6 +298,7 @@ class Engine {
     int open_peer(int rank, const void* handles);
     int set_peer(int rank, void* pool_f, void* pool_pf);
     int rank_of(const int32_t* coords) const;
+    void exchange_bytes(uint64_t* out) const;
     int sync() {
         CK(cudaStreamSynchronize(stream_));
         return 0;
@@ -848,6 +849,32 @@ void Engine::assign_owner(int slot) {
 // Ghost routing (proj/src/engine.cpp:266-296): a face ghost reads the face
 // neighbour; an edge ghost on axes a<b hops along b first, then a — an absent
 // hop yields the ambient slot even when the diagonal tile exists.
+// Real cross-GPU data volume of one step on this rank, from
+// the routing tables: what this rank's kernels read from peer pools.  Per
+// face route to a tile on another rank: the fused kernel pulls the 5
+// crossing populations of E^2 cells and reads E^2 psi ghosts, the face pass
+// pulls the 5 crossing populations of its E^2 face cells; per edge route: one
+// crossing population and one psi ghost of E cells for each, and the face
+// passes' edge pulls.  out = {bytes, remote face routes, remote edge routes}.
+void Engine::exchange_bytes(uint64_t* out) const {
+    out[0] = out[1] = out[2] = 0;
+    std::vector<int> r(18);
+    for (int s : active_) {
+        compute_routes(s, r.data());
+        for (int k = 0; k < 18; ++k) {
+            const int n = r[size_t(k)];
+            if (n == amb_ || slots_[n].rank == rank_) continue;
+            if (k < 6) {
+                ++out[1];
+                out[0] += uint64_t(5 + 1 + 5) * E2_ * C_ * sizeof(double);
+            } else {
+                ++out[2];
+                out[0] += uint64_t(1 + 1 + 2) * E_ * C_ * sizeof(double);
+            }
+        }
+    }
+}
+
 void Engine::compute_routes(int slot, int* out) const {
     const Coord c = slots_[slot].c;
     auto nb = [&](const Coord& from, int axis, int dir, Coord& o) {
@@ -1758,6 +1785,8 @@ int plbm_gpu_set_peer_pools(void* h, int rank, void* pool_f, void* pool_pf) {
 }
 
 void plbm_gpu_pool_pointers(void* h, void** pool_f, void** pool_pf) { EG(h)->pool_pointers(pool_f, pool_pf); }
+
+void plbm_gpu_exchange_bytes(void* h, uint64_t* out) { EG(h)->exchange_bytes(out); }
 
 int plbm_gpu_gather_field(void* h, const char* field, int comp, double* grid) {
     try {

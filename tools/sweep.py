@@ -1,6 +1,9 @@
 #!/usr/bin/env python
 """Measurement sweeps on one B200 (results -> JSON lines on stdout).
 
+    python tools/sweep.py c1 [--steps 500]
+        BASELINE configs[0] (the reference's CPU scenario) on both engines in
+        the same run: time to solution and identical creation log.
     python tools/sweep.py c5 [--n 256] [--steps 20]
         BASELINE configs[4] on one GPU: tile extent E in {16, 32} x components
         C in {1, 2, 3}, static full-domain MPMC (all tiles active), MLUPS per
@@ -107,9 +110,36 @@ def c4(a):
     eng.close()
 
 
+def c1(a):
+    """BASELINE configs[0], the reference's own CPU scenario, end to end on both
+    engines in the same run: 500 steps of the 64^3 single-component inflow on
+    16^3 tiles (S = 1e-12), the GPU engine (device time, speculative queue)
+    against the reference on every host core (wall time), same creation log."""
+    import os as _os
+    cores = _os.cpu_count() or 1
+    sc = S.config1(threshold=1e-12)
+    sc.devices = cores  # the reference's workers own tiles by owner % W (engine.cpp:217)
+    eng = capi.gpu_engine(sc)
+    ms, cells, _ = timed(eng, a.steps, chunk=a.steps)
+    gpu_log, gpu_c = eng.creation_log(), eng.counters()
+    eng.close()
+    ref = capi.ref_engine(sc, workers=cores)
+    t0 = time.perf_counter()
+    ref.step(a.steps)
+    ref_s = time.perf_counter() - t0
+    same = ref.creation_log() == gpu_log and all(
+        ref.counters()[k] == gpu_c[k] for k in ("iteration", "cell_updates", "tiles", "suppressed_expansions"))
+    print(json.dumps({"sweep": "c1", "steps": a.steps, "tiles_final": gpu_c["tiles"],
+                      "cell_updates": gpu_c["cell_updates"],
+                      "gpu_ms": round(ms, 2), "gpu_mlups": round(cells / (ms / 1e3) / 1e6, 1),
+                      "ref_s": round(ref_s, 3), "ref_cores": cores,
+                      "ref_mlups": round(gpu_c["cell_updates"] / ref_s / 1e6, 2),
+                      "speedup": round(ref_s * 1e3 / ms, 1), "same_log_and_counters": same}), flush=True)
+
+
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("what", choices=["c5", "c3", "c4"])
+    p.add_argument("what", choices=["c1", "c5", "c3", "c4"])
     p.add_argument("--n", type=int, default=None)
     p.add_argument("--steps", type=int, default=None)
     p.add_argument("--warmup", type=int, default=3)
@@ -119,6 +149,9 @@ def main():
         a.n = a.n or 256
         a.steps = a.steps or 20
         c5(a)
+    elif a.what == "c1":
+        a.steps = a.steps or 500
+        c1(a)
     elif a.what == "c4":
         a.steps = a.steps or 400
         a.every = 50
