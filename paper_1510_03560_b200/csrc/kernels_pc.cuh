@@ -416,8 +416,9 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
     __syncthreads();
     issue_ring(LAG);
     cp_async_commit();
-#pragma unroll 1
-    for (int p = 0; p < LAG; ++p) wait_pushed(p);
+    if (warp == 0)
+        for (int p = 0; p < LAG; ++p) wait_pushed(p);
+    __syncthreads();
 #pragma unroll 1
     for (int z = 0; z < E; ++z) {
         const int pn = z + LAG;
@@ -430,11 +431,14 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
         } else if (pn == E) {
             fill_zghost(E);
         }
+        // The peers' psi of plane z+1: one warp polls the mbarrier, the CTA
+        // barrier then releases the others (they wait in bar.sync instead of
+        // spinning) and carries the acquired data to them.
+        if (warp == 0 && z + 1 < E && z + 1 >= LAG) wait_pushed(z + 1);
         __syncthreads();  // psi plane pn visible; every warp is past collide(z-1)
         flush_xcol(z - 1);
         issue_ring(pn + 1);  // its ring slot is no longer read by anyone
         cp_async_commit();
-        if (z + 1 < E && z + 1 >= LAG) wait_pushed(z + 1);
         collide_plane(z);
     }
     cp_async_wait<0>();
