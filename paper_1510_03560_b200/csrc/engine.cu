@@ -18,6 +18,7 @@
 // ranks' double-buffered reads and writes.
 #include "kernels.cuh"
 #include "kernels_pc.cuh"
+#include "expand.cuh"
 #include "plbm_gpu.h"
 
 #include <cuda_runtime.h>
@@ -365,6 +366,33 @@ class Engine {
     int* d_coords_ = nullptr;
     double* d_u_face_ = nullptr;
     uint8_t* d_trig_ = nullptr;
+    // device-side expansion (single rank, progressive; expand.cuh)
+    bool dev_expand_ = false;
+    int* d_gslot_ = nullptr;
+    unsigned long long* d_cand_ = nullptr;
+    int* d_nactive_ = nullptr;
+    int* d_next_slot_ = nullptr;
+    int* d_next_local_ = nullptr;
+    int* d_owner_ = nullptr;
+    uint8_t* d_geomdev_ = nullptr;
+    uint8_t* d_p2p_ = nullptr;
+    unsigned long long* d_per_dev_ = nullptr;
+    unsigned long long* d_acc_ = nullptr;  // cell_updates, bytes[3], active_cells, step_bytes[3]
+    BirthRec* d_births_ = nullptr;
+    int* d_nbirths_ = nullptr;
+    int* d_post_flags_ = nullptr;
+    int synced_births_ = 0;
+    int launch_tiles_ = 0;
+    void sync_births();
+    // tiles the launches leave room for beyond the current map (births past
+    // it go to the host); PLBM_EXPAND_HEADROOM overrides (tests)
+    int expand_headroom() const {
+        if (const char* h = std::getenv("PLBM_EXPAND_HEADROOM")) return std::max(0, std::atoi(h));
+        return std::max(64, int(all_active_.size()) / 4);
+    }
+    void upload_expand_state(bool initial);
+    ExpandDev expand_dev() const;
+    void launch_check_expand(long it);
     uint8_t* d_bmask_ = nullptr;  // [slot] faces whose trigger would be a birth
     uint8_t* d_omask_ = nullptr;  // [slot] faces whose trigger is out of bounds (suppressed)
     int* d_halt_ = nullptr;       // sticky halt flag of the speculative step queue
@@ -568,6 +596,35 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     d_halt_ = dmalloc<int>(1);
     CK(cudaMemsetAsync(d_halt_, 0, sizeof(int), stream_));
     CK(cudaMallocHost(&h_flags_, 8 * sizeof(int)));
+    {
+        const char* de = std::getenv("PLBM_DEVICE_EXPAND");
+        dev_expand_ = world_ == 1 && mode_ == PLBM_MODE_PROGRESSIVE && spec_depth_ > 1 && !(de && de[0] == '0');
+    }
+    if (dev_expand_) {
+        const size_t ngrid = size_t(grid_[0]) * grid_[1] * grid_[2];
+        d_gslot_ = dmalloc<int>(ngrid);
+        d_cand_ = dmalloc<unsigned long long>(ngrid);
+        CK(cudaMemsetAsync(d_cand_, 0xff, ngrid * sizeof(unsigned long long), stream_));
+        d_nactive_ = dmalloc<int>(1);
+        d_next_slot_ = dmalloc<int>(1);
+        d_next_local_ = dmalloc<int>(1);
+        d_owner_ = dmalloc<int>(nslot);
+        d_p2p_ = dmalloc<uint8_t>(size_t(devices_) * devices_);
+        CK(cudaMemcpyAsync(d_p2p_, p2p_.data(), p2p_.size(), cudaMemcpyHostToDevice, stream_));
+        if (!geom_.empty()) {
+            d_geomdev_ = dmalloc<uint8_t>(geom_.size());
+            CK(cudaMemcpyAsync(d_geomdev_, geom_.data(), geom_.size(), cudaMemcpyHostToDevice, stream_));
+        }
+        d_per_dev_ = dmalloc<unsigned long long>(size_t(devices_));
+        d_acc_ = dmalloc<unsigned long long>(8);
+        CK(cudaMemsetAsync(d_acc_, 0, 8 * sizeof(unsigned long long), stream_));
+        d_births_ = dmalloc<BirthRec>(size_t(cap_) + 1);
+        d_nbirths_ = dmalloc<int>(1);
+        CK(cudaMemsetAsync(d_nbirths_, 0, sizeof(int), stream_));
+        d_post_flags_ = dmalloc<int>(1);
+        CK(cudaMemsetAsync(d_post_flags_, 0, sizeof(int), stream_));
+        CK(cudaStreamSynchronize(stream_));
+    }
     for (auto& e : flag_ev_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     if (const char* sd = std::getenv("PLBM_SPEC_DEPTH")) spec_depth_ = std::max(1, std::min(8, std::atoi(sd)));
     d_pokes_ = dmalloc<Poke>(64);
@@ -637,6 +694,7 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     d_.halt = nullptr;
     d_.pokes = nullptr;
     d_.npoke = 0;
+    d_.nactive = nullptr;
 
     // ---- host mirror + initial tiles (make_state, engine.cpp:134-159)
     grid_slot_.assign(n_tiles, -1);
@@ -725,7 +783,9 @@ void Engine::release() {
     void* ptrs[] = {d_pool_f_, d_pool_pf_, d_slot_f_[0], d_slot_f_[1], d_slot_pf_[0], d_slot_pf_[1],
                     d_route_[0], d_route_[1], d_lidx_, d_solid_, d_has_solid_, d_mode_, d_coords_,
                     d_u_face_, d_trig_, d_capture_, d_cnt_, d_err_, d_active_, d_scratch_slots_,
-                    d_readback_, d_dep_cnt_, d_dep_need_, d_geo_, d_bmask_, d_omask_, d_halt_, d_pokes_};
+                    d_readback_, d_dep_cnt_, d_dep_need_, d_geo_, d_bmask_, d_omask_, d_halt_, d_pokes_,
+                    d_gslot_, d_cand_, d_nactive_, d_next_slot_, d_next_local_, d_owner_, d_geomdev_, d_p2p_,
+                    d_per_dev_, d_acc_, d_births_, d_nbirths_, d_post_flags_};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (h_flags_) cudaFreeHost(h_flags_);
@@ -1034,15 +1094,156 @@ void Engine::upload_map(const std::vector<int>& new_slots, bool initial) {
     for (int s : mine)
         if (h_has_solid_[s]) stats_.h2d_bytes += solid_words_ * sizeof(uint32_t);
     recompute_step_bytes();
+    if (dev_expand_) upload_expand_state(initial);
     // the host vectors must outlive the async copies
     CK(cudaStreamSynchronize(stream_));
+}
+
+// The host mirror is authoritative after a host-side expansion (initial tiles
+// or a halt): the device-side expansion state follows it.
+void Engine::upload_expand_state(bool initial) {
+    const size_t nslot = size_t(cap_ + 1);
+    std::vector<int> owner(nslot, -1);
+    for (int s : all_active_) owner[size_t(s)] = slots_[s].owner;
+    CK(cudaMemcpyAsync(d_gslot_, grid_slot_.data(), grid_slot_.size() * sizeof(int), cudaMemcpyHostToDevice,
+                       stream_));
+    CK(cudaMemcpyAsync(d_owner_, owner.data(), nslot * sizeof(int), cudaMemcpyHostToDevice, stream_));
+    CK(cudaMemcpyAsync(d_per_dev_, per_dev_.data(), per_dev_.size() * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                       stream_));
+    const int ints[3] = {int(all_active_.size()), cap_ - int(free_slots_.size()), next_local_[0]};
+    CK(cudaMemcpyAsync(d_nactive_, &ints[0], sizeof(int), cudaMemcpyHostToDevice, stream_));
+    CK(cudaMemcpyAsync(d_next_slot_, &ints[1], sizeof(int), cudaMemcpyHostToDevice, stream_));
+    CK(cudaMemcpyAsync(d_next_local_, &ints[2], sizeof(int), cudaMemcpyHostToDevice, stream_));
+    const unsigned long long map_acc[4] = {active_cells_, step_bytes_[0], step_bytes_[1], step_bytes_[2]};
+    CK(cudaMemcpyAsync(d_acc_ + 4, map_acc, sizeof map_acc, cudaMemcpyHostToDevice, stream_));
+    const int flags = initial ? 1 : 3;  // GEN modes to reset; pull routes to catch up
+    CK(cudaMemcpyAsync(d_post_flags_, &flags, sizeof(int), cudaMemcpyHostToDevice, stream_));
+    CK(cudaStreamSynchronize(stream_));
+    any_gen_ = routes_differ_ = false;  // k_post_main does them
+    launch_tiles_ = std::min(cap_, int(all_active_.size()) + expand_headroom());
+}
+
+// Replays the device's births into the host mirror (slots, log, owners,
+// counts), so counters, tiles, creation log and read-back see the device map.
+void Engine::sync_births() {
+    if (!dev_expand_) return;
+    // tiles that have stepped are in PULL mode on the device (k_post_main)
+    for (size_t s = 0; s < h_mode_.size(); ++s)
+        if (h_mode_[s] != MODE_PULL && slots_[s].birth < iteration_) h_mode_[s] = MODE_PULL;
+    int nb = 0;
+    CK(cudaMemcpyAsync(&nb, d_nbirths_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+    CK(cudaStreamSynchronize(stream_));
+    if (nb <= synced_births_) return;
+    std::vector<BirthRec> recs(size_t(nb - synced_births_));
+    CK(cudaMemcpyAsync(recs.data(), d_births_ + synced_births_, recs.size() * sizeof(BirthRec),
+                       cudaMemcpyDeviceToHost, stream_));
+    CK(cudaStreamSynchronize(stream_));
+    stats_.d2h_bytes += sizeof(int) + recs.size() * sizeof(BirthRec);
+    for (const BirthRec& r : recs) {
+        const int s = r.slot;
+        if (free_slots_.empty() || free_slots_.back() != s)
+            throw std::runtime_error("device expansion: slot order diverged from the host mirror");
+        free_slots_.pop_back();
+        SlotInfo& si = slots_[s];
+        si = SlotInfo{};
+        si.c = {r.x, r.y, r.z};
+        si.birth = long(r.it);
+        si.fluid = r.fluid;
+        si.has_solid = r.has_solid != 0;
+        si.owner = r.owner;
+        si.rank = 0;
+        si.local = r.local;
+        si.log_index = log_.size();
+        log_.push_back({long(r.it), si.c, r.trigger, r.owner});
+        grid_slot_[lin(si.c)] = s;
+        ++per_dev_[size_t(r.owner)];
+        next_local_[0] = r.local + 1;
+        h_mode_[s] = long(r.it) >= iteration_ ? MODE_GEN_AMBIENT : MODE_PULL;
+        h_has_solid_[s] = uint8_t(r.has_solid);
+        h_coords_[3 * size_t(s)] = r.x;
+        h_coords_[3 * size_t(s) + 1] = r.y;
+        h_coords_[3 * size_t(s) + 2] = r.z;
+        h_lidx_[s] = r.local;
+        active_cells_ += uint64_t(r.fluid);
+        local_cells_ += uint64_t(r.fluid);
+    }
+    all_active_.clear();
+    active_.clear();
+    for (size_t k = 0; k < grid_slot_.size(); ++k)
+        if (grid_slot_[k] >= 0) {
+            all_active_.push_back(grid_slot_[k]);
+            active_.push_back(grid_slot_[k]);
+        }
+    recompute_step_bytes();
+    synced_births_ = nb;
+    launch_tiles_ = std::min(cap_, int(all_active_.size()) + expand_headroom());
+}
+
+void Engine::launch_check_expand(long it) {
+    const ExpandDev x = expand_dev();
+    switch (E_) {
+    case 8: k_check_expand<8><<<1, 1024, 0, stream_>>>(d_, x, it, d_halt_); break;
+    case 16: k_check_expand<16><<<1, 1024, 0, stream_>>>(d_, x, it, d_halt_); break;
+    default: k_check_expand<32><<<1, 1024, 0, stream_>>>(d_, x, it, d_halt_); break;
+    }
+}
+
+ExpandDev Engine::expand_dev() const {
+    ExpandDev x{};
+    x.gslot = d_gslot_;
+    x.cand = d_cand_;
+    x.active = d_active_;
+    x.nactive = d_nactive_;
+    x.next_slot = d_next_slot_;
+    x.next_local = d_next_local_;
+    x.owner = d_owner_;
+    x.coords = d_coords_;
+    x.mode = d_mode_;
+    x.has_solid = d_has_solid_;
+    x.solid = d_solid_;
+    x.lidx = d_lidx_;
+    x.route_psi = d_route_[ROUTE_PSI];
+    x.bmask = d_bmask_;
+    x.omask = d_omask_;
+    for (int b = 0; b < 2; ++b) {
+        x.slot_f[b] = d_slot_f_[b];
+        x.slot_pf[b] = d_slot_pf_[b];
+    }
+    x.pool_f = d_pool_f_;
+    x.pool_pf = d_pool_pf_;
+    x.per_slot = per_slot_;
+    x.per_pf = per_pf_;
+    x.lcap = lcap_;
+    x.geom = d_geomdev_;
+    x.p2p = d_p2p_;
+    x.per_dev = d_per_dev_;
+    x.acc = d_acc_;
+    x.births = d_births_;
+    x.nbirths = d_nbirths_;
+    x.post_flags = d_post_flags_;
+    x.capture = d_capture_;
+    x.cap = cap_;
+    x.amb = amb_;
+    x.devices = devices_;
+    x.policy = policy_;
+    x.max_active = launch_tiles_;
+    x.solid_words = solid_words_;
+    for (int a = 0; a < 3; ++a) {
+        x.periodic[a] = periodic_[a];
+        x.dom[a] = dom_[a];
+    }
+    x.w_p2p = w_p2p_;
+    x.w_staged = w_staged_;
+    x.face_xfer = face_xfer_;
+    return x;
 }
 
 void Engine::launch_face(int src, int flags, long iter) {
     if (active_.empty()) return;
     EvPair* ev = profiling_ ? &next_event(1, 0) : nullptr;
     if (ev) CK(cudaEventRecord(ev->a, stream_));
-    K_.face(d_, d_active_, src, flags, iter, unsigned(active_.size()), stream_);
+    K_.face(d_, d_active_, src, flags, iter, unsigned(dev_expand_ && d_.nactive ? launch_tiles_ : int(active_.size())),
+            stream_);
     CK(cudaGetLastError());
     ++stats_.kernels_launched;
     if (ev) CK(cudaEventRecord(ev->b, stream_));
@@ -1055,7 +1256,7 @@ void Engine::launch_main(long iter) {
     const int wu = mode_ == PLBM_MODE_PROGRESSIVE ? 1 : 0;
     MainFn fn = K_.main_plain;
     // single rank: the pc kernels run the face pass themselves (no k_face)
-    const auto fusable = [&](MainFn f) { return world_ == 1 && f && (f == K_.main_pc || f == K_.main_pc2 || f == K_.main_pc128); };
+    const auto fusable = [&](MainFn f) { return world_ == 1 && f && (f == K_.main_pc || f == K_.main_pc2 || f == K_.main_pc128) && !dev_expand_; };
     if (variant_ == 0) fn = K_.main_pc ? K_.main_pc : (K_.main_tm ? K_.main_tm : K_.main_plain);
     if (K_.main_tm && variant_ >= 2 && variant_ < 18 && K_.main_tm_opt[variant_ - 2])
         fn = K_.main_tm_opt[variant_ - 2];
@@ -1067,7 +1268,8 @@ void Engine::launch_main(long iter) {
     d_.xcol_ok = (fn == K_.main_pc || fn == K_.main_pc2 || fn == K_.main_pc128) && !no_xcol_;
     d_.face_flags = face_fused_ ? (FACE_FUSED | FACE_NAN | (mode_ == PLBM_MODE_PROGRESSIVE ? FACE_CRITERION : 0))
                                 : 0;
-    fn(d_, d_active_, cur_, wu, iter, unsigned(active_.size()), stream_);
+    fn(d_, d_active_, cur_, wu, iter,
+       unsigned(dev_expand_ && d_.nactive ? launch_tiles_ : int(active_.size())), stream_);
     CK(cudaGetLastError());
     if (d_.npoke) {  // pokes apply to one step's f_in
         d_.npoke = 0;
@@ -1283,6 +1485,13 @@ void Engine::host_expand(const uint8_t* merged, long it) {
 void Engine::enqueue_step(long it) {
     launch_main(it);
     cur_ ^= 1;
+    if (dev_expand_) {
+        const int nslot = cap_ + 1;
+        k_post_main<<<std::max(1, std::min(256, (nslot * 18 + 255) / 256)), 256, 0, stream_>>>(
+            d_mode_, d_route_[ROUTE_PULL], d_route_[ROUTE_PSI], nslot, d_post_flags_, d_halt_);
+        CK(cudaGetLastError());
+        ++stats_.kernels_launched;
+    }
     if (any_gen_) {
         CK(cudaMemsetAsync(d_mode_, MODE_PULL, size_t(cap_ + 1), stream_));
         std::fill(h_mode_.begin(), h_mode_.end(), uint8_t(MODE_PULL));
@@ -1314,6 +1523,7 @@ int Engine::step_speculative(int n, plbm_error* err) {
     };
     std::deque<Queued> q;
     d_.halt = d_halt_;
+    if (dev_expand_) d_.nactive = d_nactive_;
     in_spec_ = true;
     int done = 0, enqueued = 0, flag_ctr = 0;
     int rc = 0;
@@ -1323,7 +1533,8 @@ int Engine::step_speculative(int n, plbm_error* err) {
             enqueue_step(e.it);
             e.cur_after = cur_;
             e.ev_after = ev_used_;
-            k_check<<<1, 256, 0, stream_>>>(d_, d_bmask_, d_omask_, cap_ + 1, d_halt_);
+            if (dev_expand_) launch_check_expand(e.it);
+            else k_check<<<1, 256, 0, stream_>>>(d_, d_bmask_, d_omask_, cap_ + 1, d_halt_);
             CK(cudaGetLastError());
             ++stats_.kernels_launched;
             CK(cudaMemcpyAsync(&h_flags_[e.flag], d_halt_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
@@ -1335,10 +1546,12 @@ int Engine::step_speculative(int n, plbm_error* err) {
         const Queued e = q.front();
         q.pop_front();
         CK(cudaEventSynchronize(flag_ev_[e.flag]));
-        if (h_flags_[e.flag] == 0) {  // no birth, no error: the step is final
+        if (h_flags_[e.flag] == 0) {  // final (births, if any, done on the device)
             iteration_ = e.it;
-            cell_updates_ += e.updates;
-            for (int a = 0; a < 3; ++a) bytes_[a] += step_bytes_[a];
+            if (!dev_expand_) {  // else counted by k_check_expand
+                cell_updates_ += e.updates;
+                for (int a = 0; a < 3; ++a) bytes_[a] += step_bytes_[a];
+            }
             ++done;
             continue;
         }
@@ -1354,9 +1567,12 @@ int Engine::step_speculative(int n, plbm_error* err) {
             break;
         }
         iteration_ = e.it;
-        cell_updates_ += e.updates;
-        for (int a = 0; a < 3; ++a) bytes_[a] += step_bytes_[a];
+        if (!dev_expand_) {
+            cell_updates_ += e.updates;
+            for (int a = 0; a < 3; ++a) bytes_[a] += step_bytes_[a];
+        }
         ++done;
+        sync_births();  // the mirror catches up with the device's earlier births
         std::vector<uint8_t> trig(trig_bytes_);
         CK(cudaMemcpyAsync(trig.data(), d_trig_, trig_bytes_, cudaMemcpyDeviceToHost, stream_));
         stats_.d2h_bytes += trig_bytes_;
@@ -1367,7 +1583,9 @@ int Engine::step_speculative(int n, plbm_error* err) {
     if (!q.empty() || rc) CK(cudaStreamSynchronize(stream_));
     CK(cudaMemsetAsync(d_halt_, 0, sizeof(int), stream_));
     d_.halt = nullptr;
+    d_.nactive = nullptr;
     in_spec_ = false;
+    sync_births();
     return rc;
 }
 
@@ -1478,6 +1696,13 @@ void Engine::counters(plbm_counters* out) {
     out->zero_rho_forcings = c[CNT_ZERO_RHO];
     out->suppressed_expansions = suppressed_ + c[CNT_SUPP];  // host expand + device k_check
     for (int a = 0; a < 3; ++a) out->bytes[a] = bytes_[a];
+    if (dev_expand_) {  // accumulated by k_check_expand
+        unsigned long long acc[4] = {};
+        CK(cudaMemcpyAsync(acc, d_acc_, sizeof acc, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+        out->cell_updates += acc[0];
+        for (int a = 0; a < 3; ++a) out->bytes[a] += acc[1 + a];
+    }
     out->tiles = all_active_.size();
     out->active_cells = active_cells_;
     const uint64_t g = uint64_t(E_ + 2) * (E_ + 2) * (E_ + 2);

@@ -87,6 +87,7 @@ struct Dev {
     const int* halt;            // speculative queue: a step kernel finding *halt != 0 does nothing
     const struct Poke* pokes;   // test hook (plbm_gpu_poke_f): overrides of f_in for the next step
     int npoke;
+    const int* nactive;         // device-side expansion: tiles beyond *nactive in the launch are idle
 };
 
 struct Poke {
@@ -352,6 +353,7 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
     __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
     __shared__ int s_tc[3];
 
+    if (d.nactive && int(blockIdx.x / NZC) >= *d.nactive) return;
     const int slot = active[blockIdx.x / NZC];
     const int z0 = (blockIdx.x % NZC) * BZ;
     const uint8_t mode = d.mode[slot];
@@ -814,6 +816,7 @@ __global__ void __launch_bounds__(NT) k_face(Dev d, const int* __restrict__ acti
     __shared__ RouteTab rt;
     __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
     __shared__ int s_tc[3];
+    if (d.nactive && int(blockIdx.x / 6) >= *d.nactive) return;
     const int slot = active[blockIdx.x / 6];
     const int face = blockIdx.x % 6;
     const uint8_t mode = d.mode[slot];

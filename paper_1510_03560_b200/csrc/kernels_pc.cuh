@@ -126,6 +126,7 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
     const int c = rank / NB;                   // this CTA's component
     const int yb = rank % NB;
     const int y0 = yb * BY;
+    if (d.nactive && tile_i >= *d.nactive) return;  // (whole clusters: same tile)
     const int slot = active[tile_i];
     const uint8_t mode = d.mode[slot];
     const bool hs = d.has_solid[slot] != 0;

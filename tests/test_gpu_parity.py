@@ -74,3 +74,23 @@ def test_poked_nan_matches_reference(built, name, variant):
     assert errs[0] is not None
     for k in ("iteration", "cell_updates"):
         assert ref.counters()[k] == gpu.counters()[k]
+
+
+@pytest.mark.parametrize("mode", ["device", "host_overflow", "host"])
+@pytest.mark.parametrize("name", ["mpmc_progressive_e16", "c1_progressive_S0", "mpmc_channel_e16"])
+def test_expansion_paths_match_oracle(built, name, mode, monkeypatch):
+    """The device-side expansion (k_check_expand), its overflow to the host
+    (births beyond the launched grid, headroom 0) and the host-only path give
+    the reference's creation log, owners, counters and fields."""
+    if mode == "host":
+        monkeypatch.setenv("PLBM_DEVICE_EXPAND", "0")
+    if mode == "host_overflow":
+        monkeypatch.setenv("PLBM_EXPAND_HEADROOM", "0")
+    make, steps = scenarios.ALL[name]
+    sc = make()
+    orc = capi.oracle_engine(sc)
+    gpu = capi.gpu_engine(sc, capture=True)
+    for chunk in (1, steps - 1):
+        orc.step(chunk)
+        gpu.step(chunk)
+        assert_same_state(orc, gpu, label=f"{name}/{mode}")
