@@ -215,8 +215,9 @@ def main():
 
     os.makedirs(os.path.join(REPO, "gpurun_out"), exist_ok=True)
     # ---- device-timed region -------------------------------------------------
+    # (no per-kernel events inside it: they cost ~3 %; the kernel split for
+    # the roofline comes from a separate profiled pass of the same steps below)
     eng.reset_kernel_stats()
-    eng.set_profiling(True)
     c0 = eng.counters()["cell_updates"]
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -228,9 +229,16 @@ def main():
         barrier()
     ms = ev0.elapsed_time(ev1)
     cells = eng.counters()["cell_updates"] - c0
+    launches = eng.kernel_stats()["kernels_launched"]
+    tiles_at_end = eng.counters()["tiles"]
+
+    # ---- per-kernel CUDA events (roofline of the fused kernel) ----------------
+    eng.reset_kernel_stats()
+    eng.set_profiling(True)
+    run(a.steps)
+    barrier()
     ks = eng.kernel_stats()
     eng.set_profiling(False)
-    tiles_at_end = eng.counters()["tiles"]
 
     # ---- end to end through the C-ABI: step + per-step host read of the
     # report counters (what the reference driver reads each step) -------------
@@ -293,7 +301,7 @@ def main():
         "e2e": {"value": round(e2e, 2), "unit": "MLUPS/comp",
                 "h2d_bytes_per_step": int(e_ks["h2d_bytes"] / max(a.steps, 1)),
                 "d2h_bytes_per_step": int(e_ks["d2h_bytes"] / max(a.steps, 1))},
-        "gpu_launches": int(ks["kernels_launched"]),
+        "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
                      "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4) if achieved else None,
