@@ -142,6 +142,9 @@ int plbm_gpu_sync(void* h);
  * reference's modeled record_exchange classes (plbm_counters.bytes).
  * out[0] = bytes, out[1] = remote face routes, out[2] = remote edge routes. */
 void plbm_gpu_exchange_bytes(void* h, uint64_t* out);
+/* Measurement hook (env PLBM_PROBE at create): per-CTA {SM id, start ns, end
+ * ns} of the last fused-kernel launch, 3 words per CTA; returns the CTAs.    */
+int plbm_gpu_probe(void* h, uint64_t* out, int max);
 
 /* ---- output path -----------------------------------------
  * iobench::gather_field (dump.cpp:21-57): one field ("rho", "u_magnitude",

@@ -300,6 +300,12 @@ class Engine {
     int set_peer(int rank, void* pool_f, void* pool_pf);
     int rank_of(const int32_t* coords) const;
     void exchange_bytes(uint64_t* out) const;
+    int probe(uint64_t* out, int max) {
+        if (!d_.probe) return 0;
+        const int n = std::min(max, 3 * (cap_ + 1) * 16);
+        CK(cudaMemcpy(out, d_.probe, size_t(n) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        return n / 3;
+    }
     int sync() {
         CK(cudaStreamSynchronize(stream_));
         return 0;
@@ -695,6 +701,9 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     d_.pokes = nullptr;
     d_.npoke = 0;
     d_.nactive = nullptr;
+    d_.probe = nullptr;
+    d_.tile_base = 0;
+    if (std::getenv("PLBM_PROBE")) d_.probe = dmalloc<unsigned long long>(3 * size_t(cap_ + 1) * 16);
 
     // ---- host mirror + initial tiles (make_state, engine.cpp:134-159)
     grid_slot_.assign(n_tiles, -1);
@@ -1268,8 +1277,8 @@ void Engine::launch_main(long iter) {
     d_.xcol_ok = (fn == K_.main_pc || fn == K_.main_pc2 || fn == K_.main_pc128) && !no_xcol_;
     d_.face_flags = face_fused_ ? (FACE_FUSED | FACE_NAN | (mode_ == PLBM_MODE_PROGRESSIVE ? FACE_CRITERION : 0))
                                 : 0;
-    fn(d_, d_active_, cur_, wu, iter,
-       unsigned(dev_expand_ && d_.nactive ? launch_tiles_ : int(active_.size())), stream_);
+    const int ntiles = dev_expand_ && d_.nactive ? launch_tiles_ : int(active_.size());
+    fn(d_, d_active_, cur_, wu, iter, unsigned(ntiles), stream_);
     CK(cudaGetLastError());
     if (d_.npoke) {  // pokes apply to one step's f_in
         d_.npoke = 0;
@@ -2012,6 +2021,10 @@ int plbm_gpu_set_peer_pools(void* h, int rank, void* pool_f, void* pool_pf) {
 void plbm_gpu_pool_pointers(void* h, void** pool_f, void** pool_pf) { EG(h)->pool_pointers(pool_f, pool_pf); }
 
 void plbm_gpu_exchange_bytes(void* h, uint64_t* out) { EG(h)->exchange_bytes(out); }
+
+// measurement hook (PLBM_PROBE set at create): per-CTA {smid, start ns, end ns}
+// of the last fused-kernel launch; returns the number of CTAs recorded.
+int plbm_gpu_probe(void* h, uint64_t* out, int max) { return EG(h)->probe(out, max); }
 
 int plbm_gpu_gather_field(void* h, const char* field, int comp, double* grid) {
     try {

@@ -88,7 +88,20 @@ struct Dev {
     const struct Poke* pokes;   // test hook (plbm_gpu_poke_f): overrides of f_in for the next step
     int npoke;
     const int* nactive;         // device-side expansion: tiles beyond *nactive in the launch are idle
+    unsigned long long* probe;  // measurement: per-CTA {smid, start, end} globaltimer (or nullptr)
+    int tile_base;              // this launch's tiles start at active[tile_base] (co-scheduled split)
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned smid() {
+    unsigned s;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+    return s;
+}
 
 struct Poke {
     int slot, comp, i, cell;
@@ -353,7 +366,7 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
     __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
     __shared__ int s_tc[3];
 
-    if (d.nactive && int(blockIdx.x / NZC) >= *d.nactive) return;
+    if (d.nactive && d.tile_base + int(blockIdx.x / NZC) >= *d.nactive) return;
     const int slot = active[blockIdx.x / NZC];
     const int z0 = (blockIdx.x % NZC) * BZ;
     const uint8_t mode = d.mode[slot];
@@ -816,7 +829,7 @@ __global__ void __launch_bounds__(NT) k_face(Dev d, const int* __restrict__ acti
     __shared__ RouteTab rt;
     __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
     __shared__ int s_tc[3];
-    if (d.nactive && int(blockIdx.x / 6) >= *d.nactive) return;
+    if (d.nactive && d.tile_base + int(blockIdx.x / 6) >= *d.nactive) return;
     const int slot = active[blockIdx.x / 6];
     const int face = blockIdx.x % 6;
     const uint8_t mode = d.mode[slot];

@@ -101,6 +101,7 @@ template <int E, int C, int LAG, int NT_ = 256>
 __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __restrict__ active,
                                                             int src_buf, int write_uface, long iter) {
     if (halted(d)) return;
+    const unsigned long long t_start = d.probe ? global_ns() : 0ull;
     using T = PcCfg<E, C, LAG, NT_>;
     constexpr int NMB = T::NMB;
     constexpr int NT = T::NT, BY = T::BY, NB = T::NB, PW = T::PW, PH = T::PH, PP = T::PP;
@@ -126,7 +127,7 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
     const int c = rank / NB;                   // this CTA's component
     const int yb = rank % NB;
     const int y0 = yb * BY;
-    if (d.nactive && tile_i >= *d.nactive) return;  // (whole clusters: same tile)
+    if (d.nactive && d.tile_base + tile_i >= *d.nactive) return;  // (whole clusters: same tile)
     const int slot = active[tile_i];
     const uint8_t mode = d.mode[slot];
     const bool hs = d.has_solid[slot] != 0;
@@ -461,6 +462,11 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
         }
     };
     cluster_sync();  // every push into a peer has landed; the whole tile is written
+    if (d.probe && tid == 0) {
+        d.probe[3 * blockIdx.x] = smid();
+        d.probe[3 * blockIdx.x + 1] = t_start;
+        d.probe[3 * blockIdx.x + 2] = global_ns();
+    }
     if (!fused) return;
 
     // ---- fused face pass ---------------------------------------------------------

@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(256, 2) k_main_tm(Dev d, const int* __restrict
     const int tile_i = blockIdx.x / NB;
     const int yb = blockIdx.x % NB;
     const int y0 = yb * BY;
-    if (d.nactive && tile_i >= *d.nactive) return;  // (whole clusters: same tile)
+    if (d.nactive && d.tile_base + tile_i >= *d.nactive) return;  // (whole clusters: same tile)
     const int slot = active[tile_i];
     const uint8_t mode = d.mode[slot];
     const bool hs = d.has_solid[slot] != 0;
