@@ -107,6 +107,7 @@ struct Kernels {
     MainFn main_pc2;    // variant 22: as 21 with psi computed two planes ahead
     MainFn main_pc128;  // variant 23: 4-warp CTAs (measured slower, 3.64 ms; not instantiated)
     void (*face)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
+    void (*face_v[2])(Dev, const int*, int, int, long, unsigned, cudaStream_t);
     void (*readback)(Dev, int, int, int, double*, cudaStream_t);
     void (*gather)(Dev, const int*, int, int, int, int, double*, int, int, cudaStream_t);
     int nt;
@@ -189,9 +190,15 @@ Kernels make_kernels() {
             k.main_pc2 = launch_pc<E, C, 2>;
         }
     }
-    k.face = [](Dev d, const int* act, int src, int flags, long it, unsigned ntiles, cudaStream_t s) {
-        k_face<E, C, NT><<<ntiles * 6, NT, 0, s>>>(d, act, src, flags, it);
+    // k_face at 4 CTAs/SM, one item in flight per thread (64 registers),
+    // measured faster than 2 CTAs/SM with a one-item prefetch (PLBM_FACE_VARIANT=1)
+    k.face_v[0] = [](Dev d, const int* act, int src, int flags, long it, unsigned ntiles, cudaStream_t s) {
+        k_face<E, C, NT, 4, false><<<ntiles * 6, NT, 0, s>>>(d, act, src, flags, it);
     };
+    k.face_v[1] = [](Dev d, const int* act, int src, int flags, long it, unsigned ntiles, cudaStream_t s) {
+        k_face<E, C, NT, 2, true><<<ntiles * 6, NT, 0, s>>>(d, act, src, flags, it);
+    };
+    k.face = k.face_v[0];
     k.readback = [](Dev d, int slot, int c, int src, double* out, cudaStream_t s) {
         k_readback<E><<<(E * E * E + 255) / 256, 256, 0, s>>>(d, slot, c, src, out);
     };
@@ -633,6 +640,7 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     }
     for (auto& e : flag_ev_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     if (const char* sd = std::getenv("PLBM_SPEC_DEPTH")) spec_depth_ = std::max(1, std::min(8, std::atoi(sd)));
+    if (const char* fv = std::getenv("PLBM_FACE_VARIANT")) K_.face = K_.face_v[std::atoi(fv) == 1 ? 1 : 0];
     d_pokes_ = dmalloc<Poke>(64);
     d_dep_cnt_ = dmalloc<int>(nslot);
     d_dep_need_ = dmalloc<int>(nslot);

@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(1024) k_check_expand(Dev d, ExpandDev x, long 
     constexpr int NT = 1024;
     const int gx = P.grid[0], gy = P.grid[1], gz = P.grid[2];
     const int ngrid = gx * gy * gz;
-    __shared__ int s_err, s_nb, s_chunk, s_solid_any;
+    __shared__ int s_err, s_nb, s_chunk, s_solid_any, s_any;
     __shared__ unsigned long long s_supp;
     __shared__ int s_wsum[32];
     auto wrap = [&](int* q) {  // periodic wrap; false if out of bounds
@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(1024) k_check_expand(Dev d, ExpandDev x, long 
         s_err = (*d.err != ~0ull) ? 1 : 0;
         s_supp = 0;
         s_nb = 0;
+        s_any = 0;
         *x.post_flags = 0;  // consumed by this step's k_post_main
     }
     __syncthreads();
@@ -146,13 +147,14 @@ __global__ void __launch_bounds__(1024) k_check_expand(Dev d, ExpandDev x, long 
         const int t = lin(q);
         if (x.gslot[t] >= 0) continue;
         atomicMin(&x.cand[t], (unsigned long long)lin(&x.coords[3 * s]) * 8ull + (unsigned long long)f);
+        s_any = 1;
     }
     supp = __reduce_add_sync(0xffffffffu, supp);
     if ((tid & 31) == 0 && supp) atomicAdd(&s_supp, (unsigned long long)supp);
     __syncthreads();
     // ---- 2. births in coordinate order (grid scan = coordinate order) -------
-    int nb = 0;
-    for (int base = 0; base < ngrid; base += NT) {
+    int nb = 0;  // no candidate written (the usual step): cand is all ~0, nb = 0
+    for (int base = 0; s_any && base < ngrid; base += NT) {
         const int t = base + tid;
         block_scan(t < ngrid && x.cand[t] != ~0ull);
         nb += s_chunk;

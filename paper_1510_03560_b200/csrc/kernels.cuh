@@ -644,8 +644,10 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
 // and component, pull f_in^(k+1), psi for the next step's ghost faces, the P5
 // NaN check (engine.cpp:509-512) and, on a frontier face, the activation
 // criterion (tilemap.cpp:182-218).  Work items are (face cell, component)
-// pairs; each thread prefetches its next item's 19 populations before it
-// finishes the current one, so two items' loads are in flight per thread.
+// pairs; with PF each thread prefetches its next item's 19 populations before
+// it finishes the current one (two items in flight per thread, 126 registers);
+// without PF one item is in flight and occupancy supplies the parallelism (the
+// standalone k_face runs that way at 4 CTAs/SM, measured 0.216 vs 0.245 ms).
 template <int E>
 __device__ __forceinline__ void face_xyz(int face, int idx, int& x, int& y, int& z) {
     const int axis = face >> 1;
@@ -752,7 +754,7 @@ __device__ __forceinline__ bool face_finish(const Dev& d, int mode, int c, bool 
 // Items t = 0, 1, ... of this thread: cell k = k0 + tid + (t / nc) * NT of
 // the 6 E^2 face cells (k < k1), component c0 + t % nc.  Returns the bitmask
 // of faces whose criterion fired (OR over the warp, set by lane 0 only).
-template <int E, int NT, bool COH>
+template <int E, int NT, bool COH, bool PF = true>
 __device__ unsigned face_run(const Dev& d, const RouteTab& rt, int mode, const int* tc, bool hs,
                              const uint32_t* sb, int c0, int nc, int k0, int k1, const int* routes,
                              bool criterion, bool nan_check, int li, double* pf, long iter,
@@ -780,14 +782,23 @@ __device__ unsigned face_run(const Dev& d, const RouteTab& rt, int mode, const i
             fired |= 1u << face;
         return true;
     };
-    double fa[Q], fb[Q];
-    load(0, fa);
+    if constexpr (PF) {
+        double fa[Q], fb[Q];
+        load(0, fa);
 #pragma unroll 1
-    for (int t = 0;; t += 2) {
-        load(t + 1, fb);
-        if (!finish(t, fa)) break;
-        load(t + 2, fa);
-        if (!finish(t + 1, fb)) break;
+        for (int t = 0;; t += 2) {
+            load(t + 1, fb);
+            if (!finish(t, fa)) break;
+            load(t + 2, fa);
+            if (!finish(t + 1, fb)) break;
+        }
+    } else {
+        double fa[Q];
+#pragma unroll 1
+        for (int t = 0;; ++t) {
+            load(t, fa);
+            if (!finish(t, fa)) break;
+        }
     }
     return __reduce_or_sync(0xffffffffu, fired);
 }
@@ -820,8 +831,8 @@ __device__ void face_pass_part(const Dev& d, int slot, int c0, int nc, int k0, i
 
 // k_face: the face pass as its own launch (multi-rank runs, the non-fused
 // kernels, and the initial psi faces).  One CTA per (tile, face).
-template <int E, int C, int NT>
-__global__ void __launch_bounds__(NT) k_face(Dev d, const int* __restrict__ active, int src_buf,
+template <int E, int C, int NT, int MINB = 1, bool PF = true>
+__global__ void __launch_bounds__(NT, MINB) k_face(Dev d, const int* __restrict__ active, int src_buf,
                                              int flags, long iter) {
     if (halted(d)) return;
     constexpr int E2 = E * E;
@@ -842,7 +853,7 @@ __global__ void __launch_bounds__(NT) k_face(Dev d, const int* __restrict__ acti
             s_solid[k] = d.solid[size_t(slot) * d.solid_words + k];
     __syncthreads();
     const int tile_lin = (s_tc[0] * P.grid[1] + s_tc[1]) * P.grid[2] + s_tc[2];
-    const unsigned f = face_run<E, NT, false>(d, rt, mode, s_tc, hs, s_solid, 0, C, face * E2,
+    const unsigned f = face_run<E, NT, false, PF>(d, rt, mode, s_tc, hs, s_solid, 0, C, face * E2,
                                               (face + 1) * E2, d.route[ROUTE_PSI] + size_t(slot) * 18,
                                               (flags & 1) != 0, (flags & 2) != 0, d.lidx[slot],
                                               d.slot_pf[int((iter + 1) & 1)][slot], iter, tile_lin);
