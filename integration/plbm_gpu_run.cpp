@@ -11,7 +11,9 @@
 //
 // Build: integration/Makefile links the reference objects compiled from
 // /root/reference/proj/src (oracle/Makefile) with libplbm_gpu.so.
-//   integration/_bin/plbm_gpu_run <scenario.toml> [--output DIR] [--device N]
+//   integration/_bin/plbm_gpu_run <scenario.toml> [--output DIR] [--device N] [--compare 1]
+// --compare 1 is the reference's `compare` subcommand (proj/src/cli.cpp:133-157).
+#include "plbm/dump.hpp"
 #include "plbm/engine.hpp"
 #include "plbm/geometry.hpp"
 #include "plbm/report.hpp"
@@ -24,9 +26,12 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <filesystem>
+#include <fstream>
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -167,7 +172,9 @@ std::string snapshot_base(const std::string& field, int comp, long iteration) {
 }
 
 // engine::run_scenario's output contract (engine.cpp:580-704) on GpuEngine.
-int run(const iobench::ScenarioConfig& cfg, int device) {
+engine::RunResult run(const iobench::ScenarioConfig& cfg, int device) {
+    engine::RunResult res;
+    res.output_dir = cfg.output_dir;
     namespace fs = std::filesystem;
     iobench::GeometryMask geom = cfg.geometry_path.empty()
                                      ? iobench::make_empty_geometry(cfg.domain[0], cfg.domain[1], cfg.domain[2])
@@ -187,14 +194,16 @@ int run(const iobench::ScenarioConfig& cfg, int device) {
     if (snapshots) fs::create_directories(cfg.output_dir + "/snapshots");
     auto take_snapshot = [&](long iter) {
         for (const std::string& field : cfg.snapshot_fields)
-            for (int c = 0; c < cfg.n_components(); ++c)
-                eng.dump_field(field, c, iter, cfg.output_dir + "/snapshots/" + snapshot_base(field, c, iter),
-                               cfg.snapshot_pgm);
+            for (int c = 0; c < cfg.n_components(); ++c) {
+                const std::string base = snapshot_base(field, c, iter);
+                eng.dump_field(field, c, iter, cfg.output_dir + "/snapshots/" + base, cfg.snapshot_pgm);
+                res.snapshot_bases.push_back("snapshots/" + base);
+            }
     };
     if (snapshots) take_snapshot(0);
 
     const std::uint64_t bbox_cells = std::uint64_t(cfg.domain[0]) * cfg.domain[1] * cfg.domain[2];
-    std::vector<iobench::ReportRow> rows;
+    std::vector<iobench::ReportRow>& rows = res.rows;
     std::uint64_t peak_bytes = eng.counters().bytes_resident;
     double total_seconds = 0.0, win_seconds = 0.0;
     std::uint64_t win_updates = 0, win_steps = 0;
@@ -245,7 +254,7 @@ int run(const iobench::ScenarioConfig& cfg, int device) {
     const plbm_counters c = eng.counters();
     if (aborted && win_steps > 0) flush_row(long(c.iteration));
 
-    iobench::RunSummary sum;
+    iobench::RunSummary& sum = res.summary;
     sum.name = cfg.name;
     sum.mode = cfg.mode == iobench::RunMode::Static ? "static" : "progressive";
     sum.policy = cfg.policy == sched::AssignPolicy::Simple ? "simple" : "optimized";
@@ -276,28 +285,139 @@ int run(const iobench::ScenarioConfig& cfg, int device) {
     std::printf("%s: %ld iterations, %llu cell updates, %.3f s, %.1f MLUPS -> %s\n", cfg.name.c_str(),
                 sum.iterations, (unsigned long long)sum.total_cell_updates, total_seconds, sum.mlups,
                 cfg.output_dir.c_str());
-    return aborted ? 1 : 0;
+    res.aborted = aborted;
+    res.abort_context = abort_context;
+    return res;
+}
+
+// ---- compare mode (proj/src/cli.cpp:133-157) --------------------------------
+// Both modes on the GPU engine under <out>/static and <out>/progressive, the
+// max |a - b| of every snapshot pair, and the joined compare.csv /
+// compare_summary.json in the reference's formats (cli.cpp:35-131).
+struct PairDiff {
+    std::string base;
+    double max_abs;
+};
+
+double max_abs_diff(const std::string& a_dir, const std::string& b_dir, const std::string& base) {
+    const std::vector<double> a = iobench::read_raw(a_dir + "/" + base + ".raw");
+    const std::vector<double> b = iobench::read_raw(b_dir + "/" + base + ".raw");
+    if (a.size() != b.size()) throw std::runtime_error("compare: snapshot size mismatch at " + base);
+    double m = 0.0;
+    for (size_t i = 0; i < a.size(); ++i) m = std::max(m, std::abs(a[i] - b[i]));
+    return m;
+}
+
+std::string fmt(const char* f, double v) {
+    char buf[64];
+    std::snprintf(buf, sizeof buf, f, v);
+    return buf;
+}
+
+void write_compare_csv(const iobench::ScenarioConfig& cfg, const engine::RunResult& st,
+                       const engine::RunResult& pr, const std::vector<PairDiff>& diffs, const std::string& path) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw std::runtime_error("cannot write " + path);
+    const std::uint64_t fp =
+        mesh::tile_footprint_bytes(cfg.tile_extent, cfg.three_d(), cfg.n_components(), cfg.three_d() ? 19 : 9);
+    std::map<long, double> at;  // snapshot iteration ("..._i<iter>") -> max over fields and components
+    for (const PairDiff& d : diffs) {
+        const long it = std::stol(d.base.substr(d.base.rfind("_i") + 2));
+        auto [e, fresh] = at.try_emplace(it, d.max_abs);
+        if (!fresh) e->second = std::max(e->second, d.max_abs);
+    }
+    out << "iteration";
+    for (const std::string side : {"static", "progressive"})
+        for (const char* col : {"_tiles", "_active_cells", "_resident_bytes", "_bytes_intra", "_bytes_p2p",
+                                "_bytes_staged", "_window_mlups", "_window_mlups_bbox"})
+            out << ',' << side << col;
+    out << ",field_diff_max\n";
+    for (size_t i = 0; i < std::min(st.rows.size(), pr.rows.size()); ++i) {
+        out << st.rows[i].iteration;
+        for (const iobench::ReportRow* r : {&st.rows[i], &pr.rows[i]})
+            out << ',' << r->tiles << ',' << r->active_cells << ',' << r->tiles * fp << ',' << r->bytes[0] << ','
+                << r->bytes[1] << ',' << r->bytes[2] << fmt(",%.6g", r->window_mlups)
+                << fmt(",%.6g", r->window_mlups_bbox);
+        const auto e = at.find(st.rows[i].iteration);
+        out << (e == at.end() ? std::string(",") : fmt(",%.17g", e->second)) << '\n';
+    }
+}
+
+void write_compare_summary(const iobench::ScenarioConfig& cfg, const engine::RunResult& st,
+                           const engine::RunResult& pr, const std::vector<PairDiff>& diffs, double dmax,
+                           const std::string& path) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw std::runtime_error("cannot write " + path);
+    char buf[512];
+    out << "{\n  \"scenario\": \"" << cfg.name << "\",\n";
+    for (const auto* side : {&st, &pr}) {
+        const iobench::RunSummary& s = side->summary;
+        std::snprintf(buf, sizeof buf,
+                      "  \"%s\": {\"status\": \"%s\", \"iterations\": %ld, \"tiles_final\": %llu, "
+                      "\"peak_resident_bytes\": %llu, \"mlups\": %.6g, \"mlups_bbox\": %.6g, "
+                      "\"bytes_intra\": %llu, \"bytes_p2p\": %llu, \"bytes_staged\": %llu},\n",
+                      side == &st ? "static" : "progressive", s.status.c_str(), s.iterations,
+                      (unsigned long long)s.tiles_final, (unsigned long long)s.peak_resident_bytes, s.mlups,
+                      s.mlups_bbox, (unsigned long long)s.bytes[0], (unsigned long long)s.bytes[1],
+                      (unsigned long long)s.bytes[2]);
+        out << buf;
+    }
+    const double ratio = st.summary.peak_resident_bytes ? double(pr.summary.peak_resident_bytes) /
+                                                              double(st.summary.peak_resident_bytes)
+                                                        : 0.0;
+    out << fmt("  \"peak_bytes_ratio\": %.6g,\n", ratio) << "  \"snapshot_diffs\": [";
+    for (size_t i = 0; i < diffs.size(); ++i) {
+        std::snprintf(buf, sizeof buf, "%s{\"base\": \"%s\", \"max\": %.17g}", i ? ", " : "",
+                      diffs[i].base.c_str(), diffs[i].max_abs);
+        out << buf;
+    }
+    out << "],\n" << fmt("  \"field_diff_max\": %.17g\n", dmax) << "}\n";
+}
+
+int compare(const iobench::ScenarioConfig& cfg, int device) {
+    iobench::ScenarioConfig sc = cfg, pc = cfg;
+    sc.mode = iobench::RunMode::Static;
+    sc.output_dir = cfg.output_dir + "/static";
+    pc.mode = iobench::RunMode::Progressive;
+    pc.output_dir = cfg.output_dir + "/progressive";
+    const engine::RunResult st = run(sc, device);
+    const engine::RunResult pr = run(pc, device);
+    std::vector<PairDiff> diffs;
+    double dmax = 0.0;
+    for (const std::string& base : pr.snapshot_bases) {
+        diffs.push_back({base, max_abs_diff(sc.output_dir, pc.output_dir, base)});
+        dmax = std::max(dmax, diffs.back().max_abs);
+    }
+    write_compare_csv(cfg, st, pr, diffs, cfg.output_dir + "/compare.csv");
+    write_compare_summary(cfg, st, pr, diffs, dmax, cfg.output_dir + "/compare_summary.json");
+    std::printf("compare: max field diff over %zu snapshots %.3g -> %s\n", diffs.size(), dmax,
+                cfg.output_dir.c_str());
+    return (st.aborted || pr.aborted) ? 1 : 0;
 }
 
 }  // namespace
 
 int main(int argc, char** argv) {
     if (argc < 2) {
-        std::fprintf(stderr, "usage: %s <scenario.toml> [--output DIR] [--iterations N] [--device N]\n", argv[0]);
+        std::fprintf(stderr, "usage: %s <scenario.toml> [--output DIR] [--iterations N] [--device N] [--compare 1]\n",
+                     argv[0]);
         return 2;
     }
     try {
         iobench::ScenarioConfig cfg = iobench::load_config(argv[1]);
         int device = 0;
+        bool cmp = false;
         for (int k = 2; k + 1 < argc; k += 2) {
             const std::string opt = argv[k];
             if (opt == "--output") cfg.output_dir = argv[k + 1];
             else if (opt == "--iterations") cfg.iterations = std::atol(argv[k + 1]);
             else if (opt == "--device") device = std::atoi(argv[k + 1]);
+            else if (opt == "--compare") cmp = std::atoi(argv[k + 1]) != 0;
             else throw std::runtime_error("unknown option " + opt);
         }
         iobench::validate_config(cfg);
-        return run(cfg, device);
+        if (cmp) return compare(cfg, device);
+        return run(cfg, device).aborted ? 1 : 0;
     } catch (const std::exception& e) {
         std::fprintf(stderr, "plbm_gpu_run: %s\n", e.what());
         return 2;

@@ -13,6 +13,7 @@
 //   plbm_ref_step    -> Engine::step() n times (proj/src/engine.cpp:537-563)
 //   plbm_ref_read_tile / counters / creation_log -> the state callers read
 //                       between steps (SURVEY §8b "State read by callers").
+#include "plbm/cli.hpp"
 #include "plbm/dump.hpp"
 #include "plbm/engine.hpp"
 #include "plbm/scenario.hpp"
@@ -415,6 +416,21 @@ int plbm_ref_run_toml(const char* path, const char* output_dir) {
         engine::run_scenario(cfg);
     } catch (const std::exception& e) {
         std::fprintf(stderr, "plbm_ref_run_toml: %s\n", e.what());
+        return -2;
+    }
+    return 0;
+}
+
+// The reference's compare mode (proj/src/cli.cpp:133-157): the scenario in
+// both modes under <output_dir>/{static,progressive}, every snapshot pair
+// diffed, compare.csv and compare_summary.json written.
+int plbm_ref_run_compare_toml(const char* path, const char* output_dir) {
+    try {
+        auto cfg = iobench::load_config(path);
+        cfg.output_dir = output_dir;
+        iobench::run_compare(cfg);
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "plbm_ref_run_compare_toml: %s\n", e.what());
         return -2;
     }
     return 0;

@@ -9,6 +9,10 @@ same three report files with the same formats (proj/src/report.cpp:24-81):
     <out>/summary.json      RunSummary as nlohmann::json::dump(2)
     <out>/snapshots/<field>_c<k>_i<iter>.raw/.meta[/.pgm]  (dump.cpp:59-125)
 
+`run_compare` mirrors the compare mode (proj/src/cli.cpp:133-157): both
+modes under <out>/static and <out>/progressive, every snapshot pair diffed,
+<out>/compare.csv and <out>/compare_summary.json (cli.cpp:35-131).
+
 Counters, creation log, byte classes and snapshot files are identical to the
 reference's for the same scenario (tests/test_output_path.py); the timing
 columns are this engine's own wall-clock.  `workers` is reported as the
@@ -16,6 +20,7 @@ reference would (one per device) — there are no CPU worker threads here.
 """
 from __future__ import annotations
 
+import dataclasses
 import json
 import os
 import time
@@ -166,3 +171,75 @@ def _write_summary(s: dict, path: str) -> None:  # proj/src/report.cpp:51-79
     # nlohmann::json objects are std::map-ordered (sorted keys), dump(2)
     with open(path, "w") as fh:
         fh.write(json.dumps(s, indent=2, sort_keys=True) + "\n")
+
+
+# ---- compare mode (proj/src/cli.cpp:133-157) --------------------------------
+def _fmt_g(v: float, p: int) -> str:
+    return "%.*g" % (p, v)
+
+
+def _snapshot_diff(a_dir: str, b_dir: str, base: str) -> float:
+    """max |a - b| over a snapshot pair (cli.cpp:20-31, read_raw dump.cpp:127)."""
+    import numpy as np
+    a = np.fromfile(os.path.join(a_dir, base + ".raw"), dtype="<f8")
+    b = np.fromfile(os.path.join(b_dir, base + ".raw"), dtype="<f8")
+    if a.size != b.size:
+        raise RuntimeError("compare: snapshot size mismatch at " + base)
+    return float(np.max(np.abs(a - b))) if a.size else 0.0
+
+
+def run_compare(sc: S.Scenario, output_dir: str, iterations: int, name: str = "scenario",
+                make_engine=None, **kw) -> dict:
+    """`make_engine(scenario)` overrides the engine (tests pass the reference
+    engine to check these writers against the reference's on CPU)."""
+    def one(mode, sub):
+        m = dataclasses.replace(sc, mode=mode)
+        eng = make_engine(m) if make_engine else None
+        try:
+            return run_scenario(m, os.path.join(output_dir, sub), iterations, name=name, engine=eng, **kw)
+        finally:
+            if eng is not None:
+                eng.close()
+    st = one(S.MODE_STATIC, "static")
+    pr = one(S.MODE_PROGRESSIVE, "progressive")
+    diffs = [(b, _snapshot_diff(os.path.join(output_dir, "static"), os.path.join(output_dir, "progressive"), b))
+             for b in pr["snapshot_bases"]]
+    dmax = max([d for _, d in diffs], default=0.0)
+    # compare.csv (cli.cpp:33-82): footprint = tile_footprint_bytes (tile.cpp:7-13)
+    g = sc.tile_extent + 2
+    fp = g * g * g * (sc.n_components * (2 * 19 + 8) * 8 + 1)
+    at = {}
+    for b, d in diffs:
+        it = int(b[b.rfind("_i") + 2:])
+        at[it] = max(at.get(it, d), d)
+    cols = ["iteration"]
+    for side in ("static", "progressive"):
+        cols += [side + c for c in ("_tiles", "_active_cells", "_resident_bytes", "_bytes_intra",
+                                    "_bytes_p2p", "_bytes_staged", "_window_mlups", "_window_mlups_bbox")]
+    lines = [",".join(cols + ["field_diff_max"])]
+    for rs, rp in zip(st["rows"], pr["rows"]):
+        f = [str(rs["iteration"])]
+        for r in (rs, rp):
+            f += [str(r["tiles"]), str(r["active_cells"]), str(r["tiles"] * fp)] + [str(v) for v in r["bytes"]]
+            f += [_fmt_g(r["window_mlups"], 6), _fmt_g(r["window_mlups_bbox"], 6)]
+        f.append(_fmt_g(at[rs["iteration"]], 17) if rs["iteration"] in at else "")
+        lines.append(",".join(f))
+    with open(os.path.join(output_dir, "compare.csv"), "w", newline="\n") as fh:
+        fh.write("\n".join(lines) + "\n")
+    # compare_summary.json (cli.cpp:84-131)
+    out = ["{", '  "scenario": "%s",' % name]
+    for key, r in (("static", st), ("progressive", pr)):
+        s = r["summary"]
+        out.append('  "%s": {"status": "%s", "iterations": %d, "tiles_final": %d, "peak_resident_bytes": %d, '
+                   '"mlups": %s, "mlups_bbox": %s, "bytes_intra": %d, "bytes_p2p": %d, "bytes_staged": %d},'
+                   % (key, s["status"], s["iterations"], s["tiles_final"], s["peak_resident_bytes"],
+                      _fmt_g(s["mlups"], 6), _fmt_g(s["mlups_bbox"], 6), s["bytes"]["intra"],
+                      s["bytes"]["p2p"], s["bytes"]["staged"]))
+    ps, ss = pr["summary"]["peak_resident_bytes"], st["summary"]["peak_resident_bytes"]
+    out.append('  "peak_bytes_ratio": %s,' % _fmt_g(ps / ss if ss else 0.0, 6))
+    out.append('  "snapshot_diffs": [%s],' % ", ".join('{"base": "%s", "max": %s}' % (b, _fmt_g(d, 17))
+                                                       for b, d in diffs))
+    out.append('  "field_diff_max": %s' % _fmt_g(dmax, 17))
+    with open(os.path.join(output_dir, "compare_summary.json"), "w", newline="\n") as fh:
+        fh.write("\n".join(out) + "\n}\n")
+    return {"static_run": st, "progressive_run": pr, "diffs": diffs, "max_abs_diff": dmax}

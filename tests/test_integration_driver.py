@@ -75,3 +75,70 @@ def test_cpp_driver_matches_reference_driver(built, tmp_path, name):
     r = subprocess.run([BIN, toml, "--output", str(tmp_path / "gpu")], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     assert_same_outputs(str(tmp_path / "ref"), str(tmp_path / "gpu"))
+
+
+# ---- compare mode (proj/src/cli.cpp:133-157) ---------------------------------
+def ref_run_compare_toml(path, out):
+    lib = capi.load(capi.REF_LIB, "plbm_ref")
+    lib.plbm_ref_run_compare_toml.restype = C.c_int
+    lib.plbm_ref_run_compare_toml.argtypes = [C.c_char_p, C.c_char_p]
+    assert lib.plbm_ref_run_compare_toml(path.encode(), out.encode()) == 0
+
+
+def assert_same_compare(a, b):
+    """compare.csv / compare_summary.json equal except the wall-clock
+    columns; both runs' own outputs equal as in assert_same_outputs."""
+    for side in ("static", "progressive"):
+        assert_same_outputs(f"{a}/{side}", f"{b}/{side}")
+    ra = list(csv.DictReader(open(f"{a}/compare.csv")))
+    rb = list(csv.DictReader(open(f"{b}/compare.csv")))
+    assert open(f"{a}/compare.csv").readline() == open(f"{b}/compare.csv").readline()
+    assert len(ra) == len(rb) > 0
+    timing = {s + c for s in ("static", "progressive") for c in ("_window_mlups", "_window_mlups_bbox")}
+    for x, y in zip(ra, rb):
+        assert {k: v for k, v in x.items() if k not in timing} == {k: v for k, v in y.items() if k not in timing}
+    assert any(r["field_diff_max"] for r in ra)
+    sa, sb = json.load(open(f"{a}/compare_summary.json")), json.load(open(f"{b}/compare_summary.json"))
+    for s in (sa, sb):
+        for side in ("static", "progressive"):
+            s[side].pop("mlups"), s[side].pop("mlups_bbox")
+    assert sa == sb
+    assert len(sa["snapshot_diffs"]) > 0
+
+
+def _compare_toml(tmp_path, name):
+    make, steps = scenarios.ALL[name]
+    sc = make()
+    toml = str(tmp_path / "s.toml")
+    sc.to_toml(toml, iterations=steps, report_interval=4, snapshot_interval=5,
+               snapshot_fields=("rho", "psi"), snapshot_pgm=True)
+    return sc, steps, toml
+
+
+def test_compare_writers_match_reference_on_cpu(built, tmp_path):
+    """driver.run_compare's writers fed by the reference engine == the
+    reference's own run_compare (CPU only: checks the compare.csv /
+    compare_summary.json restatement, not the GPU engine)."""
+    sc, steps, toml = _compare_toml(tmp_path, "c1_progressive")
+    ref_run_compare_toml(toml, str(tmp_path / "ref"))
+    from paper_1510_03560_b200 import driver
+    driver.run_compare(sc, str(tmp_path / "py"), steps, name=sc.name, make_engine=capi.ref_engine,
+                       report_interval=4, snapshot_interval=5, snapshot_fields=("rho", "psi"),
+                       snapshot_pgm=True)
+    assert_same_compare(str(tmp_path / "ref"), str(tmp_path / "py"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("driver_kind", ["cpp", "python"])
+def test_compare_mode_matches_reference(built, tmp_path, driver_kind):
+    sc, steps, toml = _compare_toml(tmp_path, "mpmc_channel_e16")
+    ref_run_compare_toml(toml, str(tmp_path / "ref"))
+    out = str(tmp_path / "gpu")
+    if driver_kind == "cpp":
+        r = subprocess.run([BIN, toml, "--output", out, "--compare", "1"], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+    else:
+        from paper_1510_03560_b200 import driver
+        driver.run_compare(sc, out, steps, name=sc.name, report_interval=4, snapshot_interval=5,
+                           snapshot_fields=("rho", "psi"), snapshot_pgm=True)
+    assert_same_compare(str(tmp_path / "ref"), out)
