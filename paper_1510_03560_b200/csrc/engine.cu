@@ -248,6 +248,7 @@ struct SlotInfo {
     size_t log_index = 0;
     int fluid = 0;
     bool has_solid = false;
+    bool device_sliced = false;  // mask written by k_slice, not uploaded from h_solid_
 };
 
 struct LogRow {
@@ -444,7 +445,8 @@ class Engine {
     size_t lin(const Coord& c) const { return (size_t(c.x) * grid_[1] + c.y) * grid_[2] + c.z; }
     int slot_at(const Coord& c) const { return grid_slot_[lin(c)]; }
     bool neighbor_coords(const Coord& from, int face, Coord& out) const;
-    int create_tile(const Coord& c, long iteration, int trigger);
+    int create_tile(const Coord& c, long iteration, int trigger, bool slice = true);
+    void slice_on_device(const std::vector<int>& slots);
     void assign_owner(int slot);
     int classify(int a, int b) const {
         if (a == b) return 0;
@@ -624,10 +626,6 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
         d_owner_ = dmalloc<int>(nslot);
         d_p2p_ = dmalloc<uint8_t>(size_t(devices_) * devices_);
         CK(cudaMemcpyAsync(d_p2p_, p2p_.data(), p2p_.size(), cudaMemcpyHostToDevice, stream_));
-        if (!geom_.empty()) {
-            d_geomdev_ = dmalloc<uint8_t>(geom_.size());
-            CK(cudaMemcpyAsync(d_geomdev_, geom_.data(), geom_.size(), cudaMemcpyHostToDevice, stream_));
-        }
         d_per_dev_ = dmalloc<unsigned long long>(size_t(devices_));
         d_acc_ = dmalloc<unsigned long long>(8);
         CK(cudaMemsetAsync(d_acc_, 0, 8 * sizeof(unsigned long long), stream_));
@@ -637,6 +635,10 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
         d_post_flags_ = dmalloc<int>(1);
         CK(cudaMemsetAsync(d_post_flags_, 0, sizeof(int), stream_));
         CK(cudaStreamSynchronize(stream_));
+    }
+    if (!geom_.empty()) {  // initial slicing (k_slice) and device expansion
+        d_geomdev_ = dmalloc<uint8_t>(geom_.size());
+        CK(cudaMemcpyAsync(d_geomdev_, geom_.data(), geom_.size(), cudaMemcpyHostToDevice, stream_));
     }
     for (auto& e : flag_ev_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     if (const char* sd = std::getenv("PLBM_SPEC_DEPTH")) spec_depth_ = std::max(1, std::min(8, std::atoi(sd)));
@@ -764,14 +766,22 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
                         if (hit) initial[(size_t(tx) * grid_[1] + ty) * grid_[2] + tz] = 1;
                     }
     }
+    // with a geometry the initial tiles are sliced on the device (k_slice);
+    // owners are assigned after the fluid counts are known, in creation order
+    // (a later tile has owner -1 until then, which assign_device skips)
+    const bool dev_slice = d_geomdev_ != nullptr;
     std::vector<int> created;
     for (size_t k = 0; k < n_tiles; ++k) {
         if (!initial[k]) continue;
         const Coord c{int(k / (size_t(grid_[1]) * grid_[2])), int((k / grid_[2]) % grid_[1]),
                       int(k % grid_[2])};
-        const int s = create_tile(c, 0, -1);
-        assign_owner(s);
+        const int s = create_tile(c, 0, -1, !dev_slice);
+        if (!dev_slice) assign_owner(s);
         created.push_back(s);
+    }
+    if (dev_slice) {
+        slice_on_device(created);
+        for (int s : created) assign_owner(s);
     }
     for (int s : created) h_mode_[s] = MODE_GEN_SEEDED;
     upload_map(created, true);
@@ -830,7 +840,7 @@ bool Engine::neighbor_coords(const Coord& from, int face, Coord& out) const {
 }
 
 // proj/src/tilemap.cpp:83-175 (metadata + solid slicing; fields live on the device)
-int Engine::create_tile(const Coord& c, long iteration, int trigger) {
+int Engine::create_tile(const Coord& c, long iteration, int trigger, bool slice) {
     if (free_slots_.empty()) throw std::runtime_error("block pool exhausted");
     const int s = free_slots_.back();
     free_slots_.pop_back();
@@ -843,7 +853,7 @@ int Engine::create_tile(const Coord& c, long iteration, int trigger) {
     std::fill_n(bits, solid_words_, 0u);
     int fluid = 0;
     bool any = false;
-    for (int lz = -1; lz <= E_; ++lz)
+    for (int lz = -1; slice && lz <= E_; ++lz)
         for (int ly = -1; ly <= E_; ++ly)
             for (int lx = -1; lx <= E_; ++lx) {
                 int g[3] = {c.x * E_ + lx, c.y * E_ + ly, c.z * E_ + lz};
@@ -877,6 +887,51 @@ int Engine::create_tile(const Coord& c, long iteration, int trigger) {
     h_coords_[3 * size_t(s) + 1] = c.y;
     h_coords_[3 * size_t(s) + 2] = c.z;
     return s;
+}
+
+// create_tile's solid slicing for a batch of new tiles on the device; the
+// host mirror keeps the fluid count and has_solid (the mask stays on the GPU:
+// upload_map skips the slots marked device_sliced).
+void Engine::slice_on_device(const std::vector<int>& slots) {
+    if (slots.empty()) return;
+    const int n = int(slots.size());
+    std::vector<int> coords(size_t(3) * n);
+    for (int k = 0; k < n; ++k) {
+        const Coord& c = slots_[slots[k]].c;
+        coords[3 * k] = c.x;
+        coords[3 * k + 1] = c.y;
+        coords[3 * k + 2] = c.z;
+    }
+    int* d_buf = dmalloc<int>(size_t(5) * n);  // slots, coords, fluid; has_solid bytes after
+    int *d_slots = d_buf, *d_coords = d_buf + n, *d_fluid = d_buf + 4 * n;
+    uint8_t* d_hs = dmalloc<uint8_t>(n);
+    CK(cudaMemcpyAsync(d_slots, slots.data(), n * sizeof(int), cudaMemcpyHostToDevice, stream_));
+    CK(cudaMemcpyAsync(d_coords, coords.data(), coords.size() * sizeof(int), cudaMemcpyHostToDevice, stream_));
+    auto go = [&](auto kern) {
+        kern<<<n, 256, 0, stream_>>>(d_slots, d_coords, n, d_geomdev_, dom_[0], dom_[1], dom_[2], periodic_[0],
+                                     periodic_[1], periodic_[2], d_solid_, solid_words_, d_hs, d_fluid);
+    };
+    switch (E_) {
+    case 8: go(k_slice<8>); break;
+    case 16: go(k_slice<16>); break;
+    default: go(k_slice<32>); break;
+    }
+    CK(cudaGetLastError());
+    std::vector<int> fluid(n);
+    std::vector<uint8_t> hs(n);
+    CK(cudaMemcpyAsync(fluid.data(), d_fluid, n * sizeof(int), cudaMemcpyDeviceToHost, stream_));
+    CK(cudaMemcpyAsync(hs.data(), d_hs, n, cudaMemcpyDeviceToHost, stream_));
+    CK(cudaStreamSynchronize(stream_));
+    CK(cudaFree(d_buf));
+    CK(cudaFree(d_hs));
+    for (int k = 0; k < n; ++k) {
+        SlotInfo& si = slots_[slots[k]];
+        si.fluid = fluid[k];
+        si.has_solid = hs[k] != 0;
+        si.device_sliced = true;
+        h_has_solid_[slots[k]] = hs[k];
+        active_cells_ += uint64_t(fluid[k]);
+    }
 }
 
 // proj/src/engine.cpp:30-41 -> proj/src/assign.cpp:8-38; then the GPU rank
@@ -1038,7 +1093,7 @@ void Engine::upload_map(const std::vector<int>& new_slots, bool initial) {
     for (int s : new_slots) {
         if (slots_[s].rank != rank_) continue;
         mine.push_back(s);
-        if (h_has_solid_[s])
+        if (h_has_solid_[s] && !slots_[s].device_sliced)
             CK(cudaMemcpyAsync(d_solid_ + size_t(s) * solid_words_, &h_solid_[size_t(s) * solid_words_],
                                solid_words_ * sizeof(uint32_t), cudaMemcpyHostToDevice, stream_));
         if (d_capture_)

@@ -406,4 +406,59 @@ __global__ void k_post_main(uint8_t* mode, int* route_pull, const int* route_psi
     }
 }
 
+// Solid slicing of the initial tiles (create_tile, tilemap.cpp:94-127: the
+// tile's (E+2)^3 box incl. the ghost ring from the domain geometry, periodic
+// wrap, ambient fluid outside a non-periodic domain) on the device: one CTA
+// per tile, the mask built in shared memory, fluid count and has_solid out.
+template <int E>
+__global__ void __launch_bounds__(256) k_slice(const int* __restrict__ slots, const int* __restrict__ coords,
+                                               int n, const uint8_t* __restrict__ geom, int dx, int dy,
+                                               int dz, int px, int py, int pz, uint32_t* solid,
+                                               int solid_words, uint8_t* has_solid, int* fluid_out) {
+    constexpr int G = E + 2;
+    constexpr int W = (G * G * G + 31) / 32;
+    __shared__ uint32_t bits[W];
+    __shared__ int s_fluid, s_any;
+    const int k = blockIdx.x;
+    if (k >= n) return;
+    const int slot = slots[k];
+    const int t[3] = {coords[3 * k], coords[3 * k + 1], coords[3 * k + 2]};
+    const int dom[3] = {dx, dy, dz}, per[3] = {px, py, pz};
+    for (int w = threadIdx.x; w < W; w += blockDim.x) bits[w] = 0u;
+    if (threadIdx.x == 0) s_fluid = s_any = 0;
+    __syncthreads();
+    int fluid = 0, any = 0;
+    for (int c = threadIdx.x; c < G * G * G; c += blockDim.x) {
+        const int l[3] = {c % G - 1, (c / G) % G - 1, c / (G * G) - 1};
+        int g[3];
+        bool outside = false;
+        for (int a = 0; a < 3; ++a) {
+            g[a] = t[a] * E + l[a];
+            if (g[a] < 0 || g[a] >= dom[a]) {
+                if (per[a]) g[a] = (g[a] + dom[a]) % dom[a];
+                else outside = true;
+            }
+        }
+        const bool sol = !outside && geom[size_t(g[0]) + size_t(dom[0]) * (size_t(g[1]) + size_t(dom[1]) * g[2])];
+        if (sol) {
+            atomicOr(&bits[c >> 5], 1u << (c & 31));
+            any = 1;
+        } else if (l[0] >= 0 && l[0] < E && l[1] >= 0 && l[1] < E && l[2] >= 0 && l[2] < E) {
+            ++fluid;
+        }
+    }
+    fluid = __reduce_add_sync(0xffffffffu, fluid);
+    any = __any_sync(0xffffffffu, any);
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&s_fluid, fluid);
+        if (any) s_any = 1;
+    }
+    __syncthreads();
+    for (int w = threadIdx.x; w < solid_words; w += blockDim.x) solid[size_t(slot) * solid_words + w] = bits[w];
+    if (threadIdx.x == 0) {
+        has_solid[k] = uint8_t(s_any);
+        fluid_out[k] = s_fluid;
+    }
+}
+
 }  // namespace plbm
