@@ -159,15 +159,18 @@ template <int E, int C, bool NOPSI>
 Kernels make_kernels() {
     constexpr int NT = E * E < 256 ? E * E : 256;
     constexpr int BZ = E < 8 ? E : 8;
+    constexpr int YB = E == 64 ? 16 : E;  // y-chunk of the plain kernel (E = 64: psi ring in smem)
     constexpr int G = E + 2;
-    constexpr size_t SMEM_PLAIN = NOPSI ? 0 : size_t(3) * C * G * G * sizeof(double);
+    constexpr size_t SMEM_PLAIN = NOPSI ? 0 : size_t(3) * C * G * (YB + 2) * sizeof(double);
     Kernels k;
     k.nt = NT;
-    if (SMEM_PLAIN > 48 * 1024)
-        cudaFuncSetAttribute(k_main<E, C, BZ, NT, NOPSI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    // (static shared memory counts against the same 48 KB default: opt in
+    // whenever there is a dynamic ring)
+    if (SMEM_PLAIN > 0)
+        cudaFuncSetAttribute(k_main<E, C, BZ, NT, NOPSI, YB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(SMEM_PLAIN));
     k.main_plain = [](Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
-        k_main<E, C, BZ, NT, NOPSI><<<ntiles * (E / BZ), NT, SMEM_PLAIN, s>>>(d, act, src, wu, it);
+        k_main<E, C, BZ, NT, NOPSI, YB><<<ntiles * (E / BZ) * (E / YB), NT, SMEM_PLAIN, s>>>(d, act, src, wu, it);
     };
     k.main_tm = nullptr;
     k.main_pc = k.main_pc2 = k.main_pc128 = nullptr;
@@ -224,7 +227,8 @@ Kernels pick_kernels(int E, int C, bool nopsi) {
     case 8: return pick_c<8>(C, nopsi);
     case 16: return pick_c<16>(C, nopsi);
     case 32: return pick_c<32>(C, nopsi);
-    default: throw std::invalid_argument("tile_extent must be 8, 16 or 32 on the GPU path");
+    case 64: return pick_c<64>(C, nopsi);
+    default: throw std::invalid_argument("tile_extent must be 8, 16, 32 or 64 on the GPU path");
     }
 }
 
@@ -914,7 +918,8 @@ void Engine::slice_on_device(const std::vector<int>& slots) {
     switch (E_) {
     case 8: go(k_slice<8>); break;
     case 16: go(k_slice<16>); break;
-    default: go(k_slice<32>); break;
+    case 32: go(k_slice<32>); break;
+    default: go(k_slice<64>); break;
     }
     CK(cudaGetLastError());
     std::vector<int> fluid(n);
@@ -1256,7 +1261,8 @@ void Engine::launch_check_expand(long it) {
     switch (E_) {
     case 8: k_check_expand<8><<<1, 1024, 0, stream_>>>(d_, x, it, d_halt_); break;
     case 16: k_check_expand<16><<<1, 1024, 0, stream_>>>(d_, x, it, d_halt_); break;
-    default: k_check_expand<32><<<1, 1024, 0, stream_>>>(d_, x, it, d_halt_); break;
+    case 32: k_check_expand<32><<<1, 1024, 0, stream_>>>(d_, x, it, d_halt_); break;
+    default: k_check_expand<64><<<1, 1024, 0, stream_>>>(d_, x, it, d_halt_); break;
     }
 }
 

@@ -346,29 +346,33 @@ __device__ __forceinline__ double psi_ghost(const RouteTab& rt, int c, bool hs, 
 
 // ---------------------------------------------------------------------------
 // k_main: the plain fused kernel (variant 1).  One CTA = one tile x one z-chunk
-// of BZ planes; psi planes (with halo planes recomputed) in a shared ring, and
-// every population pulled twice (psi pass + collide).  Used for E = 8 and for
-// psi-free scenarios (NOPSI: no pseudo-potential stencil at all — a single
-// pull-collide pass per cell).
-template <int E, int C, int BZ, int NT, bool NOPSI>
+// of BZ planes x one y-chunk of YB rows; psi planes (with halo planes and rows
+// recomputed) in a shared ring, and every population pulled twice (psi pass +
+// collide).  Used for E = 8, E = 64 (YB = 16: the whole-plane ring would not
+// fit shared memory) and psi-free scenarios (NOPSI: no pseudo-potential
+// stencil at all — a single pull-collide pass per cell).
+template <int E, int C, int BZ, int NT, bool NOPSI, int YB = E>
 __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ active, int src_buf,
                                              int write_uface, long iter) {
     if (halted(d)) return;
     constexpr int G = E + 2;
-    constexpr int GG = G * G;
+    constexpr int GG = G * (YB + 2);  // one psi plane of the chunk incl. its halo
     constexpr int E2 = E * E;
     constexpr int E3 = E * E * E;
     constexpr int NZC = E / BZ;
-    constexpr int CPT = (E2 + NT - 1) / NT;  // cells per thread per plane
+    constexpr int NYC = E / YB;
+    constexpr int CPT = (E * YB + NT - 1) / NT;          // cells per thread per plane
+    constexpr int PPT = (E * (YB + 2) + NT - 1) / NT;    // psi positions per thread (x inside)
     extern __shared__ double smem[];
     double* psi = smem;  // [3][C][GG] ring of planes (unused when NOPSI)
     __shared__ RouteTab rt_pull, rt_psi;
     __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
     __shared__ int s_tc[3];
 
-    if (d.nactive && d.tile_base + int(blockIdx.x / NZC) >= *d.nactive) return;
-    const int slot = active[blockIdx.x / NZC];
+    if (d.nactive && d.tile_base + int(blockIdx.x / (NZC * NYC)) >= *d.nactive) return;
+    const int slot = active[blockIdx.x / (NZC * NYC)];
     const int z0 = (blockIdx.x % NZC) * BZ;
+    const int y0 = ((blockIdx.x / NZC) % NYC) * YB;
     const uint8_t mode = d.mode[slot];
     const bool hs = d.has_solid[slot] != 0;
     const int amb = P.amb_slot;
@@ -384,21 +388,23 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
     __syncthreads();
     const int tile_lin = (s_tc[0] * P.grid[1] + s_tc[1]) * P.grid[2] + s_tc[2];
 
-    // ---- psi of plane pz (ring slot r) incl. the xy ghost ring -------------
+    // ---- psi of plane pz (ring slot r) on rows y0-1 .. y0+YB incl. the x
+    // ghost columns (rows outside the tile are ghost rows) ---------------------
     auto psi_plane = [&](int pz) {
         const int r = (pz + 3) % 3;
         const bool inside = pz >= 0 && pz < E;
-        const bool owned = pz >= z0 && pz < z0 + BZ;
+        const bool zowned = pz >= z0 && pz < z0 + BZ;
         int negs = 0, clamps = 0;  // per-thread tallies, reduced per warp below
 #pragma unroll 1
-        for (int k = 0; k < CPT; ++k) {
+        for (int k = 0; k < PPT; ++k) {
             const int idx = threadIdx.x + k * NT;
-            if (idx >= E2) break;
-            const int x = idx % E, y = idx / E;
+            if (idx >= E * (YB + 2)) break;
+            const int x = idx % E, y = y0 - 1 + idx / E;
+            const bool owned = zowned && y >= y0 && y < y0 + YB;
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 double v = 0.0;
-                if (!inside) {
+                if (!inside || y < 0 || y >= E) {
                     v = psi_ghost<E>(rt_psi, c, hs, s_solid, x, y, pz);
                 } else if (!(hs && solid_at<E>(s_solid, x, y, pz))) {
                     double f[Q], u0, u1, u2;
@@ -424,23 +430,20 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
                         }
                     }
                 }
-                psi[(r * C + c) * GG + (x + 1) + G * (y + 1)] = v;
+                psi[(r * C + c) * GG + (x + 1) + G * (y - y0 + 1)] = v;
             }
         }
-        // ghost ring of this plane: 4E+4 positions
-        for (int k = threadIdx.x; k < 4 * E + 4; k += NT) {
-            int x, y;
-            if (k < G) { x = k - 1; y = -1; }
-            else if (k < 2 * G) { x = k - G - 1; y = E; }
-            else if (k < 2 * G + E) { x = -1; y = k - 2 * G; }
-            else { x = E; y = k - 2 * G - E; }
-            const bool corner3 = !inside && (x < 0 || x >= E) && (y < 0 || y >= E);
+        // x ghost columns of rows y0-1 .. y0+YB: 2 (YB+2) positions
+        for (int k = threadIdx.x; k < 2 * (YB + 2); k += NT) {
+            const int x = k < YB + 2 ? -1 : E;
+            const int y = y0 - 1 + (k < YB + 2 ? k : k - (YB + 2));
+            const bool corner3 = !inside && (y < 0 || y >= E);
 #pragma unroll
             for (int c = 0; c < C; ++c)
-                psi[(r * C + c) * GG + (x + 1) + G * (y + 1)] =
+                psi[(r * C + c) * GG + (x + 1) + G * (y - y0 + 1)] =
                     corner3 ? 0.0 : psi_ghost<E>(rt_psi, c, hs, s_solid, x, y, pz);
         }
-        if (owned) {
+        if (zowned) {
             const unsigned m1 = __reduce_add_sync(0xffffffffu, (unsigned)negs);
             const unsigned m2 = __reduce_add_sync(0xffffffffu, (unsigned)clamps);
             if ((threadIdx.x & 31) == 0) {
@@ -457,12 +460,12 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
 #pragma unroll 1
         for (int k = 0; k < CPT; ++k) {
             const int idx = threadIdx.x + k * NT;
-            if (idx >= E2) break;
-            const int x = idx % E, y = idx / E;
+            if (idx >= E * YB) break;
+            const int x = idx % E, y = y0 + idx / E;
             if (hs && solid_at<E>(s_solid, x, y, z)) continue;
             const int cell = (z * E + y) * E + x;
             const int rc = (z + 3) % 3, rm = (z + 2) % 3, rp = (z + 4) % 3;
-            const int pc = (x + 1) + G * (y + 1);
+            const int pc = (x + 1) + G * (y - y0 + 1);
 #pragma unroll 1
             for (int c = 0; c < C; ++c) {
                 double f[Q];

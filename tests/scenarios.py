@@ -122,3 +122,35 @@ ALL.update({
     "mpmc3_e32": (mpmc3_e32, 6),
     "mpmc_e16_solid_S0": (mpmc_e16_solid, 10),
 })
+
+
+def mpmc_e64():
+    """C5's largest tile size (E = 64, plain kernel with 16-row y-chunks):
+    progressive at S = 0, liquid sphere next to the tile boundary."""
+    sc = S.mpmc_release(extent=64, threshold=0.0, r_core=3, devices=2, domain=(128, 64, 64))
+    sc.seeds = S.ramped_sphere_seeds((54.0, 32.0, 32.0), 3, 6.5, sc.components[0].rho_ambient, 6)
+    return sc
+
+
+def mpmc3_e64_solid():
+    sc = S.mpmc_release(extent=64, mode=S.MODE_STATIC, r_core=6, n_components=3, domain=(64, 64, 128))
+    sc.seeds = S.ramped_sphere_seeds((32.0, 32.0, 60.0), 6, 6.5, sc.components[0].rho_ambient, 6)
+    sc.periodic = (0, 1, 0)
+    g = np.zeros((128, 64, 64), np.uint8)  # [z, y, x]
+    g[60:70, 10:50, 20:24] = 1
+    sc.geometry = g
+    return sc
+
+
+def mp1_e64():
+    """single-component PR multiphase at E = 64 (smallest psi ring)."""
+    sc = S.mpmc_release(extent=64, mode=S.MODE_STATIC, r_core=6, n_components=1, domain=(64, 128, 64))
+    sc.seeds = S.ramped_sphere_seeds((32.0, 60.0, 32.0), 6, 6.5, sc.components[0].rho_ambient, 6)
+    return sc
+
+
+ALL.update({
+    "mp1_e64": (mp1_e64, 4),
+    "mpmc_e64": (mpmc_e64, 8),
+    "mpmc3_e64_solid": (mpmc3_e64_solid, 4),
+})

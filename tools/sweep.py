@@ -53,7 +53,7 @@ def timed(eng, steps, chunk=1):
 
 
 def c5(a):
-    for E in (16, 32):
+    for E in (16, 32, 64):
         for C in (1, 2, 3):
             sc = S.mpmc_release(n=a.n, extent=E, mode=S.MODE_STATIC, n_components=C)
             eng = capi.gpu_engine(sc)
