@@ -105,7 +105,6 @@ struct Kernels {
     MainFn main_tm_opt[16]; // variant 2 + OPT: the same kernel with OPT bits (A/B)
     MainFn main_pc;     // variant 21: one CTA per (block, component), cp.async staged
     MainFn main_pc2;    // variant 22: as 21 with psi computed two planes ahead
-    MainFn main_pc128;  // variant 23: 4-warp CTAs (measured slower, 3.64 ms; not instantiated)
     void (*face)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
     void (*face_v[2])(Dev, const int*, int, int, long, unsigned, cudaStream_t);
     void (*readback)(Dev, int, int, int, double*, cudaStream_t);
@@ -173,7 +172,7 @@ Kernels make_kernels() {
         k_main<E, C, BZ, NT, NOPSI, YB><<<ntiles * (E / BZ) * (E / YB), NT, SMEM_PLAIN, s>>>(d, act, src, wu, it);
     };
     k.main_tm = nullptr;
-    k.main_pc = k.main_pc2 = k.main_pc128 = nullptr;
+    k.main_pc = k.main_pc2 = nullptr;
     for (auto& f : k.main_tm_opt) f = nullptr;  // OPT values not instantiated fall back
     if constexpr (!NOPSI && (E == 16 || E == 32) && C <= 2) {
         constexpr int S = TmCfg<E, C>::SMEM;
@@ -1334,16 +1333,15 @@ void Engine::launch_main(long iter) {
     const int wu = mode_ == PLBM_MODE_PROGRESSIVE ? 1 : 0;
     MainFn fn = K_.main_plain;
     // single rank: the pc kernels run the face pass themselves (no k_face)
-    const auto fusable = [&](MainFn f) { return world_ == 1 && f && (f == K_.main_pc || f == K_.main_pc2 || f == K_.main_pc128) && !dev_expand_; };
+    const auto fusable = [&](MainFn f) { return world_ == 1 && f && (f == K_.main_pc || f == K_.main_pc2) && !dev_expand_; };
     if (variant_ == 0) fn = K_.main_pc ? K_.main_pc : (K_.main_tm ? K_.main_tm : K_.main_plain);
     if (K_.main_tm && variant_ >= 2 && variant_ < 18 && K_.main_tm_opt[variant_ - 2])
         fn = K_.main_tm_opt[variant_ - 2];
     if (K_.main_pc && variant_ == 21) fn = K_.main_pc;
     if (K_.main_pc2 && variant_ == 22) fn = K_.main_pc2;
-    if (K_.main_pc128 && variant_ == 23) fn = K_.main_pc128;
     face_fused_ = fusable(fn) && fuse_;
     // the pc kernels write the xcol side buffers the face pass reads
-    d_.xcol_ok = (fn == K_.main_pc || fn == K_.main_pc2 || fn == K_.main_pc128) && !no_xcol_;
+    d_.xcol_ok = (fn == K_.main_pc || fn == K_.main_pc2) && !no_xcol_;
     d_.face_flags = face_fused_ ? (FACE_FUSED | FACE_NAN | (mode_ == PLBM_MODE_PROGRESSIVE ? FACE_CRITERION : 0))
                                 : 0;
     const int ntiles = dev_expand_ && d_.nactive ? launch_tiles_ : int(active_.size());
