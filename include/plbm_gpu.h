@@ -89,7 +89,9 @@ void plbm_gpu_reset_kernel_stats(void* h);
  *   10 = k_main_tm memory-only probe: same loads/stash/stores, no physics
  *        (measurement only; NOT a valid step)
  *   21 = k_main_pc: one CTA per (y-block, component) in a cluster, pulls
- *        staged by cp.async one plane ahead, TMEM two-plane stash
+ *        staged by cp.async one plane ahead, TMEM two-plane stash; the
+ *        collision head (TMEM load, u) after the cluster wait (the default
+ *        runs it before the wait)
  *   22 = k_main_pc with psi computed two planes ahead (three TMEM slots)
  * Modifiers (added to the variant): +100 = run the face pass in the k_main_pc
  * tail ("last arriver" dependency counting, single rank) instead of a k_face

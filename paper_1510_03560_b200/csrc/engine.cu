@@ -104,6 +104,7 @@ struct Kernels {
     MainFn main_tm;     // variant 0: TMEM/smem stash, 4-CTA cluster (default OPT)
     MainFn main_tm_opt[16]; // variant 2 + OPT: the same kernel with OPT bits (A/B)
     MainFn main_pc;     // variant 21: one CTA per (block, component), cp.async staged
+    MainFn main_pc_late;  // variant 21: the collision head after the cluster wait
     MainFn main_pc2;    // variant 22: as 21 with psi computed two planes ahead
     void (*face)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
     void (*face_v[2])(Dev, const int*, int, int, long, unsigned, cudaStream_t);
@@ -130,7 +131,7 @@ void launch_tm(Dev d, const int* act, int src, int wu, long it, unsigned ntiles,
     cudaLaunchKernelEx(&cfg, k_main_tm<E, C, OPT>, d, act, src, wu, it);
 }
 
-template <int E, int C, int LAG, int NT = 256>
+template <int E, int C, int LAG, int NT = 256, bool EARLY = true>
 void launch_pc(Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
     using T = PcCfg<E, C, LAG, NT>;
     cudaLaunchConfig_t cfg = {};
@@ -145,7 +146,7 @@ void launch_pc(Dev d, const int* act, int src, int wu, long it, unsigned ntiles,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_main_pc<E, C, LAG, NT>, d, act, src, wu, it);
+    cudaLaunchKernelEx(&cfg, k_main_pc<E, C, LAG, NT, EARLY>, d, act, src, wu, it);
 }
 
 template <int E, int C, int OPT>
@@ -172,7 +173,7 @@ Kernels make_kernels() {
         k_main<E, C, BZ, NT, NOPSI, YB><<<ntiles * (E / BZ) * (E / YB), NT, SMEM_PLAIN, s>>>(d, act, src, wu, it);
     };
     k.main_tm = nullptr;
-    k.main_pc = k.main_pc2 = nullptr;
+    k.main_pc = k.main_pc2 = k.main_pc_late = nullptr;
     for (auto& f : k.main_tm_opt) f = nullptr;  // OPT values not instantiated fall back
     if constexpr (!NOPSI && (E == 16 || E == 32) && C <= 2) {
         constexpr int S = TmCfg<E, C>::SMEM;
@@ -187,6 +188,8 @@ Kernels make_kernels() {
         };
         setup(k_main_pc<E, C, 1>, PcCfg<E, C, 1>::SMEM, PcCfg<E, C, 1>::CL);
         k.main_pc = launch_pc<E, C, 1>;
+        setup(k_main_pc<E, C, 1, 256, false>, PcCfg<E, C, 1>::SMEM, PcCfg<E, C, 1>::CL);
+        k.main_pc_late = launch_pc<E, C, 1, 256, false>;
         if constexpr (C <= 2) {
             setup(k_main_pc<E, C, 2>, PcCfg<E, C, 2>::SMEM, PcCfg<E, C, 2>::CL);
             k.main_pc2 = launch_pc<E, C, 2>;
@@ -1333,15 +1336,15 @@ void Engine::launch_main(long iter) {
     const int wu = mode_ == PLBM_MODE_PROGRESSIVE ? 1 : 0;
     MainFn fn = K_.main_plain;
     // single rank: the pc kernels run the face pass themselves (no k_face)
-    const auto fusable = [&](MainFn f) { return world_ == 1 && f && (f == K_.main_pc || f == K_.main_pc2) && !dev_expand_; };
+    const auto fusable = [&](MainFn f) { return world_ == 1 && f && (f == K_.main_pc || f == K_.main_pc2 || f == K_.main_pc_late) && !dev_expand_; };
     if (variant_ == 0) fn = K_.main_pc ? K_.main_pc : (K_.main_tm ? K_.main_tm : K_.main_plain);
     if (K_.main_tm && variant_ >= 2 && variant_ < 18 && K_.main_tm_opt[variant_ - 2])
         fn = K_.main_tm_opt[variant_ - 2];
-    if (K_.main_pc && variant_ == 21) fn = K_.main_pc;
+    if (K_.main_pc_late && variant_ == 21) fn = K_.main_pc_late;
     if (K_.main_pc2 && variant_ == 22) fn = K_.main_pc2;
     face_fused_ = fusable(fn) && fuse_;
     // the pc kernels write the xcol side buffers the face pass reads
-    d_.xcol_ok = (fn == K_.main_pc || fn == K_.main_pc2) && !no_xcol_;
+    d_.xcol_ok = (fn == K_.main_pc || fn == K_.main_pc2 || fn == K_.main_pc_late) && !no_xcol_;
     d_.face_flags = face_fused_ ? (FACE_FUSED | FACE_NAN | (mode_ == PLBM_MODE_PROGRESSIVE ? FACE_CRITERION : 0))
                                 : 0;
     const int ntiles = dev_expand_ && d_.nactive ? launch_tiles_ : int(active_.size());

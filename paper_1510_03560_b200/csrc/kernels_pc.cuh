@@ -97,7 +97,10 @@ struct PcCfg {
 // LAG = planes between a plane's psi pass and its collision: 1 (psi of z+1
 // is computed and pushed in the iteration that collides z) or 2 (pushed one
 // iteration before it is needed, three TMEM plane slots).
-template <int E, int C, int LAG, int NT_ = 256>
+// EARLY: the thread-local head of the collision of plane z (TMEM load of f
+// and rho, u = m / rho) runs before the wait for the peers' psi of plane z+1,
+// overlapping the divisions with the cluster synchronisation.
+template <int E, int C, int LAG, int NT_ = 256, bool EARLY = true>
 __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __restrict__ active,
                                                             int src_buf, int write_uface, long iter) {
     if (halted(d)) return;
@@ -334,15 +337,23 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
     };
 
     // ---- collide plane z (this CTA's component) ------------------------------
-    auto collide_plane = [&](int z) {
+    // head: f and rho from TMEM, u (thread-local; no psi needed)
+    auto collide_head = [&](int z, double (&f)[Q], double& rho, double& u0, double& u1, double& u2) {
+        const bool sol = hs && solid_at<E>(s_solid, x, y, z);
+        tm_load20(tbase + uint32_t((z % T::TSLOTS) * T::CB), f, rho);  // warp-convergent
+        u0 = u1 = u2 = 0.0;
+        if (!sol) {
+            if (mode == MODE_PULL) velocity(f, rho, u0, u1, u2);
+            else gen_u<E>(mode, c, s_tc, x, y, z, u0, u1, u2);
+        }
+    };
+    auto collide_plane = [&](int z, double (&f)[Q], double rho, double u0, double u1, double u2) {
         const bool sol = hs && solid_at<E>(s_solid, x, y, z);
         const int cell = (z * E + y) * E + x;
         const double* pm = psi + pidx(z - 1, 0, x, yl);
         const double* p0 = psi + pidx(z, 0, x, yl);
         const double* ppl = psi + pidx(z + 1, 0, x, yl);
         constexpr int CP = PP;
-        double f[Q], rho;
-        tm_load20(tbase + uint32_t((z % T::TSLOTS) * T::CB), f, rho);  // warp-convergent
         int zero_rho = 0;
         if (!sol) {
             // forces (engine.cpp:420-449): intra of c, inter from the other
@@ -352,9 +363,6 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
             const CompConst& kc = P.comp[c];
             const double c1 = kc.c1f * p0[c * CP];
             double F0 = 0.0, F1 = 0.0, F2 = 0.0;
-            double u0 = 0.0, u1 = 0.0, u2 = 0.0;
-            if (mode == MODE_PULL) velocity(f, rho, u0, u1, u2);
-            else gen_u<E>(mode, c, s_tc, x, y, z, u0, u1, u2);
             if (kc.has_gravity) {
                 F0 = rho * kc.gravity[0];
                 F1 = rho * kc.gravity[1];
@@ -433,6 +441,8 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
         } else if (pn == E) {
             fill_zghost(E);
         }
+        double f[Q], rho, u0, u1, u2;
+        if constexpr (EARLY) collide_head(z, f, rho, u0, u1, u2);
         // The peers' psi of plane z+1: one warp polls the mbarrier, the CTA
         // barrier then releases the others (they wait in bar.sync instead of
         // spinning) and carries the acquired data to them.
@@ -441,7 +451,8 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
         flush_xcol(z - 1);
         issue_ring(pn + 1);  // its ring slot is no longer read by anyone
         cp_async_commit();
-        collide_plane(z);
+        if constexpr (!EARLY) collide_head(z, f, rho, u0, u1, u2);
+        collide_plane(z, f, rho, u0, u1, u2);
     }
     cp_async_wait<0>();
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");

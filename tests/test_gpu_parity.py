@@ -11,7 +11,7 @@ from tests.compare import assert_same_state
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 22, 100, 200], ids=["default_percomp", "plain", "tmem_both_comps", "percomp_lag2", "percomp_fused_face", "percomp_strided_xfaces"])
+@pytest.mark.parametrize("variant", [0, 1, 2, 21, 22, 100, 200], ids=["default_percomp", "plain", "tmem_both_comps", "percomp_late_head", "percomp_lag2", "percomp_fused_face", "percomp_strided_xfaces"])
 @pytest.mark.parametrize("name", sorted(scenarios.ALL))
 def test_gpu_matches_oracle(built, name, variant):
     make, steps = scenarios.ALL[name]
