@@ -154,3 +154,19 @@ ALL.update({
     "mpmc_e64": (mpmc_e64, 8),
     "mpmc3_e64_solid": (mpmc3_e64_solid, 4),
 })
+
+
+def mpmc_islands():
+    """Optimized placement on a non-uniform topology: 4 devices in two NVLink
+    islands (p2p inside, staged across), S = 0 growth from an off-centre
+    sphere — exercises classify / gamma_cost with all three link classes."""
+    sc = S.mpmc_release(n=64, extent=16, threshold=0.0, r_core=4, devices=4)
+    sc.seeds = S.ramped_sphere_seeds((20.0, 30.0, 34.0), 4, 6.5, sc.components[0].rho_ambient, 4)
+    sc.p2p = np.array([[1, 1, 0, 0], [1, 1, 0, 0], [0, 0, 1, 1], [0, 0, 1, 1]], np.uint8)
+    sc.weight_p2p, sc.weight_staged = 0.4, 1.3
+    return sc
+
+
+ALL.update({
+    "mpmc_islands": (mpmc_islands, 12),
+})

@@ -15,6 +15,16 @@
         BASELINE configs[2], the paper's comparison: the same MPMC release run
         on the progressive mesh and on the static full-domain mesh for the
         same number of steps; wall time on the device, tiles over time.
+    python tools/sweep.py placement [--steps 400]
+        The paper's GPU-assignment study (simple vs optimized assign_device,
+        PAPER.md Figures 13/16) on C4's channel network with 8 simulated
+        devices in two NVLink islands of 4 (staged links between islands):
+        placement runs inside the device-side expansion on one B200; reported
+        per policy: tiles per device, the reference's modeled byte classes
+        (record_exchange), and the cross-device face exchanges of the final
+        mesh (what an 8-GPU run would move per step: 11 E^2 C doubles per
+        face read by the kernels, 5 crossing populations + psi + the 5 of the
+        face pass).
 """
 import argparse
 import json
@@ -137,9 +147,45 @@ def c1(a):
                       "speedup": round(ref_s * 1e3 / ms, 1), "same_log_and_counters": same}), flush=True)
 
 
+def placement(a):
+    import numpy as np
+    n_dev = 8
+    island = np.array([[1 if i // 4 == j // 4 else 0 for j in range(n_dev)] for i in range(n_dev)], np.uint8)
+    for policy, name in ((S.POLICY_SIMPLE, "simple"), (S.POLICY_OPTIMIZED, "optimized")):
+        sc = S.mpmc_channel(nx=a.n * 2, ny=a.n, nz=a.n, extent=32, threshold=1e-9, devices=n_dev)
+        sc.p2p = island
+        sc.policy = policy
+        eng = capi.gpu_engine(sc)
+        ms, cells, _ = timed(eng, a.steps, chunk=a.steps)
+        c = eng.counters()
+        tiles = eng.tiles()
+        owner = {tuple(t[0]): t[1] for t in tiles}
+        faces = {"intra": 0, "p2p": 0, "staged": 0}
+        for xyz, o in owner.items():
+            for ax in range(3):
+                for sgn in (-1, 1):
+                    nb = list(xyz)
+                    nb[ax] += sgn
+                    q = owner.get(tuple(nb))
+                    if q is None:
+                        continue
+                    faces["intra" if q == o else ("p2p" if island[o][q] else "staged")] += 1
+        E, C = sc.tile_extent, sc.n_components
+        per_face = 11 * E * E * C * 8
+        print(json.dumps({
+            "sweep": "placement", "policy": name, "domain": list(sc.domain), "devices": n_dev,
+            "topology": "2 islands x 4 (p2p inside, staged across)", "steps": a.steps,
+            "tiles": c["tiles"], "tiles_per_device": [sum(1 for o in owner.values() if o == d) for d in range(n_dev)],
+            "modeled_bytes": {"intra": c["bytes"][0], "p2p": c["bytes"][1], "staged": c["bytes"][2]},
+            "final_mesh_face_links": faces,
+            "cross_device_bytes_per_step": {"p2p": faces["p2p"] * per_face, "staged": faces["staged"] * per_face},
+            "gpu_ms": round(ms, 1)}), flush=True)
+        eng.close()
+
+
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("what", choices=["c1", "c5", "c3", "c4"])
+    p.add_argument("what", choices=["c1", "c5", "c3", "c4", "placement"])
     p.add_argument("--n", type=int, default=None)
     p.add_argument("--steps", type=int, default=None)
     p.add_argument("--warmup", type=int, default=3)
@@ -156,6 +202,10 @@ def main():
         a.steps = a.steps or 400
         a.every = 50
         c4(a)
+    elif a.what == "placement":
+        a.n = a.n or 512
+        a.steps = a.steps or 400
+        placement(a)
     else:
         a.n = a.n or 512
         a.steps = a.steps or 300
