@@ -22,7 +22,7 @@ from tests import scenarios  # noqa: E402
 from tests.compare import FIELDS  # noqa: E402
 
 GOLDEN = ["c1_progressive", "c1_progressive_S0", "mpmc_progressive_e16", "mpmc_e32",
-          "periodic_solid_gravity", "mpmc_e16_solid_S0"]
+          "periodic_solid_gravity", "mpmc_e16_solid_S0", "mpmc_islands", "mpmc_e64", "mpmc3_e64_solid"]
 
 
 def state_digest(eng):
