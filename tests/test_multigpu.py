@@ -72,7 +72,8 @@ def _two_rank_run(sc, steps, world=2):
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,world", [("mpmc_e32", 2), ("mpmc_progressive_e16", 2),
                                         ("mpmc_e32_solid_periodic", 2), ("mpmc_s0_3dev", 3),
-                                        ("c1_progressive", 2)])
+                                        ("c1_progressive", 2), ("mpmc_islands", 2),
+                                        ("mpmc_e64", 2)])
 def test_ranks_in_one_process_match_single_engine(built, name, world):
     import numpy as np
     from tests.compare import FIELDS
