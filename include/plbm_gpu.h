@@ -93,6 +93,8 @@ void plbm_gpu_reset_kernel_stats(void* h);
  *        collision head (TMEM load, u) after the cluster wait (the default
  *        runs it before the wait)
  *   22 = k_main_pc with psi computed two planes ahead (three TMEM slots)
+ *   24 = PROBE ONLY (E = 32, C = 2; results are wrong): k_main_pc's memory
+ *        pipeline with the physics removed, for the roofline study
  * Modifiers (added to the variant): +100 = run the face pass in the k_main_pc
  * tail ("last arriver" dependency counting, single rank) instead of a k_face
  * launch; +200 = face pass reads the x faces from the SoA block instead of the

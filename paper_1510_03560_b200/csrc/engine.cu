@@ -105,6 +105,7 @@ struct Kernels {
     MainFn main_tm_opt[16]; // variant 2 + OPT: the same kernel with OPT bits (A/B)
     MainFn main_pc;     // variant 21: one CTA per (block, component), cp.async staged
     MainFn main_pc_late;  // variant 21: the collision head after the cluster wait
+    MainFn main_pc_mem;   // variant 24: memory-only probe (E = 32, C = 2)
     MainFn main_pc2;    // variant 22: as 21 with psi computed two planes ahead
     void (*face)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
     void (*face_v[2])(Dev, const int*, int, int, long, unsigned, cudaStream_t);
@@ -131,7 +132,7 @@ void launch_tm(Dev d, const int* act, int src, int wu, long it, unsigned ntiles,
     cudaLaunchKernelEx(&cfg, k_main_tm<E, C, OPT>, d, act, src, wu, it);
 }
 
-template <int E, int C, int LAG, int NT = 256, bool EARLY = true>
+template <int E, int C, int LAG, int NT = 256, bool EARLY = true, bool MEMONLY = false>
 void launch_pc(Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
     using T = PcCfg<E, C, LAG, NT>;
     cudaLaunchConfig_t cfg = {};
@@ -146,7 +147,7 @@ void launch_pc(Dev d, const int* act, int src, int wu, long it, unsigned ntiles,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_main_pc<E, C, LAG, NT, EARLY>, d, act, src, wu, it);
+    cudaLaunchKernelEx(&cfg, k_main_pc<E, C, LAG, NT, EARLY, MEMONLY>, d, act, src, wu, it);
 }
 
 template <int E, int C, int OPT>
@@ -173,7 +174,7 @@ Kernels make_kernels() {
         k_main<E, C, BZ, NT, NOPSI, YB><<<ntiles * (E / BZ) * (E / YB), NT, SMEM_PLAIN, s>>>(d, act, src, wu, it);
     };
     k.main_tm = nullptr;
-    k.main_pc = k.main_pc2 = k.main_pc_late = nullptr;
+    k.main_pc = k.main_pc2 = k.main_pc_late = k.main_pc_mem = nullptr;
     for (auto& f : k.main_tm_opt) f = nullptr;  // OPT values not instantiated fall back
     if constexpr (!NOPSI && (E == 16 || E == 32) && C <= 2) {
         constexpr int S = TmCfg<E, C>::SMEM;
@@ -190,6 +191,10 @@ Kernels make_kernels() {
         k.main_pc = launch_pc<E, C, 1>;
         setup(k_main_pc<E, C, 1, 256, false>, PcCfg<E, C, 1>::SMEM, PcCfg<E, C, 1>::CL);
         k.main_pc_late = launch_pc<E, C, 1, 256, false>;
+        if constexpr (E == 32 && C == 2) {
+            setup(k_main_pc<E, C, 1, 256, true, true>, PcCfg<E, C, 1>::SMEM, PcCfg<E, C, 1>::CL);
+            k.main_pc_mem = launch_pc<E, C, 1, 256, true, true>;
+        }
         if constexpr (C <= 2) {
             setup(k_main_pc<E, C, 2>, PcCfg<E, C, 2>::SMEM, PcCfg<E, C, 2>::CL);
             k.main_pc2 = launch_pc<E, C, 2>;
@@ -1341,10 +1346,11 @@ void Engine::launch_main(long iter) {
     if (K_.main_tm && variant_ >= 2 && variant_ < 18 && K_.main_tm_opt[variant_ - 2])
         fn = K_.main_tm_opt[variant_ - 2];
     if (K_.main_pc_late && variant_ == 21) fn = K_.main_pc_late;
+    if (K_.main_pc_mem && variant_ == 24) fn = K_.main_pc_mem;  // probe: not a correct step
     if (K_.main_pc2 && variant_ == 22) fn = K_.main_pc2;
     face_fused_ = fusable(fn) && fuse_;
     // the pc kernels write the xcol side buffers the face pass reads
-    d_.xcol_ok = (fn == K_.main_pc || fn == K_.main_pc2 || fn == K_.main_pc_late) && !no_xcol_;
+    d_.xcol_ok = (fn == K_.main_pc || fn == K_.main_pc2 || fn == K_.main_pc_late || fn == K_.main_pc_mem) && !no_xcol_;
     d_.face_flags = face_fused_ ? (FACE_FUSED | FACE_NAN | (mode_ == PLBM_MODE_PROGRESSIVE ? FACE_CRITERION : 0))
                                 : 0;
     const int ntiles = dev_expand_ && d_.nactive ? launch_tiles_ : int(active_.size());

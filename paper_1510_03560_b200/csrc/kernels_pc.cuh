@@ -100,7 +100,10 @@ struct PcCfg {
 // EARLY: the thread-local head of the collision of plane z (TMEM load of f
 // and rho, u = m / rho) runs before the wait for the peers' psi of plane z+1,
 // overlapping the divisions with the cluster synchronisation.
-template <int E, int C, int LAG, int NT_ = 256, bool EARLY = true>
+// MEMONLY (probe, variant 24, NOT a correct step): the same pulls, psi
+// pushes, TMEM stash, stores and xcol staging with the physics removed (psi
+// = 0, f stored unchanged) — the memory pipeline's own ceiling.
+template <int E, int C, int LAG, int NT_ = 256, bool EARLY = true, bool MEMONLY = false>
 __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __restrict__ active,
                                                             int src_buf, int write_uface, long iter) {
     if (halted(d)) return;
@@ -311,7 +314,8 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
                 rho += f[i];
                 negs += f[i] < 0.0;
             }
-            if (!isfinite(rho)) {
+            if (MEMONLY) {
+            } else if (!isfinite(rho)) {
                 atomic_err(d.err, iter, tile_lin, ERR_P1_NAN);
             } else {
                 double press;
@@ -342,7 +346,7 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
         const bool sol = hs && solid_at<E>(s_solid, x, y, z);
         tm_load20(tbase + uint32_t((z % T::TSLOTS) * T::CB), f, rho);  // warp-convergent
         u0 = u1 = u2 = 0.0;
-        if (!sol) {
+        if (!sol && !MEMONLY) {
             if (mode == MODE_PULL) velocity(f, rho, u0, u1, u2);
             else gen_u<E>(mode, c, s_tc, x, y, z, u0, u1, u2);
         }
@@ -355,7 +359,14 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
         const double* ppl = psi + pidx(z + 1, 0, x, yl);
         constexpr int CP = PP;
         int zero_rho = 0;
-        if (!sol) {
+        if (MEMONLY) {
+            double* xc = (xcls >= 0 && wx) ? xst + ((z & 1) * 4 + xcls) * Q * BY + yl : nullptr;
+#pragma unroll
+            for (int i = 0; i < Q; ++i) {
+                fo[cell + size_t(i) * E3] = f[i];
+                if (xc) xc[i * BY] = f[i];
+            }
+        } else if (!sol) {
             // forces (engine.cpp:420-449): intra of c, inter from the other
             // component's s1 (the same sum as its intra s1)
             double s1[3], s2[3];
