@@ -293,6 +293,35 @@ __device__ __forceinline__ void pull_addr_fast(const RouteTab& rt, int c, int x,
     }
 }
 
+// The same for a y-edge row (y == 0 or y == E-1; warp-uniform) of a tile with
+// no solid cell, z interior: directions whose y shift leaves the tile read the
+// -y / +y neighbour (rt.p 10 / 16, and the xy-diagonal tiles 9, 11 / 15, 17 on
+// the x-edge lanes) at row E-1 / 0 — the addresses pull_addr computes, from
+// three more base pointers instead of a per-direction route lookup.
+template <int E, class Op>
+__device__ __forceinline__ void pull_addr_fast_yedge(const RouteTab& rt, int c, int x, int y, int z,
+                                                     Op&& op) {
+    constexpr int E2 = E * E;
+    constexpr int E3 = E * E * E;
+    const size_t cs = size_t(Q) * E3;
+    const int row = (z * E + y) * E;
+    const double* own = rt.p[13] + c * cs + row + x;
+    const double* bp = x == 0 ? rt.p[12] + c * cs + row + (E - 1) : own - 1;
+    const double* bm = x == E - 1 ? rt.p[14] + c * cs + row : own + 1;
+    const int oy = y == 0 ? -1 : 1;      // the neighbour row the crossing directions read
+    const int wrap = y == 0 ? E2 : -E2;  // row -1 -> E-1, row E -> 0
+    const double* ownY = rt.p[13 + 3 * oy] + c * cs + row + x + wrap;
+    const double* bpY = x == 0 ? rt.p[12 + 3 * oy] + c * cs + row + (E - 1) + wrap : ownY - 1;
+    const double* bmY = x == E - 1 ? rt.p[14 + 3 * oy] + c * cs + row + wrap : ownY + 1;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+        const int off = i * E3 - ey_(i) * E - ez_(i) * E2;
+        const bool cy = (ey_(i) > 0 && y == 0) || (ey_(i) < 0 && y == E - 1);
+        const double* b = ex_(i) > 0 ? (cy ? bpY : bp) : (ex_(i) < 0 ? (cy ? bmY : bm) : (cy ? ownY : own));
+        op(i, b + off);
+    }
+}
+
 template <int E>
 __device__ __forceinline__ void pull_cell(const RouteTab& rt, int c, bool hs, const uint32_t* sb,
                                           int x, int y, int z, double* f) {

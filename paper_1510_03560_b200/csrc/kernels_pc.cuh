@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
         }
     };
     const bool fast_rows = mode == MODE_PULL && !hs && y >= 1 && y <= E - 2;
+    const bool fast_yedge = mode == MODE_PULL && !hs && !fast_rows;  // y == 0 or E-1
     auto pidx = [&](int pz, int cc, int xx, int yy_local) {
         return (((pz & (R - 1)) * C + cc) * PH + (yy_local + 1)) * PW + (xx + 1);
     };
@@ -288,6 +289,7 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
         if (pz >= E || mode != MODE_PULL || (hs && solid_at<E>(s_solid, x, y, pz))) return;
         auto op = [&](int i, const double* p) { cp_async8(land_u32 + uint32_t(i * NT + tid) * 8u, p); };
         if (fast_rows && pz >= 1 && pz <= E - 2) pull_addr_fast<E>(rt_pull, c, x, y, pz, op);
+        else if (fast_yedge && pz >= 1 && pz <= E - 2) pull_addr_fast_yedge<E>(rt_pull, c, x, y, pz, op);
         else pull_addr<E>(rt_pull, c, hs, s_solid, x, y, pz, op);
     };
 
