@@ -181,7 +181,9 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
     auto flush_xcol = [&](int pz) {
         if (!wx || pz < 0) return;
         const double* src = xst + (pz & 1) * 4 * Q * BY;
-        for (int k = tid; k < XN * BY; k += NT) {
+        // items beyond NT land on warps 2-3 (warp 0 polls the mbarrier, warps
+        // 0 / BY-1 are the tile-edge rows of the edge blocks)
+        for (int k = (tid + NT - 64) % NT; k < XN * BY; k += NT) {
             const int s = k / BY, r = k - s * BY;
             xcol[size_t(s) * E2 + pz * E + y0 + r] = src[(xslot_cls(s) * Q + c_xdir[s]) * BY + r];
         }
@@ -263,7 +265,11 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
     };
     auto issue_ring = [&](int pz) {  // x ring + tile-edge halo rows, asynchronously
         if (pz >= E) return;
-        for (int k = tid; k < 2 * PH + 2 * E; k += NT) {
+        // run by the middle warps (never the poller, never a tile-edge row)
+        constexpr int RITEMS = 2 * PH + 2 * E;
+        constexpr int RT0 = NT > RITEMS ? ((NT - RITEMS) / 2) & ~31 : 0;
+        for (int k = tid - RT0; k < RITEMS; k += NT) {
+            if (k < 0) continue;
             int xx, yyl;
             if (k < 2 * PH) {
                 xx = (k & 1) ? E : -1;
