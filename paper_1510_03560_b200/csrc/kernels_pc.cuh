@@ -238,6 +238,9 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
                          "r"(expect_bytes)
                          : "memory");
     };
+    // the warp that polls the mbarrier: a middle row (no tile-edge pushes), no
+    // ring issue (warps RT0/32 ..), no xcol-flush remainder (warps 2-3)
+    constexpr int POLL_WARP = NT / 32 - 3;
     auto wait_pushed = [&](int pz) {
         if (T::CL == 1) return;
         const uint32_t bar = mbar_u32 + uint32_t((pz & (NMB - 1)) * 8);
@@ -465,7 +468,7 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
         // The peers' psi of plane z+1: one warp polls the mbarrier, the CTA
         // barrier then releases the others (they wait in bar.sync instead of
         // spinning) and carries the acquired data to them.
-        if (warp == 0 && z + 1 < E && z + 1 >= LAG) wait_pushed(z + 1);
+        if (warp == POLL_WARP && z + 1 < E && z + 1 >= LAG) wait_pushed(z + 1);
         __syncthreads();  // psi plane pn visible; every warp is past collide(z-1)
         flush_xcol(z - 1);
         issue_ring(pn + 1);  // its ring slot is no longer read by anyone
