@@ -719,6 +719,12 @@ __device__ __forceinline__ void face_load(const RouteTab& rt, int mode, const in
         }
         return;
     }
+    if (mode == MODE_PULL && !hs && (face == 2 || face == 3) && z >= 1 && z <= E - 2) {
+        // y faces: the tile-edge-row fast pull (no per-direction route lookup)
+        if (COH) pull_addr_fast_yedge<E>(rt, c, x, y, z, [&](int i, const double* p) { f[i] = __ldcg(p); });
+        else pull_addr_fast_yedge<E>(rt, c, x, y, z, [&](int i, const double* p) { f[i] = __ldg(p); });
+        return;
+    }
     if (mode == MODE_PULL) {
         if (COH) pull_addr<E>(rt, c, hs, sb, x, y, z, [&](int i, const double* p) { f[i] = __ldcg(p); });
         else pull_addr<E>(rt, c, hs, sb, x, y, z, [&](int i, const double* p) { f[i] = __ldg(p); });
