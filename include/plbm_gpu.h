@@ -84,21 +84,15 @@ void plbm_gpu_reset_kernel_stats(void* h);
  *        kernel
  *   1  = plain kernel that pulls every population twice (always used for
  *        E = 8, C = 3 and psi-free scenarios)
- *   2  = k_main_tm: both components per thread, TMEM + smem two-plane stash,
- *        synchronous pulls (the previous default)
- *   10 = k_main_tm memory-only probe: same loads/stash/stores, no physics
- *        (measurement only; NOT a valid step)
- *   21 = k_main_pc: one CTA per (y-block, component) in a cluster, pulls
- *        staged by cp.async one plane ahead, TMEM two-plane stash; the
- *        collision head (TMEM load, u) after the cluster wait (the default
- *        runs it before the wait)
+ *   21 = k_main_pc with the collision head (TMEM load, u) after the cluster
+ *        wait (the default runs it before the wait)
  *   22 = k_main_pc with psi computed two planes ahead (three TMEM slots)
- *   24 = PROBE ONLY (E = 32, C = 2; results are wrong): k_main_pc's memory
- *        pipeline with the physics removed, for the roofline study
  * Modifiers (added to the variant): +100 = run the face pass in the k_main_pc
  * tail ("last arriver" dependency counting, single rank) instead of a k_face
  * launch; +200 = face pass reads the x faces from the SoA block instead of the
- * xcol side buffers.                                                          */
+ * xcol side buffers.  Returns 0, or -1 for an unknown variant (the current
+ * one is kept).  The memory-only roofline probe (24, NOT a valid step) exists
+ * only in builds compiled with -DPLBM_PROBES.                                 */
 int plbm_gpu_set_kernel_variant(void* h, int variant);
 
 /* The engine's CUDA stream (cudaStream_t) for callers that time with events. */

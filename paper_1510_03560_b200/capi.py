@@ -341,8 +341,10 @@ class GpuEngine(StepEngine):
         return out.reshape(d[2], d[1], d[0])
 
     def set_kernel_variant(self, variant: int) -> None:
-        """0 = TMEM/smem-stash cluster kernel where it applies, 1 = plain kernel."""
-        self.lib.plbm_gpu_set_kernel_variant(self._h, int(variant))
+        """Fused-kernel variant (include/plbm_gpu.h): 0 = default, 1 = plain
+        kernel, 21 / 22 = k_main_pc A/B variants, +100 / +200 modifiers."""
+        if self.lib.plbm_gpu_set_kernel_variant(self._h, int(variant)) != 0:
+            raise ValueError(f"unknown kernel variant {variant}")
 
     def stream(self) -> int:
         return self.lib.plbm_gpu_stream(self._h)

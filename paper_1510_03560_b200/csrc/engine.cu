@@ -101,36 +101,17 @@ T* dmalloc(size_t n) {
 using MainFn = void (*)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
 struct Kernels {
     MainFn main_plain;  // variant 1 (and the only kernel for E = 8 / psi-free)
-    MainFn main_tm;     // variant 0: TMEM/smem stash, 4-CTA cluster (default OPT)
-    MainFn main_tm_opt[16]; // variant 2 + OPT: the same kernel with OPT bits (A/B)
-    MainFn main_pc;     // variant 21: one CTA per (block, component), cp.async staged
+    MainFn main_pc;     // variant 0: one CTA per (block, component), cp.async staged
     MainFn main_pc_late;  // variant 21: the collision head after the cluster wait
-    MainFn main_pc_mem;   // variant 24: memory-only probe (E = 32, C = 2)
-    MainFn main_pc2;    // variant 22: as 21 with psi computed two planes ahead
+    MainFn main_pc_mem;   // variant 24 (PLBM_PROBES builds only): memory-only probe (E = 32, C = 2)
+    MainFn main_pc2;    // variant 22: psi computed two planes ahead
     void (*face)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
     void (*face_v[2])(Dev, const int*, int, int, long, unsigned, cudaStream_t);
+    void (*p5)(Dev, const int*, int, long, unsigned, cudaStream_t);
     void (*readback)(Dev, int, int, int, double*, cudaStream_t);
     void (*gather)(Dev, const int*, int, int, int, int, double*, int, int, cudaStream_t);
     int nt;
 };
-
-template <int E, int C, int OPT>
-void launch_tm(Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
-    using T = TmCfg<E, C>;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ntiles * T::NB);
-    cfg.blockDim = dim3(T::NT);
-    cfg.dynamicSmemBytes = T::SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = T::NB;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_main_tm<E, C, OPT>, d, act, src, wu, it);
-}
 
 template <int E, int C, int LAG, int NT = 256, bool EARLY = true, bool MEMONLY = false>
 void launch_pc(Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
@@ -150,12 +131,6 @@ void launch_pc(Dev d, const int* act, int src, int wu, long it, unsigned ntiles,
     cudaLaunchKernelEx(&cfg, k_main_pc<E, C, LAG, NT, EARLY, MEMONLY>, d, act, src, wu, it);
 }
 
-template <int E, int C, int OPT>
-void reg_tm(MainFn* tab, int smem) {
-    cudaFuncSetAttribute(k_main_tm<E, C, OPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    tab[OPT] = launch_tm<E, C, OPT>;
-}
-
 template <int E, int C, bool NOPSI>
 Kernels make_kernels() {
     constexpr int NT = E * E < 256 ? E * E : 256;
@@ -173,15 +148,7 @@ Kernels make_kernels() {
     k.main_plain = [](Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
         k_main<E, C, BZ, NT, NOPSI, YB><<<ntiles * (E / BZ) * (E / YB), NT, SMEM_PLAIN, s>>>(d, act, src, wu, it);
     };
-    k.main_tm = nullptr;
     k.main_pc = k.main_pc2 = k.main_pc_late = k.main_pc_mem = nullptr;
-    for (auto& f : k.main_tm_opt) f = nullptr;  // OPT values not instantiated fall back
-    if constexpr (!NOPSI && (E == 16 || E == 32) && C <= 2) {
-        constexpr int S = TmCfg<E, C>::SMEM;
-        reg_tm<E, C, 0>(k.main_tm_opt, S);
-        reg_tm<E, C, TM_MEMONLY>(k.main_tm_opt, S);
-        k.main_tm = k.main_tm_opt[TM_DEFAULT_OPT];
-    }
     if constexpr (!NOPSI && (E == 16 || E == 32)) {
         auto setup = [](auto fn, int smem, int cl) {
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -191,10 +158,12 @@ Kernels make_kernels() {
         k.main_pc = launch_pc<E, C, 1>;
         setup(k_main_pc<E, C, 1, 256, false>, PcCfg<E, C, 1>::SMEM, PcCfg<E, C, 1>::CL);
         k.main_pc_late = launch_pc<E, C, 1, 256, false>;
+#ifdef PLBM_PROBES
         if constexpr (E == 32 && C == 2) {
             setup(k_main_pc<E, C, 1, 256, true, true>, PcCfg<E, C, 1>::SMEM, PcCfg<E, C, 1>::CL);
             k.main_pc_mem = launch_pc<E, C, 1, 256, true, true>;
         }
+#endif
         if constexpr (C <= 2) {
             setup(k_main_pc<E, C, 2>, PcCfg<E, C, 2>::SMEM, PcCfg<E, C, 2>::CL);
             k.main_pc2 = launch_pc<E, C, 2>;
@@ -209,6 +178,9 @@ Kernels make_kernels() {
         k_face<E, C, NT, 2, true><<<ntiles * 6, NT, 0, s>>>(d, act, src, flags, it);
     };
     k.face = k.face_v[0];
+    k.p5 = [](Dev d, const int* act, int src, long it, unsigned ntiles, cudaStream_t s) {
+        k_p5<E, C, 256><<<ntiles, 256, 0, s>>>(d, act, src, it);
+    };
     k.readback = [](Dev d, int slot, int c, int src, double* out, cudaStream_t s) {
         k_readback<E><<<(E * E * E + 255) / 256, 256, 0, s>>>(d, slot, c, src, out);
     };
@@ -296,10 +268,18 @@ class Engine {
     int set_capture(bool on);
     int poke_f(const int32_t* coords, int comp, int i, const int32_t* local, double v);
     void set_profiling(bool on) { profiling_ = on; }
-    void set_variant(int v) {
-        variant_ = v % 100;
+    int set_variant(int v) {
+        const int base = v % 100;
+        const bool ok = v >= 0 && v < 400 && (base == 0 || base == 1 || base == 21 || base == 22
+#ifdef PLBM_PROBES
+                                              || base == 24
+#endif
+                                              );
+        if (!ok) return -1;  // unknown (or probe-only) variant: keep the current one
+        variant_ = base;
         fuse_ = (v / 100) & 1;     // +100: face pass in the fused kernel's tail (A/B)
         no_xcol_ = (v / 200) & 1;  // +200: face pass reads x faces from the SoA block
+        return 0;
     }
     plbm_kernel_stats stats();
     void reset_stats() {
@@ -432,6 +412,7 @@ class Engine {
     int* d_geo_ = nullptr;       // [slot][18] active geometric neighbour or -1
     bool face_fused_ = false;    // the last k_main ran the face pass itself
     double* d_capture_ = nullptr;
+    uint8_t* d_suspect_ = nullptr;  // [slot] P5 screen marks (k_main* -> k_p5)
     unsigned long long* d_cnt_ = nullptr;
     unsigned long long* d_err_ = nullptr;
     int* d_active_ = nullptr;
@@ -468,10 +449,13 @@ class Engine {
     void upload_pointers();
     void recompute_step_bytes();
     void launch_face(int src, int flags, long iter);
+    void launch_p5(long iter);
     void launch_main(long iter);
     void expand(const std::vector<std::pair<Coord, int>>& triggers, long iteration,
                 std::vector<int>& created);
     void check_error(plbm_error* err, bool& failed);
+    long err_it_ = 0;     // iteration of the last error check_error decoded
+    bool err_p5_ = false; // ... and whether it was a P5 error (that step's exchange bytes count)
     EvPair& next_event(int kind, uint64_t cells);
     void resolve_events();
     bool peers_ready() const {
@@ -622,6 +606,9 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     d_halt_ = dmalloc<int>(1);
     CK(cudaMemsetAsync(d_halt_, 0, sizeof(int), stream_));
     CK(cudaMallocHost(&h_flags_, 8 * sizeof(int)));
+    // (environment overrides first: device expansion depends on the queue depth)
+    if (const char* sd = std::getenv("PLBM_SPEC_DEPTH")) spec_depth_ = std::max(1, std::min(8, std::atoi(sd)));
+    if (const char* fv = std::getenv("PLBM_FACE_VARIANT")) K_.face = K_.face_v[std::atoi(fv) == 1 ? 1 : 0];
     {
         const char* de = std::getenv("PLBM_DEVICE_EXPAND");
         dev_expand_ = world_ == 1 && mode_ == PLBM_MODE_PROGRESSIVE && spec_depth_ > 1 && !(de && de[0] == '0');
@@ -652,8 +639,6 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
         CK(cudaMemcpyAsync(d_geomdev_, geom_.data(), geom_.size(), cudaMemcpyHostToDevice, stream_));
     }
     for (auto& e : flag_ev_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    if (const char* sd = std::getenv("PLBM_SPEC_DEPTH")) spec_depth_ = std::max(1, std::min(8, std::atoi(sd)));
-    if (const char* fv = std::getenv("PLBM_FACE_VARIANT")) K_.face = K_.face_v[std::atoi(fv) == 1 ? 1 : 0];
     d_pokes_ = dmalloc<Poke>(64);
     d_dep_cnt_ = dmalloc<int>(nslot);
     d_dep_need_ = dmalloc<int>(nslot);
@@ -661,6 +646,8 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     CK(cudaMemsetAsync(d_dep_cnt_, 0, nslot * sizeof(int), stream_));
     d_cnt_ = dmalloc<unsigned long long>(CNT_N);
     d_err_ = dmalloc<unsigned long long>(1);
+    d_suspect_ = dmalloc<uint8_t>(nslot);
+    CK(cudaMemsetAsync(d_suspect_, 0, nslot, stream_));
     d_active_ = dmalloc<int>(nslot);
     d_scratch_slots_ = dmalloc<int>(nslot);
     d_readback_ = dmalloc<double>(size_t(23) * E3_);
@@ -724,6 +711,13 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     d_.nactive = nullptr;
     d_.probe = nullptr;
     d_.tile_base = 0;
+    d_.suspect = d_suspect_;
+    // the P5 screen's argument needs every pulled ambient population in range
+    d_.screen_all = 0;
+    for (int c = 0; c < C_; ++c)
+        for (int i = 0; i < Q; ++i)
+            if (!screen_ok(p.comp[c].feq_amb[i])) d_.screen_all = 1;
+    if (std::getenv("PLBM_P5_ALL")) d_.screen_all = 1;  // test hook: exact check of every tile
     if (std::getenv("PLBM_PROBE")) d_.probe = dmalloc<unsigned long long>(3 * size_t(cap_ + 1) * 16);
 
     // ---- host mirror + initial tiles (make_state, engine.cpp:134-159)
@@ -823,7 +817,7 @@ void Engine::release() {
                     d_u_face_, d_trig_, d_capture_, d_cnt_, d_err_, d_active_, d_scratch_slots_,
                     d_readback_, d_dep_cnt_, d_dep_need_, d_geo_, d_bmask_, d_omask_, d_halt_, d_pokes_,
                     d_gslot_, d_cand_, d_nactive_, d_next_slot_, d_next_local_, d_owner_, d_geomdev_, d_p2p_,
-                    d_per_dev_, d_acc_, d_births_, d_nbirths_, d_post_flags_};
+                    d_per_dev_, d_acc_, d_births_, d_nbirths_, d_post_flags_, d_suspect_};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (h_flags_) cudaFreeHost(h_flags_);
@@ -1334,6 +1328,16 @@ void Engine::launch_face(int src, int flags, long iter) {
     if (ev) CK(cudaEventRecord(ev->b, stream_));
 }
 
+// P5 of step `iter` (k_p5): exact moments check of the tiles the fused
+// kernel's screen marked, on the post-stream state in buffer cur_.
+void Engine::launch_p5(long iter) {
+    if (active_.empty()) return;
+    K_.p5(d_, d_active_, cur_, iter, unsigned(dev_expand_ && d_.nactive ? launch_tiles_ : int(active_.size())),
+          stream_);
+    CK(cudaGetLastError());
+    ++stats_.kernels_launched;
+}
+
 void Engine::launch_main(long iter) {
     if (active_.empty()) return;
     EvPair* ev = profiling_ ? &next_event(0, local_cells_) : nullptr;
@@ -1342,9 +1346,7 @@ void Engine::launch_main(long iter) {
     MainFn fn = K_.main_plain;
     // single rank: the pc kernels run the face pass themselves (no k_face)
     const auto fusable = [&](MainFn f) { return world_ == 1 && f && (f == K_.main_pc || f == K_.main_pc2 || f == K_.main_pc_late) && !dev_expand_; };
-    if (variant_ == 0) fn = K_.main_pc ? K_.main_pc : (K_.main_tm ? K_.main_tm : K_.main_plain);
-    if (K_.main_tm && variant_ >= 2 && variant_ < 18 && K_.main_tm_opt[variant_ - 2])
-        fn = K_.main_tm_opt[variant_ - 2];
+    if (variant_ == 0 && K_.main_pc) fn = K_.main_pc;
     if (K_.main_pc_late && variant_ == 21) fn = K_.main_pc_late;
     if (K_.main_pc_mem && variant_ == 24) fn = K_.main_pc_mem;  // probe: not a correct step
     if (K_.main_pc2 && variant_ == 22) fn = K_.main_pc2;
@@ -1413,7 +1415,9 @@ void Engine::check_error(plbm_error* err, bool& failed) {
     if (!failed) return;
     const int code = int(h_err & 0xf);
     const long tl = long((h_err >> 4) & 0xffffffffull);
-    const long it = long(h_err >> 36);
+    const long it = long(h_err >> 37);
+    err_it_ = it;
+    err_p5_ = code == ERR_P5_NAN;
     const int tx = int(tl / (long(grid_[1]) * grid_[2]));
     const int ty = int((tl / grid_[2]) % grid_[1]);
     const int tz = int(tl % grid_[2]);
@@ -1511,6 +1515,7 @@ int Engine::step_main(plbm_error* err) {
 int Engine::step_face() {
     if (phase_ != 1) return 0;
     if (!face_fused_) launch_face(cur_, mode_ == PLBM_MODE_PROGRESSIVE ? 3 : 2, iteration_ + 1);
+    launch_p5(iteration_ + 1);
     phase_ = 2;
     return 0;
 }
@@ -1531,7 +1536,12 @@ int Engine::step_end(const uint8_t* merged, plbm_error* err) {
     const long it = iteration_ + 1;
     bool failed = false;
     check_error(err, failed);
-    if (failed) return 1;
+    if (failed) {
+        // P2 and P4 recorded this step's exchanges before P5 threw
+        if (err_p5_)
+            for (int a = 0; a < 3; ++a) bytes_[a] += step_bytes_[a];
+        return 1;
+    }
     const uint64_t updates = active_cells_;
     for (int a = 0; a < 3; ++a) bytes_[a] += step_bytes_[a];
     if (mode_ == PLBM_MODE_PROGRESSIVE) {
@@ -1588,6 +1598,7 @@ void Engine::enqueue_step(long it) {
         routes_differ_ = false;
     }
     if (!face_fused_) launch_face(cur_, 3, it);
+    launch_p5(it);
 }
 
 // Progressive single-rank stepping without a host round trip per step: up to
@@ -1649,6 +1660,10 @@ int Engine::step_speculative(int n, plbm_error* err) {
         check_error(err, failed);  // synchronises the stream
         if (failed) {
             rc = 1;
+            if (err_p5_) {  // P2 and P4 recorded this step's exchanges before P5 threw
+                sync_births();
+                for (int a = 0; a < 3; ++a) bytes_[a] += step_bytes_[a];
+            }
             break;
         }
         iteration_ = e.it;
@@ -1695,26 +1710,39 @@ int Engine::step(int n, plbm_error* err) {
         return 0;
     }
     // Static meshes never change: the whole batch is queued without a host
-    // round trip and the error flag (earliest iteration wins) is read once.
+    // round trip and the error flag (earliest iteration wins) is read once; a
+    // recorded error halts the steps queued behind it (k_err_halt).
     const long it0 = iteration_;
+    std::vector<int> cur_after;
+    cur_after.reserve(size_t(n));
+    d_.halt = d_halt_;
+    int rc = 0;
     for (int k = 0; k < n; ++k) {
-        const int rc = step_begin(err);
-        if (rc) return rc;
+        rc = step_begin(err);
+        if (rc) break;
         phase_ = 0;
-        for (int a = 0; a < 3; ++a) bytes_[a] += step_bytes_[a];
-        ++iteration_;
-        cell_updates_ += active_cells_;
+        ++iteration_;  // (the next step's kernels run as iteration + 1)
+        cur_after.push_back(cur_);
+        k_err_halt<<<1, 1, 0, stream_>>>(d_err_, d_halt_);
+        CK(cudaGetLastError());
+        ++stats_.kernels_launched;
+    }
+    d_.halt = nullptr;
+    if (rc) {
+        iteration_ = it0;
+        return rc;
     }
     if (n > 0) {
         bool failed = false;
         check_error(err, failed);
+        CK(cudaMemsetAsync(d_halt_, 0, sizeof(int), stream_));
+        const long bad = failed ? err_it_ : it0 + n + 1;
+        const long done = std::max(0L, std::min(long(n), bad - 1 - it0));
+        iteration_ = it0 + done;
+        cell_updates_ += uint64_t(done) * active_cells_;
+        for (int a = 0; a < 3; ++a) bytes_[a] += uint64_t(done + (failed && err_p5_ ? 1 : 0)) * step_bytes_[a];
         if (failed) {
-            // roll the counters back to the step before the failing one
-            const long bad = err ? long(err->iteration) : it0 + 1;
-            const long done = std::max(0L, bad - 1 - it0);
-            iteration_ = it0 + done;
-            cell_updates_ -= uint64_t(n - done) * active_cells_;
-            for (int a = 0; a < 3; ++a) bytes_[a] -= uint64_t(n - done) * step_bytes_[a];
+            cur_ = cur_after[size_t(std::min(long(n), done + 1)) - 1];  // the failing step's output
             return 1;
         }
     }
@@ -2187,10 +2215,7 @@ void plbm_gpu_reset_kernel_stats(void* h) {
 
 void* plbm_gpu_stream(void* h) { return EG(h)->stream(); }
 
-int plbm_gpu_set_kernel_variant(void* h, int variant) {
-    EG(h)->set_variant(variant);
-    return 0;
-}
+int plbm_gpu_set_kernel_variant(void* h, int variant) { return EG(h)->set_variant(variant); }
 
 void plbm_gpu_destroy(void* h) { delete EG(h); }
 

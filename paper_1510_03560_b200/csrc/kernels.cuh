@@ -90,6 +90,8 @@ struct Dev {
     const int* nactive;         // device-side expansion: tiles beyond *nactive in the launch are idle
     unsigned long long* probe;  // measurement: per-CTA {smid, start, end} globaltimer (or nullptr)
     int tile_base;              // this launch's tiles start at active[tile_base] (co-scheduled split)
+    uint8_t* suspect;           // [slot] P5 screen: a stored f_post value left [2^-400, 2^400)
+    int screen_all;             // the ambient populations fail the screen: k_p5 checks every tile
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -161,12 +163,15 @@ __host__ __device__ constexpr int face_pattern(int face) {
     return face == 0 ? 12 : face == 1 ? 14 : face == 2 ? 10 : face == 3 ? 16 : face == 4 ? 4 : 22;
 }
 
-// Error key: earliest iteration, then lowest tile in coordinate order (the
-// 1-worker reference order), then code.  atomicMin keeps the first.
+// Error key: earliest iteration, then phase (every tile's P1 runs before any
+// tile's P5 in the reference, engine.cpp:537-563), then lowest tile in
+// coordinate order (the 1-worker reference order), then code.  atomicMin
+// keeps the first.  Layout: iter << 37 | phase << 36 | tile_lin << 4 | code.
 __device__ __forceinline__ void atomic_err(unsigned long long* err, long iter, int tile_lin,
                                            int code) {
-    atomicMin(err, ((unsigned long long)iter << 36) | ((unsigned long long)(unsigned)tile_lin << 4) |
-                       (unsigned)code);
+    const unsigned long long phase = code == ERR_P5_NAN ? 1ull : 0ull;
+    atomicMin(err, ((unsigned long long)iter << 37) | (phase << 36) |
+                       ((unsigned long long)(unsigned)tile_lin << 4) | (unsigned)code);
 }
 
 // Extended-grid solid bit of the tile (local coords in [-1, E]).
@@ -486,6 +491,7 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
     auto collide_plane = [&](int z) {
         int zero_rho = 0;
         int negs = 0;
+        int suspect = 0;
 #pragma unroll 1
         for (int k = 0; k < CPT; ++k) {
             const int idx = threadIdx.x + k * NT;
@@ -610,13 +616,16 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
                 const double wr0 = PLBM_W0 * rho, wr1 = PLBM_W1 * rho, wr2 = PLBM_W2 * rho;
                 const bool unforced = (F0 == 0.0 && F1 == 0.0 && F2 == 0.0);
                 if (!unforced && rho <= 0.0) ++zero_rho;
+                Screen scr;
                 if (unforced || rho <= 0.0) {
 #define PLBM_RELAX(I)                                                                 \
     {                                                                                 \
         const double wr = (I == 0) ? wr0 : ((I <= 6) ? wr1 : wr2);                    \
         const double eu = (I == 0) ? 0.0 : eu_pair<(I == 0 ? 1 : I - ((I + 1) & 1))>(u0, u1, u2); \
         const double e0 = feq_dir<I>(wr, eu, t3);                                     \
-        out[size_t(I) * E3] = f[I] + om * (e0 - f[I]);                                \
+        const double o_ = f[I] + om * (e0 - f[I]);                                     \
+        out[size_t(I) * E3] = o_;                                                     \
+        scr.add(o_);                                                                  \
     }
                     PLBM_RELAX(0) PLBM_RELAX(1) PLBM_RELAX(2) PLBM_RELAX(3) PLBM_RELAX(4)
                     PLBM_RELAX(5) PLBM_RELAX(6) PLBM_RELAX(7) PLBM_RELAX(8) PLBM_RELAX(9)
@@ -635,7 +644,9 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
         const double ev = (I == 0) ? 0.0 : eu_pair<IP>(v0, v1, v2);                   \
         const double e0 = feq_dir<I>(wr, eu, t3);                                     \
         const double e1 = feq_dir<I>(wr, ev, s3);                                     \
-        out[size_t(I) * E3] = f[I] + ((om * (e0 - f[I]) + e1) - e0);                  \
+        const double o_ = f[I] + ((om * (e0 - f[I]) + e1) - e0);                       \
+        out[size_t(I) * E3] = o_;                                                     \
+        scr.add(o_);                                                                  \
     }
                     PLBM_FORCED(0) PLBM_FORCED(1) PLBM_FORCED(2) PLBM_FORCED(3) PLBM_FORCED(4)
                     PLBM_FORCED(5) PLBM_FORCED(6) PLBM_FORCED(7) PLBM_FORCED(8) PLBM_FORCED(9)
@@ -644,10 +655,12 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
                     PLBM_FORCED(18)
 #undef PLBM_FORCED
                 }
+                suspect |= scr.suspect();
             }
         }
         const unsigned zr = __reduce_add_sync(0xffffffffu, (unsigned)zero_rho);
         if ((threadIdx.x & 31) == 0 && zr) atomicAdd(&d.cnt[CNT_ZERO_RHO], (unsigned long long)zr);
+        if (__any_sync(0xffffffffu, suspect) && (threadIdx.x & 31) == 0) d.suspect[slot] = 1;
         if constexpr (NOPSI) {
             const unsigned ng = __reduce_add_sync(0xffffffffu, (unsigned)negs);
             if ((threadIdx.x & 31) == 0 && ng) atomicAdd(&d.cnt[CNT_NEG], (unsigned long long)ng);
@@ -896,6 +909,54 @@ __global__ void __launch_bounds__(NT, MINB) k_face(Dev d, const int* __restrict_
                                               (flags & 1) != 0, (flags & 2) != 0, d.lidx[slot],
                                               d.slot_pf[int((iter + 1) & 1)][slot], iter, tile_lin);
     set_triggers(d, slot, f);
+}
+
+// k_p5: the exact P5 check (proj/src/engine.cpp:500-512: moments of every
+// fluid cell of the post-stream state, EngineError(it, tile, "P5") on a
+// non-finite rho or u) for the tiles the fused kernel's screen marked suspect
+// (lattice.cuh Screen: an unmarked tile provably has finite moments).  Runs
+// after the face pass of step `iter`, before that step's expansion; one CTA
+// per tile, an unmarked tile exits at once.  Clears the marks it consumes.
+template <int E, int C, int NT>
+__global__ void __launch_bounds__(NT) k_p5(Dev d, const int* __restrict__ active, int src_buf, long iter) {
+    if (halted(d)) return;
+    constexpr int E3 = E * E * E;
+    constexpr int G = E + 2;
+    __shared__ RouteTab rt;
+    __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
+    __shared__ int s_tc[3];
+    if (d.nactive && d.tile_base + int(blockIdx.x) >= *d.nactive) return;
+    const int slot = active[blockIdx.x];
+    const bool marked = d.suspect[slot] != 0;
+    if (!marked && !d.screen_all) return;
+    if (d.mode[slot] != MODE_PULL) return;  // (every tile that stepped pulls by now)
+    const bool hs = d.has_solid[slot] != 0;
+    load_routes(rt, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, P.amb_slot, d.slot_f[src_buf]);
+    if (threadIdx.x < 3) s_tc[threadIdx.x] = d.coords[slot * 3 + threadIdx.x];
+    if (hs)
+        for (int k = threadIdx.x; k < d.solid_words; k += NT) s_solid[k] = d.solid[size_t(slot) * d.solid_words + k];
+    __syncthreads();
+    if (threadIdx.x == 0 && marked) d.suspect[slot] = 0;
+    const int tile_lin = (s_tc[0] * P.grid[1] + s_tc[1]) * P.grid[2] + s_tc[2];
+    bool bad = false;
+    for (int cell = threadIdx.x; cell < E3 && !bad; cell += NT) {
+        const int x = cell % E, y = (cell / E) % E, z = cell / (E * E);
+        if (hs && solid_at<E>(s_solid, x, y, z)) continue;
+#pragma unroll 1
+        for (int c = 0; c < C; ++c) {
+            double f[Q], rho, u0, u1, u2;
+            pull_cell<E>(rt, c, hs, s_solid, x, y, z, f);
+            moments(f, rho, u0, u1, u2);
+            if (!isfinite(rho) || !isfinite(u0) || !isfinite(u1) || !isfinite(u2)) bad = true;
+        }
+    }
+    if (bad) atomic_err(d.err, iter, tile_lin, ERR_P5_NAN);
+}
+
+// Static batches: after each step, a recorded error halts the steps queued
+// behind it (the state then stays at the failing step, as the reference's).
+__global__ void k_err_halt(const unsigned long long* err, int* halt) {
+    if (*(volatile const unsigned long long*)err != ~0ull) *halt = 1;
 }
 
 // Reference-view read-back of one tile (f_read, rho, u) into out:

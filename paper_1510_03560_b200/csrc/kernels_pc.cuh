@@ -26,7 +26,7 @@
 //               | collide z from TMEM.
 #pragma once
 
-#include "kernels_tm.cuh"
+#include "physics.cuh"
 
 namespace plbm {
 
@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
         const double* p0 = psi + pidx(z, 0, x, yl);
         const double* ppl = psi + pidx(z + 1, 0, x, yl);
         constexpr int CP = PP;
-        int zero_rho = 0;
+        int zero_rho = 0, suspect = 0;
         if (MEMONLY) {
             double* xc = (xcls >= 0 && wx) ? xst + ((z & 1) * 4 + xcls) * Q * BY + yl : nullptr;
 #pragma unroll
@@ -424,11 +424,12 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
                 cp[2 * E3 + cell] = u1;
                 cp[3 * E3 + cell] = u2;
             }
-            collide_bgk(f, rho, u0, u1, u2, F0, F1, F2, kc.omega, fo + cell, size_t(E3), zero_rho,
+            collide_bgk(f, rho, u0, u1, u2, F0, F1, F2, kc.omega, fo + cell, size_t(E3), zero_rho, suspect,
                         (xcls >= 0 && wx) ? xst + ((z & 1) * 4 + xcls) * Q * BY + yl : nullptr, BY);
         }
         const unsigned zr = __reduce_add_sync(0xffffffffu, (unsigned)zero_rho);
         if ((tid & 31) == 0 && zr) atomicAdd(&d.cnt[CNT_ZERO_RHO], (unsigned long long)zr);
+        if (__any_sync(0xffffffffu, suspect) && (tid & 31) == 0) d.suspect[slot] = 1;
     };
 
     // ---- pipeline -------------------------------------------------------------

@@ -218,4 +218,34 @@ __device__ __forceinline__ double pseudo_potential(double rho, double press, con
     return sqrt(radicand);
 }
 
+// P5 screen (proj/src/engine.cpp:500-512 checks rho and u of every post-stream
+// cell for non-finite values).  Claim: if every population a cell pulls is 0 or
+// has 2^-400 <= |f| < 2^400, its moments are finite.  Every such value is a
+// multiple of 2^-452, so every partial sum of rho (and m) is an exact multiple
+// of 2^-452 (a rounded sum of multiples stays a multiple), hence rho == 0 (u =
+// 0 by moments' rule) or |rho| >= 2^-452; with |m| < 19 * 2^400 < 2^405 the
+// quotient |u| <= 2^857 is finite.  The fused kernels therefore track the
+// exponent range of every stored post-collision value; a tile whose values
+// leave [2^-400, 2^400) (exact zeros included, conservatively) is marked
+// suspect and k_p5 checks its post-stream moments exactly.  The ambient
+// populations (the other pulled source) are checked once on the host.
+constexpr uint32_t SCREEN_LO = 623u << 20;   // |hi word| of 2^-400
+constexpr uint32_t SCREEN_HI = 1423u << 20;  // |hi word| of 2^400
+struct Screen {
+    uint32_t mn = 0xffffffffu, mx = 0u;
+    __device__ __forceinline__ void add2(double a, double b) {
+        const uint32_t ha = uint32_t(__double2hiint(a)) & 0x7fffffffu;
+        const uint32_t hb = uint32_t(__double2hiint(b)) & 0x7fffffffu;
+        mn = __vimin3_u32(mn, ha, hb);
+        mx = __vimax3_u32(mx, ha, hb);
+    }
+    __device__ __forceinline__ void add(double a) { add2(a, a); }
+    __device__ __forceinline__ bool suspect() const { return mn < SCREEN_LO || mx >= SCREEN_HI; }
+};
+__host__ __device__ inline bool screen_ok(double v) {
+    if (v == 0.0) return true;
+    const double a = v < 0 ? -v : v;
+    return a >= 0x1p-400 && a < 0x1p400;
+}
+
 }  // namespace plbm
