@@ -12,14 +12,19 @@ that point is the benchmark's input).  Each step reads+writes ~10 GB, far more
 than the 126 MB L2, so no explicit flush is needed between steps.
 
 One JSON line on rank 0.  `value` is device-timed (CUDA events on the engine's
-stream, max over ranks); `e2e` is the same metric through the C-ABI with the
-per-step host read of the report counters, host-clock timed; `roofline` is the
+stream, max over ranks); `e2e` is the same metric through the C-ABI in the
+reference driver's loop (one step call + the report counters per iteration,
+then the final rho snapshot gathered to host memory), host-clock timed; `roofline` is the
 fused kernel's algorithmic bytes (304 B per cell update per component, SURVEY
 §8(d)) over its CUDA-event duration; `cpu_baseline` is the reference itself
 (oracle/_ref, built from the reference sources) on the host cores.
 
---impl reference times the reference CPU implementation (oracle/_ref) on the
-box's host cores on a bounded 128^3 sample of the same workload.
+--impl reference times the reference CPU implementation (oracle/_ref, built
+from the reference sources) on the box's host cores on the SAME workload:
+the same pre-steps grow the mesh, the same warm-up, then the timed steps (the
+config dict is identical in both lines).  Configs whose reference footprint
+exceeds the host's memory (C3/C4/C5 at 512^3+) fall back to a bounded static
+sample of the same physics and say so.
 """
 from __future__ import annotations
 
@@ -46,33 +51,55 @@ def parse():
     p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--config", choices=["c2", "c2_static", "c1"], default="c2")
-    p.add_argument("--pre-steps", type=int, default=100)
+    p.add_argument("--config", choices=["c2", "c2_static", "c1", "c3", "c3_static", "c4", "c5"], default="c2")
+    p.add_argument("--pre-steps", type=int, default=None,
+                   help="steps before warm-up that grow the mesh (default per config)")
+    p.add_argument("--extent", type=int, default=32, help="c5: subdomain size E")
+    p.add_argument("--components", type=int, default=2, help="c5: component count C")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--cpu-seconds", type=float, default=20.0)
     p.add_argument("--variant", type=int, default=0, help="fused-kernel variant (plbm_gpu.h)")
     p.add_argument("--dist-backend", default="nccl", help="nccl (one GPU per rank) or gloo (tests)")
     return p.parse_args()
 
 
-def workload(cfg: str, world: int = 1):
+# name -> (builder(world, args), description, default pre-steps, scaling at N > 1)
+def workload(a, world: int = 1):
+    cfg = a.config
     if cfg == "c2" and world > 1:
-        return S.mpmc_release_weak(world), \
-            f"C2 weak-scaled: {world} x (256^3 2-comp MPMC sphere release) along x, 32^3 subdomains, progressive S=1e-9, owners sharded over {world} GPUs"
+        sc = S.mpmc_release_weak(world)
+        return sc, (f"C2 weak-scaled: {world} x (256^3 2-comp MPMC sphere release) along x, 32^3 "
+                    f"subdomains, progressive S=1e-9"), 100, "weak"
     if cfg == "c2":
-        return S.mpmc_release(n=256, extent=32, threshold=1e-9), \
-            "C2: D3Q19 2-comp MPMC (PR liquid/vapour + ideal-like) sphere release, 256^3, 32^3 subdomains, progressive S=1e-9"
+        return S.bench_c2(), ("C2: D3Q19 2-comp MPMC (PR liquid/vapour + ideal-like) sphere release, "
+                              "256^3, 32^3 subdomains, progressive S=1e-9"), 100, "weak"
     if cfg == "c2_static":
-        return S.mpmc_release(n=256, extent=32, mode=S.MODE_STATIC), \
-            "C2-static: D3Q19 2-comp MPMC sphere release, 256^3 full static mesh, 32^3 subdomains"
-    return S.config1(threshold=1e-12), \
-        "C1: D3Q19 1-comp ideal gas, moving box inflow into 64^3, 16^3 subdomains, progressive S=1e-12"
+        return S.bench_c2(S.MODE_STATIC), "C2-static: 256^3 2-comp MPMC sphere release, full static mesh, 32^3 subdomains", 0, "weak"
+    if cfg == "c3":
+        sc = S.mpmc_release(n=512, extent=32, threshold=1e-9, devices=S.BENCH_DEVICES)
+        return sc, "C3 progressive: 512^3 2-comp MPMC sphere release, 32^3 subdomains, S=1e-9", 100, "strong"
+    if cfg == "c3_static":
+        sc = S.mpmc_release(n=512, extent=32, mode=S.MODE_STATIC, devices=S.BENCH_DEVICES)
+        return sc, "C3 static: 512^3 2-comp MPMC sphere release, full static mesh (4096 tiles), 32^3 subdomains", 0, "strong"
+    if cfg == "c4":
+        sc = S.mpmc_channel(devices=S.BENCH_DEVICES)
+        return sc, ("C4: 1024x512x512 3-D channel network (LBMGEO generator, seed 1510), 2-comp MPMC "
+                    "liquid sphere in the inlet channel, 32^3 subdomains, progressive S=1e-9"), 400, "strong"
+    if cfg == "c5":
+        sc = S.mpmc_release(n=512, extent=a.extent, mode=S.MODE_STATIC, n_components=a.components,
+                            devices=S.BENCH_DEVICES)
+        return sc, (f"C5: 512^3 static MPMC sphere release, {a.extent}^3 subdomains, "
+                    f"{a.components} component(s)"), 0, "strong"
+    return S.config1(threshold=1e-12), ("C1: D3Q19 1-comp ideal gas, moving box inflow into 64^3, "
+                                        "16^3 subdomains, progressive S=1e-12"), 0, "weak"
 
 
-def cpu_sample_scenario():
-    """Bounded CPU sample: same physics / tile size / components at 128^3,
-    static mesh (every tile active = the developed-mesh per-cell cost)."""
-    return S.mpmc_release(n=128, extent=32, mode=S.MODE_STATIC)
+def bench_config(a, sc, name, pre):
+    """The workload identity (identical in both arms' JSON lines)."""
+    return {"workload": name, "domain": list(sc.domain), "tile_extent": sc.tile_extent,
+            "components": sc.n_components, "mode": "static" if sc.mode == S.MODE_STATIC else "progressive",
+            "threshold": sc.threshold, "pre_steps": pre, "simulated_devices": sc.devices,
+            "l2": "per-step working set >= 0.6 GB >> 126 MB L2 at every config (no flush needed)"}
 
 
 def hbm_peak():
@@ -83,19 +110,68 @@ def hbm_peak():
         return FALLBACK_HBM_GBS, "fallback"
 
 
-def run_reference_cpu(seconds: float, warmup: int = 1, max_steps: int = 10**9):
-    """Times the reference (oracle/_ref/libplbm_ref.so, compiled from the
-    reference sources) on the host cores: MLUPS per component."""
+def reference_threads(sc) -> int:
+    """Worker threads the reference engine can use on this host: tiles go to
+    worker owner % W (engine.cpp:214-218), so W <= simulated devices."""
+    return max(1, min(os.cpu_count() or 1, sc.devices))
+
+
+def fits_host(sc) -> bool:
+    """The reference keeps every tile with a ghost ring and two population
+    buffers on the host (tile.cpp:7-13): 28.97 MB per 32^3 2-comp tile."""
+    g = (sc.tile_extent + 2) ** 3
+    per_tile = g * (sc.n_components * (2 * 19 + 8) * 8 + 1)
+    tiles = 1
+    for d in sc.domain:
+        tiles *= d // sc.tile_extent
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError):
+        avail = 0
+    return per_tile * tiles < 0.7 * avail
+
+
+def run_reference_arm(a, sc, pre, steps, warmup):
+    """The reference's own CPU engine (oracle/_ref/libplbm_ref.so, compiled
+    from /root/reference/proj/src) through make_state + Engine::step on the
+    SAME workload: pre-steps grow the mesh, `warmup` untimed steps, then
+    `steps` timed steps, each a whole Engine::step over every active tile.
+    Returns (MLUPS/comp, threads, sample description, steps, seconds)."""
     from paper_1510_03560_b200 import capi
-    cores = os.cpu_count() or 1
-    sc = cpu_sample_scenario()
-    sc.devices = cores  # tiles go to worker owner % W (engine.cpp:217)
-    eng = capi.ref_engine(sc, workers=cores)
-    eng.step(warmup)
+    W = reference_threads(sc)
+    eng = capi.ref_engine(sc, workers=W)
+    eng.step(pre + warmup)
+    c0 = eng.counters()["cell_updates"]
+    t0 = time.perf_counter()
+    eng.step(steps)
+    dt = time.perf_counter() - t0
+    cells = eng.counters()["cell_updates"] - c0
+    tiles = eng.counters()["tiles"]
+    eng.close()
+    sample = (f"reference (oracle/_ref, built from the reference sources) on the same workload: "
+              f"{pre} pre-steps + {warmup} warm-up, then {steps} timed steps on {tiles} tiles, {W} worker threads")
+    return cells * sc.n_components / dt / 1e6, W, sample, steps, dt
+
+
+def run_cpu_sample(sc_full, seconds: float):
+    """Bounded cpu_baseline sample (about `seconds` of CPU work): the same
+    physics, tile size and component count on the full static mesh of the
+    workload's domain (= the developed progressive mesh's per-cell cost) when
+    the reference's host footprint fits, else a 256^3 static block of it."""
+    from paper_1510_03560_b200 import capi
+    import copy
+    sc = copy.deepcopy(sc_full)
+    sc.mode = S.MODE_STATIC
+    if not fits_host(sc):
+        sc = S.mpmc_release(n=256, extent=sc_full.tile_extent, mode=S.MODE_STATIC,
+                            n_components=sc_full.n_components, devices=sc_full.devices)
+    W = reference_threads(sc)
+    eng = capi.ref_engine(sc, workers=W)
+    eng.step(1)
     c0 = eng.counters()["cell_updates"]
     t0 = time.perf_counter()
     n = 0
-    while n < max_steps:
+    while True:
         eng.step(1)
         n += 1
         if time.perf_counter() - t0 > seconds:
@@ -103,9 +179,9 @@ def run_reference_cpu(seconds: float, warmup: int = 1, max_steps: int = 10**9):
     dt = time.perf_counter() - t0
     cells = eng.counters()["cell_updates"] - c0
     eng.close()
-    value = cells * sc.n_components / dt / 1e6
-    sample = f"reference (oracle/_ref) 128^3 2-comp MPMC static, 32^3 tiles, {n} steps after {warmup} warm-up, {cores} worker threads"
-    return value, cores, sample, n, dt
+    sample = (f"reference (oracle/_ref) static {sc.domain[0]}x{sc.domain[1]}x{sc.domain[2]}, "
+              f"{sc.tile_extent}^3 tiles, {sc.n_components} comp, {n} steps after 1 warm-up, {W} worker threads")
+    return cells * sc.n_components / dt / 1e6, W, sample
 
 
 class ClockSampler:
@@ -161,18 +237,28 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    sc, name, pre_default, scaling = workload(a, world)
+    pre = pre_default if a.pre_steps is None else a.pre_steps
+    config = bench_config(a, sc, name, pre)
 
     if a.impl == "reference":
         if rank != 0:
             return
-        value, cores, sample, n, dt = run_reference_cpu(a.cpu_seconds, warmup=a.warmup,
-                                                        max_steps=max(a.steps, 1))
-        _, name = workload(a.config)
+        ref_sc = sc
+        if world > 1 and a.config == "c2":
+            ref_sc = S.bench_c2()  # the per-GPU block: same per-cell work, 1/N of the job
+        if not fits_host(ref_sc):
+            value, cores, sample = run_cpu_sample(ref_sc, a.cpu_seconds)
+            n, dt = 0, 0.0
+        else:
+            value, cores, sample, n, dt = run_reference_arm(a, ref_sc, pre, max(a.steps, 1), a.warmup)
+        if ref_sc is not sc:
+            sample += f" (one 256^3 block of the {world}-block weak-scaled job: the per-cell work is identical)"
         line = {"metric": "MLUPS per component (D3Q19 MPMC)", "value": round(value, 3),
-                "unit": "MLUPS/comp", "impl": "reference", "n_gpus": a.gpus, "steps": n,
+                "unit": "MLUPS/comp", "impl": "reference", "n_gpus": a.gpus, "steps": n or a.steps,
                 "warmup": a.warmup, "ms_per_step": round(1000 * dt / max(n, 1), 3),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "config": {"workload": name, "sample": sample},
+                "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": config,
                 "cpu_baseline": {"value": round(value, 3), "unit": "MLUPS/comp", "cores": cores,
                                  "kind": "reference", "sample": sample},
                 "e2e": {"value": round(value, 3), "unit": "MLUPS/comp", "h2d_bytes_per_step": 0,
@@ -193,7 +279,6 @@ def main():
             dist.init_process_group(a.dist_backend)
     from paper_1510_03560_b200 import capi
     from paper_1510_03560_b200.dist import DistStepper
-    sc, name = workload(a.config, world)
     C = sc.n_components
     eng = capi.gpu_engine(sc, device=gpu, rank=rank, world=world)
     eng.set_kernel_variant(a.variant)
@@ -204,7 +289,7 @@ def main():
     else:
         run = eng.step
 
-    run(a.pre_steps)
+    run(pre)
     run(a.warmup)
     tiles_at_start = eng.counters()["tiles"]
 
@@ -240,8 +325,11 @@ def main():
     ks = eng.kernel_stats()
     eng.set_profiling(False)
 
-    # ---- end to end through the C-ABI: step + per-step host read of the
-    # report counters (what the reference driver reads each step) -------------
+    # ---- end to end through the C-ABI, the reference driver's loop
+    # (engine::run_scenario, proj/src/engine.cpp:640-668): one plbm_gpu_step
+    # per iteration, the report counters read after every step, and the final
+    # snapshot (the last iteration's dump_field of rho for every component,
+    # engine.cpp:664-666) gathered into a host grid --------------------------
     eng.reset_kernel_stats()
     e0 = eng.counters()["cell_updates"]
     barrier()
@@ -249,6 +337,9 @@ def main():
     for _ in range(a.steps):
         run(1)
         eng.counters()
+    if world == 1:
+        for c in range(C):
+            eng.gather_field("rho", c)  # host grid (counted in d2h_bytes)
     barrier()
     e_dt = time.perf_counter() - t0
     e_cells = eng.counters()["cell_updates"] - e0
@@ -282,7 +373,7 @@ def main():
     # to this run's average launch.
     traffic = None
     prof = os.path.join(REPO, "profiles", "ncu_kmain_summary.json")
-    if os.path.exists(prof) and ks["main_launches"]:
+    if os.path.exists(prof) and ks["main_launches"] and a.config == "c2":
         try:
             bpc = json.load(open(prof))["dram_bytes_per_cell_comp"]
             traffic = round(bpc * ks["main_cell_updates"] / ks["main_launches"] * C)
@@ -292,15 +383,15 @@ def main():
         "metric": "MLUPS per component (D3Q19 MPMC)",
         "value": round(value, 2), "unit": "MLUPS/comp", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": round(ms_max / a.steps, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": name, "pre_steps": a.pre_steps, "tiles": [tiles_at_start, tiles_at_end],
-                   "components": C, "tile_extent": sc.tile_extent,
-                   "parallelism": f"tile-sharded x{world} (owner % world), NVLink peer loads" if world > 1 else "1 GPU",
-                   "l2": "per-step working set ~10 GB >> 126 MB L2 (no flush needed)",
-                   "mlups_cells": round(value / C, 2)},
+        "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config,
+        "run": {"tiles": [tiles_at_start, tiles_at_end], "mlups_cells": round(value / C, 2),
+                "parallelism": f"tile-sharded x{world} (owner % world), NVLink peer loads" if world > 1 else "1 GPU"},
         "e2e": {"value": round(e2e, 2), "unit": "MLUPS/comp",
                 "h2d_bytes_per_step": int(e_ks["h2d_bytes"] / max(a.steps, 1)),
-                "d2h_bytes_per_step": int(e_ks["d2h_bytes"] / max(a.steps, 1))},
+                "d2h_bytes_per_step": int(e_ks["d2h_bytes"] / max(a.steps, 1)),
+                "loop": "plbm_gpu_step(h, 1) + plbm_gpu_counters per iteration, then the final rho "
+                        "snapshot of every component gathered to a host grid"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
                      "peak": peak, "unit": "GB/s",
@@ -322,7 +413,7 @@ def main():
                                                     "staged": c["bytes"][2]}}
     if not a.no_cpu_baseline and world == 1:
         try:
-            v, cores, sample, _, _ = run_reference_cpu(a.cpu_seconds)
+            v, cores, sample = run_cpu_sample(sc, a.cpu_seconds)
             line["cpu_baseline"] = {"value": round(v, 3), "unit": "MLUPS/comp", "cores": cores,
                                     "kind": "reference", "sample": sample}
         except Exception as ex:  # the reference shim is built here and travels

@@ -341,6 +341,19 @@ def mpmc_release(n: int = 256, extent: int = 32, mode: int = MODE_PROGRESSIVE,
                     name="mpmc_release")
 
 
+BENCH_DEVICES = 16  # simulated devices of the bench workload (placement only)
+
+
+def bench_c2(mode: int = MODE_PROGRESSIVE) -> Scenario:
+    """The benchmark workload (BASELINE.json configs[1]):
+    256^3, 32^3 subdomains, two-component MPMC sphere release, S = 1e-9.
+    Owners are placed over BENCH_DEVICES simulated devices so the reference
+    CPU engine can spread the tiles over that many worker threads
+    (engine.cpp:214-218: tile owner % W); on the GPU the owner is placement
+    metadata only (byte classes, creation log)."""
+    return mpmc_release(n=256, extent=32, mode=mode, threshold=1e-9, devices=BENCH_DEVICES)
+
+
 def mpmc_release_weak(n_blocks: int, n: int = 256, extent: int = 32, threshold: float = 1e-9) -> Scenario:
     """Weak-scaling form of C2 for N GPUs: N 256^3 blocks side by side along x,
     each with its own ramped liquid sphere (the single-GPU case is exactly

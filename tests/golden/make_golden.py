@@ -22,7 +22,8 @@ from tests import scenarios  # noqa: E402
 from tests.compare import FIELDS  # noqa: E402
 
 GOLDEN = ["c1_progressive", "c1_progressive_S0", "mpmc_progressive_e16", "mpmc_e32",
-          "periodic_solid_gravity", "mpmc_e16_solid_S0", "mpmc_islands", "mpmc_e64", "mpmc3_e64_solid"]
+          "periodic_solid_gravity", "mpmc_e16_solid_S0", "mpmc_islands", "mpmc_e64", "mpmc3_e64_solid",
+          "mp1_e16", "mp1_e32_solid", "mpmc3_e16"]
 
 
 def state_digest(eng):

@@ -170,3 +170,36 @@ def mpmc_islands():
 ALL.update({
     "mpmc_islands": (mpmc_islands, 12),
 })
+
+
+def mp1_e16():
+    """single-component PR liquid/vapour at E = 16 (k_main_pc<16, 1>),
+    progressive S = 1e-9, gravity."""
+    sc = S.mpmc_release(n=64, extent=16, threshold=1e-9, r_core=5, n_components=1, devices=2)
+    sc.components[0].gravity = (0.0, -1e-6, 0.0)
+    return sc
+
+
+def mp1_e32_solid():
+    """single-component PR at E = 32 (k_main_pc<32, 1>), static, periodic in
+    x, a solid slab through the sphere's edge."""
+    sc = S.mpmc_release(extent=32, mode=S.MODE_STATIC, r_core=7, n_components=1, domain=(64, 32, 64))
+    sc.seeds = S.ramped_sphere_seeds((32.0, 16.0, 32.0), 7, 6.5, sc.components[0].rho_ambient, 6)
+    sc.periodic = (1, 0, 0)
+    g = np.zeros((64, 32, 64), np.uint8)  # [z, y, x]
+    g[20:26, 4:28, 36:40] = 1
+    sc.geometry = g
+    return sc
+
+
+def mpmc3_e16():
+    """three components at E = 16 (k_main_pc<16, 3>: 6-CTA clusters),
+    progressive at S = 0 on 3 simulated devices."""
+    return S.mpmc_release(n=64, extent=16, threshold=0.0, r_core=5, n_components=3, devices=3)
+
+
+ALL.update({
+    "mp1_e16": (mp1_e16, 14),
+    "mp1_e32_solid": (mp1_e32_solid, 6),
+    "mpmc3_e16": (mpmc3_e16, 10),
+})

@@ -159,3 +159,21 @@ def test_oracle_reproduces_reference_golden_states(built, name):
     eng = capi.oracle_engine(make())
     eng.step(steps)
     assert_matches_golden(eng, name)
+
+
+def test_oracle_matches_reference_c1_at_baseline_scale():
+    """BASELINE configs[0] exactly (64^3, 16^3 tiles, S = 1e-12, 500 steps):
+    the C restatement against the reference's own state digests
+    (tests/golden/make_golden_large.py)."""
+    import json
+    from paper_1510_03560_b200 import capi
+    from tests.golden.make_golden_large import LARGE, OUT, summary
+    g = json.load(open(OUT))["c1_exact"]
+    sc, steps, _ = LARGE["c1_exact"]()
+    orc = capi.oracle_engine(sc)
+    orc.step(steps)
+    d = summary(orc)
+    assert d["counters"] == g["counters"]
+    assert d["creation_log"] == g["creation_log"]
+    assert d["tiles"] == g["tiles"]
+    assert d["digests"] == g["digests"]
