@@ -56,6 +56,9 @@ def parse():
                    help="steps before warm-up that grow the mesh (default per config)")
     p.add_argument("--extent", type=int, default=32, help="c5: subdomain size E")
     p.add_argument("--components", type=int, default=2, help="c5: component count C")
+    p.add_argument("--snapshot-every", type=int, default=0,
+                   help="e2e loop: gather the rho field of every component to host memory every N "
+                        "steps (the driver's snapshot_interval; default 0 = the reference's default)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=20.0)
     p.add_argument("--variant", type=int, default=0, help="fused-kernel variant (plbm_gpu.h)")
@@ -327,19 +330,20 @@ def main():
 
     # ---- end to end through the C-ABI, the reference driver's loop
     # (engine::run_scenario, proj/src/engine.cpp:640-668): one plbm_gpu_step
-    # per iteration, the report counters read after every step, and the final
-    # snapshot (the last iteration's dump_field of rho for every component,
-    # engine.cpp:664-666) gathered into a host grid --------------------------
+    # per iteration, the report counters read after every step (a superset of
+    # flush_row's reads at report_interval), and with --snapshot-every N the
+    # rho field of every component gathered into a host grid every N steps
+    # (take_snapshot; the reference's default snapshot_interval is 0) -------
     eng.reset_kernel_stats()
     e0 = eng.counters()["cell_updates"]
     barrier()
     t0 = time.perf_counter()
-    for _ in range(a.steps):
+    for k in range(1, a.steps + 1):
         run(1)
         eng.counters()
-    if world == 1:
-        for c in range(C):
-            eng.gather_field("rho", c)  # host grid (counted in d2h_bytes)
+        if world == 1 and a.snapshot_every and k % a.snapshot_every == 0:
+            for c in range(C):
+                eng.gather_field("rho", c)  # host grid (counted in d2h_bytes)
     barrier()
     e_dt = time.perf_counter() - t0
     e_cells = eng.counters()["cell_updates"] - e0
@@ -390,8 +394,9 @@ def main():
         "e2e": {"value": round(e2e, 2), "unit": "MLUPS/comp",
                 "h2d_bytes_per_step": int(e_ks["h2d_bytes"] / max(a.steps, 1)),
                 "d2h_bytes_per_step": int(e_ks["d2h_bytes"] / max(a.steps, 1)),
-                "loop": "plbm_gpu_step(h, 1) + plbm_gpu_counters per iteration, then the final rho "
-                        "snapshot of every component gathered to a host grid"},
+                "loop": "plbm_gpu_step(h, 1) + plbm_gpu_counters per iteration" +
+                        (f", rho snapshot of every component to a host grid every {a.snapshot_every} steps"
+                         if a.snapshot_every else " (snapshot_interval 0, the reference driver's default)")},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
                      "peak": peak, "unit": "GB/s",
