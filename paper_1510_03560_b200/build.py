@@ -58,6 +58,22 @@ def build_gpu(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_exp(out: str, defines) -> str:
+    """Measurement / A-B builds (not the product): engine.cu with extra -D
+    flags into `out`, loaded through PLBM_GPU_LIB.  E.g.
+        python -m paper_1510_03560_b200.build --exp build/exp/libphases.so PLBM_PHASES PLBM_ONLY_E32C2"""
+    os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
+    cmd = ["nvcc", *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-I", CSRC,
+           os.path.join(CSRC, "engine.cu"), "-o", out, "-lcudart"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"nvcc failed for {out}")
+    with open(out + ".ptxas.txt", "w") as fh:
+        fh.write(r.stderr)
+    return out
+
+
 def build_oracle() -> None:
     """Parity checkers (test infrastructure): the C restatement always, the
     reference itself only where /root/reference exists (this container)."""
@@ -75,6 +91,10 @@ def build_integration() -> None:
 
 
 if __name__ == "__main__":
+    if "--exp" in sys.argv:
+        i = sys.argv.index("--exp")
+        print(build_exp(sys.argv[i + 1], sys.argv[i + 2:]))
+        sys.exit(0)
     build_gpu(force="--force" in sys.argv, verbose=True)
     build_oracle()
     build_integration()

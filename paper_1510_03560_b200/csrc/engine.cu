@@ -202,6 +202,10 @@ Kernels pick_c(int C, bool nopsi) {
 }
 
 Kernels pick_kernels(int E, int C, bool nopsi) {
+#ifdef PLBM_ONLY_E32C2  // experiment builds: the bench instantiation only (fast compile)
+    if (E == 32 && C == 2 && !nopsi) return make_kernels<32, 2, false>();
+    throw std::invalid_argument("PLBM_ONLY_E32C2 build: E = 32, C = 2 only");
+#endif
     switch (E) {
     case 8: return pick_c<8>(C, nopsi);
     case 16: return pick_c<16>(C, nopsi);
@@ -413,6 +417,7 @@ class Engine {
     bool face_fused_ = false;    // the last k_main ran the face pass itself
     double* d_capture_ = nullptr;
     uint8_t* d_suspect_ = nullptr;  // [slot] P5 screen marks (k_main* -> k_p5)
+    unsigned* d_susp_any_ = nullptr;  // [2] per step parity: a tile was marked
     unsigned long long* d_cnt_ = nullptr;
     unsigned long long* d_err_ = nullptr;
     int* d_active_ = nullptr;
@@ -648,6 +653,8 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     d_err_ = dmalloc<unsigned long long>(1);
     d_suspect_ = dmalloc<uint8_t>(nslot);
     CK(cudaMemsetAsync(d_suspect_, 0, nslot, stream_));
+    d_susp_any_ = dmalloc<unsigned>(2);
+    CK(cudaMemsetAsync(d_susp_any_, 0, 2 * sizeof(unsigned), stream_));
     d_active_ = dmalloc<int>(nslot);
     d_scratch_slots_ = dmalloc<int>(nslot);
     d_readback_ = dmalloc<double>(size_t(23) * E3_);
@@ -718,6 +725,19 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
         for (int i = 0; i < Q; ++i)
             if (!screen_ok(p.comp[c].feq_amb[i])) d_.screen_all = 1;
     if (std::getenv("PLBM_P5_ALL")) d_.screen_all = 1;  // test hook: exact check of every tile
+    // integer negative-population count (k_main_pc): every f_in value must be
+    // nonzero-or-+0, finite and not -0; the constants a step can pull are
+    // checked here, the stored populations by the previous step's screen
+    // (whose marks are per rank: multi-rank runs keep the FP compares)
+    d_.susp_any = world_ == 1 ? d_susp_any_ : nullptr;
+    d_.neg_exact = d_.screen_all;
+    auto sign_ok = [](double v) { return std::isfinite(v) && !(v == 0.0 && std::signbit(v)); };
+    for (int c = 0; c < C_; ++c)
+        for (int i = 0; i < Q; ++i)
+            if (!sign_ok(p.comp[c].feq_amb[i])) d_.neg_exact = 1;
+    for (size_t sd = 0; sd < seeds_.size(); ++sd)
+        for (int i = 0; i < Q; ++i)
+            if (!sign_ok(p.seeds[sd].feq[i])) d_.neg_exact = 1;
     if (std::getenv("PLBM_PROBE")) d_.probe = dmalloc<unsigned long long>(3 * size_t(cap_ + 1) * 16);
 
     // ---- host mirror + initial tiles (make_state, engine.cpp:134-159)
@@ -817,7 +837,7 @@ void Engine::release() {
                     d_u_face_, d_trig_, d_capture_, d_cnt_, d_err_, d_active_, d_scratch_slots_,
                     d_readback_, d_dep_cnt_, d_dep_need_, d_geo_, d_bmask_, d_omask_, d_halt_, d_pokes_,
                     d_gslot_, d_cand_, d_nactive_, d_next_slot_, d_next_local_, d_owner_, d_geomdev_, d_p2p_,
-                    d_per_dev_, d_acc_, d_births_, d_nbirths_, d_post_flags_, d_suspect_};
+                    d_per_dev_, d_acc_, d_births_, d_nbirths_, d_post_flags_, d_suspect_, d_susp_any_};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (h_flags_) cudaFreeHost(h_flags_);

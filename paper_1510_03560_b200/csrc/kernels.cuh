@@ -92,6 +92,8 @@ struct Dev {
     int tile_base;              // this launch's tiles start at active[tile_base] (co-scheduled split)
     uint8_t* suspect;           // [slot] P5 screen: a stored f_post value left [2^-400, 2^400)
     int screen_all;             // the ambient populations fail the screen: k_p5 checks every tile
+    unsigned* susp_any;         // [2] by step parity: some tile was marked (nullptr: multi-rank)
+    int neg_exact;              // always count negative populations with FP compares (see k_main_pc)
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -660,7 +662,10 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
         }
         const unsigned zr = __reduce_add_sync(0xffffffffu, (unsigned)zero_rho);
         if ((threadIdx.x & 31) == 0 && zr) atomicAdd(&d.cnt[CNT_ZERO_RHO], (unsigned long long)zr);
-        if (__any_sync(0xffffffffu, suspect) && (threadIdx.x & 31) == 0) d.suspect[slot] = 1;
+        if (__any_sync(0xffffffffu, suspect) && (threadIdx.x & 31) == 0) {
+            d.suspect[slot] = 1;
+            if (d.susp_any) atomicOr(&d.susp_any[iter & 1], 1u);
+        }
         if constexpr (NOPSI) {
             const unsigned ng = __reduce_add_sync(0xffffffffu, (unsigned)negs);
             if ((threadIdx.x & 31) == 0 && ng) atomicAdd(&d.cnt[CNT_NEG], (unsigned long long)ng);
@@ -920,6 +925,9 @@ __global__ void __launch_bounds__(NT, MINB) k_face(Dev d, const int* __restrict_
 template <int E, int C, int NT>
 __global__ void __launch_bounds__(NT) k_p5(Dev d, const int* __restrict__ active, int src_buf, long iter) {
     if (halted(d)) return;
+    // step iter-1's "some tile marked" flag was last read by this step's fused
+    // kernel: clear it for step iter+1 to set
+    if (blockIdx.x == 0 && threadIdx.x == 0 && d.susp_any) d.susp_any[(iter + 1) & 1] = 0u;
     constexpr int E3 = E * E * E;
     constexpr int G = E + 2;
     __shared__ RouteTab rt;

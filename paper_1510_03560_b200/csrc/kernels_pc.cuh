@@ -212,8 +212,8 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
     const uint32_t mbar_u32 = smem_u32(&s_mbar[0]);
     auto push = [&](int dst_rank, int pz, int yy_local, double v) {
         uint32_t ra, rb;
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(psi_u32), "r"(dst_rank));
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rb) : "r"(mbar_u32), "r"(dst_rank));
+        asm("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(psi_u32), "r"(dst_rank));
+        asm("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rb) : "r"(mbar_u32), "r"(dst_rank));
         asm volatile(
             "st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n" ::"r"(
                 ra + uint32_t(pidx(pz, c, x, yy_local)) * 8u),
@@ -302,12 +302,20 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
         else pull_addr<E>(rt_pull, c, hs, s_solid, x, y, pz, op);
     };
 
+    // Per-thread diagnostics, reduced once at the end of the kernel.
+    // Negative populations: when every population this step can pull passed
+    // the previous step's screen (no tile marked; the constants checked on
+    // the host; no poke), none is -0, NaN or subnormal, so f < 0 is exactly
+    // its sign bit — an integer op instead of an FP64 compare per value.
+    unsigned negs = 0, clamps = 0, zero_rho = 0;
+    int suspect = 0;
+    const bool neg_exact = d.neg_exact || d.npoke || !d.susp_any || d.susp_any[(iter - 1) & 1] != 0u;
+
     // ---- psi pass of plane pz ---------------------------------------------------
     auto psi_pass = [&](int pz) {
         const bool sol = hs && solid_at<E>(s_solid, x, y, pz);
         double f[Q];
         double v = 0.0, rho = 0.0;
-        int negs = 0, clamps = 0;
         if (sol) {
 #pragma unroll
             for (int i = 0; i < Q; ++i) f[i] = 0.0;
@@ -321,9 +329,13 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
             }
             apply_pokes<E>(d, slot, c, x, y, pz, f);
 #pragma unroll
-            for (int i = 0; i < Q; ++i) {
-                rho += f[i];
-                negs += f[i] < 0.0;
+            for (int i = 0; i < Q; ++i) rho += f[i];
+            if (neg_exact) {
+#pragma unroll
+                for (int i = 0; i < Q; ++i) negs += f[i] < 0.0;
+            } else {
+#pragma unroll
+                for (int i = 0; i < Q; ++i) negs += uint32_t(__double2hiint(f[i])) >> 31;
             }
             if (MEMONLY) {
             } else if (!isfinite(rho)) {
@@ -343,12 +355,6 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
         push_all(pz, v);
         tm_store20(tbase + uint32_t((pz % T::TSLOTS) * T::CB), f, rho);
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-        const unsigned m1 = __reduce_add_sync(0xffffffffu, (unsigned)negs);
-        const unsigned m2 = __reduce_add_sync(0xffffffffu, (unsigned)clamps);
-        if ((tid & 31) == 0) {
-            if (m1) atomicAdd(&d.cnt[CNT_NEG], (unsigned long long)m1);
-            if (m2) atomicAdd(&d.cnt[CNT_CLAMP], (unsigned long long)m2);
-        }
     };
 
     // ---- collide plane z (this CTA's component) ------------------------------
@@ -369,7 +375,6 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
         const double* p0 = psi + pidx(z, 0, x, yl);
         const double* ppl = psi + pidx(z + 1, 0, x, yl);
         constexpr int CP = PP;
-        int zero_rho = 0, suspect = 0;
         if (MEMONLY) {
             double* xc = (xcls >= 0 && wx) ? xst + ((z & 1) * 4 + xcls) * Q * BY + yl : nullptr;
 #pragma unroll
@@ -427,12 +432,21 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
             collide_bgk(f, rho, u0, u1, u2, F0, F1, F2, kc.omega, fo + cell, size_t(E3), zero_rho, suspect,
                         (xcls >= 0 && wx) ? xst + ((z & 1) * 4 + xcls) * Q * BY + yl : nullptr, BY);
         }
-        const unsigned zr = __reduce_add_sync(0xffffffffu, (unsigned)zero_rho);
-        if ((tid & 31) == 0 && zr) atomicAdd(&d.cnt[CNT_ZERO_RHO], (unsigned long long)zr);
-        if (__any_sync(0xffffffffu, suspect) && (tid & 31) == 0) d.suspect[slot] = 1;
     };
 
     // ---- pipeline -------------------------------------------------------------
+#ifdef PLBM_PHASES  // measurement build: per-warp cycle accounting of the plane loop
+    unsigned long long ph_acc[8] = {};
+    long long ph_t = clock64();
+#define PLBM_PHASE(k)                  \
+    {                                  \
+        const long long t_ = clock64(); \
+        ph_acc[k] += t_ - ph_t;        \
+        ph_t = t_;                     \
+    }
+#else
+#define PLBM_PHASE(k)
+#endif
     fill_zghost(-1);
 #pragma unroll 1
     for (int p = 0; p < LAG; ++p) {
@@ -458,24 +472,52 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
         if (pn < E) {
             expect(pn);
             cp_async_wait<0>();  // pulls and ghost ring of plane pn have landed
+            PLBM_PHASE(0)
             psi_pass(pn);
+            PLBM_PHASE(1)
             issue_pulls(pn + 1);  // this thread's landing slots were just read
             cp_async_commit();
+            PLBM_PHASE(2)
         } else if (pn == E) {
             fill_zghost(E);
         }
         double f[Q], rho, u0, u1, u2;
         if constexpr (EARLY) collide_head(z, f, rho, u0, u1, u2);
+        PLBM_PHASE(3)
         // The peers' psi of plane z+1: one warp polls the mbarrier, the CTA
         // barrier then releases the others (they wait in bar.sync instead of
         // spinning) and carries the acquired data to them.
         if (warp == POLL_WARP && z + 1 < E && z + 1 >= LAG) wait_pushed(z + 1);
+        PLBM_PHASE(4)
         __syncthreads();  // psi plane pn visible; every warp is past collide(z-1)
+        PLBM_PHASE(5)
         flush_xcol(z - 1);
         issue_ring(pn + 1);  // its ring slot is no longer read by anyone
         cp_async_commit();
+        PLBM_PHASE(6)
         if constexpr (!EARLY) collide_head(z, f, rho, u0, u1, u2);
         collide_plane(z, f, rho, u0, u1, u2);
+        PLBM_PHASE(7)
+    }
+#ifdef PLBM_PHASES
+    if (d.probe && (tid & 31) == 0)
+        for (int k = 0; k < 8; ++k) atomicAdd(&d.probe[warp * 8 + k], ph_acc[k]);
+#endif
+#undef PLBM_PHASE
+    {
+        const unsigned m1 = __reduce_add_sync(0xffffffffu, negs);
+        const unsigned m2 = __reduce_add_sync(0xffffffffu, clamps);
+        const unsigned m3 = __reduce_add_sync(0xffffffffu, zero_rho);
+        const bool sus = __any_sync(0xffffffffu, suspect);
+        if ((tid & 31) == 0) {
+            if (m1) atomicAdd(&d.cnt[CNT_NEG], (unsigned long long)m1);
+            if (m2) atomicAdd(&d.cnt[CNT_CLAMP], (unsigned long long)m2);
+            if (m3) atomicAdd(&d.cnt[CNT_ZERO_RHO], (unsigned long long)m3);
+            if (sus) {
+                d.suspect[slot] = 1;
+                if (d.susp_any) atomicOr(&d.susp_any[iter & 1], 1u);
+            }
+        }
     }
     cp_async_wait<0>();
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -496,11 +538,13 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
         }
     };
     cluster_sync();  // every push into a peer has landed; the whole tile is written
+#ifndef PLBM_PHASES
     if (d.probe && tid == 0) {
         d.probe[3 * blockIdx.x] = smid();
         d.probe[3 * blockIdx.x + 1] = t_start;
         d.probe[3 * blockIdx.x + 2] = global_ns();
     }
+#endif
     if (!fused) return;
 
     // ---- fused face pass ---------------------------------------------------------

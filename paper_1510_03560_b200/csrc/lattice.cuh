@@ -232,15 +232,15 @@ __device__ __forceinline__ double pseudo_potential(double rho, double press, con
 constexpr uint32_t SCREEN_LO = 623u << 20;   // |hi word| of 2^-400
 constexpr uint32_t SCREEN_HI = 1423u << 20;  // |hi word| of 2^400
 struct Screen {
-    uint32_t mn = 0xffffffffu, mx = 0u;
-    __device__ __forceinline__ void add2(double a, double b) {
-        const uint32_t ha = uint32_t(__double2hiint(a)) & 0x7fffffffu;
-        const uint32_t hb = uint32_t(__double2hiint(b)) & 0x7fffffffu;
-        mn = __vimin3_u32(mn, ha, hb);
-        mx = __vimax3_u32(mx, ha, hb);
+    // (|hi| << 1) - (LO << 1) wraps for values below the range, so one unsigned
+    // max over the 19 values covers both ends: suspect iff max >= 2 (HI - LO)
+    uint32_t mx = 0u;
+    __device__ __forceinline__ static uint32_t key(double a) {
+        return (uint32_t(__double2hiint(a)) << 1) - (SCREEN_LO << 1);
     }
-    __device__ __forceinline__ void add(double a) { add2(a, a); }
-    __device__ __forceinline__ bool suspect() const { return mn < SCREEN_LO || mx >= SCREEN_HI; }
+    __device__ __forceinline__ void add2(double a, double b) { mx = __vimax3_u32(mx, key(a), key(b)); }
+    __device__ __forceinline__ void add(double a) { mx = max(mx, key(a)); }
+    __device__ __forceinline__ bool suspect() const { return mx >= ((SCREEN_HI - SCREEN_LO) << 1); }
 };
 __host__ __device__ inline bool screen_ok(double v) {
     if (v == 0.0) return true;

@@ -105,7 +105,7 @@ __device__ __forceinline__ void sc_sums(const double* pm, const double* p0, cons
 __device__ __forceinline__ void collide_bgk(double* f, double rho, double u0, double u1,
                                             double u2, double F0, double F1, double F2,
                                             double om, double* out, size_t dstride,
-                                            int& zero_rho, int& suspect, double* xc = nullptr,
+                                            unsigned& zero_rho, int& suspect, double* xc = nullptr,
                                             int xstride = 0) {
 
     const double uu = u0 * u0 + u1 * u1 + u2 * u2;
