@@ -62,6 +62,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=20.0)
     p.add_argument("--variant", type=int, default=0, help="fused-kernel variant (plbm_gpu.h)")
+    p.add_argument("--storage", choices=["ab", "aa"], default="ab",
+                   help="population storage: A-B double buffer or A-A in place (one buffer)")
     p.add_argument("--dist-backend", default="nccl", help="nccl (one GPU per rank) or gloo (tests)")
     return p.parse_args()
 
@@ -102,7 +104,8 @@ def bench_config(a, sc, name, pre):
     return {"workload": name, "domain": list(sc.domain), "tile_extent": sc.tile_extent,
             "components": sc.n_components, "mode": "static" if sc.mode == S.MODE_STATIC else "progressive",
             "threshold": sc.threshold, "pre_steps": pre, "simulated_devices": sc.devices,
-            "l2": "per-step working set >= 0.6 GB >> 126 MB L2 at every config (no flush needed)"}
+            "l2": "per-step working set >= 0.6 GB >> 126 MB L2 at every config (no flush needed)",
+            "storage": getattr(a, "storage", "ab")}
 
 
 def hbm_peak():
@@ -283,7 +286,7 @@ def main():
     from paper_1510_03560_b200 import capi
     from paper_1510_03560_b200.dist import DistStepper
     C = sc.n_components
-    eng = capi.gpu_engine(sc, device=gpu, rank=rank, world=world)
+    eng = capi.gpu_engine(sc, device=gpu, rank=rank, world=world, storage=a.storage)
     eng.set_kernel_variant(a.variant)
     stream = torch.cuda.ExternalStream(eng.stream(), device=torch.device("cuda", gpu))
     if world > 1:

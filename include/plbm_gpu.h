@@ -30,6 +30,23 @@ extern "C" {
  * (no host field buffers).  `device` is the CUDA ordinal.  NULL on failure. */
 void* plbm_gpu_create(const plbm_scenario_desc* desc, int device, plbm_error* err);
 
+/* Creation options (zero-initialise; unknown fields must stay 0).
+ *   storage: PLBM_STORAGE_AB — two population buffers, pull from one, store
+ *            the next state into the other (the reference's f[2] double
+ *            buffer + swap, tile.hpp:39, engine.cpp:482-490);
+ *            PLBM_STORAGE_AA — one buffer updated in place with the A-A
+ *            pattern (kernels.cuh AA_*): half the population
+ *            footprint, bit-identical results; tile_extent <= 32.  After an
+ *            EngineError the fields of an A-A engine are not rolled back.   */
+enum { PLBM_STORAGE_AB = 0, PLBM_STORAGE_AA = 1 };
+typedef struct plbm_gpu_options {
+    int32_t storage;
+    int32_t reserved[7];
+} plbm_gpu_options;
+/* plbm_gpu_create / plbm_gpu_create_dist with options (opt may be NULL).    */
+void* plbm_gpu_create_ex(const plbm_scenario_desc* desc, int device, int rank, int world,
+                         const plbm_gpu_options* opt, plbm_error* err);
+
 /* Engine::step() n times (engine.cpp:537-563).  Returns 0, or err->code on an
  * EngineError (NaN / EOS pole: iteration and cell_updates do not advance).  */
 int plbm_gpu_step(void* h, int n, plbm_error* err);

@@ -189,29 +189,37 @@ class KernelStats(C.Structure):
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
 
 
+class Options(C.Structure):
+    """plbm_gpu_options (include/plbm_gpu.h)."""
+    _fields_ = [("storage", C.c_int32), ("reserved", C.c_int32 * 7)]
+
+
+STORAGE = {"ab": 0, "aa": 1}  # PLBM_STORAGE_AB / PLBM_STORAGE_AA
+
+
 class GpuEngine(StepEngine):
     """The product engine (libplbm_gpu.so).  There is no fallback: a missing
     library or CUDA device raises.  rank/world > 1 builds one rank of a
     multi-GPU run (include/plbm_gpu.h, "multi-GPU")."""
 
     def __init__(self, sc: Scenario, device: int = 0, capture: bool = False,
-                 rank: int = 0, world: int = 1):
-        self.rank, self.world = rank, world
-        if world == 1:
-            super().__init__(sc, GPU_LIB, "plbm_gpu", device)
-        else:
-            self.scenario, self.prefix = sc, "plbm_gpu"
-            self.lib = load(GPU_LIB, "plbm_gpu")
-            self.lib.plbm_gpu_create_dist.restype = C.c_void_p
-            self.lib.plbm_gpu_create_dist.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int,
-                                                      C.POINTER(Error)]
-            self._c = sc.to_c()
-            err = Error()
-            self._h = self.lib.plbm_gpu_create_dist(C.cast(self._c.ptr(), C.c_void_p), device,
-                                                    rank, world, C.byref(err))
-            if not self._h:
-                raise ValueError(f"plbm_gpu_create_dist failed: {err.message.decode()}")
-            self.ncell = sc.tile_extent ** 3
+                 rank: int = 0, world: int = 1, storage: str = "ab"):
+        if storage not in STORAGE:
+            raise ValueError(f"storage must be one of {sorted(STORAGE)}")
+        self.rank, self.world, self.storage = rank, world, storage
+        self.scenario, self.prefix = sc, "plbm_gpu"
+        self.lib = load(GPU_LIB, "plbm_gpu")
+        self.lib.plbm_gpu_create_ex.restype = C.c_void_p
+        self.lib.plbm_gpu_create_ex.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                                C.POINTER(Options), C.POINTER(Error)]
+        self._c = sc.to_c()
+        err = Error()
+        opt = Options(storage=STORAGE[storage])
+        self._h = self.lib.plbm_gpu_create_ex(C.cast(self._c.ptr(), C.c_void_p), device, rank, world,
+                                              C.byref(opt), C.byref(err))
+        if not self._h:
+            raise ValueError(f"plbm_gpu_create_ex failed: {err.message.decode()}")
+        self.ncell = sc.tile_extent ** 3
         lib = self.lib
         P = C.c_void_p
         for name, res, args in [
@@ -351,5 +359,6 @@ class GpuEngine(StepEngine):
 
 
 def gpu_engine(sc: Scenario, device: int = 0, capture: bool = False, rank: int = 0,
-               world: int = 1) -> GpuEngine:
-    return GpuEngine(sc, device, capture, rank, world)
+               world: int = 1, storage: str = "ab") -> GpuEngine:
+    """storage "ab" (two population buffers) or "aa" (one buffer, A-A in place)."""
+    return GpuEngine(sc, device, capture, rank, world, storage)

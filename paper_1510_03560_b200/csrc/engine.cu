@@ -105,15 +105,16 @@ struct Kernels {
     MainFn main_pc_late;  // variant 21: the collision head after the cluster wait
     MainFn main_pc_mem;   // variant 24 (PLBM_PROBES builds only): memory-only probe (E = 32, C = 2)
     MainFn main_pc2;    // variant 22: psi computed two planes ahead
+    MainFn main_aa[2];  // A-A storage: AA_LOCAL / AA_NEIGH steps (k_main_pc, else the whole-tile plain kernel)
     void (*face)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
     void (*face_v[2])(Dev, const int*, int, int, long, unsigned, cudaStream_t);
     void (*p5)(Dev, const int*, int, long, unsigned, cudaStream_t);
-    void (*readback)(Dev, int, int, int, double*, cudaStream_t);
-    void (*gather)(Dev, const int*, int, int, int, int, double*, int, int, cudaStream_t);
+    void (*readback)(Dev, int, int, int, double*, int, cudaStream_t);
+    void (*gather)(Dev, const int*, int, int, int, int, double*, int, int, int, cudaStream_t);
     int nt;
 };
 
-template <int E, int C, int LAG, int NT = 256, bool EARLY = true, bool MEMONLY = false>
+template <int E, int C, int LAG, int NT = 256, bool EARLY = true, bool MEMONLY = false, int AA = AA_OFF>
 void launch_pc(Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
     using T = PcCfg<E, C, LAG, NT>;
     cudaLaunchConfig_t cfg = {};
@@ -128,7 +129,7 @@ void launch_pc(Dev d, const int* act, int src, int wu, long it, unsigned ntiles,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_main_pc<E, C, LAG, NT, EARLY, MEMONLY>, d, act, src, wu, it);
+    cudaLaunchKernelEx(&cfg, k_main_pc<E, C, LAG, NT, EARLY, MEMONLY, AA>, d, act, src, wu, it);
 }
 
 template <int E, int C, bool NOPSI>
@@ -149,6 +150,7 @@ Kernels make_kernels() {
         k_main<E, C, BZ, NT, NOPSI, YB><<<ntiles * (E / BZ) * (E / YB), NT, SMEM_PLAIN, s>>>(d, act, src, wu, it);
     };
     k.main_pc = k.main_pc2 = k.main_pc_late = k.main_pc_mem = nullptr;
+    k.main_aa[0] = k.main_aa[1] = nullptr;
     if constexpr (!NOPSI && (E == 16 || E == 32)) {
         auto setup = [](auto fn, int smem, int cl) {
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -168,6 +170,29 @@ Kernels make_kernels() {
             setup(k_main_pc<E, C, 2>, PcCfg<E, C, 2>::SMEM, PcCfg<E, C, 2>::CL);
             k.main_pc2 = launch_pc<E, C, 2>;
         }
+#ifndef PLBM_NO_AA
+        setup(k_main_pc<E, C, 1, 256, true, false, AA_LOCAL>, PcCfg<E, C, 1>::SMEM, PcCfg<E, C, 1>::CL);
+        setup(k_main_pc<E, C, 1, 256, true, false, AA_NEIGH>, PcCfg<E, C, 1>::SMEM, PcCfg<E, C, 1>::CL);
+        k.main_aa[0] = launch_pc<E, C, 1, 256, true, false, AA_LOCAL>;
+        k.main_aa[1] = launch_pc<E, C, 1, 256, true, false, AA_NEIGH>;
+#endif
+    } else if constexpr (E <= 32) {
+#ifndef PLBM_NO_AA
+        // A-A with the plain kernel: one CTA per tile (no recomputed halos)
+        constexpr size_t SMEM_AA = NOPSI ? 0 : size_t(3) * C * G * G * sizeof(double);
+        if (SMEM_AA > 0) {
+            cudaFuncSetAttribute(k_main<E, C, E, NT, NOPSI, E, AA_LOCAL>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_AA));
+            cudaFuncSetAttribute(k_main<E, C, E, NT, NOPSI, E, AA_NEIGH>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_AA));
+        }
+        k.main_aa[0] = [](Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
+            k_main<E, C, E, NT, NOPSI, E, AA_LOCAL><<<ntiles, NT, SMEM_AA, s>>>(d, act, src, wu, it);
+        };
+        k.main_aa[1] = [](Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
+            k_main<E, C, E, NT, NOPSI, E, AA_NEIGH><<<ntiles, NT, SMEM_AA, s>>>(d, act, src, wu, it);
+        };
+#endif
     }
     // k_face at 4 CTAs/SM, one item in flight per thread (64 registers),
     // measured faster than 2 CTAs/SM with a one-item prefetch (PLBM_FACE_VARIANT=1)
@@ -181,12 +206,13 @@ Kernels make_kernels() {
     k.p5 = [](Dev d, const int* act, int src, long it, unsigned ntiles, cudaStream_t s) {
         k_p5<E, C, 256><<<ntiles, 256, 0, s>>>(d, act, src, it);
     };
-    k.readback = [](Dev d, int slot, int c, int src, double* out, cudaStream_t s) {
-        k_readback<E><<<(E * E * E + 255) / 256, 256, 0, s>>>(d, slot, c, src, out);
+    k.readback = [](Dev d, int slot, int c, int src, double* out, int skind, cudaStream_t s) {
+        k_readback<E><<<(E * E * E + 255) / 256, 256, 0, s>>>(d, slot, c, src, out, skind);
     };
     k.gather = [](Dev d, const int* act, int ntiles, int kind, int c, int src, double* grid, int D0, int D1,
-                  cudaStream_t s) {
-        k_gather<E><<<dim3((E * E * E + 255) / 256, ntiles), 256, 0, s>>>(d, act, kind, c, src, grid, D0, D1);
+                  int skind, cudaStream_t s) {
+        k_gather<E><<<dim3((E * E * E + 255) / 256, ntiles), 256, 0, s>>>(d, act, kind, c, src, grid, D0, D1,
+                                                                          skind);
     };
     return k;
 }
@@ -249,7 +275,8 @@ struct LogRow {
 
 class Engine {
   public:
-    Engine(const plbm_scenario_desc& d, int device, int rank, int world) {
+    Engine(const plbm_scenario_desc& d, int device, int rank, int world, int storage = PLBM_STORAGE_AB) {
+        aa_ = storage == PLBM_STORAGE_AA;
         init(d, device, rank, world);
     }
     ~Engine() { release(); }
@@ -273,6 +300,7 @@ class Engine {
     int poke_f(const int32_t* coords, int comp, int i, const int32_t* local, double v);
     void set_profiling(bool on) { profiling_ = on; }
     int set_variant(int v) {
+        if (aa_) return v == 0 ? 0 : -1;  // A-A storage has one kernel pair
         const int base = v % 100;
         const bool ok = v >= 0 && v < 400 && (base == 0 || base == 1 || base == 21 || base == 22
 #ifdef PLBM_PROBES
@@ -367,7 +395,9 @@ class Engine {
     std::vector<bool> peer_opened_;
     double** d_slot_f_[2]{};
     double** d_slot_pf_[2]{};
-    int* d_route_[2]{};
+    int* d_route_[3]{};
+    bool aa_ = false;  // A-A in-place population storage (one buffer)
+    int nbuf_ = 2;
     int* d_lidx_ = nullptr;
     uint32_t* d_solid_ = nullptr;
     uint8_t* d_has_solid_ = nullptr;
@@ -581,7 +611,9 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
         lcap_ = std::min(int(n_tiles), owners_per_rank * tiles_per_owner);
         if (world_ == 1) lcap_ = int(n_tiles);
     }
-    per_slot_ = size_t(C_) * Q * E3_ + size_t(C_) * XN * E2_;  // f block + xcol side buffer
+    // f block + xcol side buffer (A-B); A-A keeps one f block and no xcol
+    per_slot_ = size_t(C_) * Q * E3_ + (aa_ ? 0 : size_t(C_) * XN * E2_);
+    nbuf_ = aa_ ? 1 : 2;
     per_pf_ = size_t(C_) * 6 * E2_;
     const int nslot = cap_ + 1;
     const int G = E_ + 2;
@@ -591,14 +623,15 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     CK(cudaSetDevice(dev_));
     CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     K_ = pick_kernels(E_, C_, nopsi_);
-    d_pool_f_ = dmalloc<double>(2 * per_slot_ * size_t(lcap_ + 1));
+    if (aa_ && !K_.main_aa[0])
+        throw std::invalid_argument("A-A storage needs tile_extent <= 32 (one CTA or cluster per tile)");
+    d_pool_f_ = dmalloc<double>(size_t(nbuf_) * per_slot_ * size_t(lcap_ + 1));
     d_pool_pf_ = dmalloc<double>(2 * per_pf_ * size_t(lcap_ + 1));
     for (int b = 0; b < 2; ++b) {
         d_slot_f_[b] = dmalloc<double*>(nslot);
         d_slot_pf_[b] = dmalloc<double*>(nslot);
     }
-    d_route_[0] = dmalloc<int>(size_t(nslot) * 18);
-    d_route_[1] = dmalloc<int>(size_t(nslot) * 18);
+    for (int r = 0; r < 3; ++r) d_route_[r] = dmalloc<int>(size_t(nslot) * 18);
     d_lidx_ = dmalloc<int>(nslot);
     d_solid_ = dmalloc<uint32_t>(size_t(nslot) * solid_words_);
     d_has_solid_ = dmalloc<uint8_t>(nslot);
@@ -670,7 +703,7 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
         for (int c = 0; c < C_; ++c)
             for (int i = 0; i < Q; ++i) {
                 std::fill_n(amb.begin() + (size_t(c) * Q + i) * E3_, E3_, p.comp[c].feq_amb[i]);
-                for (int cls = 0; cls < 4; ++cls)
+                for (int cls = 0; cls < 4 && !aa_; ++cls)
                     if (xslot_(cls, i) >= 0)
                         std::fill_n(amb.begin() + size_t(C_) * Q * E3_ + (size_t(c) * XN + xslot_(cls, i)) * E2_,
                                     E2_, p.comp[c].feq_amb[i]);
@@ -679,8 +712,9 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
         for (int c = 0; c < C_; ++c)
             std::fill_n(pf.begin() + size_t(c) * 6 * E2_, 6 * E2_, p.comp[c].psi_amb);
         for (int b = 0; b < 2; ++b) {
-            CK(cudaMemcpy(d_pool_f_ + (size_t(b) * (lcap_ + 1) + lcap_) * per_slot_, amb.data(),
-                          per_slot_ * sizeof(double), cudaMemcpyHostToDevice));
+            if (b < nbuf_)
+                CK(cudaMemcpy(d_pool_f_ + (size_t(b) * (lcap_ + 1) + lcap_) * per_slot_, amb.data(),
+                              per_slot_ * sizeof(double), cudaMemcpyHostToDevice));
             CK(cudaMemcpy(d_pool_pf_ + (size_t(b) * (lcap_ + 1) + lcap_) * per_pf_, pf.data(),
                           per_pf_ * sizeof(double), cudaMemcpyHostToDevice));
         }
@@ -694,8 +728,8 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
         d_.slot_f[b] = d_slot_f_[b];
         d_.slot_pf[b] = d_slot_pf_[b];
     }
-    d_.route[0] = d_route_[0];
-    d_.route[1] = d_route_[1];
+    for (int r = 0; r < 3; ++r) d_.route[r] = d_route_[r];
+    d_.aa = aa_ ? 1 : 0;
     d_.lidx = d_lidx_;
     d_.solid = d_solid_;
     d_.has_solid = d_has_solid_;
@@ -833,7 +867,7 @@ void Engine::release() {
             cudaIpcCloseMemHandle(peer_pf_[r]);
         }
     void* ptrs[] = {d_pool_f_, d_pool_pf_, d_slot_f_[0], d_slot_f_[1], d_slot_pf_[0], d_slot_pf_[1],
-                    d_route_[0], d_route_[1], d_lidx_, d_solid_, d_has_solid_, d_mode_, d_coords_,
+                    d_route_[0], d_route_[1], d_route_[2], d_lidx_, d_solid_, d_has_solid_, d_mode_, d_coords_,
                     d_u_face_, d_trig_, d_capture_, d_cnt_, d_err_, d_active_, d_scratch_slots_,
                     d_readback_, d_dep_cnt_, d_dep_need_, d_geo_, d_bmask_, d_omask_, d_halt_, d_pokes_,
                     d_gslot_, d_cand_, d_nactive_, d_next_slot_, d_next_local_, d_owner_, d_geomdev_, d_p2p_,
@@ -1082,7 +1116,7 @@ void Engine::upload_pointers() {
     auto fill = [&](int s, int r, int local) {
         for (int b = 0; b < 2; ++b) {
             if (!peer_f_[r]) continue;
-            f[b][s] = peer_f_[r] + (size_t(b) * (lcap_ + 1) + local) * per_slot_;
+            f[b][s] = peer_f_[r] + (size_t(b % nbuf_) * (lcap_ + 1) + local) * per_slot_;
             pf[b][s] = peer_pf_[r] + (size_t(b) * (lcap_ + 1) + local) * per_pf_;
         }
     };
@@ -1159,6 +1193,13 @@ void Engine::upload_map(const std::vector<int>& new_slots, bool initial) {
             need[s] = n;
         }
         CK(cudaMemcpyAsync(d_geo_, geo.data(), geo.size() * sizeof(int), cudaMemcpyHostToDevice, stream_));
+        // ROUTE_W (A-A stores): the geometric neighbour in the new map, or ambient
+        std::vector<int> rw(geo);
+        for (int& v : rw)
+            if (v < 0) v = amb_;
+        CK(cudaMemcpyAsync(d_route_[ROUTE_W], rw.data(), rw.size() * sizeof(int), cudaMemcpyHostToDevice,
+                           stream_));
+        CK(cudaStreamSynchronize(stream_));
         // speculative queue: which trigger bits need the host (births) and
         // which only count as suppressed expansions (out of bounds)
         std::vector<uint8_t> bm(nslot, 0), om(nslot, 0);
@@ -1302,6 +1343,8 @@ ExpandDev Engine::expand_dev() const {
     x.solid = d_solid_;
     x.lidx = d_lidx_;
     x.route_psi = d_route_[ROUTE_PSI];
+    x.route_w = d_route_[ROUTE_W];
+    x.nbuf = nbuf_;
     x.bmask = d_bmask_;
     x.omask = d_omask_;
     for (int b = 0; b < 2; ++b) {
@@ -1370,6 +1413,7 @@ void Engine::launch_main(long iter) {
     if (K_.main_pc_late && variant_ == 21) fn = K_.main_pc_late;
     if (K_.main_pc_mem && variant_ == 24) fn = K_.main_pc_mem;  // probe: not a correct step
     if (K_.main_pc2 && variant_ == 22) fn = K_.main_pc2;
+    if (aa_) fn = K_.main_aa[aa_kind(1, iter) - 1];
     face_fused_ = fusable(fn) && fuse_;
     // the pc kernels write the xcol side buffers the face pass reads
     d_.xcol_ok = (fn == K_.main_pc || fn == K_.main_pc2 || fn == K_.main_pc_late || fn == K_.main_pc_mem) && !no_xcol_;
@@ -1878,7 +1922,7 @@ int Engine::read_tile(const int32_t* cc, int comp, int field, double* out) {
         CK(cudaStreamSynchronize(stream_));
         return 0;
     }
-    K_.readback(d_, s, comp, cur_, d_readback_, stream_);
+    K_.readback(d_, s, comp, cur_, d_readback_, aa_kind(d_.aa, iteration_ + 1), stream_);
     CK(cudaGetLastError());
     ++stats_.kernels_launched;
     if (field == PLBM_FIELD_F) {
@@ -1908,7 +1952,8 @@ int Engine::gather_field(const char* field, int comp, double* grid) {
     CK(cudaMallocAsync(&d_grid, n * sizeof(double), stream_));
     k_fill<<<148 * 8, 256, 0, stream_>>>(d_grid, n, fill);
     if (!active_.empty())
-        K_.gather(d_, d_active_, int(active_.size()), kind, comp, cur_, d_grid, dom_[0], dom_[1], stream_);
+        K_.gather(d_, d_active_, int(active_.size()), kind, comp, cur_, d_grid, dom_[0], dom_[1],
+                  aa_kind(d_.aa, iteration_ + 1), stream_);
     CK(cudaGetLastError());
     stats_.kernels_launched += 2;
     CK(cudaMemcpyAsync(grid, d_grid, n * sizeof(double), cudaMemcpyDeviceToHost, stream_));
@@ -2033,6 +2078,22 @@ plbm::Engine* EG(void* h) { return static_cast<plbm::Engine*>(h); }
 }  // namespace
 
 extern "C" {
+
+void* plbm_gpu_create_ex(const plbm_scenario_desc* desc, int device, int rank, int world,
+                         const plbm_gpu_options* opt, plbm_error* err) {
+    fill_err(err, 0, "");
+    try {
+        const int storage = opt ? opt->storage : PLBM_STORAGE_AB;
+        if (storage != PLBM_STORAGE_AB && storage != PLBM_STORAGE_AA)
+            throw std::invalid_argument("unknown storage kind");
+        return new plbm::Engine(*desc, device, rank, world, storage);
+    } catch (const plbm::CudaError& e) {
+        fill_err(err, 3, e.what());
+    } catch (const std::exception& e) {
+        fill_err(err, 2, e.what());
+    }
+    return nullptr;
+}
 
 void* plbm_gpu_create_dist(const plbm_scenario_desc* desc, int device, int rank, int world,
                            plbm_error* err) {

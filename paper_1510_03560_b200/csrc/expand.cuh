@@ -53,6 +53,8 @@ struct ExpandDev {
     uint32_t* solid;              // [slot][solid_words]
     int* lidx;                    // [slot]
     int* route_psi;               // [slot][18]
+    int* route_w;                 // [slot][18] geometric neighbours (A-A stores)
+    int nbuf;                     // population buffers (2 = A-B, 1 = A-A)
     uint8_t* bmask;               // [slot]
     uint8_t* omask;               // [slot]
     double** slot_f[2];           // pointer tables (local pool)
@@ -294,7 +296,7 @@ __global__ void __launch_bounds__(1024) k_check_expand(Dev d, ExpandDev x, long 
             x.lidx[b.slot] = local;
             b.local = local;
             for (int bb = 0; bb < 2; ++bb) {
-                x.slot_f[bb][b.slot] = x.pool_f + (size_t(bb) * (x.lcap + 1) + local) * x.per_slot;
+                x.slot_f[bb][b.slot] = x.pool_f + (size_t(bb % x.nbuf) * (x.lcap + 1) + local) * x.per_slot;
                 x.slot_pf[bb][b.slot] = x.pool_pf + (size_t(bb) * (x.lcap + 1) + local) * x.per_pf;
             }
             add_cells += (unsigned long long)b.fluid;
@@ -362,6 +364,19 @@ __global__ void __launch_bounds__(1024) k_check_expand(Dev d, ExpandDev x, long 
                         if (wrap(q2) && x.gslot[lin(q2)] >= 0) r = x.gslot[lin(q2)];
                     }
                     out[edge_class(a, b, da, db)] = r;
+                }
+        // geometric neighbours of the new map (A-A store targets)
+        int* ow = x.route_w + size_t(s) * 18;
+        for (int f = 0; f < 6; ++f) ow[f] = out[f];
+        for (int p = 0; p < 3; ++p)
+            for (int da = -1; da <= 1; da += 2)
+                for (int db = -1; db <= 1; db += 2) {
+                    const int a = pairs[p][0], b = pairs[p][1];
+                    int q[3] = {c[0], c[1], c[2]};
+                    q[a] += da;
+                    q[b] += db;
+                    const int ns = wrap(q) ? x.gslot[lin(q)] : -1;
+                    ow[edge_class(a, b, da, db)] = ns >= 0 ? ns : x.amb;
                 }
     }
     // modeled step bytes (engine.cu recompute_step_bytes)

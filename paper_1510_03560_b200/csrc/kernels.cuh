@@ -36,7 +36,25 @@
 namespace plbm {
 
 enum TileMode : uint8_t { MODE_PULL = 0, MODE_GEN_SEEDED = 1, MODE_GEN_AMBIENT = 2 };
-enum { ROUTE_PULL = 0, ROUTE_PSI = 1 };
+enum { ROUTE_PULL = 0, ROUTE_PSI = 1, ROUTE_W = 2 };
+// Population storage.  A-B (AA_OFF): two buffers, step k pulls f_post^(k-1)
+// from one and stores f_post^(k) into the other.  A-A (SURVEY §8(f)3,
+// PAPER.md:85): ONE buffer updated in place, the step kinds alternating
+//   AA_LOCAL (odd steps):  cell x reads (x, i) for every i and stores
+//                          f_post(x)[i] at (x, opp i);
+//   AA_NEIGH (even steps): cell x reads f_post(x - e_i)[i] at (x - e_i, opp i)
+//                          (bounce-back: f_post(x)[opp i] at (x, i)) and stores
+//                          f_post(x)[i] at (x + e_i, i), or at (x, opp i) when
+//                          x + e_i is solid.
+// Every location (cell, dir) is read and written by exactly one cell in a
+// step, so no step needs a second buffer.  Frontier rules are the A-B ones:
+// a source in an absent tile (ROUTE_PULL -> ambient) reads feq_amb[i]; a store
+// into an absent geometric neighbour (ROUTE_W -> ambient) is dropped (nobody
+// reads it: a tile born later starts from feq_amb, GEN_AMBIENT).
+enum { AA_OFF = 0, AA_LOCAL = 1, AA_NEIGH = 2 };
+__host__ __device__ inline int aa_kind(int aa, long iter) {
+    return aa ? ((iter & 1) ? AA_LOCAL : AA_NEIGH) : AA_OFF;
+}
 enum { ERR_NONE = 0, ERR_P1_NAN = 1, ERR_P1_POLE = 2, ERR_P5_NAN = 3 };
 enum { CNT_NEG = 0, CNT_CLAMP = 1, CNT_ZERO_RHO = 2, CNT_SUPP = 3, CNT_N = 4 };
 
@@ -65,7 +83,8 @@ struct Params {
 struct Dev {
     double* const* slot_f[2];   // [slot] -> f block in buffer b (local or peer)
     double* const* slot_pf[2];  // [slot] -> psi faces for step parity p
-    const int* route[2];        // [slot][18]
+    const int* route[3];        // [slot][18]: ROUTE_PULL, ROUTE_PSI, ROUTE_W (geometric, A-A stores)
+    int aa;                     // 1: A-A in-place storage (slot_f[0] == slot_f[1])
     const int* lidx;            // [slot] -> local index (u_face / capture), -1 remote
     const uint32_t* solid;      // [slot][solid_words]
     const uint8_t* has_solid;   // [slot]
@@ -251,29 +270,85 @@ __device__ __forceinline__ void load_routes(RouteTab& rt, const int* routes, int
 // Pull of one cell's 19 populations of component c from f_post (the
 // reference's P4a ghost fill + stream_pull, proj/src/kernels.cpp:5-30):
 //   f_in[i](x) = solid(x - e_i) ? f_post(x)[opp i] : f_post(route(x - e_i))[i]
-// `op(i, ptr)` receives each population's source address.
-template <int E, class Op>
+// `op(i, ptr)` receives each population's source address.  AA selects where
+// the A-A storage kinds keep those values (see AA_LOCAL / AA_NEIGH above).
+template <int E, int AA = AA_OFF, class Op>
 __device__ __forceinline__ void pull_addr(const RouteTab& rt, int c, bool hs, const uint32_t* sb,
                                           int x, int y, int z, Op&& op) {
     constexpr int E3 = E * E * E;
     const size_t cs = size_t(Q) * E3;
+    const int own = (z * E + y) * E + x;
 #pragma unroll
     for (int i = 0; i < Q; ++i) {
         const int sx = x - ex_(i), sy = y - ey_(i), sz = z - ez_(i);
         const int ox = sx < 0 ? -1 : (sx >= E ? 1 : 0);
         const int oy = sy < 0 ? -1 : (sy >= E ? 1 : 0);
         const int oz = sz < 0 ? -1 : (sz >= E ? 1 : 0);
-        const double* base = rt.p[(ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)];
+        const int pat = (ox + 1) + 3 * (oy + 1) + 9 * (oz + 1);
+        const double* base = rt.p[pat];
         int cell = ((sz & (E - 1)) * E + (sy & (E - 1))) * E + (sx & (E - 1));
         int dir = i;
         if (hs && solid_at<E>(sb, sx, sy, sz)) {
             base = rt.p[13];
-            cell = (z * E + y) * E + x;
-            dir = opp_(i);
+            cell = own;
+            dir = AA == AA_OFF ? opp_(i) : i;
+        } else if constexpr (AA != AA_OFF) {
+            if (rt.s[pat] == P.amb_slot) {
+                cell = own;  // feq_amb[i], any cell of the ambient slot
+            } else if (AA == AA_LOCAL) {
+                base = rt.p[13];
+                cell = own;
+            } else {
+                dir = opp_(i);
+            }
         }
         op(i, base + c * cs + size_t(dir) * E3 + cell);
     }
 }
+
+// A-A store address of f_post(x)[i] on an AA_NEIGH step: (x + e_i, i) in the
+// geometric neighbour (rw = ROUTE_W table over the same buffer), (x, opp i)
+// when x + e_i is solid, nullptr when the neighbour tile is absent.
+template <int E>
+__device__ __forceinline__ double* aa_push_addr(const RouteTab& rw, int c, bool hs, const uint32_t* sb,
+                                                int x, int y, int z, int i) {
+    constexpr int E3 = E * E * E;
+    const size_t cs = size_t(Q) * E3;
+    const int tx = x + ex_(i), ty = y + ey_(i), tz = z + ez_(i);
+    if (hs && solid_at<E>(sb, tx, ty, tz))
+        return const_cast<double*>(rw.p[13]) + c * cs + size_t(opp_(i)) * E3 + (z * E + y) * E + x;
+    const int ox = tx < 0 ? -1 : (tx >= E ? 1 : 0);
+    const int oy = ty < 0 ? -1 : (ty >= E ? 1 : 0);
+    const int oz = tz < 0 ? -1 : (tz >= E ? 1 : 0);
+    const int pat = (ox + 1) + 3 * (oy + 1) + 9 * (oz + 1);
+    if (rw.s[pat] == P.amb_slot) return nullptr;
+    return const_cast<double*>(rw.p[pat]) + c * cs + size_t(i) * E3 +
+           ((tz & (E - 1)) * E + (ty & (E - 1))) * E + (tx & (E - 1));
+}
+
+// Store functor of one cell's 19 post-collision populations for a storage
+// kind: A-B -> (x, i) of the output buffer; AA_LOCAL -> (x, opp i);
+// AA_NEIGH -> aa_push_addr.  `own` = the cell's address for direction 0 in
+// this component's block.
+template <int E, int AA>
+struct StoreF {
+    double* own;
+    const RouteTab* rw;
+    int c, x, y, z;
+    bool hs;
+    const uint32_t* sb;
+    __device__ __forceinline__ void operator()(int i, double v) const {
+        constexpr int E3 = E * E * E;
+        if constexpr (AA == AA_OFF) {
+            own[size_t(i) * E3] = v;
+        } else if constexpr (AA == AA_LOCAL) {
+            own[size_t(opp_(i)) * E3] = v;
+        } else {
+            double* p = aa_push_addr<E>(*rw, c, hs, sb, x, y, z, i);
+            if (p) *p = v;
+        }
+    }
+};
 
 // Fast pull for a cell whose y and z neighbours all lie inside the tile and
 // whose tile has no solid cell (warp-uniform in callers: one warp = one x row).
@@ -329,10 +404,18 @@ __device__ __forceinline__ void pull_addr_fast_yedge(const RouteTab& rt, int c, 
     }
 }
 
-template <int E>
+template <int E, int AA = AA_OFF>
 __device__ __forceinline__ void pull_cell(const RouteTab& rt, int c, bool hs, const uint32_t* sb,
                                           int x, int y, int z, double* f) {
-    pull_addr<E>(rt, c, hs, sb, x, y, z, [&](int i, const double* p) { f[i] = __ldg(p); });
+    pull_addr<E, AA>(rt, c, hs, sb, x, y, z, [&](int i, const double* p) { f[i] = __ldg(p); });
+}
+// The same with the storage kind chosen at run time (read-back, checks).
+template <int E>
+__device__ __forceinline__ void pull_cell_k(int kind, const RouteTab& rt, int c, bool hs,
+                                            const uint32_t* sb, int x, int y, int z, double* f) {
+    if (kind == AA_LOCAL) pull_cell<E, AA_LOCAL>(rt, c, hs, sb, x, y, z, f);
+    else if (kind == AA_NEIGH) pull_cell<E, AA_NEIGH>(rt, c, hs, sb, x, y, z, f);
+    else pull_cell<E>(rt, c, hs, sb, x, y, z, f);
 }
 template <int E>
 __device__ __forceinline__ void pull_cell_fast(const RouteTab& rt, int c, int x, int y, int z,
@@ -341,11 +424,11 @@ __device__ __forceinline__ void pull_cell_fast(const RouteTab& rt, int c, int x,
 }
 
 // f_in for any mode (u is only meaningful for GEN modes).
-template <int E>
+template <int E, int AA = AA_OFF>
 __device__ __forceinline__ void fin_cell(const RouteTab& rt, int mode, const int* tc, int c,
                                          bool hs, const uint32_t* sb, int x, int y, int z,
                                          double* f, double& u0, double& u1, double& u2) {
-    if (mode == MODE_PULL) pull_cell<E>(rt, c, hs, sb, x, y, z, f);
+    if (mode == MODE_PULL) pull_cell<E, AA>(rt, c, hs, sb, x, y, z, f);
     else gen_fin<E>(mode, c, tc, x, y, z, f, u0, u1, u2);
 }
 
@@ -386,10 +469,13 @@ __device__ __forceinline__ double psi_ghost(const RouteTab& rt, int c, bool hs, 
 // recomputed) in a shared ring, and every population pulled twice (psi pass +
 // collide).  Used for E = 8, E = 64 (YB = 16: the whole-plane ring would not
 // fit shared memory) and psi-free scenarios (NOPSI: no pseudo-potential
-// stencil at all — a single pull-collide pass per cell).
-template <int E, int C, int BZ, int NT, bool NOPSI, int YB = E>
+// stencil at all — a single pull-collide pass per cell).  A-A storage (AA !=
+// AA_OFF) needs the whole tile in one CTA (BZ = YB = E): recomputed halo
+// planes / rows would read cells another CTA updates in place.
+template <int E, int C, int BZ, int NT, bool NOPSI, int YB = E, int AA = AA_OFF>
 __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ active, int src_buf,
                                              int write_uface, long iter) {
+    static_assert(AA == AA_OFF || (BZ == E && YB == E), "A-A needs one CTA per tile");
     if (halted(d)) return;
     constexpr int G = E + 2;
     constexpr int GG = G * (YB + 2);  // one psi plane of the chunk incl. its halo
@@ -401,7 +487,7 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
     constexpr int PPT = (E * (YB + 2) + NT - 1) / NT;    // psi positions per thread (x inside)
     extern __shared__ double smem[];
     double* psi = smem;  // [3][C][GG] ring of planes (unused when NOPSI)
-    __shared__ RouteTab rt_pull, rt_psi;
+    __shared__ RouteTab rt_pull, rt_psi, rt_w;
     __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
     __shared__ int s_tc[3];
 
@@ -417,6 +503,7 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
     const int li = d.lidx[slot];
     load_routes(rt_pull, d.route[ROUTE_PULL] + size_t(slot) * 18, slot, amb, d.slot_f[src_buf]);
     load_routes(rt_psi, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, amb, d.slot_pf[par], d.mode);
+    if constexpr (AA == AA_NEIGH) load_routes(rt_w, d.route[ROUTE_W] + size_t(slot) * 18, slot, amb, d.slot_f[0]);
     if (threadIdx.x < 3) s_tc[threadIdx.x] = d.coords[slot * 3 + threadIdx.x];
     if (hs)
         for (int k = threadIdx.x; k < d.solid_words; k += NT)
@@ -444,7 +531,7 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
                     v = psi_ghost<E>(rt_psi, c, hs, s_solid, x, y, pz);
                 } else if (!(hs && solid_at<E>(s_solid, x, y, pz))) {
                     double f[Q], u0, u1, u2;
-                    fin_cell<E>(rt_pull, mode, s_tc, c, hs, s_solid, x, y, pz, f, u0, u1, u2);
+                    fin_cell<E, AA>(rt_pull, mode, s_tc, c, hs, s_solid, x, y, pz, f, u0, u1, u2);
                     apply_pokes<E>(d, slot, c, x, y, pz, f);
                     double rho = 0.0;
 #pragma unroll
@@ -507,7 +594,7 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
             for (int c = 0; c < C; ++c) {
                 double f[Q];
                 double u0 = 0.0, u1 = 0.0, u2 = 0.0, rho;
-                fin_cell<E>(rt_pull, mode, s_tc, c, hs, s_solid, x, y, z, f, u0, u1, u2);
+                fin_cell<E, AA>(rt_pull, mode, s_tc, c, hs, s_solid, x, y, z, f, u0, u1, u2);
                 apply_pokes<E>(d, slot, c, x, y, z, f);
                 if (mode == MODE_PULL) {
                     moments(f, rho, u0, u1, u2);
@@ -612,7 +699,7 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
                 }
                 // ---- collision (engine.cpp:450-475)
                 const double om = kc.omega;
-                double* out = fo + c * size_t(Q) * E3 + cell;
+                const StoreF<E, AA> out{fo + c * size_t(Q) * E3 + cell, &rt_w, c, x, y, z, hs, s_solid};
                 const double uu = u0 * u0 + u1 * u1 + u2 * u2;
                 const double t3 = (0.5 * uu) * 3.0;
                 const double wr0 = PLBM_W0 * rho, wr1 = PLBM_W1 * rho, wr2 = PLBM_W2 * rho;
@@ -626,7 +713,7 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
         const double eu = (I == 0) ? 0.0 : eu_pair<(I == 0 ? 1 : I - ((I + 1) & 1))>(u0, u1, u2); \
         const double e0 = feq_dir<I>(wr, eu, t3);                                     \
         const double o_ = f[I] + om * (e0 - f[I]);                                     \
-        out[size_t(I) * E3] = o_;                                                     \
+        out(I, o_);                                                                   \
         scr.add(o_);                                                                  \
     }
                     PLBM_RELAX(0) PLBM_RELAX(1) PLBM_RELAX(2) PLBM_RELAX(3) PLBM_RELAX(4)
@@ -647,7 +734,7 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
         const double e0 = feq_dir<I>(wr, eu, t3);                                     \
         const double e1 = feq_dir<I>(wr, ev, s3);                                     \
         const double o_ = f[I] + ((om * (e0 - f[I]) + e1) - e0);                       \
-        out[size_t(I) * E3] = o_;                                                     \
+        out(I, o_);                                                                   \
         scr.add(o_);                                                                  \
     }
                     PLBM_FORCED(0) PLBM_FORCED(1) PLBM_FORCED(2) PLBM_FORCED(3) PLBM_FORCED(4)
@@ -713,10 +800,21 @@ __device__ __forceinline__ void face_xyz(int face, int idx, int& x, int& y, int&
 template <int E, bool COH>
 __device__ __forceinline__ void face_load(const RouteTab& rt, int mode, const int* tc, int c, bool hs,
                                           const uint32_t* sb, int face, int idx, double* f,
-                                          bool xcol = false) {
+                                          bool xcol = false, int kind = AA_OFF) {
     int x, y, z;
     face_xyz<E>(face, idx, x, y, z);
     if (hs && solid_at<E>(sb, x, y, z)) return;
+    if (kind != AA_OFF) {  // A-A storage: no xcol buffers, general addressing
+        if (mode != MODE_PULL) {
+            double a0, a1, a2;
+            gen_fin<E>(mode, c, tc, x, y, z, f, a0, a1, a2);
+        } else if (kind == AA_LOCAL) {
+            pull_addr<E, AA_LOCAL>(rt, c, hs, sb, x, y, z, [&](int i, const double* p) { f[i] = COH ? __ldcg(p) : __ldg(p); });
+        } else {
+            pull_addr<E, AA_NEIGH>(rt, c, hs, sb, x, y, z, [&](int i, const double* p) { f[i] = COH ? __ldcg(p) : __ldg(p); });
+        }
+        return;
+    }
     if (xcol && face < 2 && !hs && mode == MODE_PULL) {
         // x faces from the routed tiles' xcol buffers (lattice.cuh): the
         // source column x - e_x is 0 / 1 / E-2 / E-1 of the own tile or x = E-1
@@ -826,9 +924,10 @@ __device__ unsigned face_run(const Dev& d, const RouteTab& rt, int mode, const i
         return true;
     };
     const bool xcol = d.xcol_ok != 0;
+    const int kind = aa_kind(d.aa, iter + 1);  // the storage kind the next step reads
     auto load = [&](int t, double* f) {
         int face, idx, c;
-        if (item(t, face, idx, c)) face_load<E, COH>(rt, mode, tc, c, hs, sb, face, idx, f, xcol);
+        if (item(t, face, idx, c)) face_load<E, COH>(rt, mode, tc, c, hs, sb, face, idx, f, xcol, kind);
     };
     auto finish = [&](int t, const double* f) {
         int face, idx, c;
@@ -953,7 +1052,7 @@ __global__ void __launch_bounds__(NT) k_p5(Dev d, const int* __restrict__ active
 #pragma unroll 1
         for (int c = 0; c < C; ++c) {
             double f[Q], rho, u0, u1, u2;
-            pull_cell<E>(rt, c, hs, s_solid, x, y, z, f);
+            pull_cell_k<E>(aa_kind(d.aa, iter + 1), rt, c, hs, s_solid, x, y, z, f);
             moments(f, rho, u0, u1, u2);
             if (!isfinite(rho) || !isfinite(u0) || !isfinite(u1) || !isfinite(u2)) bad = true;
         }
@@ -970,7 +1069,7 @@ __global__ void k_err_halt(const unsigned long long* err, int* halt) {
 // Reference-view read-back of one tile (f_read, rho, u) into out:
 // [19*E3 f][E3 rho][E3 ux][E3 uy][E3 uz]
 template <int E>
-__global__ void k_readback(Dev d, int slot, int c, int src_buf, double* out) {
+__global__ void k_readback(Dev d, int slot, int c, int src_buf, double* out, int kind) {
     constexpr int E3 = E * E * E;
     constexpr int G = E + 2;
     __shared__ RouteTab rt;
@@ -991,7 +1090,7 @@ __global__ void k_readback(Dev d, int slot, int c, int src_buf, double* out) {
         if (sol) {
             for (int i = 0; i < Q; ++i) f[i] = P.comp[c].feq_amb[i];
         } else if (mode == MODE_PULL) {
-            pull_cell<E>(rt, c, hs, s_solid, x, y, z, f);
+            pull_cell_k<E>(kind, rt, c, hs, s_solid, x, y, z, f);
             moments(f, rho, u0, u1, u2);
         } else {
             gen_fin<E>(mode, c, s_tc, x, y, z, f, u0, u1, u2);
@@ -1014,7 +1113,7 @@ __global__ void k_readback(Dev d, int slot, int c, int src_buf, double* out) {
 // step's P1).  grid is pre-filled with the ambient value; grid.y = tile.
 template <int E>
 __global__ void k_gather(Dev d, const int* __restrict__ active, int kind, int c, int src_buf,
-                         double* grid, int D0, int D1) {
+                         double* grid, int D0, int D1, int skind) {
     constexpr int E3 = E * E * E;
     constexpr int G = E + 2;
     __shared__ RouteTab rt;
@@ -1041,7 +1140,7 @@ __global__ void k_gather(Dev d, const int* __restrict__ active, int kind, int c,
             if (sol) {
                 // u of a solid cell is never written by the reference: 0
             } else if (mode == MODE_PULL) {
-                pull_cell<E>(rt, c, hs, s_solid, x, y, z, f);
+                pull_cell_k<E>(skind, rt, c, hs, s_solid, x, y, z, f);
                 moments(f, rho, u0, u1, u2);
             } else {
                 gen_fin<E>(mode, c, s_tc, x, y, z, f, u0, u1, u2);

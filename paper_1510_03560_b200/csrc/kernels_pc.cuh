@@ -103,7 +103,9 @@ struct PcCfg {
 // MEMONLY (probe, variant 24, NOT a correct step): the same pulls, psi
 // pushes, TMEM stash, stores and xcol staging with the physics removed (psi
 // = 0, f stored unchanged) — the memory pipeline's own ceiling.
-template <int E, int C, int LAG, int NT_ = 256, bool EARLY = true, bool MEMONLY = false>
+// AA: population storage kind of this step (kernels.cuh AA_*); A-A steps
+// write no xcol side buffers (the face pass reads the SoA block).
+template <int E, int C, int LAG, int NT_ = 256, bool EARLY = true, bool MEMONLY = false, int AA = AA_OFF>
 __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __restrict__ active,
                                                             int src_buf, int write_uface, long iter) {
     if (halted(d)) return;
@@ -119,7 +121,7 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
     double* psi = smem;                // [R][C][PH][PW] ring of psi planes, all components
     double* land = smem + R * C * PP;  // [Q][NT] landed populations of the next plane
     double* xst = land + Q * NT;       // [2][4][Q][BY] x-column values of the block's rows, by plane parity
-    __shared__ RouteTab rt_pull, rt_psi;
+    __shared__ RouteTab rt_pull, rt_psi, rt_w;
     __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
     __shared__ int s_tc[3];
     __shared__ uint32_t s_tmem;
@@ -130,8 +132,15 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
     const int warp = tid >> 5;
     const int rank = int(blockIdx.x % T::CL);  // = cluster CTA rank (1-D clusters)
     const int tile_i = int(blockIdx.x / T::CL);
+#ifdef PLBM_RANK_IL  // experiment: components interleaved in the cluster rank
+    const int c = rank % C;
+    const int yb = rank / C;
+    auto crank = [&](int cc, int bb) { return bb * C + cc; };
+#else
     const int c = rank / NB;                   // this CTA's component
     const int yb = rank % NB;
+    auto crank = [&](int cc, int bb) { return cc * NB + bb; };
+#endif
     const int y0 = yb * BY;
     if (d.nactive && d.tile_base + tile_i >= *d.nactive) return;  // (whole clusters: same tile)
     const int slot = active[tile_i];
@@ -150,6 +159,7 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
     }
     load_routes(rt_pull, d.route[ROUTE_PULL] + size_t(slot) * 18, slot, amb, d.slot_f[src_buf]);
     load_routes(rt_psi, d.route[ROUTE_PSI] + size_t(slot) * 18, slot, amb, d.slot_pf[par], d.mode);
+    if constexpr (AA == AA_NEIGH) load_routes(rt_w, d.route[ROUTE_W] + size_t(slot) * 18, slot, amb, d.slot_f[0]);
     if (tid < 3) s_tc[tid] = d.coords[slot * 3 + tid];
     if (hs)
         for (int k = tid; k < d.solid_words; k += NT) s_solid[k] = d.solid[size_t(slot) * d.solid_words + k];
@@ -174,7 +184,7 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
     const int y = y0 + yl;
     const int xcls = x == 0 ? 0 : x == 1 ? 1 : x == E - 2 ? 2 : x == E - 1 ? 3 : -1;  // xcol lanes
     double* const xcol = d.slot_f[src_buf ^ 1][slot] + size_t(C) * Q * E3 + size_t(c) * XN * E2;
-    const bool wx = d.xcol_ok != 0;
+    const bool wx = AA == AA_OFF && d.xcol_ok != 0;
     // xcol: the x-column lanes stage their values in shared memory during the
     // collision; after the next CTA barrier the block writes them out as
     // 8-row (64-byte) segments of xcol[c][slot][z][y]
@@ -223,9 +233,9 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
     auto push_all = [&](int pz, double v) {
 #pragma unroll
         for (int c2 = 0; c2 < C; ++c2) {
-            if (c2 != c) push(c2 * NB + yb, pz, yl, v);
-            if (yl == 0 && yb > 0) push(c2 * NB + yb - 1, pz, BY, v);
-            if (yl == BY - 1 && yb < NB - 1) push(c2 * NB + yb + 1, pz, -1, v);
+            if (c2 != c) push(crank(c2, yb), pz, yl, v);
+            if (yl == 0 && yb > 0) push(crank(c2, yb - 1), pz, BY, v);
+            if (yl == BY - 1 && yb < NB - 1) push(crank(c2, yb + 1), pz, -1, v);
         }
     };
     constexpr uint32_t PLANE_BYTES = uint32_t((C - 1) * BY * E * 8);
@@ -297,7 +307,8 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
     auto issue_pulls = [&](int pz) {
         if (pz >= E || mode != MODE_PULL || (hs && solid_at<E>(s_solid, x, y, pz))) return;
         auto op = [&](int i, const double* p) { cp_async8(land_u32 + uint32_t(i * NT + tid) * 8u, p); };
-        if (fast_rows && pz >= 1 && pz <= E - 2) pull_addr_fast<E>(rt_pull, c, x, y, pz, op);
+        if constexpr (AA != AA_OFF) pull_addr<E, AA>(rt_pull, c, hs, s_solid, x, y, pz, op);
+        else if (fast_rows && pz >= 1 && pz <= E - 2) pull_addr_fast<E>(rt_pull, c, x, y, pz, op);
         else if (fast_yedge && pz >= 1 && pz <= E - 2) pull_addr_fast_yedge<E>(rt_pull, c, x, y, pz, op);
         else pull_addr<E>(rt_pull, c, hs, s_solid, x, y, pz, op);
     };
@@ -429,7 +440,8 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
                 cp[2 * E3 + cell] = u1;
                 cp[3 * E3 + cell] = u2;
             }
-            collide_bgk(f, rho, u0, u1, u2, F0, F1, F2, kc.omega, fo + cell, size_t(E3), zero_rho, suspect,
+            const StoreF<E, AA> st{fo + cell, &rt_w, c, x, y, z, hs, s_solid};
+            collide_bgk(f, rho, u0, u1, u2, F0, F1, F2, kc.omega, st, zero_rho, suspect,
                         (xcls >= 0 && wx) ? xst + ((z & 1) * 4 + xcls) * Q * BY + yl : nullptr, BY);
         }
     };

@@ -99,12 +99,14 @@ __device__ __forceinline__ void sc_sums(const double* pm, const double* p0, cons
 
 // One component's BGK collision with the velocity-shift forcing
 // (engine.cpp:450-475) given the total force F.  f is overwritten with the
-// post-collision populations; xc (x-column lanes only, else nullptr) receives
-// a copy of all 19 at stride xstride.  `suspect` is set when a stored value
+// post-collision populations, each stored through out(i, value) (StoreF:
+// A-B or A-A placement); xc (x-column lanes only, else nullptr) receives a
+// copy of all 19 at stride xstride.  `suspect` is set when a stored value
 // leaves the P5 screen's range (lattice.cuh Screen).
+template <class St>
 __device__ __forceinline__ void collide_bgk(double* f, double rho, double u0, double u1,
                                             double u2, double F0, double F1, double F2,
-                                            double om, double* out, size_t dstride,
+                                            double om, const St& out,
                                             unsigned& zero_rho, int& suspect, double* xc = nullptr,
                                             int xstride = 0) {
 
@@ -121,7 +123,7 @@ __device__ __forceinline__ void collide_bgk(double* f, double rho, double u0, do
         const double eu = (I == 0) ? 0.0 : eu_pair<IP>(u0, u1, u2);                           \
         const double e0 = feq_dir<I>(wr, eu, t3);                                             \
         f[I] = f[I] + om * (e0 - f[I]);                                                       \
-        out[size_t(I) * dstride] = f[I];                                                      \
+        out(I, f[I]);                                                                        \
     }
         PLBM_TM_RELAX(0) PLBM_TM_RELAX(1) PLBM_TM_RELAX(2) PLBM_TM_RELAX(3) PLBM_TM_RELAX(4)
         PLBM_TM_RELAX(5) PLBM_TM_RELAX(6) PLBM_TM_RELAX(7) PLBM_TM_RELAX(8) PLBM_TM_RELAX(9)
@@ -149,7 +151,7 @@ __device__ __forceinline__ void collide_bgk(double* f, double rho, double u0, do
         const double e0 = feq_dir<I>(wr, eu, t3);                                             \
         const double e1 = feq_dir<I>(wr, ev, s3);                                             \
         f[I] = f[I] + ((om * (e0 - f[I]) + e1) - e0);                                         \
-        out[size_t(I) * dstride] = f[I];                                                      \
+        out(I, f[I]);                                                                        \
     }
         PLBM_TM_FORCED(0) PLBM_TM_FORCED(1) PLBM_TM_FORCED(2) PLBM_TM_FORCED(3)
         PLBM_TM_FORCED(4) PLBM_TM_FORCED(5) PLBM_TM_FORCED(6) PLBM_TM_FORCED(7)

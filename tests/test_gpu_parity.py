@@ -186,3 +186,61 @@ def test_p5_screen_has_no_false_alarm(built, name):
     assert errs[0] == errs[1], errs
     for k in ("iteration", "cell_updates"):
         assert ref.counters()[k] == gpu.counters()[k]
+
+
+def _aa_scenarios():
+    return sorted(n for n, (make, _) in scenarios.ALL.items() if make().tile_extent <= 32)
+
+
+@pytest.mark.parametrize("name", _aa_scenarios())
+def test_aa_storage_matches_oracle(built, name):
+    """A-A in-place streaming (one population buffer): the
+    same bit-exact state as the oracle after the first step (an AA_LOCAL
+    step), after the second (AA_NEIGH) and at the end — the read-back itself
+    goes through the A-A addressing of the next step's kind."""
+    make, steps = scenarios.ALL[name]
+    sc = make()
+    orc = capi.oracle_engine(sc)
+    gpu = capi.gpu_engine(sc, capture=True, storage="aa")
+    for k in (1, 1, steps - 2):
+        orc.step(k)
+        gpu.step(k)
+        assert_same_state(orc, gpu, label=f"{name}/aa@{orc.counters()['iteration']}")
+
+
+@pytest.mark.parametrize("mode", ["device", "host"])
+@pytest.mark.parametrize("name", ["mpmc_progressive_e16", "c1_progressive_S0", "mpmc_channel_e16"])
+def test_aa_expansion_paths_match_oracle(built, name, mode, monkeypatch):
+    """A-A with births: stores into newborn tiles follow ROUTE_W, whether the
+    device (k_check_expand) or the host mirror grows the map."""
+    if mode == "host":
+        monkeypatch.setenv("PLBM_DEVICE_EXPAND", "0")
+    make, steps = scenarios.ALL[name]
+    sc = make()
+    orc = capi.oracle_engine(sc)
+    gpu = capi.gpu_engine(sc, capture=True, storage="aa")
+    for chunk in (1, 2, steps - 3):
+        orc.step(chunk)
+        gpu.step(chunk)
+        assert_same_state(orc, gpu, label=f"{name}/aa/{mode}")
+
+
+def test_aa_halves_population_memory(built):
+    """The A-A engine allocates one population buffer: the device memory an
+    engine takes drops by about the size of one buffer."""
+    import torch
+    sc = scenarios.ALL["mpmc_e32"][0]()
+    free0 = torch.cuda.mem_get_info()[0]
+    ab = capi.gpu_engine(sc)
+    free_ab = torch.cuda.mem_get_info()[0]
+    ab.close()
+    free1 = torch.cuda.mem_get_info()[0]
+    aa = capi.gpu_engine(sc, storage="aa")
+    free_aa = torch.cuda.mem_get_info()[0]
+    aa.close()
+    used_ab, used_aa = free0 - free_ab, free1 - free_aa
+    n = 1
+    for d in sc.domain:
+        n *= d
+    one_buffer = n * sc.n_components * 19 * 8
+    assert used_ab - used_aa >= 0.9 * one_buffer, (used_ab, used_aa, one_buffer)

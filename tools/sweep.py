@@ -8,9 +8,11 @@
         BASELINE configs[4] on one GPU: tile extent E in {16, 32} x components
         C in {1, 2, 3}, static full-domain MPMC (all tiles active), MLUPS per
         component of the whole step and of the fused kernel.
-    python tools/sweep.py c4 [--steps 400]
+    python tools/sweep.py c4 [--steps 400] [--storage aa] [--static]
         BASELINE configs[3] on one GPU: MPMC release in the 3-D channel
-        network (scenario.channel_network) at 1024x512x512, progressive.
+        network (scenario.channel_network) at 1024x512x512, progressive; with
+        --static also the static full mesh (8192 tiles: 174 GB of populations
+        with two buffers, so --storage aa, one in-place buffer, to fit).
     python tools/sweep.py c3 [--n 512] [--steps 300]
         BASELINE configs[2], the paper's comparison: the same MPMC release run
         on the progressive mesh and on the static full-domain mesh for the
@@ -66,7 +68,7 @@ def c5(a):
     for E in (16, 32, 64):
         for C in (1, 2, 3):
             sc = S.mpmc_release(n=a.n, extent=E, mode=S.MODE_STATIC, n_components=C)
-            eng = capi.gpu_engine(sc)
+            eng = capi.gpu_engine(sc, storage=a.storage)
             eng.step(a.warmup)
             ms, cells, ks = timed(eng, a.steps, chunk=a.steps)
             main = ks["main_cell_updates"] * C * BYTES / (ks["main_ms"] / 1e3) / 1e9
@@ -84,7 +86,7 @@ def c3(a):
     out = {}
     for mode, name in ((S.MODE_PROGRESSIVE, "progressive"), (S.MODE_STATIC, "static")):
         sc = S.mpmc_release(n=a.n, extent=32, mode=mode, threshold=1e-9)
-        eng = capi.gpu_engine(sc)
+        eng = capi.gpu_engine(sc, storage=a.storage)
         series = []
         total_ms = 0.0
         for k0 in range(0, a.steps, a.every):
@@ -100,24 +102,33 @@ def c3(a):
 
 def c4(a):
     """BASELINE configs[3] on one GPU: the 3-D channel network at full size,
-    progressive mesh (the static full domain, 8192 tiles, does not fit one
-    GPU's HBM with two population buffers)."""
-    t0 = time.time()
-    sc = S.mpmc_channel(nx=1024, ny=512, nz=512, extent=32, threshold=1e-9)
-    eng = capi.gpu_engine(sc)
-    setup_s = time.time() - t0
-    series, total_ms, cells = [], 0.0, 0
-    for k0 in range(0, a.steps, a.every):
-        ms, c, ks = timed(eng, min(a.every, a.steps - k0))
-        total_ms += ms
-        cells += c
-        series.append({"step": k0 + a.every, "tiles": eng.counters()["tiles"], "ms": round(ms, 3),
-                       "mlups_per_comp": round(c * 2 / (ms / 1e3) / 1e6, 1)})
-    print(json.dumps({"sweep": "c4", "domain": list(sc.domain), "fluid_fraction": round(1 - float(sc.geometry.mean()), 4),
-                      "setup_s": round(setup_s, 2), "steps": a.steps, "total_ms": round(total_ms, 2),
-                      "final_tiles": eng.counters()["tiles"], "tiles_total": 8192,
-                      "mlups_per_comp": round(cells * 2 / (total_ms / 1e3) / 1e6, 1), "series": series}), flush=True)
-    eng.close()
+    progressive mesh, and with --static the static full domain on the same
+    scenario (8192 tiles; fits one B200 only with A-A storage)."""
+    modes = [(S.MODE_PROGRESSIVE, "progressive")] + ([(S.MODE_STATIC, "static")] if a.static else [])
+    out = {}
+    for mode, name in modes:
+        t0 = time.time()
+        sc = S.mpmc_channel(nx=1024, ny=512, nz=512, extent=32, threshold=1e-9, mode=mode)
+        eng = capi.gpu_engine(sc, storage=a.storage)
+        setup_s = time.time() - t0
+        series, total_ms, cells = [], 0.0, 0
+        for k0 in range(0, a.steps, a.every):
+            ms, c, ks = timed(eng, min(a.every, a.steps - k0),
+                              chunk=1 if mode == S.MODE_PROGRESSIVE else a.every)
+            total_ms += ms
+            cells += c
+            series.append({"step": k0 + a.every, "tiles": eng.counters()["tiles"], "ms": round(ms, 3),
+                           "mlups_per_comp": round(c * 2 / (ms / 1e3) / 1e6, 1)})
+        out[name] = {"setup_s": round(setup_s, 2), "total_ms": round(total_ms, 2),
+                     "final_tiles": eng.counters()["tiles"], "cell_updates": eng.counters()["cell_updates"],
+                     "mlups_per_comp": round(cells * 2 / (total_ms / 1e3) / 1e6, 1), "series": series}
+        fluid = round(1 - float(sc.geometry.mean()), 4)
+        eng.close()
+    line = {"sweep": "c4", "domain": [1024, 512, 512], "fluid_fraction": fluid, "storage": a.storage,
+            "steps": a.steps, "tiles_total": 8192, **out}
+    if "static" in out:
+        line["speedup_progressive_vs_static"] = round(out["static"]["total_ms"] / out["progressive"]["total_ms"], 3)
+    print(json.dumps(line), flush=True)
 
 
 def c1(a):
@@ -129,7 +140,7 @@ def c1(a):
     cores = _os.cpu_count() or 1
     sc = S.config1(threshold=1e-12)
     sc.devices = cores  # the reference's workers own tiles by owner % W (engine.cpp:217)
-    eng = capi.gpu_engine(sc)
+    eng = capi.gpu_engine(sc, storage=a.storage)
     ms, cells, _ = timed(eng, a.steps, chunk=a.steps)
     gpu_log, gpu_c = eng.creation_log(), eng.counters()
     eng.close()
@@ -190,6 +201,9 @@ def main():
     p.add_argument("--steps", type=int, default=None)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--every", type=int, default=25)
+    p.add_argument("--storage", choices=["ab", "aa"], default="ab",
+                   help="population storage: two buffers (ab) or one in-place A-A buffer (aa)")
+    p.add_argument("--static", action="store_true", help="c4: also the static full mesh")
     a = p.parse_args()
     if a.what == "c5":
         a.n = a.n or 256
