@@ -118,22 +118,28 @@ void* plbm_gpu_stream(void* h);
 /* ---- multi-GPU (one process per GPU) -----------------------
  * Every rank builds the same deterministic host mirror from the same
  * descriptor; tile owner o (assign_device) lives on rank o % world.  Each
- * rank's block pool is exported as CUDA IPC handles; peers map it and the
+ * rank's block pool, psi-face pool and sync block (barrier flags, error key,
+ * trigger bytes) are exported as CUDA IPC handles; peers map them and the
  * fused kernel reads remote neighbour tiles over NVLink in place.
  *
  *   h = plbm_gpu_create_dist(desc, local_device, rank, world, &err)
  *   plbm_gpu_ipc_handles(h, buf)           -> exchange (all_gather) ->
  *   plbm_gpu_open_peer(h, r, handles_r)    for every other rank r
  *   plbm_gpu_prepare(h)                    then a barrier across ranks
- *   per step: plbm_gpu_step_main(h)        (fused kernel of this rank's tiles)
- *             barrier across ranks          (k_face pulls peers' new f_post)
- *             plbm_gpu_step_face(h)        (psi faces, criterion, trigger bits)
- *             all-reduce(MAX) the plbm_gpu_trigger_bytes(h) bytes at
- *             plbm_gpu_triggers_device(h) on plbm_gpu_stream(h)
- *             plbm_gpu_step_end(h, merged)  (expansion on the merged bits)
- * The two stream-ordered collectives also order the ranks' double-buffered
- * pools; step_end writes nothing a peer reads.  plbm_gpu_step_begin =
- * step_main + step_face (single rank).                                      */
+ *   plbm_gpu_step(h, n, &err)              on every rank with the same n
+ *
+ * plbm_gpu_step on several ranks needs no host collective: per step the
+ * fused kernel, a device-side rank barrier (flag words in the peers' sync
+ * blocks, NVLink stores), the face pass, a second barrier, then the
+ * expansion kernel on EVERY rank over the merged trigger bytes and the
+ * lowest error key of all ranks (read from the peers' sync blocks) — so the
+ * map, placement and any EngineError are identical on every rank, and steps
+ * are queued ahead without a host round trip (Engine::step_speculative).
+ *
+ * The host-merge protocol of round 1 remains for callers that merge the
+ * triggers themselves: step_main, a barrier across ranks, step_face, an
+ * all-reduce(MAX) of the plbm_gpu_trigger_bytes(h) bytes at
+ * plbm_gpu_triggers_device(h), then step_end(h, merged).                     */
 void* plbm_gpu_create_dist(const plbm_scenario_desc* desc, int device, int rank, int world,
                            plbm_error* err);
 int plbm_gpu_prepare(void* h);
@@ -144,12 +150,14 @@ int plbm_gpu_step_end(void* h, const uint8_t* merged_triggers, plbm_error* err);
 int plbm_gpu_trigger_bytes(void* h);
 void* plbm_gpu_triggers_device(void* h);
 int plbm_gpu_local_triggers(void* h, uint8_t* out, int n);   /* D2H copy, syncs */
-int plbm_gpu_ipc_handles(void* h, void* out);                /* 2 x cudaIpcMemHandle_t */
+int plbm_gpu_ipc_handles(void* h, void* out);                /* 3 x cudaIpcMemHandle_t */
 int plbm_gpu_open_peer(void* h, int rank, const void* handles);
 /* Same-process peers (several ranks' engines in one process on one GPU):
  * attach another engine's pools directly.                                    */
 int plbm_gpu_set_peer_pools(void* h, int rank, void* pool_f, void* pool_pf);
 void plbm_gpu_pool_pointers(void* h, void** pool_f, void** pool_pf);
+void* plbm_gpu_sync_block(void* h);                          /* same-process peers */
+int plbm_gpu_set_peer_sync(void* h, int rank, void* sync_block);
 int plbm_gpu_tile_rank(void* h, const int32_t* coords);      /* -1 if absent */
 int plbm_gpu_sync(void* h);
 /* Real byte accounting: bytes this rank's kernels read from

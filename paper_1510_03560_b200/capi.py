@@ -235,6 +235,8 @@ class GpuEngine(StepEngine):
                 ("open_peer", C.c_int, [P, C.c_int, C.c_void_p]),
                 ("set_peer_pools", C.c_int, [P, C.c_int, C.c_void_p, C.c_void_p]),
                 ("pool_pointers", None, [P, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+                ("sync_block", C.c_void_p, [P]),
+                ("set_peer_sync", C.c_int, [P, C.c_int, C.c_void_p]),
                 ("tile_rank", C.c_int, [P, C.POINTER(C.c_int32)]),
                 ("sync", C.c_int, [P])]:
             fn = getattr(lib, f"plbm_gpu_{name}")
@@ -313,13 +315,17 @@ class GpuEngine(StepEngine):
             raise RuntimeError(f"plbm_gpu_open_peer({rank}) failed")
 
     def pool_pointers(self):
+        """(population pool, psi-face pool, sync block) device pointers."""
         f, pf = C.c_void_p(), C.c_void_p()
         self.lib.plbm_gpu_pool_pointers(self._h, C.byref(f), C.byref(pf))
-        return f.value, pf.value
+        return f.value, pf.value, self.lib.plbm_gpu_sync_block(self._h)
 
     def set_peer_pools(self, rank: int, pools) -> None:
+        """Attach a same-process peer engine's pools (pool_pointers())."""
         if self.lib.plbm_gpu_set_peer_pools(self._h, rank, pools[0], pools[1]) != 0:
             raise RuntimeError("plbm_gpu_set_peer_pools failed")
+        if len(pools) > 2 and self.lib.plbm_gpu_set_peer_sync(self._h, rank, pools[2]) != 0:
+            raise RuntimeError("plbm_gpu_set_peer_sync failed")
 
     def tile_rank(self, coords) -> int:
         return self.lib.plbm_gpu_tile_rank(self._h, (C.c_int32 * 3)(*coords))

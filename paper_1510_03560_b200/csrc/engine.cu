@@ -17,7 +17,7 @@
 // trigger bits of all ranks (one small all-reduce), which also orders the
 // ranks' double-buffered reads and writes.
 #include "kernels.cuh"
-#include "kernels_pc.cuh"
+#include "dispatch.cuh"
 #include "expand.cuh"
 #include "plbm_gpu.h"
 
@@ -97,148 +97,19 @@ T* dmalloc(size_t n) {
     return p;
 }
 
-// ---- kernel dispatch over (E, C, NOPSI) --------------------------------------
-using MainFn = void (*)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
-struct Kernels {
-    MainFn main_plain;  // variant 1 (and the only kernel for E = 8 / psi-free)
-    MainFn main_pc;     // variant 0: one CTA per (block, component), cp.async staged
-    MainFn main_pc_late;  // variant 21: the collision head after the cluster wait
-    MainFn main_pc_mem;   // variant 24 (PLBM_PROBES builds only): memory-only probe (E = 32, C = 2)
-    MainFn main_pc2;    // variant 22: psi computed two planes ahead
-    MainFn main_aa[2];  // A-A storage: AA_LOCAL / AA_NEIGH steps (k_main_pc, else the whole-tile plain kernel)
-    void (*face)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
-    void (*face_v[2])(Dev, const int*, int, int, long, unsigned, cudaStream_t);
-    void (*p5)(Dev, const int*, int, long, unsigned, cudaStream_t);
-    void (*readback)(Dev, int, int, int, double*, int, cudaStream_t);
-    void (*gather)(Dev, const int*, int, int, int, int, double*, int, int, int, cudaStream_t);
-    int nt;
-};
-
-template <int E, int C, int LAG, int NT = 256, bool EARLY = true, bool MEMONLY = false, int AA = AA_OFF>
-void launch_pc(Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
-    using T = PcCfg<E, C, LAG, NT>;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ntiles * T::CL);
-    cfg.blockDim = dim3(T::NT);
-    cfg.dynamicSmemBytes = T::SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = T::CL;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_main_pc<E, C, LAG, NT, EARLY, MEMONLY, AA>, d, act, src, wu, it);
-}
-
-template <int E, int C, bool NOPSI>
-Kernels make_kernels() {
-    constexpr int NT = E * E < 256 ? E * E : 256;
-    constexpr int BZ = E < 8 ? E : 8;
-    constexpr int YB = E == 64 ? 16 : E;  // y-chunk of the plain kernel (E = 64: psi ring in smem)
-    constexpr int G = E + 2;
-    constexpr size_t SMEM_PLAIN = NOPSI ? 0 : size_t(3) * C * G * (YB + 2) * sizeof(double);
-    Kernels k;
-    k.nt = NT;
-    // (static shared memory counts against the same 48 KB default: opt in
-    // whenever there is a dynamic ring)
-    if (SMEM_PLAIN > 0)
-        cudaFuncSetAttribute(k_main<E, C, BZ, NT, NOPSI, YB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(SMEM_PLAIN));
-    k.main_plain = [](Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
-        k_main<E, C, BZ, NT, NOPSI, YB><<<ntiles * (E / BZ) * (E / YB), NT, SMEM_PLAIN, s>>>(d, act, src, wu, it);
-    };
-    k.main_pc = k.main_pc2 = k.main_pc_late = k.main_pc_mem = nullptr;
-    k.main_aa[0] = k.main_aa[1] = nullptr;
-    if constexpr (!NOPSI && (E == 16 || E == 32)) {
-        auto setup = [](auto fn, int smem, int cl) {
-            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            if (cl > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        };
-        setup(k_main_pc<E, C, 1>, PcCfg<E, C, 1>::SMEM, PcCfg<E, C, 1>::CL);
-        k.main_pc = launch_pc<E, C, 1>;
-        setup(k_main_pc<E, C, 1, 256, false>, PcCfg<E, C, 1>::SMEM, PcCfg<E, C, 1>::CL);
-        k.main_pc_late = launch_pc<E, C, 1, 256, false>;
-#ifdef PLBM_PROBES
-        if constexpr (E == 32 && C == 2) {
-            setup(k_main_pc<E, C, 1, 256, true, true>, PcCfg<E, C, 1>::SMEM, PcCfg<E, C, 1>::CL);
-            k.main_pc_mem = launch_pc<E, C, 1, 256, true, true>;
-        }
-#endif
-        if constexpr (C <= 2) {
-            setup(k_main_pc<E, C, 2>, PcCfg<E, C, 2>::SMEM, PcCfg<E, C, 2>::CL);
-            k.main_pc2 = launch_pc<E, C, 2>;
-        }
-#ifndef PLBM_NO_AA
-        setup(k_main_pc<E, C, 1, 256, true, false, AA_LOCAL>, PcCfg<E, C, 1>::SMEM, PcCfg<E, C, 1>::CL);
-        setup(k_main_pc<E, C, 1, 256, true, false, AA_NEIGH>, PcCfg<E, C, 1>::SMEM, PcCfg<E, C, 1>::CL);
-        k.main_aa[0] = launch_pc<E, C, 1, 256, true, false, AA_LOCAL>;
-        k.main_aa[1] = launch_pc<E, C, 1, 256, true, false, AA_NEIGH>;
-#endif
-    } else if constexpr (E <= 32) {
-#ifndef PLBM_NO_AA
-        // A-A with the plain kernel: one CTA per tile (no recomputed halos)
-        constexpr size_t SMEM_AA = NOPSI ? 0 : size_t(3) * C * G * G * sizeof(double);
-        if (SMEM_AA > 0) {
-            cudaFuncSetAttribute(k_main<E, C, E, NT, NOPSI, E, AA_LOCAL>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_AA));
-            cudaFuncSetAttribute(k_main<E, C, E, NT, NOPSI, E, AA_NEIGH>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_AA));
-        }
-        k.main_aa[0] = [](Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
-            k_main<E, C, E, NT, NOPSI, E, AA_LOCAL><<<ntiles, NT, SMEM_AA, s>>>(d, act, src, wu, it);
-        };
-        k.main_aa[1] = [](Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
-            k_main<E, C, E, NT, NOPSI, E, AA_NEIGH><<<ntiles, NT, SMEM_AA, s>>>(d, act, src, wu, it);
-        };
-#endif
-    }
-    // k_face at 4 CTAs/SM, one item in flight per thread (64 registers),
-    // measured faster than 2 CTAs/SM with a one-item prefetch (PLBM_FACE_VARIANT=1)
-    k.face_v[0] = [](Dev d, const int* act, int src, int flags, long it, unsigned ntiles, cudaStream_t s) {
-        k_face<E, C, NT, 4, false><<<ntiles * 6, NT, 0, s>>>(d, act, src, flags, it);
-    };
-    k.face_v[1] = [](Dev d, const int* act, int src, int flags, long it, unsigned ntiles, cudaStream_t s) {
-        k_face<E, C, NT, 2, true><<<ntiles * 6, NT, 0, s>>>(d, act, src, flags, it);
-    };
-    k.face = k.face_v[0];
-    k.p5 = [](Dev d, const int* act, int src, long it, unsigned ntiles, cudaStream_t s) {
-        k_p5<E, C, 256><<<ntiles, 256, 0, s>>>(d, act, src, it);
-    };
-    k.readback = [](Dev d, int slot, int c, int src, double* out, int skind, cudaStream_t s) {
-        k_readback<E><<<(E * E * E + 255) / 256, 256, 0, s>>>(d, slot, c, src, out, skind);
-    };
-    k.gather = [](Dev d, const int* act, int ntiles, int kind, int c, int src, double* grid, int D0, int D1,
-                  int skind, cudaStream_t s) {
-        k_gather<E><<<dim3((E * E * E + 255) / 256, ntiles), 256, 0, s>>>(d, act, kind, c, src, grid, D0, D1,
-                                                                          skind);
-    };
-    return k;
-}
-
-template <int E>
-Kernels pick_c(int C, bool nopsi) {
-    switch (C) {
-    case 1: return nopsi ? make_kernels<E, 1, true>() : make_kernels<E, 1, false>();
-    case 2: return nopsi ? make_kernels<E, 2, true>() : make_kernels<E, 2, false>();
-    case 3: return nopsi ? make_kernels<E, 3, true>() : make_kernels<E, 3, false>();
-    default: throw std::invalid_argument("n_components must be 1..3 on the GPU path");
-    }
-}
-
 Kernels pick_kernels(int E, int C, bool nopsi) {
-#ifdef PLBM_ONLY_E32C2  // experiment builds: the bench instantiation only (fast compile)
-    if (E == 32 && C == 2 && !nopsi) return make_kernels<32, 2, false>();
+#ifdef PLBM_ONLY_E32C2  // experiment builds link inst_e32.cu only
+    if (E == 32) return pick_kernels_e32(C, nopsi);
     throw std::invalid_argument("PLBM_ONLY_E32C2 build: E = 32, C = 2 only");
-#endif
+#else
     switch (E) {
-    case 8: return pick_c<8>(C, nopsi);
-    case 16: return pick_c<16>(C, nopsi);
-    case 32: return pick_c<32>(C, nopsi);
-    case 64: return pick_c<64>(C, nopsi);
+    case 8: return pick_kernels_e8(C, nopsi);
+    case 16: return pick_kernels_e16(C, nopsi);
+    case 32: return pick_kernels_e32(C, nopsi);
+    case 64: return pick_kernels_e64(C, nopsi);
     default: throw std::invalid_argument("tile_extent must be 8, 16, 32 or 64 on the GPU path");
     }
+#endif
 }
 
 struct Coord {
@@ -329,6 +200,8 @@ class Engine {
     int ipc_handles(void* out) const;
     int open_peer(int rank, const void* handles);
     int set_peer(int rank, void* pool_f, void* pool_pf);
+    int set_peer_sync(int rank, void* sync);
+    void* sync_block() const { return d_sync_; }
     int rank_of(const int32_t* coords) const;
     void exchange_bytes(uint64_t* out) const;
     int probe(uint64_t* out, int max) {
@@ -404,8 +277,20 @@ class Engine {
     uint8_t* d_mode_ = nullptr;
     int* d_coords_ = nullptr;
     double* d_u_face_ = nullptr;
-    uint8_t* d_trig_ = nullptr;
-    // device-side expansion (single rank, progressive; expand.cuh)
+    uint8_t* d_trig_ = nullptr;   // [parity][trig_bytes_] inside d_sync_ (one parity on one rank)
+    // Sync block (IPC-exported next to the pools): [0..7] barrier flag words
+    // (slot r = the last epoch rank r reached), [8] error key, [9] merged
+    // error key, [16..] trigger bytes of both step parities.
+    unsigned long long* d_sync_ = nullptr;
+    std::vector<unsigned long long*> peer_sync_;
+    unsigned long long epoch_ = 0;  // rank barriers queued so far (identical on every rank)
+    uint8_t* d_merged_ = nullptr;   // world > 1: merged trigger bytes of the last check
+    int* d_all_active_ = nullptr;   // world > 1: every rank's slots (the expansion's map)
+    int* d_nall_ = nullptr;
+    void rank_barrier(long it);
+    void reset_err();
+    unsigned long long* err_word() const { return world_ > 1 ? d_sync_ + 9 : d_err_; }
+    // device-side expansion (one rank progressive, or any multi-rank run; expand.cuh)
     bool dev_expand_ = false;
     int* d_gslot_ = nullptr;
     unsigned long long* d_cand_ = nullptr;
@@ -439,6 +324,7 @@ class Engine {
     cudaEvent_t flag_ev_[8] = {};
     int spec_depth_ = 3;          // steps queued ahead (1 = a host round trip every step)
     bool in_spec_ = false;        // a speculative queue is open (profiling events stay unresolved)
+    bool post_pending_ = false;   // upload_expand_state left a k_post_main to the next step_main
     Poke* d_pokes_ = nullptr;     // test hook: f_in overrides for the next step
     std::vector<Poke> pokes_;
     int* d_dep_cnt_ = nullptr;   // fused face pass: per-slot completion counts
@@ -495,9 +381,10 @@ class Engine {
     void resolve_events();
     bool peers_ready() const {
         for (int r = 0; r < world_; ++r)
-            if (!peer_f_[r]) return false;
+            if (!peer_f_[r] || !peer_sync_[r]) return false;
         return true;
     }
+    int launch_bound() const;
 };
 
 // ---------------------------------------------------------------------------
@@ -625,6 +512,19 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     K_ = pick_kernels(E_, C_, nopsi_);
     if (aa_ && !K_.main_aa[0])
         throw std::invalid_argument("A-A storage needs tile_extent <= 32 (one CTA or cluster per tile)");
+    K_.preload();
+    {   // this unit's kernels too (lazy loading, see dispatch.cuh preload)
+        cudaFuncAttributes a;
+        const void* fs[] = {(const void*)k_post_main, (const void*)k_rank_barrier, (const void*)k_check,
+                            (const void*)k_err_halt, (const void*)k_fill};
+        for (const void* f : fs) CK(cudaFuncGetAttributes(&a, f));
+        switch (E_) {
+        case 8: CK(cudaFuncGetAttributes(&a, (const void*)k_check_expand<8>)); break;
+        case 16: CK(cudaFuncGetAttributes(&a, (const void*)k_check_expand<16>)); break;
+        case 32: CK(cudaFuncGetAttributes(&a, (const void*)k_check_expand<32>)); break;
+        default: CK(cudaFuncGetAttributes(&a, (const void*)k_check_expand<64>)); break;
+        }
+    }
     d_pool_f_ = dmalloc<double>(size_t(nbuf_) * per_slot_ * size_t(lcap_ + 1));
     d_pool_pf_ = dmalloc<double>(2 * per_pf_ * size_t(lcap_ + 1));
     for (int b = 0; b < 2; ++b) {
@@ -638,7 +538,13 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     d_mode_ = dmalloc<uint8_t>(nslot);
     d_coords_ = dmalloc<int>(size_t(nslot) * 3);
     d_u_face_ = dmalloc<double>(size_t(lcap_ + 1) * C_ * 6 * 3 * E2_);
-    d_trig_ = dmalloc<uint8_t>(trig_bytes_);
+    {
+        const size_t sync_words = 16 + (2 * trig_bytes_ + 7) / 8;
+        d_sync_ = dmalloc<unsigned long long>(sync_words);
+        CK(cudaMemsetAsync(d_sync_, 0, sync_words * sizeof(unsigned long long), stream_));
+        d_err_ = d_sync_ + 8;
+        d_trig_ = reinterpret_cast<uint8_t*>(d_sync_ + 16);
+    }
     d_bmask_ = dmalloc<uint8_t>(nslot);
     d_omask_ = dmalloc<uint8_t>(nslot);
     d_halt_ = dmalloc<int>(1);
@@ -649,7 +555,11 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     if (const char* fv = std::getenv("PLBM_FACE_VARIANT")) K_.face = K_.face_v[std::atoi(fv) == 1 ? 1 : 0];
     {
         const char* de = std::getenv("PLBM_DEVICE_EXPAND");
-        dev_expand_ = world_ == 1 && mode_ == PLBM_MODE_PROGRESSIVE && spec_depth_ > 1 && !(de && de[0] == '0');
+        // several ranks always expand on the device (the same merged inputs
+        // on every rank); one rank does for progressive runs with a queue
+        dev_expand_ = world_ > 1 ||
+                      (mode_ == PLBM_MODE_PROGRESSIVE && spec_depth_ > 1 && !(de && de[0] == '0'));
+        if (world_ > 8) throw std::invalid_argument("at most 8 ranks (one node)");
     }
     if (dev_expand_) {
         const size_t ngrid = size_t(grid_[0]) * grid_[1] * grid_[2];
@@ -658,7 +568,12 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
         CK(cudaMemsetAsync(d_cand_, 0xff, ngrid * sizeof(unsigned long long), stream_));
         d_nactive_ = dmalloc<int>(1);
         d_next_slot_ = dmalloc<int>(1);
-        d_next_local_ = dmalloc<int>(1);
+        d_next_local_ = dmalloc<int>(size_t(world_));
+        if (world_ > 1) {
+            d_all_active_ = dmalloc<int>(nslot);
+            d_nall_ = dmalloc<int>(1);
+            d_merged_ = dmalloc<uint8_t>(nslot);
+        }
         d_owner_ = dmalloc<int>(nslot);
         d_p2p_ = dmalloc<uint8_t>(size_t(devices_) * devices_);
         CK(cudaMemcpyAsync(d_p2p_, p2p_.data(), p2p_.size(), cudaMemcpyHostToDevice, stream_));
@@ -683,7 +598,6 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     d_geo_ = dmalloc<int>(size_t(nslot) * 18);
     CK(cudaMemsetAsync(d_dep_cnt_, 0, nslot * sizeof(int), stream_));
     d_cnt_ = dmalloc<unsigned long long>(CNT_N);
-    d_err_ = dmalloc<unsigned long long>(1);
     d_suspect_ = dmalloc<uint8_t>(nslot);
     CK(cudaMemsetAsync(d_suspect_, 0, nslot, stream_));
     d_susp_any_ = dmalloc<unsigned>(2);
@@ -692,10 +606,10 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     d_scratch_slots_ = dmalloc<int>(nslot);
     d_readback_ = dmalloc<double>(size_t(23) * E3_);
     CK(cudaMemsetAsync(d_u_face_, 0, size_t(lcap_ + 1) * C_ * 6 * 3 * E2_ * sizeof(double), stream_));
-    CK(cudaMemsetAsync(d_trig_, 0, trig_bytes_, stream_));
     CK(cudaMemsetAsync(d_cnt_, 0, CNT_N * sizeof(unsigned long long), stream_));
-    CK(cudaMemsetAsync(d_err_, 0xff, sizeof(unsigned long long), stream_));
+    reset_err();
     CK(cudaMemcpyToSymbolAsync(P, &params_, sizeof(Params), 0, cudaMemcpyHostToDevice, stream_));
+    K_.set_params(params_, stream_);  // the kernel unit's own copy
     // this rank's ambient slot (local index lcap): feq_amb in both buffers and
     // psi_amb on its faces for both parities
     {
@@ -724,6 +638,8 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     peer_opened_.assign(world_, false);
     peer_f_[rank_] = d_pool_f_;
     peer_pf_[rank_] = d_pool_pf_;
+    peer_sync_.assign(world_, nullptr);
+    peer_sync_[rank_] = d_sync_;
     for (int b = 0; b < 2; ++b) {
         d_.slot_f[b] = d_slot_f_[b];
         d_.slot_pf[b] = d_slot_pf_[b];
@@ -865,10 +781,12 @@ void Engine::release() {
         if (peer_opened_[r]) {
             cudaIpcCloseMemHandle(peer_f_[r]);
             cudaIpcCloseMemHandle(peer_pf_[r]);
+            cudaIpcCloseMemHandle(peer_sync_[r]);
         }
     void* ptrs[] = {d_pool_f_, d_pool_pf_, d_slot_f_[0], d_slot_f_[1], d_slot_pf_[0], d_slot_pf_[1],
                     d_route_[0], d_route_[1], d_route_[2], d_lidx_, d_solid_, d_has_solid_, d_mode_, d_coords_,
-                    d_u_face_, d_trig_, d_capture_, d_cnt_, d_err_, d_active_, d_scratch_slots_,
+                    d_u_face_, d_sync_, d_capture_, d_cnt_, d_all_active_, d_nall_, d_merged_, d_active_,
+                    d_scratch_slots_,
                     d_readback_, d_dep_cnt_, d_dep_need_, d_geo_, d_bmask_, d_omask_, d_halt_, d_pokes_,
                     d_gslot_, d_cand_, d_nactive_, d_next_slot_, d_next_local_, d_owner_, d_geomdev_, d_p2p_,
                     d_per_dev_, d_acc_, d_births_, d_nbirths_, d_post_flags_, d_suspect_, d_susp_any_};
@@ -1249,17 +1167,36 @@ void Engine::upload_expand_state(bool initial) {
     CK(cudaMemcpyAsync(d_owner_, owner.data(), nslot * sizeof(int), cudaMemcpyHostToDevice, stream_));
     CK(cudaMemcpyAsync(d_per_dev_, per_dev_.data(), per_dev_.size() * sizeof(uint64_t), cudaMemcpyHostToDevice,
                        stream_));
-    const int ints[3] = {int(all_active_.size()), cap_ - int(free_slots_.size()), next_local_[0]};
-    CK(cudaMemcpyAsync(d_nactive_, &ints[0], sizeof(int), cudaMemcpyHostToDevice, stream_));
+    const int ints[3] = {int(all_active_.size()), cap_ - int(free_slots_.size()), int(active_.size())};
     CK(cudaMemcpyAsync(d_next_slot_, &ints[1], sizeof(int), cudaMemcpyHostToDevice, stream_));
-    CK(cudaMemcpyAsync(d_next_local_, &ints[2], sizeof(int), cudaMemcpyHostToDevice, stream_));
+    CK(cudaMemcpyAsync(d_next_local_, next_local_.data(), size_t(world_) * sizeof(int), cudaMemcpyHostToDevice,
+                       stream_));
+    if (world_ > 1) {  // the expansion's map (all ranks) + this rank's launch list
+        CK(cudaMemcpyAsync(d_nall_, &ints[0], sizeof(int), cudaMemcpyHostToDevice, stream_));
+        CK(cudaMemcpyAsync(d_all_active_, all_active_.data(), all_active_.size() * sizeof(int),
+                           cudaMemcpyHostToDevice, stream_));
+        CK(cudaMemcpyAsync(d_nactive_, &ints[2], sizeof(int), cudaMemcpyHostToDevice, stream_));
+    } else {
+        CK(cudaMemcpyAsync(d_nactive_, &ints[0], sizeof(int), cudaMemcpyHostToDevice, stream_));
+    }
     const unsigned long long map_acc[4] = {active_cells_, step_bytes_[0], step_bytes_[1], step_bytes_[2]};
     CK(cudaMemcpyAsync(d_acc_ + 4, map_acc, sizeof map_acc, cudaMemcpyHostToDevice, stream_));
     const int flags = initial ? 1 : 3;  // GEN modes to reset; pull routes to catch up
     CK(cudaMemcpyAsync(d_post_flags_, &flags, sizeof(int), cudaMemcpyHostToDevice, stream_));
     CK(cudaStreamSynchronize(stream_));
     any_gen_ = routes_differ_ = false;  // k_post_main does them
+    post_pending_ = true;               // (the host-merge protocol's step_main launches it)
     launch_tiles_ = std::min(cap_, int(all_active_.size()) + expand_headroom());
+}
+
+// CTAs (tiles) this rank's launches cover while the global map holds at most
+// launch_tiles_ tiles: every owner has <= ceil(n / devices) tiles (fairness
+// spread <= 1, assign.cpp:8-15) and a rank holds ceil(devices / world) owners.
+int Engine::launch_bound() const {
+    if (world_ == 1) return launch_tiles_;
+    const int per_owner = (launch_tiles_ + devices_ - 1) / devices_;
+    const int owners = (devices_ + world_ - 1) / world_;
+    return std::min(lcap_, per_owner * owners);
 }
 
 // Replays the device's births into the host mirror (slots, log, owners,
@@ -1290,28 +1227,28 @@ void Engine::sync_births() {
         si.fluid = r.fluid;
         si.has_solid = r.has_solid != 0;
         si.owner = r.owner;
-        si.rank = 0;
+        si.rank = r.owner % world_;
         si.local = r.local;
         si.log_index = log_.size();
         log_.push_back({long(r.it), si.c, r.trigger, r.owner});
         grid_slot_[lin(si.c)] = s;
         ++per_dev_[size_t(r.owner)];
-        next_local_[0] = r.local + 1;
+        next_local_[size_t(si.rank)] = r.local + 1;
         h_mode_[s] = long(r.it) >= iteration_ ? MODE_GEN_AMBIENT : MODE_PULL;
         h_has_solid_[s] = uint8_t(r.has_solid);
         h_coords_[3 * size_t(s)] = r.x;
         h_coords_[3 * size_t(s) + 1] = r.y;
         h_coords_[3 * size_t(s) + 2] = r.z;
-        h_lidx_[s] = r.local;
+        h_lidx_[s] = si.rank == rank_ ? r.local : -1;
         active_cells_ += uint64_t(r.fluid);
-        local_cells_ += uint64_t(r.fluid);
+        if (si.rank == rank_) local_cells_ += uint64_t(r.fluid);
     }
     all_active_.clear();
     active_.clear();
     for (size_t k = 0; k < grid_slot_.size(); ++k)
         if (grid_slot_[k] >= 0) {
             all_active_.push_back(grid_slot_[k]);
-            active_.push_back(grid_slot_[k]);
+            if (slots_[grid_slot_[k]].rank == rank_) active_.push_back(grid_slot_[k]);
         }
     recompute_step_bytes();
     synced_births_ = nb;
@@ -1319,7 +1256,15 @@ void Engine::sync_births() {
 }
 
 void Engine::launch_check_expand(long it) {
-    const ExpandDev x = expand_dev();
+    ExpandDev x = expand_dev();
+    if (world_ > 1) {  // this step's parity of every rank's trigger bytes
+        const size_t par = size_t(it & 1);
+        for (int r = 0; r < world_; ++r) {
+            x.ptrig[r] = reinterpret_cast<const uint8_t*>(peer_sync_[r] + 16) + par * trig_bytes_;
+            x.perr[r] = peer_sync_[r] + 8;
+        }
+        x.trig_clear = d_trig_ + (par ^ 1) * trig_bytes_;
+    }
     switch (E_) {
     case 8: k_check_expand<8><<<1, 1024, 0, stream_>>>(d_, x, it, d_halt_); break;
     case 16: k_check_expand<16><<<1, 1024, 0, stream_>>>(d_, x, it, d_halt_); break;
@@ -1332,8 +1277,18 @@ ExpandDev Engine::expand_dev() const {
     ExpandDev x{};
     x.gslot = d_gslot_;
     x.cand = d_cand_;
-    x.active = d_active_;
-    x.nactive = d_nactive_;
+    x.active = world_ > 1 ? d_all_active_ : d_active_;
+    x.nactive = world_ > 1 ? d_nall_ : d_nactive_;
+    x.lactive = d_active_;
+    x.nlactive = d_nactive_;
+    x.world = world_;
+    x.rank = rank_;
+    x.merged = d_merged_;
+    x.merr = d_sync_ + 9;
+    for (int r = 0; r < world_; ++r) {
+        x.peer_f[r] = peer_f_[r];
+        x.peer_pf[r] = peer_pf_[r];
+    }
     x.next_slot = d_next_slot_;
     x.next_local = d_next_local_;
     x.owner = d_owner_;
@@ -1384,7 +1339,7 @@ void Engine::launch_face(int src, int flags, long iter) {
     if (active_.empty()) return;
     EvPair* ev = profiling_ ? &next_event(1, 0) : nullptr;
     if (ev) CK(cudaEventRecord(ev->a, stream_));
-    K_.face(d_, d_active_, src, flags, iter, unsigned(dev_expand_ && d_.nactive ? launch_tiles_ : int(active_.size())),
+    K_.face(d_, d_active_, src, flags, iter, unsigned(dev_expand_ && d_.nactive ? launch_bound() : int(active_.size())),
             stream_);
     CK(cudaGetLastError());
     ++stats_.kernels_launched;
@@ -1395,7 +1350,7 @@ void Engine::launch_face(int src, int flags, long iter) {
 // kernel's screen marked, on the post-stream state in buffer cur_.
 void Engine::launch_p5(long iter) {
     if (active_.empty()) return;
-    K_.p5(d_, d_active_, cur_, iter, unsigned(dev_expand_ && d_.nactive ? launch_tiles_ : int(active_.size())),
+    K_.p5(d_, d_active_, cur_, iter, unsigned(dev_expand_ && d_.nactive ? launch_bound() : int(active_.size())),
           stream_);
     CK(cudaGetLastError());
     ++stats_.kernels_launched;
@@ -1419,7 +1374,7 @@ void Engine::launch_main(long iter) {
     d_.xcol_ok = (fn == K_.main_pc || fn == K_.main_pc2 || fn == K_.main_pc_late || fn == K_.main_pc_mem) && !no_xcol_;
     d_.face_flags = face_fused_ ? (FACE_FUSED | FACE_NAN | (mode_ == PLBM_MODE_PROGRESSIVE ? FACE_CRITERION : 0))
                                 : 0;
-    const int ntiles = dev_expand_ && d_.nactive ? launch_tiles_ : int(active_.size());
+    const int ntiles = dev_expand_ && d_.nactive ? launch_bound() : int(active_.size());
     fn(d_, d_active_, cur_, wu, iter, unsigned(ntiles), stream_);
     CK(cudaGetLastError());
     if (d_.npoke) {  // pokes apply to one step's f_in
@@ -1471,11 +1426,14 @@ plbm_kernel_stats Engine::stats() {
 }
 
 void Engine::check_error(plbm_error* err, bool& failed) {
-    unsigned long long h_err = ~0ull;
-    CK(cudaMemcpyAsync(&h_err, d_err_, sizeof h_err, cudaMemcpyDeviceToHost, stream_));
+    unsigned long long h_err = ERR_NONE_KEY;
+    // several ranks: the merged key of the last device check (identical on
+    // every rank, so every rank raises the same EngineError)
+    CK(cudaMemcpyAsync(&h_err, world_ > 1 && in_spec_ ? err_word() : d_err_, sizeof h_err, cudaMemcpyDeviceToHost,
+                       stream_));
     stats_.d2h_bytes += sizeof h_err;
     CK(cudaStreamSynchronize(stream_));
-    failed = h_err != ~0ull;
+    failed = h_err != ERR_NONE_KEY;
     if (!failed) return;
     const int code = int(h_err & 0xf);
     const long tl = long((h_err >> 4) & 0xffffffffull);
@@ -1485,10 +1443,11 @@ void Engine::check_error(plbm_error* err, bool& failed) {
     const int tx = int(tl / (long(grid_[1]) * grid_[2]));
     const int ty = int((tl / grid_[2]) % grid_[1]);
     const int tz = int(tl % grid_[2]);
-    const char* phase = code == ERR_P5_NAN ? "P5" : "P1";
-    const char* what = code == ERR_P1_NAN    ? "NaN in density"
-                       : code == ERR_P1_POLE ? "pr_pressure: b*rho >= 1 (EOS pole)"
-                                             : "NaN in moments";
+    const char* phase = code == ERR_P5_NAN ? "P5" : code == ERR_PEER_TIMEOUT ? "sync" : "P1";
+    const char* what = code == ERR_P1_NAN         ? "NaN in density"
+                       : code == ERR_P1_POLE      ? "pr_pressure: b*rho >= 1 (EOS pole)"
+                       : code == ERR_PEER_TIMEOUT ? "a peer rank did not reach the step barrier"
+                                                  : "NaN in moments";
     if (err) {
         std::memset(err, 0, sizeof *err);
         err->code = 1;
@@ -1500,8 +1459,27 @@ void Engine::check_error(plbm_error* err, bool& failed) {
         std::snprintf(err->message, sizeof err->message, "iteration %ld, tile (%d,%d,%d), phase %s: %s",
                       it, tx, ty, tz, phase, what);
     }
-    CK(cudaMemsetAsync(d_err_, 0xff, sizeof(unsigned long long), stream_));
+    reset_err();
     CK(cudaStreamSynchronize(stream_));
+}
+
+// Error key words to "no error" (ERR_NONE_KEY: 0x7fff..ff, little endian).
+void Engine::reset_err() {
+    CK(cudaMemsetAsync(d_sync_ + 8, 0xff, 2 * sizeof(unsigned long long), stream_));
+    CK(cudaMemsetAsync(reinterpret_cast<uint8_t*>(d_sync_ + 8) + 7, 0x7f, 1, stream_));
+    CK(cudaMemsetAsync(reinterpret_cast<uint8_t*>(d_sync_ + 9) + 7, 0x7f, 1, stream_));
+}
+
+void Engine::rank_barrier(long it) {
+    PeerFlags pf{};
+    for (int r = 0; r < world_; ++r) pf.p[r] = peer_sync_[r];
+    static const unsigned long long timeout_ns = [] {
+        const char* t = std::getenv("PLBM_BARRIER_TIMEOUT_S");
+        return (unsigned long long)((t ? std::atof(t) : 120.0) * 1e9);
+    }();
+    k_rank_barrier<<<1, 32, 0, stream_>>>(d_sync_, pf, world_, rank_, ++epoch_, d_err_, it, timeout_ns);
+    CK(cudaGetLastError());
+    ++stats_.kernels_launched;
 }
 
 // proj/src/tilemap.cpp:220-266 + proj/src/engine.cpp:554-560
@@ -1562,6 +1540,16 @@ int Engine::step_main(plbm_error* err) {
     const long it = iteration_ + 1;
     launch_main(it);
     cur_ ^= 1;
+    if (post_pending_) {  // the mode / route catch-up upload_expand_state left to the device
+        const int nslot = cap_ + 1;
+        k_post_main<<<std::max(1, std::min(256, (nslot * 18 + 255) / 256)), 256, 0, stream_>>>(
+            d_mode_, d_route_[ROUTE_PULL], d_route_[ROUTE_PSI], nslot, d_post_flags_, d_halt_);
+        CK(cudaGetLastError());
+        CK(cudaMemsetAsync(d_post_flags_, 0, sizeof(int), stream_));
+        ++stats_.kernels_launched;
+        post_pending_ = false;
+        std::fill(h_mode_.begin(), h_mode_.end(), uint8_t(MODE_PULL));  // the mirror of its mode reset
+    }
     if (any_gen_) {
         CK(cudaMemsetAsync(d_mode_, MODE_PULL, size_t(cap_ + 1), stream_));
         std::fill(h_mode_.begin(), h_mode_.end(), uint8_t(MODE_PULL));
@@ -1631,7 +1619,7 @@ void Engine::host_expand(const uint8_t* merged, long it) {
     for (int s : all_active_)
         for (int f = 0; f < 6; ++f)
             if (merged[s] & (1u << f)) triggers.push_back({slots_[s].c, f});
-    CK(cudaMemsetAsync(d_trig_, 0, trig_bytes_, stream_));
+    CK(cudaMemsetAsync(d_trig_, 0, (world_ > 1 ? 2 : 1) * trig_bytes_, stream_));
     if (!triggers.empty()) {
         std::vector<int> created;
         expand(triggers, it, created);
@@ -1661,7 +1649,17 @@ void Engine::enqueue_step(long it) {
                            cudaMemcpyDeviceToDevice, stream_));
         routes_differ_ = false;
     }
-    if (!face_fused_) launch_face(cur_, 3, it);
+    const int fflags = mode_ == PLBM_MODE_PROGRESSIVE ? 3 : 2;
+    if (world_ > 1) {
+        rank_barrier(it);  // every rank's f_post^(it) is complete (k_face pulls across ranks)
+        d_.trig = d_trig_ + size_t(it & 1) * trig_bytes_;
+        launch_face(cur_, fflags, it);
+        launch_p5(it);
+        d_.trig = d_trig_;
+        rank_barrier(it);  // every rank's triggers, error key and psi faces of it are final
+        return;
+    }
+    if (!face_fused_) launch_face(cur_, fflags, it);
     launch_p5(it);
 }
 
@@ -1738,7 +1736,8 @@ int Engine::step_speculative(int n, plbm_error* err) {
         ++done;
         sync_births();  // the mirror catches up with the device's earlier births
         std::vector<uint8_t> trig(trig_bytes_);
-        CK(cudaMemcpyAsync(trig.data(), d_trig_, trig_bytes_, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaMemcpyAsync(trig.data(), world_ > 1 ? d_merged_ : d_trig_, world_ > 1 ? size_t(cap_ + 1) : trig_bytes_,
+                           cudaMemcpyDeviceToHost, stream_));
         stats_.d2h_bytes += trig_bytes_;
         CK(cudaStreamSynchronize(stream_));
         host_expand(trig.data(), e.it);
@@ -1754,16 +1753,18 @@ int Engine::step_speculative(int n, plbm_error* err) {
 }
 
 int Engine::step(int n, plbm_error* err) {
-    if (world_ != 1) {
+    if (world_ != 1 && !prepared_) {
         if (err) {
             std::memset(err, 0, sizeof *err);
             err->code = 2;
             std::snprintf(err->message, sizeof err->message,
-                          "multi-rank engines step with step_begin / all-reduce / step_end");
+                          "engine not prepared (attach peers, then plbm_gpu_prepare on every rank)");
         }
         return 2;
     }
-    if (mode_ == PLBM_MODE_PROGRESSIVE && spec_depth_ > 1) return step_speculative(n, err);
+    // several ranks: device-side barriers and expansion, steps queued ahead
+    // (every rank must call plbm_gpu_step with the same n)
+    if (world_ != 1 || (mode_ == PLBM_MODE_PROGRESSIVE && spec_depth_ > 1)) return step_speculative(n, err);
     if (mode_ == PLBM_MODE_PROGRESSIVE) {
         for (int k = 0; k < n; ++k) {
             int rc = step_begin(err);
@@ -1822,23 +1823,27 @@ int Engine::local_triggers(uint8_t* out, int n) {
 }
 
 int Engine::ipc_handles(void* out) const {
-    cudaIpcMemHandle_t h[2];
+    cudaIpcMemHandle_t h[3];
     CK(cudaIpcGetMemHandle(&h[0], d_pool_f_));
     CK(cudaIpcGetMemHandle(&h[1], d_pool_pf_));
+    CK(cudaIpcGetMemHandle(&h[2], d_sync_));
     std::memcpy(out, h, sizeof h);
     return int(sizeof h);
 }
 
 int Engine::open_peer(int rank, const void* handles) {
     if (rank < 0 || rank >= world_ || rank == rank_) return -1;
-    cudaIpcMemHandle_t h[2];
+    cudaIpcMemHandle_t h[3];
     std::memcpy(h, handles, sizeof h);
     void* f = nullptr;
     void* pf = nullptr;
+    void* sy = nullptr;
     CK(cudaIpcOpenMemHandle(&f, h[0], cudaIpcMemLazyEnablePeerAccess));
     CK(cudaIpcOpenMemHandle(&pf, h[1], cudaIpcMemLazyEnablePeerAccess));
+    CK(cudaIpcOpenMemHandle(&sy, h[2], cudaIpcMemLazyEnablePeerAccess));
     peer_f_[rank] = static_cast<double*>(f);
     peer_pf_[rank] = static_cast<double*>(pf);
+    peer_sync_[rank] = static_cast<unsigned long long*>(sy);
     peer_opened_[rank] = true;
     if (peers_ready()) upload_pointers();
     return 0;
@@ -1848,6 +1853,13 @@ int Engine::set_peer(int rank, void* pool_f, void* pool_pf) {
     if (rank < 0 || rank >= world_ || rank == rank_) return -1;
     peer_f_[rank] = static_cast<double*>(pool_f);
     peer_pf_[rank] = static_cast<double*>(pool_pf);
+    if (peers_ready()) upload_pointers();
+    return 0;
+}
+
+int Engine::set_peer_sync(int rank, void* sync) {
+    if (rank < 0 || rank >= world_ || rank == rank_) return -1;
+    peer_sync_[rank] = static_cast<unsigned long long*>(sync);
     if (peers_ready()) upload_pointers();
     return 0;
 }
@@ -2204,6 +2216,14 @@ int plbm_gpu_set_peer_pools(void* h, int rank, void* pool_f, void* pool_pf) {
 }
 
 void plbm_gpu_pool_pointers(void* h, void** pool_f, void** pool_pf) { EG(h)->pool_pointers(pool_f, pool_pf); }
+void* plbm_gpu_sync_block(void* h) { return EG(h)->sync_block(); }
+int plbm_gpu_set_peer_sync(void* h, int rank, void* sync_block) {
+    try {
+        return EG(h)->set_peer_sync(rank, sync_block);
+    } catch (const std::exception&) {
+        return -6;
+    }
+}
 
 void plbm_gpu_exchange_bytes(void* h, uint64_t* out) { EG(h)->exchange_bytes(out); }
 

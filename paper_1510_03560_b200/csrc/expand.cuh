@@ -21,6 +21,16 @@
 // pre-expansion map, as the reference counts them).  Anything the kernel
 // cannot take (an error, more births than the launched grid has room for)
 // sets the halt flag and leaves the triggers to the host path.
+//
+// Multi-rank (world > 1, one process per GPU): every rank runs this kernel
+// on the SAME merged inputs — the trigger bytes of every rank (each slot's
+// bits are set only by its owner rank, so OR over ranks is the merge) and
+// the lowest error key of every rank, read from the peers' sync blocks over
+// NVLink after a device-side rank barrier (k_rank_barrier) — so every rank's
+// map, placement, halts and EngineError stay identical without a host round
+// trip.  Newborn tile o lives on rank o % world (its pool index from that
+// rank's counter); this rank's launch list (lactive) is rebuilt alongside the
+// global one.
 #pragma once
 
 #include "kernels.cuh"
@@ -45,7 +55,7 @@ struct ExpandDev {
     int* active;                  // [cap] active slots in coordinate order
     int* nactive;                 // active count
     int* next_slot;               // slots are allocated 0, 1, 2, ... (never freed)
-    int* next_local;
+    int* next_local;              // [world] next pool index per rank
     int* owner;                   // [slot]
     int* coords;                  // [slot][3]
     uint8_t* mode;                // [slot]
@@ -53,6 +63,16 @@ struct ExpandDev {
     uint32_t* solid;              // [slot][solid_words]
     int* lidx;                    // [slot]
     int* route_psi;               // [slot][18]
+    int* lactive;                 // [cap] this rank's active slots (== active when world == 1)
+    int* nlactive;                // this rank's active count (== nactive when world == 1)
+    int world, rank;
+    const uint8_t* ptrig[8];      // per rank: this step's trigger bytes (world > 1)
+    const unsigned long long* perr[8];  // per rank: error key word (world > 1)
+    uint8_t* merged;              // [cap + 1] merged trigger bytes (world > 1; read by the host on a halt)
+    unsigned long long* merr;     // merged error key (world > 1; read by the host on a halt)
+    uint8_t* trig_clear;          // this rank's trigger bytes of the next step's parity (world > 1)
+    double* peer_f[8];            // per rank: population pool base
+    double* peer_pf[8];           // per rank: psi-face pool base
     int* route_w;                 // [slot][18] geometric neighbours (A-A stores)
     int nbuf;                     // population buffers (2 = A-B, 1 = A-A)
     uint8_t* bmask;               // [slot]
@@ -116,8 +136,29 @@ __global__ void __launch_bounds__(1024) k_check_expand(Dev d, ExpandDev x, long 
         __syncthreads();
         return s_wsum[w] + __popc(m & ((1u << lane) - 1));
     };
+    // this step's trigger bytes: own (one rank) or merged over every rank
+    const uint8_t* trig = d.trig;
+    if (x.world > 1) {
+        for (int s = tid; s < x.cap + 1; s += NT) {
+            uint8_t v = 0;
+            for (int r = 0; r < x.world; ++r) v |= x.ptrig[r][s];
+            x.merged[s] = v;
+        }
+        trig = x.merged;
+    }
     if (tid == 0) {
-        s_err = (*d.err != ~0ull) ? 1 : 0;
+        unsigned long long e = *(volatile const unsigned long long*)d.err;
+        if (x.world > 1) {
+            // a peer may already be a step ahead: only keys of this step or earlier
+            const unsigned long long lim = ((unsigned long long)(iter + 1)) << 37;
+            e = ERR_NONE_KEY;
+            for (int r = 0; r < x.world; ++r) {
+                const unsigned long long k = *(volatile const unsigned long long*)x.perr[r];
+                if (k < lim && k < e) e = k;
+            }
+            *x.merr = e;
+        }
+        s_err = (e != ERR_NONE_KEY) ? 1 : 0;
         s_supp = 0;
         s_nb = 0;
         s_any = 0;
@@ -139,7 +180,7 @@ __global__ void __launch_bounds__(1024) k_check_expand(Dev d, ExpandDev x, long 
     unsigned supp = 0;
     for (int k = tid; k < na * 6; k += NT) {
         const int s = x.active[k / 6], f = k % 6;
-        if (!(d.trig[s] & (1u << f))) continue;
+        if (!(trig[s] & (1u << f))) continue;
         int q[3] = {x.coords[3 * s], x.coords[3 * s + 1], x.coords[3 * s + 2]};
         q[f >> 1] += (f & 1) ? 1 : -1;
         if (!wrap(q)) {
@@ -170,7 +211,11 @@ __global__ void __launch_bounds__(1024) k_check_expand(Dev d, ExpandDev x, long 
         return;
     }
     if (tid == 0) d.cnt[CNT_SUPP] += s_supp;
-    for (int s = tid; s < x.cap + 1; s += NT) d.trig[s] = 0;
+    // consumed: one rank clears its (only) trigger array; several ranks clear
+    // their array of the NEXT step's parity (every peer finished reading it
+    // before the rank barrier this step's face pass waited on)
+    uint8_t* clr = x.world > 1 ? x.trig_clear : d.trig;
+    for (int s = tid; s < x.cap + 1; s += NT) clr[s] = 0;
     if (nb == 0) return;
     const int first_slot = *x.next_slot;
     const int b0 = *x.nbirths;
@@ -292,12 +337,16 @@ __global__ void __launch_bounds__(1024) k_check_expand(Dev d, ExpandDev x, long 
             ++x.per_dev[chosen];
             x.owner[b.slot] = chosen;
             b.owner = chosen;
-            const int local = (*x.next_local)++;
-            x.lidx[b.slot] = local;
+            // GPU rank owner % world and its next pool index (engine.cu
+            // assign_owner; the fairness spread <= 1 bounds every rank's count
+            // by the pool it allocated, lcap)
+            const int rk = chosen % x.world;
+            const int local = x.next_local[rk]++;
+            x.lidx[b.slot] = rk == x.rank ? local : -1;
             b.local = local;
             for (int bb = 0; bb < 2; ++bb) {
-                x.slot_f[bb][b.slot] = x.pool_f + (size_t(bb % x.nbuf) * (x.lcap + 1) + local) * x.per_slot;
-                x.slot_pf[bb][b.slot] = x.pool_pf + (size_t(bb) * (x.lcap + 1) + local) * x.per_pf;
+                x.slot_f[bb][b.slot] = x.peer_f[rk] + (size_t(bb % x.nbuf) * (x.lcap + 1) + local) * x.per_slot;
+                x.slot_pf[bb][b.slot] = x.peer_pf[rk] + (size_t(bb) * (x.lcap + 1) + local) * x.per_pf;
             }
             add_cells += (unsigned long long)b.fluid;
         }
@@ -311,6 +360,7 @@ __global__ void __launch_bounds__(1024) k_check_expand(Dev d, ExpandDev x, long 
     if (x.capture)
         for (int k = 0; k < nb; ++k) {
             const int slot = first_slot + k;
+            if (x.lidx[slot] < 0) continue;  // another rank's tile
             double* cp = x.capture + size_t(x.lidx[slot]) * P.C * 4 * (E * E * E);
             for (int c = tid; c < P.C * 4 * E * E * E; c += NT) cp[c] = 0.0;
         }
@@ -329,6 +379,22 @@ __global__ void __launch_bounds__(1024) k_check_expand(Dev d, ExpandDev x, long 
     }
     const int nact = s_nb;
     if (tid == 0) *x.nactive = nact;
+    if (x.world > 1) {  // this rank's launch list, coordinate order
+        __syncthreads();
+        if (tid == 0) s_nb = 0;
+        __syncthreads();
+        for (int base = 0; base < ngrid; base += NT) {
+            const int t = base + tid;
+            const int sl = t < ngrid ? x.gslot[t] : -1;
+            const bool mine = sl >= 0 && x.owner[sl] % x.world == x.rank;
+            const int pos = s_nb + block_scan(mine);
+            if (mine) x.lactive[pos] = sl;
+            __syncthreads();
+            if (tid == 0) s_nb += s_chunk;
+            __syncthreads();
+        }
+        if (tid == 0) *x.nlactive = s_nb;
+    }
     // routes (engine.cu compute_routes: faces, then edges hopping along the
     // higher axis first; an absent hop gives the ambient slot), trigger masks
     for (int k = tid; k < nact; k += NT) {
@@ -407,10 +473,44 @@ __global__ void __launch_bounds__(1024) k_check_expand(Dev d, ExpandDev x, long 
         for (int c = 0; c < 3; ++c) x.acc[5 + c] = s_sb[c];
 }
 
+// Device-side barrier of the ranks of one run (one process per GPU, pools
+// and sync blocks mapped over NVLink): every rank stores `epoch` into slot
+// `rank` of every peer's flag words (system-scope release after the fence:
+// the kernels queued before this one on the stream have completed, so their
+// stores are ordered before the flag), then waits until every peer's epoch
+// reached its own flag words.  Launched with identical epochs on every rank
+// (the host counts barriers; every rank queues the same sequence).  A peer
+// that never arrives (it died) turns into an error after `timeout_ns`
+// instead of a hang.
+struct PeerFlags {
+    unsigned long long* p[8];
+};
+static __global__ void k_rank_barrier(unsigned long long* flags, PeerFlags peers, int world, int rank,
+                               unsigned long long epoch, unsigned long long* err, long iter,
+                               unsigned long long timeout_ns) {
+    const int t = threadIdx.x;
+    if (t < world && t != rank) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(peers.p[t] + rank), "l"(epoch) : "memory");
+        const unsigned long long t0 = global_ns();
+        unsigned long long v = 0;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(flags + t) : "memory");
+            if (v >= epoch) break;
+            if (global_ns() - t0 > timeout_ns) {
+                atomicMin(err, ((unsigned long long)iter << 37) | ERR_PEER_TIMEOUT);
+                break;
+            }
+            __nanosleep(64);
+        }
+    }
+    __syncwarp();
+}
+
 // After each step's main kernel: the modes of the tiles born at the end of
 // the previous step go back to PULL, and the pull routes catch up with the
 // psi routes (engine.cu step_main's memset / copy, here device-driven).
-__global__ void k_post_main(uint8_t* mode, int* route_pull, const int* route_psi, int nslot,
+static __global__ void k_post_main(uint8_t* mode, int* route_pull, const int* route_psi, int nslot,
                             int* post_flags, const int* halt) {
     if (*(volatile const int*)halt != 0) return;
     const int f = *(volatile int*)post_flags;

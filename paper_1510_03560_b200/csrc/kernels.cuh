@@ -55,7 +55,10 @@ enum { AA_OFF = 0, AA_LOCAL = 1, AA_NEIGH = 2 };
 __host__ __device__ inline int aa_kind(int aa, long iter) {
     return aa ? ((iter & 1) ? AA_LOCAL : AA_NEIGH) : AA_OFF;
 }
-enum { ERR_NONE = 0, ERR_P1_NAN = 1, ERR_P1_POLE = 2, ERR_P5_NAN = 3 };
+enum { ERR_NONE = 0, ERR_P1_NAN = 1, ERR_P1_POLE = 2, ERR_P5_NAN = 3, ERR_PEER_TIMEOUT = 4 };
+// "no error" value of the error key (atomicMin; also an int64 MAX so a
+// signed MIN reduction across ranks keeps the earliest key)
+constexpr unsigned long long ERR_NONE_KEY = 0x7fffffffffffffffull;
 enum { CNT_NEG = 0, CNT_CLAMP = 1, CNT_ZERO_RHO = 2, CNT_SUPP = 3, CNT_N = 4 };
 
 constexpr int MAX_COMP = 4;
@@ -156,7 +159,7 @@ __device__ __forceinline__ bool halted(const Dev& d) {
 }
 enum { FACE_CRITERION = 1, FACE_NAN = 2, FACE_FUSED = 4 };
 
-__constant__ Params P;
+static __constant__ Params P;  // one copy per translation unit (dispatch.cuh)
 
 // 18 ghost classes: 0..5 faces (-x,+x,-y,+y,-z,+z), 6..17 edges.
 __host__ __device__ inline int edge_class(int a, int b, int da, int db) {
@@ -1062,8 +1065,8 @@ __global__ void __launch_bounds__(NT) k_p5(Dev d, const int* __restrict__ active
 
 // Static batches: after each step, a recorded error halts the steps queued
 // behind it (the state then stays at the failing step, as the reference's).
-__global__ void k_err_halt(const unsigned long long* err, int* halt) {
-    if (*(volatile const unsigned long long*)err != ~0ull) *halt = 1;
+static __global__ void k_err_halt(const unsigned long long* err, int* halt) {
+    if (*(volatile const unsigned long long*)err != ERR_NONE_KEY) *halt = 1;
 }
 
 // Reference-view read-back of one tile (f_read, rho, u) into out:
@@ -1153,7 +1156,7 @@ __global__ void k_gather(Dev d, const int* __restrict__ active, int kind, int c,
     }
 }
 
-__global__ void k_fill(double* p, size_t n, double v) {
+static __global__ void k_fill(double* p, size_t n, double v) {
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
         p[i] = v;
 }
@@ -1164,13 +1167,13 @@ __global__ void k_fill(double* p, size_t n, double v) {
 // Otherwise count the out-of-bounds triggers as suppressed expansions
 // (tilemap.cpp:220-266 counts every out-of-bounds trigger) and clear them, so
 // the next queued step proceeds without a host round trip.  One CTA.
-__global__ void k_check(Dev d, const uint8_t* __restrict__ bmask, const uint8_t* __restrict__ omask,
+static __global__ void k_check(Dev d, const uint8_t* __restrict__ bmask, const uint8_t* __restrict__ omask,
                         int nslot, int* halt) {
     if (*(volatile int*)halt != 0) return;
     __shared__ int s_birth;
     __shared__ unsigned long long s_supp;
     if (threadIdx.x == 0) {
-        s_birth = (*d.err != ~0ull) ? 1 : 0;
+        s_birth = (*d.err != ERR_NONE_KEY) ? 1 : 0;
         s_supp = 0;
     }
     __syncthreads();

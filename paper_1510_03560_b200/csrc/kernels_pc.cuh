@@ -30,7 +30,7 @@
 
 namespace plbm {
 
-__constant__ unsigned char c_xdir[XN] = {0, 2, 3, 4, 5, 6, 8, 10, 12, 14, 15, 16, 17, 18, 2, 8, 10, 12, 14,
+static __constant__ unsigned char c_xdir[XN] = {0, 2, 3, 4, 5, 6, 8, 10, 12, 14, 15, 16, 17, 18, 2, 8, 10, 12, 14,
                                          1, 7, 9, 11, 13, 0, 1, 3, 4, 5, 6, 7, 9, 11, 13, 15, 16, 17, 18};
 
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
@@ -132,15 +132,11 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
     const int warp = tid >> 5;
     const int rank = int(blockIdx.x % T::CL);  // = cluster CTA rank (1-D clusters)
     const int tile_i = int(blockIdx.x / T::CL);
-#ifdef PLBM_RANK_IL  // experiment: components interleaved in the cluster rank
-    const int c = rank % C;
-    const int yb = rank / C;
-    auto crank = [&](int cc, int bb) { return bb * C + cc; };
-#else
+    // (interleaving the components in the rank order measured no different:
+    // the 8 CTAs of a cluster sit on 8 different SMs, tools/probe_cluster.py)
     const int c = rank / NB;                   // this CTA's component
     const int yb = rank % NB;
     auto crank = [&](int cc, int bb) { return cc * NB + bb; };
-#endif
     const int y0 = yb * BY;
     if (d.nactive && d.tile_base + tile_i >= *d.nactive) return;  // (whole clusters: same tile)
     const int slot = active[tile_i];

@@ -1,21 +1,28 @@
 """Multi-GPU stepping: one process per GPU, torch.distributed for plumbing.
 
-The C-ABI does the heavy lifting (the fused kernel reads neighbour tiles owned
-by other ranks directly from their pools over NVLink, CUDA IPC); this module
-is the per-step protocol between ranks (include/plbm_gpu.h "multi-GPU"):
+The C-ABI does the heavy lifting.  The fused kernel reads neighbour tiles
+owned by other ranks directly from their pools over NVLink (CUDA IPC), and
+`plbm_gpu_step` on several ranks synchronises them on the device
+(include/plbm_gpu.h, "multi-GPU"):
 
-    step_main    fused kernel of this rank's tiles
-    barrier      k_face pulls peers' freshly written f_post (1-element
-                 all-reduce on the engine stream)
-    step_face    psi faces for the next step, criterion, local trigger bits
-    all-reduce   MAX over ranks of the trigger bytes (stream-ordered NCCL;
-                 also orders the double-buffered pools for the next step)
-    step_end     identical expansion / placement on every rank's mirror
+    k_main        fused kernel of this rank's tiles
+    rank barrier  flag words in the peers' sync blocks (NVLink stores)
+    k_face, k_p5  psi faces for the next step, criterion, local trigger bits
+    rank barrier
+    k_check_expand  on EVERY rank over the merged trigger bytes and the
+                    lowest error key of all ranks (read over NVLink):
+                    identical map, placement and EngineError everywhere
 
-`merge_triggers` is the pure host-side part, exercised on CPU with gloo.
+so steps are queued ahead with no host collective and no host round trip
+per step.  torch.distributed only exchanges the IPC handles once.
+
+`HostMergeStepper` keeps the round-1 protocol (the host merges the trigger
+bytes with an all-reduce every step), and `merge_triggers` is its pure
+host-side part, exercised on CPU with gloo.
 """
 from __future__ import annotations
 
+import threading
 from typing import Callable, Optional
 
 import numpy as np
@@ -28,11 +35,37 @@ def merge_triggers(local: np.ndarray, all_reduce_max: Callable[[np.ndarray], np.
     return all_reduce_max(np.ascontiguousarray(local, dtype=np.uint8))
 
 
-class DistStepper:
-    """Drives one rank's GpuEngine with torch.distributed.
+def attach_peers(engine, dist) -> None:
+    """Exchange the IPC handles of every rank's pools and sync block, map the
+    peers', prepare, and barrier (the protocol's set-up, once per run)."""
+    world, rank = dist.get_world_size(), dist.get_rank()
+    handles = [None] * world
+    dist.all_gather_object(handles, engine.ipc_handles())
+    for r, h in enumerate(handles):
+        if r != rank:
+            engine.open_peer(r, h)
+    engine.prepare()
+    dist.barrier()
 
-    NCCL (one GPU per rank): both collectives run on the engine's stream, so
-    the host never waits for the kernels except to read the merged triggers.
+
+class DistStepper:
+    """Drives one rank's GpuEngine: plbm_gpu_step with device-side rank
+    barriers and expansion (every rank calls step with the same n)."""
+
+    def __init__(self, engine, dist, device: int):
+        self.eng, self.dist = engine, dist
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        attach_peers(engine, dist)
+
+    def step(self, n: int = 1) -> None:
+        self.eng.step(n)
+
+
+class HostMergeStepper:
+    """The host-merge protocol: step_main, barrier, step_face, all-reduce(MAX)
+    of the trigger bytes, step_end with the merged bytes on every rank.
+
+    NCCL (one GPU per rank): both collectives run on the engine's stream.
     gloo (tests: several ranks sharing one GPU): the engine stream is synced
     and the collectives run on host tensors."""
 
@@ -46,16 +79,7 @@ class DistStepper:
         dev = f"cuda:{device}" if self.nccl else "cpu"
         self.trig = torch.empty(n, dtype=torch.uint8, device=dev)
         self.token = torch.zeros(1, dtype=torch.int32, device=dev)
-        self._attach_peers()
-
-    def _attach_peers(self) -> None:
-        handles = [None] * self.world
-        self.dist.all_gather_object(handles, self.eng.ipc_handles())
-        for r, h in enumerate(handles):
-            if r != self.rank:
-                self.eng.open_peer(r, h)
-        self.eng.prepare()
-        self.dist.barrier()
+        attach_peers(engine, dist)
 
     def step(self, n: int = 1) -> None:
         torch = self.torch
@@ -92,9 +116,31 @@ def _device_u8(ptr: int, n: int, device) -> "torch.Tensor":
     return torch.as_tensor(_CAI(), device=device)
 
 
+def step_ranks_threaded(engines, n: int = 1) -> None:
+    """Several ranks' engines in ONE process (tests on one GPU): each rank's
+    plbm_gpu_step runs on its own host thread (ctypes releases the GIL), the
+    ranks meet in the device-side barriers as separate processes would."""
+    errors = [None] * len(engines)
+
+    def run(k, e):
+        try:
+            e.step(n)
+        except Exception as ex:  # re-raised on the caller's thread
+            errors[k] = ex
+
+    threads = [threading.Thread(target=run, args=(k, e)) for k, e in enumerate(engines)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for ex in errors:
+        if ex is not None:
+            raise ex
+
+
 def step_same_process(engines, n: int = 1, merged_override: Optional[np.ndarray] = None) -> None:
-    """Several ranks' engines in ONE process (tests on one GPU): the merge is
-    a host-side OR of every engine's local trigger bytes."""
+    """The host-merge protocol for several ranks' engines in ONE process: the
+    merge is a host-side OR of every engine's local trigger bytes."""
     for _ in range(n):
         for e in engines:
             e.step_main()

@@ -56,8 +56,8 @@ def test_trigger_merge_over_gloo_world2():
     assert res[0] == want and res[1] == want
 
 
-def _two_rank_run(sc, steps, world=2):
-    engs = [capi.gpu_engine(sc, capture=True, rank=r, world=world) for r in range(world)]
+def _attach(sc, world, storage="ab"):
+    engs = [capi.gpu_engine(sc, capture=True, rank=r, world=world, storage=storage) for r in range(world)]
     pools = [e.pool_pointers() for e in engs]
     for r, e in enumerate(engs):
         for q in range(world):
@@ -65,24 +65,40 @@ def _two_rank_run(sc, steps, world=2):
                 e.set_peer_pools(q, pools[q])
     for e in engs:
         e.prepare()
-    dist.step_same_process(engs, steps)
+    return engs
+
+
+def _two_rank_run(sc, steps, world=2, protocol="device", storage="ab"):
+    engs = _attach(sc, world, storage)
+    if protocol == "device":  # plbm_gpu_step on every rank (device barriers + expansion)
+        for chunk in (1, 2, steps - 3):
+            dist.step_ranks_threaded(engs, chunk)
+    else:                     # host-merge protocol
+        dist.step_same_process(engs, steps)
     return engs
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("protocol,storage", [("device", "ab"), ("host", "ab"), ("device", "aa")])
 @pytest.mark.parametrize("name,world", [("mpmc_e32", 2), ("mpmc_progressive_e16", 2),
                                         ("mpmc_e32_solid_periodic", 2), ("mpmc_s0_3dev", 3),
                                         ("c1_progressive", 2), ("mpmc_islands", 2),
-                                        ("mpmc_e64", 2)])
-def test_ranks_in_one_process_match_single_engine(built, name, world):
+                                        ("mpmc_e64", 2), ("mpmc_channel_e16", 4)])
+def test_ranks_in_one_process_match_single_engine(built, name, world, protocol, storage):
+    """Several ranks' engines in one process on one GPU, attached to each
+    other's pools: the device protocol (plbm_gpu_step with rank barriers and
+    replicated device expansion, one host thread per rank) and the host-merge
+    protocol reproduce one engine bit for bit, with A-B or A-A storage."""
     import numpy as np
     from tests.compare import FIELDS
     make, steps = scenarios.ALL[name]
     sc = make()
+    if storage == "aa" and sc.tile_extent > 32:
+        pytest.skip("A-A storage needs tile_extent <= 32")
     sc.devices = max(sc.devices, world)  # owners spread over the ranks
     single = capi.gpu_engine(sc, capture=True)
     single.step(steps)
-    engs = _two_rank_run(sc, steps, world)
+    engs = _two_rank_run(sc, steps, world, protocol, storage)
     ref_c = single.counters()
     for e in engs:
         c = e.counters()
@@ -104,7 +120,7 @@ def test_ranks_in_one_process_match_single_engine(built, name, world):
     assert len(owners) == world  # the run really was split across ranks
 
 
-def _proc_rank(rank, world, port, name, steps, q):
+def _proc_rank(rank, world, port, name, steps, q, protocol="device"):
     """One rank of a real multi-process run (gloo plumbing, CUDA IPC pools) on
     GPU 0, checked against a single-engine run of the same scenario."""
     try:
@@ -119,8 +135,9 @@ def _proc_rank(rank, world, port, name, steps, q):
         sc = make()
         sc.devices = max(sc.devices, world)
         eng = capi.gpu_engine(sc, capture=True, rank=rank, world=world)
-        stepper = dist.DistStepper(eng, td, 0)
-        stepper.step(steps)
+        stepper = (dist.DistStepper if protocol == "device" else dist.HostMergeStepper)(eng, td, 0)
+        stepper.step(1)
+        stepper.step(steps - 1)
         eng.sync()
         single = capi.gpu_engine(sc, capture=True)
         single.step(steps)
@@ -149,10 +166,12 @@ def _proc_rank(rank, world, port, name, steps, q):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("protocol", ["device", "host"])
 @pytest.mark.parametrize("name", ["mpmc_progressive_e16", "mpmc_e32"])
-def test_two_processes_one_gpu_match_single_engine(built, name):
-    """The DistStepper protocol across real processes (IPC-mapped peer pools,
-    torch.distributed collectives): bit-identical to one engine."""
+def test_two_processes_one_gpu_match_single_engine(built, name, protocol):
+    """Both multi-rank protocols across real processes (IPC-mapped pools and
+    sync blocks; device barriers, or torch.distributed collectives for the
+    host merge): bit-identical to one engine."""
     import socket
     import torch.multiprocessing as mp
     s = socket.socket()
@@ -162,7 +181,7 @@ def test_two_processes_one_gpu_match_single_engine(built, name):
     _, steps = scenarios.ALL[name]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_proc_rank, args=(r, 2, port, name, steps, q)) for r in range(2)]
+    procs = [ctx.Process(target=_proc_rank, args=(r, 2, port, name, steps, q, protocol)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict((r, (m, b)) for r, m, b in (q.get(timeout=600) for _ in procs))
@@ -171,3 +190,51 @@ def test_two_processes_one_gpu_match_single_engine(built, name):
     for r in range(2):
         mine, bad = res[r]
         assert mine > 0 and not bad, (r, mine, bad)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["mpmc_progressive_e16", "mpmc_e32"])
+def test_ranks_agree_on_engine_error(built, name):
+    """EngineError on several ranks: a NaN poked into one rank's tile makes
+    EVERY rank raise the same (iteration, tile, phase) as one engine — the
+    device check merges the lowest error key of all ranks — with iteration and
+    cell_updates not advanced anywhere."""
+    from paper_1510_03560_b200.scenario import EngineError
+    make, _ = scenarios.ALL[name]
+    sc = make()
+    sc.devices = max(sc.devices, 2)
+    single = capi.gpu_engine(sc, capture=True)
+    engs = _attach(sc, 2)
+    single.step(3)
+    dist.step_ranks_threaded(engs, 3)
+    tiles = [t[0] for t in single.tiles()]
+    coords = tiles[len(tiles) // 2]
+    owner = engs[0].tile_rank(coords)
+    E = sc.tile_extent
+    local = (E // 2, E // 2 - 1, E // 2 + 1)
+    single.poke_f(coords, 0, 7, local, float("nan"))
+    engs[owner].poke_f(coords, 0, 7, local, float("nan"))
+    want = None
+    try:
+        single.step(3)
+    except EngineError as e:
+        want = (e.iteration, tuple(e.tile), e.phase)
+    assert want is not None
+    errs = [None, None]
+
+    def run(k):
+        try:
+            engs[k].step(3)
+        except EngineError as ex:
+            errs[k] = (ex.iteration, tuple(ex.tile), ex.phase)
+
+    import threading
+    th = [threading.Thread(target=run, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert errs[0] == want and errs[1] == want, (errs, want)
+    for e in engs:
+        for k in ("iteration", "cell_updates"):
+            assert e.counters()[k] == single.counters()[k], k
