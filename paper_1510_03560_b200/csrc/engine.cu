@@ -511,7 +511,8 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     K_ = pick_kernels(E_, C_, nopsi_);
     if (aa_ && !K_.main_aa[0])
-        throw std::invalid_argument("A-A storage needs tile_extent <= 32 (one CTA or cluster per tile)");
+        throw std::invalid_argument("A-A storage needs one CTA or cluster per tile: tile_extent <= 32, "
+                                    "or 64 with at most 2 components");
     K_.preload();
     {   // this unit's kernels too (lazy loading, see dispatch.cuh preload)
         cudaFuncAttributes a;

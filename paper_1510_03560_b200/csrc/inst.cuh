@@ -13,6 +13,16 @@
 namespace plbm {
 namespace {
 
+// which (E, C) run k_main_pc, and its CTA size
+template <int E>
+struct PcNT {
+    static constexpr int value = E == 64 ? 512 : 256;
+};
+template <int E, int C, bool NOPSI>
+struct HasPc {
+    static constexpr bool value = !NOPSI && (E == 16 || E == 32 || (E == 64 && C <= 2));
+};
+
 template <int E, int C, int LAG, int NT = 256, bool EARLY = true, bool MEMONLY = false, int AA = AA_OFF>
 void launch_pc(Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
     using T = PcCfg<E, C, LAG, NT>;
@@ -50,30 +60,36 @@ Kernels make_kernels() {
     };
     k.main_pc = k.main_pc2 = k.main_pc_late = k.main_pc_mem = nullptr;
     k.main_aa[0] = k.main_aa[1] = nullptr;
-    if constexpr (!NOPSI && (E == 16 || E == 32)) {
+    // k_main_pc: 256-thread CTAs (8 warps, 2 per SM) for E = 16 / 32; for
+    // E = 64 one 512-thread CTA per SM (8 rows of 64 cells, 16 warps) so that
+    // a tile is 8 y-blocks x C components: a 16-CTA cluster at C = 2
+    constexpr int PNT = PcNT<E>::value;
+    if constexpr (HasPc<E, C, NOPSI>::value) {
         auto setup = [](auto fn, int smem, int cl) {
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             if (cl > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         };
-        setup(k_main_pc<E, C, 1>, PcCfg<E, C, 1>::SMEM, PcCfg<E, C, 1>::CL);
-        k.main_pc = launch_pc<E, C, 1>;
-        setup(k_main_pc<E, C, 1, 256, false>, PcCfg<E, C, 1>::SMEM, PcCfg<E, C, 1>::CL);
-        k.main_pc_late = launch_pc<E, C, 1, 256, false>;
+        using T1 = PcCfg<E, C, 1, PNT>;
+        setup(k_main_pc<E, C, 1, PNT>, T1::SMEM, T1::CL);
+        k.main_pc = launch_pc<E, C, 1, PNT>;
+        setup(k_main_pc<E, C, 1, PNT, false>, T1::SMEM, T1::CL);
+        k.main_pc_late = launch_pc<E, C, 1, PNT, false>;
 #ifdef PLBM_PROBES
         if constexpr (E == 32 && C == 2) {
-            setup(k_main_pc<E, C, 1, 256, true, true>, PcCfg<E, C, 1>::SMEM, PcCfg<E, C, 1>::CL);
+            setup(k_main_pc<E, C, 1, 256, true, true>, T1::SMEM, T1::CL);
             k.main_pc_mem = launch_pc<E, C, 1, 256, true, true>;
         }
 #endif
         if constexpr (C <= 2) {
-            setup(k_main_pc<E, C, 2>, PcCfg<E, C, 2>::SMEM, PcCfg<E, C, 2>::CL);
-            k.main_pc2 = launch_pc<E, C, 2>;
+            using T2 = PcCfg<E, C, 2, PNT>;
+            setup(k_main_pc<E, C, 2, PNT>, T2::SMEM, T2::CL);
+            k.main_pc2 = launch_pc<E, C, 2, PNT>;
         }
 #ifndef PLBM_NO_AA
-        setup(k_main_pc<E, C, 1, 256, true, false, AA_LOCAL>, PcCfg<E, C, 1>::SMEM, PcCfg<E, C, 1>::CL);
-        setup(k_main_pc<E, C, 1, 256, true, false, AA_NEIGH>, PcCfg<E, C, 1>::SMEM, PcCfg<E, C, 1>::CL);
-        k.main_aa[0] = launch_pc<E, C, 1, 256, true, false, AA_LOCAL>;
-        k.main_aa[1] = launch_pc<E, C, 1, 256, true, false, AA_NEIGH>;
+        setup(k_main_pc<E, C, 1, PNT, true, false, AA_LOCAL>, T1::SMEM, T1::CL);
+        setup(k_main_pc<E, C, 1, PNT, true, false, AA_NEIGH>, T1::SMEM, T1::CL);
+        k.main_aa[0] = launch_pc<E, C, 1, PNT, true, false, AA_LOCAL>;
+        k.main_aa[1] = launch_pc<E, C, 1, PNT, true, false, AA_NEIGH>;
 #endif
     } else if constexpr (E <= 32) {
 #ifndef PLBM_NO_AA
@@ -121,12 +137,13 @@ Kernels make_kernels() {
             ld((const void*)k_main<E, C, E, NT, NOPSI, E, AA_LOCAL>);
             ld((const void*)k_main<E, C, E, NT, NOPSI, E, AA_NEIGH>);
         }
-        if constexpr (!NOPSI && (E == 16 || E == 32)) {
-            ld((const void*)k_main_pc<E, C, 1>);
-            ld((const void*)k_main_pc<E, C, 1, 256, false>);
-            ld((const void*)k_main_pc<E, C, 1, 256, true, false, AA_LOCAL>);
-            ld((const void*)k_main_pc<E, C, 1, 256, true, false, AA_NEIGH>);
-            if constexpr (C <= 2) ld((const void*)k_main_pc<E, C, 2>);
+        if constexpr (HasPc<E, C, NOPSI>::value) {
+            constexpr int PN = PcNT<E>::value;
+            ld((const void*)k_main_pc<E, C, 1, PN>);
+            ld((const void*)k_main_pc<E, C, 1, PN, false>);
+            ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_LOCAL>);
+            ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_NEIGH>);
+            if constexpr (C <= 2) ld((const void*)k_main_pc<E, C, 2, PN>);
         }
     };
     k.set_params = [](const Params& p, cudaStream_t s) {

@@ -71,7 +71,7 @@ __device__ __forceinline__ const double* psi_ghost_src(const RouteTab& rt, int c
 
 template <int E, int C, int LAG = 1, int NT_ = 256>
 struct PcCfg {
-    static constexpr int NT = NT_;      // 256: 8 warps, 2 CTAs/SM; 128: 4 warps, 4 CTAs/SM
+    static constexpr int NT = NT_;      // 256: 8 warps, 2 CTAs/SM; 512 (E = 64): 16 warps, 1 CTA/SM
     static constexpr int BY = NT / E;   // rows per CTA
     static constexpr int NB = E / BY;   // y-blocks per tile
     static constexpr int CL = NB * C;   // cluster size
@@ -91,7 +91,9 @@ struct PcCfg {
     static_assert(CL <= 16, "cluster size (> 8 needs the non-portable opt-in)");
     static_assert(TSLOTS * CB <= NCOLS / WPQ, "TMEM plane slots do not fit");
     static constexpr int PER_SM = 512 / NT;  // 16 warps per SM
-    static_assert(PER_SM * (SMEM + 8 * 1024) <= 228 * 1024, "CTAs per SM must fit");
+    // static shared memory: the extended-grid solid mask + route tables etc.
+    static constexpr int STATIC_EST = ((E + 2) * (E + 2) * (E + 2) + 31) / 32 * 4 + 3 * 1024;
+    static_assert(PER_SM * (SMEM + STATIC_EST + 1024) <= 228 * 1024, "CTAs per SM must fit");
 };
 
 // LAG = planes between a plane's psi pass and its collision: 1 (psi of z+1

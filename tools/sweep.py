@@ -65,8 +65,8 @@ def timed(eng, steps, chunk=1):
 
 
 def c5(a):
-    for E in (16, 32, 64):
-        for C in (1, 2, 3):
+    for E in a.extents:
+        for C in a.comps:
             sc = S.mpmc_release(n=a.n, extent=E, mode=S.MODE_STATIC, n_components=C)
             eng = capi.gpu_engine(sc, storage=a.storage)
             eng.step(a.warmup)
@@ -204,6 +204,8 @@ def main():
     p.add_argument("--storage", choices=["ab", "aa"], default="ab",
                    help="population storage: two buffers (ab) or one in-place A-A buffer (aa)")
     p.add_argument("--static", action="store_true", help="c4: also the static full mesh")
+    p.add_argument("--extents", type=int, nargs="+", default=[16, 32, 64], help="c5: tile extents")
+    p.add_argument("--comps", type=int, nargs="+", default=[1, 2, 3], help="c5: component counts")
     a = p.parse_args()
     if a.what == "c5":
         a.n = a.n or 256
