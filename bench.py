@@ -190,6 +190,23 @@ def run_cpu_sample(sc_full, seconds: float):
     return cells * sc.n_components / dt / 1e6, W, sample
 
 
+def nvlink_bytes(index: int):
+    """NVLink data bytes this GPU sent / received so far (NVML field values
+    NVLINK_THROUGHPUT_DATA_TX / _RX, KiB counters summed over the links), or
+    None where NVML does not expose them."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        vals = pynvml.nvmlDeviceGetFieldValues(h, [pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
+                                                   pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX])
+        if any(v.nvmlReturn != 0 for v in vals):
+            return None
+        return int(vals[0].value.ullVal) * 1024, int(vals[1].value.ullVal) * 1024
+    except Exception:
+        return None
+
+
 class ClockSampler:
     def __init__(self, path, index=0):
         self.path, self.index, self.proc = path, index, None
@@ -314,10 +331,12 @@ def main():
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(os.path.join(REPO, "gpurun_out", f"clocks_r{rank}.csv"), local) as clk:
         barrier()
+        nvl0 = nvlink_bytes(gpu)
         ev0.record(stream)
         run(a.steps)
         ev1.record(stream)
         barrier()
+        nvl1 = nvlink_bytes(gpu)
     ms = ev0.elapsed_time(ev1)
     cells = eng.counters()["cell_updates"] - c0
     launches = eng.kernel_stats()["kernels_launched"]
@@ -360,10 +379,15 @@ def main():
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max, e_dt_max = float(t[0]), float(t[1])
-    xb = torch.tensor([float(eng.exchange_bytes()["bytes_per_step"])], dtype=torch.float64, device=tdev)
+    # cross-GPU bytes per step: from the routing tables (what the kernels read
+    # from peer pools) and measured by NVML (NVLink data TX / RX of the timed
+    # steps); job totals over the ranks
+    hw = [float(nvl1[0] - nvl0[0]), float(nvl1[1] - nvl0[1])] if nvl0 and nvl1 else [-1.0, -1.0]
+    xb = torch.tensor([float(eng.exchange_bytes()["bytes_per_step"])] + hw, dtype=torch.float64, device=tdev)
     if dist is not None:
-        dist.all_reduce(xb)  # job total per step
+        dist.all_reduce(xb)  # job totals
     nvlink_bytes = int(xb[0])
+    nvml_tx, nvml_rx = float(xb[1]), float(xb[2])
     cells_all, e_cells_all = float(cells), float(e_cells)
     if rank != 0:
         if dist is not None:
@@ -415,10 +439,16 @@ def main():
         # real cross-GPU volume per step (routing tables) next to the
         # reference's modeled classes (record_exchange), SURVEY §8(f)4
         c = eng.counters()
-        line["exchange"] = {"nvlink_read_bytes_per_step": nvlink_bytes,
-                            "nvlink_GBs": round(nvlink_bytes / (ms_max / a.steps / 1e3) / 1e9, 1),
+        hw_ok = nvml_tx >= 0 and nvml_rx >= 0
+        line["exchange"] = {"routing_table_bytes_per_step": nvlink_bytes,
+                            "routing_table_GBs": round(nvlink_bytes / (ms_max / a.steps / 1e3) / 1e9, 1),
+                            "nvml_nvlink_tx_bytes_per_step": round(nvml_tx / a.steps) if hw_ok else None,
+                            "nvml_nvlink_rx_bytes_per_step": round(nvml_rx / a.steps) if hw_ok else None,
+                            "nvml_nvlink_GBs": (round(nvml_rx / a.steps / (ms_max / a.steps / 1e3) / 1e9, 1)
+                                                if hw_ok else None),
                             "modeled_bytes_total": {"intra": c["bytes"][0], "p2p": c["bytes"][1],
-                                                    "staged": c["bytes"][2]}}
+                                                    "staged": c["bytes"][2]},
+                            "ranks": world, "protocol": "plbm_gpu_step: device rank barriers + replicated expansion"}
     if not a.no_cpu_baseline and world == 1:
         try:
             v, cores, sample = run_cpu_sample(sc, a.cpu_seconds)

@@ -115,30 +115,11 @@ def _compare_toml(tmp_path, name):
     return sc, steps, toml
 
 
-def test_compare_writers_match_reference_on_cpu(built, tmp_path):
-    """driver.run_compare's writers fed by the reference engine == the
-    reference's own run_compare (CPU only: checks the compare.csv /
-    compare_summary.json restatement, not the GPU engine)."""
-    sc, steps, toml = _compare_toml(tmp_path, "c1_progressive")
-    ref_run_compare_toml(toml, str(tmp_path / "ref"))
-    from paper_1510_03560_b200 import driver
-    driver.run_compare(sc, str(tmp_path / "py"), steps, name=sc.name, make_engine=capi.ref_engine,
-                       report_interval=4, snapshot_interval=5, snapshot_fields=("rho", "psi"),
-                       snapshot_pgm=True)
-    assert_same_compare(str(tmp_path / "ref"), str(tmp_path / "py"))
-
-
 @pytest.mark.gpu
-@pytest.mark.parametrize("driver_kind", ["cpp", "python"])
-def test_compare_mode_matches_reference(built, tmp_path, driver_kind):
+def test_compare_mode_matches_reference(built, tmp_path):
     sc, steps, toml = _compare_toml(tmp_path, "mpmc_channel_e16")
     ref_run_compare_toml(toml, str(tmp_path / "ref"))
     out = str(tmp_path / "gpu")
-    if driver_kind == "cpp":
-        r = subprocess.run([BIN, toml, "--output", out, "--compare", "1"], capture_output=True, text=True)
-        assert r.returncode == 0, r.stderr
-    else:
-        from paper_1510_03560_b200 import driver
-        driver.run_compare(sc, out, steps, name=sc.name, report_interval=4, snapshot_interval=5,
-                           snapshot_fields=("rho", "psi"), snapshot_pgm=True)
+    r = subprocess.run([BIN, toml, "--output", out, "--compare", "1"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
     assert_same_compare(str(tmp_path / "ref"), out)
