@@ -314,12 +314,33 @@ def main():
 
     run(pre)
     run(a.warmup)
-    tiles_at_start = eng.counters()["tiles"]
 
     def barrier():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
+
+    # ---- end to end through the C-ABI, the reference driver's loop, on the
+    # same steps the reference arm times (right after pre-steps + warm-up)
+    # (engine::run_scenario, proj/src/engine.cpp:640-668): one plbm_gpu_step
+    # per iteration, the report counters read after every step (a superset of
+    # flush_row's reads at report_interval), and with --snapshot-every N the
+    # rho field of every component gathered into a host grid every N steps
+    # (take_snapshot; the reference's default snapshot_interval is 0) -------
+    eng.reset_kernel_stats()
+    e0 = eng.counters()["cell_updates"]
+    barrier()
+    t0 = time.perf_counter()
+    for k in range(1, a.steps + 1):
+        run(1)
+        eng.counters()
+        if world == 1 and a.snapshot_every and k % a.snapshot_every == 0:
+            for c in range(C):
+                eng.gather_field("rho", c)  # host grid (counted in d2h_bytes)
+    barrier()
+    e_dt = time.perf_counter() - t0
+    e_cells = eng.counters()["cell_updates"] - e0
+    e_ks = eng.kernel_stats()
 
     os.makedirs(os.path.join(REPO, "gpurun_out"), exist_ok=True)
     # ---- device-timed region -------------------------------------------------
@@ -327,6 +348,7 @@ def main():
     # the roofline comes from a separate profiled pass of the same steps below)
     eng.reset_kernel_stats()
     c0 = eng.counters()["cell_updates"]
+    tiles_at_start = eng.counters()["tiles"]
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(os.path.join(REPO, "gpurun_out", f"clocks_r{rank}.csv"), local) as clk:
@@ -350,27 +372,6 @@ def main():
     ks = eng.kernel_stats()
     eng.set_profiling(False)
 
-    # ---- end to end through the C-ABI, the reference driver's loop
-    # (engine::run_scenario, proj/src/engine.cpp:640-668): one plbm_gpu_step
-    # per iteration, the report counters read after every step (a superset of
-    # flush_row's reads at report_interval), and with --snapshot-every N the
-    # rho field of every component gathered into a host grid every N steps
-    # (take_snapshot; the reference's default snapshot_interval is 0) -------
-    eng.reset_kernel_stats()
-    e0 = eng.counters()["cell_updates"]
-    barrier()
-    t0 = time.perf_counter()
-    for k in range(1, a.steps + 1):
-        run(1)
-        eng.counters()
-        if world == 1 and a.snapshot_every and k % a.snapshot_every == 0:
-            for c in range(C):
-                eng.gather_field("rho", c)  # host grid (counted in d2h_bytes)
-    barrier()
-    e_dt = time.perf_counter() - t0
-    e_cells = eng.counters()["cell_updates"] - e0
-    e_ks = eng.kernel_stats()
-
     # ---- max over ranks / sums -------------------------------------------------
     # cell_updates is a global count (every rank's mirror sees all tiles), so
     # the job total is taken once; times are the max over ranks.
@@ -386,7 +387,7 @@ def main():
     xb = torch.tensor([float(eng.exchange_bytes()["bytes_per_step"])] + hw, dtype=torch.float64, device=tdev)
     if dist is not None:
         dist.all_reduce(xb)  # job totals
-    nvlink_bytes = int(xb[0])
+    table_bytes = int(xb[0])
     nvml_tx, nvml_rx = float(xb[1]), float(xb[2])
     cells_all, e_cells_all = float(cells), float(e_cells)
     if rank != 0:
@@ -440,8 +441,8 @@ def main():
         # reference's modeled classes (record_exchange), SURVEY §8(f)4
         c = eng.counters()
         hw_ok = nvml_tx >= 0 and nvml_rx >= 0
-        line["exchange"] = {"routing_table_bytes_per_step": nvlink_bytes,
-                            "routing_table_GBs": round(nvlink_bytes / (ms_max / a.steps / 1e3) / 1e9, 1),
+        line["exchange"] = {"routing_table_bytes_per_step": table_bytes,
+                            "routing_table_GBs": round(table_bytes / (ms_max / a.steps / 1e3) / 1e9, 1),
                             "nvml_nvlink_tx_bytes_per_step": round(nvml_tx / a.steps) if hw_ok else None,
                             "nvml_nvlink_rx_bytes_per_step": round(nvml_rx / a.steps) if hw_ok else None,
                             "nvml_nvlink_GBs": (round(nvml_rx / a.steps / (ms_max / a.steps / 1e3) / 1e9, 1)
