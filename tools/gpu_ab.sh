@@ -1,9 +1,18 @@
-# parity + A/B bench of fused-kernel variants: bash tools/gpu_ab.sh "0 2"
+# A/B of two experiment builds (E32 C2): parity subset with the candidate, then
+# alternating bench runs.  usage: bash tools/gpu_ab.sh <candidate> [<baseline>]
 set -x
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
-for v in ${1:-0}; do
-  timeout 600 python bench.py --variant $v --no-cpu-baseline --steps 20 > gpurun_out/bench_v$v.log 2>&1
+CAND=${1:-opt}; BASE=${2:-base}
+PLBM_GPU_LIB=build/exp/lib_$CAND.so timeout 900 python -m pytest tests -m gpu -q -x -k "(mpmc_e32 and (default or aa_)) or c2_100 or (blowup and e32)" > gpurun_out/pytest_$CAND.log 2>&1
+tail -n 3 gpurun_out/pytest_$CAND.log
+for lib in $BASE $CAND $BASE $CAND; do
+  PLBM_GPU_LIB=build/exp/lib_$lib.so timeout 600 python bench.py --no-cpu-baseline --steps 30 >> gpurun_out/bench_ab_$lib.log 2>&1
 done
-tail -n 3 gpurun_out/pytest_gpu.log
-for v in ${1:-0}; do python -c "import json,sys; d=json.loads(open('gpurun_out/bench_v$v.log').read().strip().splitlines()[-1]); print('v$v', d['value'], d['roofline']['kernel_ms_avg'], d['roofline']['face_ms_avg'], d['roofline']['frac'])"; done
+python - <<'PY'
+import json, glob
+for f in sorted(glob.glob("gpurun_out/bench_ab_*.log")):
+    for l in open(f):
+        if l.startswith("{"):
+            d = json.loads(l); r = d["roofline"]
+            print(f, d["value"], r["kernel_ms_avg"], r["frac"], r["face_ms_avg"])
+PY
