@@ -247,3 +247,11 @@ def test_aa_halves_population_memory(built):
         n *= d
     one_buffer = n * sc.n_components * 19 * 8
     assert used_ab - used_aa >= 0.9 * one_buffer, (used_ab, used_aa, one_buffer)
+
+
+def test_aa_rejects_shapes_without_one_cluster_per_tile(built):
+    """A-A needs one CTA or cluster per tile: E = 64 with three components
+    (a 24-CTA cluster) is refused at creation, with the reason."""
+    sc = scenarios.ALL["mpmc3_e64_solid"][0]()
+    with pytest.raises(ValueError, match="A-A storage"):
+        capi.gpu_engine(sc, storage="aa")

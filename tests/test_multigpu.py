@@ -238,3 +238,32 @@ def test_ranks_agree_on_engine_error(built, name):
     for e in engs:
         for k in ("iteration", "cell_updates"):
             assert e.counters()[k] == single.counters()[k], k
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["mpmc_progressive_e16", "c1_progressive"])
+def test_ranks_overflow_to_host_expansion(built, name, monkeypatch):
+    """Several ranks, no launch headroom (PLBM_EXPAND_HEADROOM=0): every birth
+    overflows the launched grid, the device check halts EVERY rank at the
+    same step and each rank's host mirror expands from the merged trigger
+    bytes the device kept — still bit-identical to one engine."""
+    import numpy as np
+    from tests.compare import FIELDS
+    monkeypatch.setenv("PLBM_EXPAND_HEADROOM", "0")
+    make, steps = scenarios.ALL[name]
+    sc = make()
+    sc.devices = max(sc.devices, 2)
+    single = capi.gpu_engine(sc, capture=True)
+    single.step(steps)
+    engs = _two_rank_run(sc, steps, 2, "device")
+    for e in engs:
+        for k in ("iteration", "cell_updates", "suppressed_expansions", "tiles", "bytes"):
+            assert e.counters()[k] == single.counters()[k], k
+        assert e.creation_log() == single.creation_log()
+    for coords, _, _ in single.tiles():
+        r = engs[0].tile_rank(coords)
+        for comp in range(sc.n_components):
+            for f in FIELDS:
+                a = single.read_tile(coords, comp, f)
+                b = engs[r].read_tile(coords, comp, f)
+                assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), (coords, comp, f)
