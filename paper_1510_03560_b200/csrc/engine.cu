@@ -280,14 +280,19 @@ class Engine {
     uint8_t* d_trig_ = nullptr;   // [parity][trig_bytes_] inside d_sync_ (one parity on one rank)
     // Sync block (IPC-exported next to the pools): [0..7] barrier flag words
     // (slot r = the last epoch rank r reached), [8] error key, [9] merged
-    // error key, [16..] trigger bytes of both step parities.
+    // error key, [16..23] this rank's diagnostic counters by step parity
+    // (snapshot at the step's second barrier), [24..] trigger bytes of both
+    // step parities.
+    static constexpr int SYNC_SNAP = 16, SYNC_TRIG = 24;
     unsigned long long* d_sync_ = nullptr;
+    unsigned long long* d_gcnt_ = nullptr;  // job-wide diagnostics of the last device-checked step
+    bool gcnt_valid_ = false;
     std::vector<unsigned long long*> peer_sync_;
     unsigned long long epoch_ = 0;  // rank barriers queued so far (identical on every rank)
     uint8_t* d_merged_ = nullptr;   // world > 1: merged trigger bytes of the last check
     int* d_all_active_ = nullptr;   // world > 1: every rank's slots (the expansion's map)
     int* d_nall_ = nullptr;
-    void rank_barrier(long it);
+    void rank_barrier(long it, bool snapshot = false);
     void reset_err();
     unsigned long long* err_word() const { return world_ > 1 ? d_sync_ + 9 : d_err_; }
     // device-side expansion (one rank progressive, or any multi-rank run; expand.cuh)
@@ -540,11 +545,13 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     d_coords_ = dmalloc<int>(size_t(nslot) * 3);
     d_u_face_ = dmalloc<double>(size_t(lcap_ + 1) * C_ * 6 * 3 * E2_);
     {
-        const size_t sync_words = 16 + (2 * trig_bytes_ + 7) / 8;
+        const size_t sync_words = SYNC_TRIG + (2 * trig_bytes_ + 7) / 8;
         d_sync_ = dmalloc<unsigned long long>(sync_words);
         CK(cudaMemsetAsync(d_sync_, 0, sync_words * sizeof(unsigned long long), stream_));
         d_err_ = d_sync_ + 8;
-        d_trig_ = reinterpret_cast<uint8_t*>(d_sync_ + 16);
+        d_trig_ = reinterpret_cast<uint8_t*>(d_sync_ + SYNC_TRIG);
+        d_gcnt_ = dmalloc<unsigned long long>(CNT_N);
+        CK(cudaMemsetAsync(d_gcnt_, 0, CNT_N * sizeof(unsigned long long), stream_));
     }
     d_bmask_ = dmalloc<uint8_t>(nslot);
     d_omask_ = dmalloc<uint8_t>(nslot);
@@ -786,7 +793,7 @@ void Engine::release() {
         }
     void* ptrs[] = {d_pool_f_, d_pool_pf_, d_slot_f_[0], d_slot_f_[1], d_slot_pf_[0], d_slot_pf_[1],
                     d_route_[0], d_route_[1], d_route_[2], d_lidx_, d_solid_, d_has_solid_, d_mode_, d_coords_,
-                    d_u_face_, d_sync_, d_capture_, d_cnt_, d_all_active_, d_nall_, d_merged_, d_active_,
+                    d_u_face_, d_sync_, d_gcnt_, d_capture_, d_cnt_, d_all_active_, d_nall_, d_merged_, d_active_,
                     d_scratch_slots_,
                     d_readback_, d_dep_cnt_, d_dep_need_, d_geo_, d_bmask_, d_omask_, d_halt_, d_pokes_,
                     d_gslot_, d_cand_, d_nactive_, d_next_slot_, d_next_local_, d_owner_, d_geomdev_, d_p2p_,
@@ -1261,8 +1268,9 @@ void Engine::launch_check_expand(long it) {
     if (world_ > 1) {  // this step's parity of every rank's trigger bytes
         const size_t par = size_t(it & 1);
         for (int r = 0; r < world_; ++r) {
-            x.ptrig[r] = reinterpret_cast<const uint8_t*>(peer_sync_[r] + 16) + par * trig_bytes_;
+            x.ptrig[r] = reinterpret_cast<const uint8_t*>(peer_sync_[r] + SYNC_TRIG) + par * trig_bytes_;
             x.perr[r] = peer_sync_[r] + 8;
+            x.psnap[r] = peer_sync_[r] + SYNC_SNAP + par * CNT_N;
         }
         x.trig_clear = d_trig_ + (par ^ 1) * trig_bytes_;
     }
@@ -1286,6 +1294,7 @@ ExpandDev Engine::expand_dev() const {
     x.rank = rank_;
     x.merged = d_merged_;
     x.merr = d_sync_ + 9;
+    x.gcnt = d_gcnt_;
     for (int r = 0; r < world_; ++r) {
         x.peer_f[r] = peer_f_[r];
         x.peer_pf[r] = peer_pf_[r];
@@ -1471,14 +1480,16 @@ void Engine::reset_err() {
     CK(cudaMemsetAsync(reinterpret_cast<uint8_t*>(d_sync_ + 9) + 7, 0x7f, 1, stream_));
 }
 
-void Engine::rank_barrier(long it) {
+void Engine::rank_barrier(long it, bool snapshot) {
     PeerFlags pf{};
     for (int r = 0; r < world_; ++r) pf.p[r] = peer_sync_[r];
+    unsigned long long* snap = snapshot ? d_sync_ + SYNC_SNAP + size_t(it & 1) * CNT_N : nullptr;
     static const unsigned long long timeout_ns = [] {
         const char* t = std::getenv("PLBM_BARRIER_TIMEOUT_S");
         return (unsigned long long)((t ? std::atof(t) : 120.0) * 1e9);
     }();
-    k_rank_barrier<<<1, 32, 0, stream_>>>(d_sync_, pf, world_, rank_, ++epoch_, d_err_, it, timeout_ns);
+    k_rank_barrier<<<1, 32, 0, stream_>>>(d_sync_, pf, world_, rank_, ++epoch_, d_err_, it, timeout_ns, d_cnt_,
+                                          snap);
     CK(cudaGetLastError());
     ++stats_.kernels_launched;
 }
@@ -1657,7 +1668,9 @@ void Engine::enqueue_step(long it) {
         launch_face(cur_, fflags, it);
         launch_p5(it);
         d_.trig = d_trig_;
-        rank_barrier(it);  // every rank's triggers, error key and psi faces of it are final
+        // every rank's triggers, error key, psi faces and diagnostics of it are final
+        rank_barrier(it, true);
+        gcnt_valid_ = true;
         return;
     }
     if (!face_fused_) launch_face(cur_, fflags, it);
@@ -1881,9 +1894,17 @@ void Engine::counters(plbm_counters* out) {
     stats_.d2h_bytes += sizeof c;
     out->iteration = iteration_;
     out->cell_updates = cell_updates_;
-    out->negative_populations = c[CNT_NEG];  // this rank's tiles
+    out->negative_populations = c[CNT_NEG];  // this rank's tiles (one rank: all)
     out->psi_clamps = c[CNT_CLAMP];
     out->zero_rho_forcings = c[CNT_ZERO_RHO];
+    if (world_ > 1 && gcnt_valid_) {  // job-wide sums of the last step (k_check_expand)
+        unsigned long long g[CNT_N] = {};
+        CK(cudaMemcpyAsync(g, d_gcnt_, sizeof g, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+        out->negative_populations = g[CNT_NEG];
+        out->psi_clamps = g[CNT_CLAMP];
+        out->zero_rho_forcings = g[CNT_ZERO_RHO];
+    }
     out->suppressed_expansions = suppressed_ + c[CNT_SUPP];  // host expand + device k_check
     for (int a = 0; a < 3; ++a) out->bytes[a] = bytes_[a];
     if (dev_expand_) {  // accumulated by k_check_expand

@@ -71,6 +71,8 @@ struct ExpandDev {
     uint8_t* merged;              // [cap + 1] merged trigger bytes (world > 1; read by the host on a halt)
     unsigned long long* merr;     // merged error key (world > 1; read by the host on a halt)
     uint8_t* trig_clear;          // this rank's trigger bytes of the next step's parity (world > 1)
+    const unsigned long long* psnap[8];  // per rank: diagnostic counters at this step's barrier
+    unsigned long long* gcnt;     // job-wide diagnostics (sum over ranks; world > 1)
     double* peer_f[8];            // per rank: population pool base
     double* peer_pf[8];           // per rank: psi-face pool base
     int* route_w;                 // [slot][18] geometric neighbours (A-A stores)
@@ -157,6 +159,12 @@ __global__ void __launch_bounds__(1024) k_check_expand(Dev d, ExpandDev x, long 
                 if (k < lim && k < e) e = k;
             }
             *x.merr = e;
+            // job-wide diagnostics: every rank's counters as of this step
+            for (int k = 0; k < CNT_SUPP; ++k) {
+                unsigned long long sum = 0;
+                for (int r = 0; r < x.world; ++r) sum += *(volatile const unsigned long long*)(x.psnap[r] + k);
+                x.gcnt[k] = sum;
+            }
         }
         s_err = (e != ERR_NONE_KEY) ? 1 : 0;
         s_supp = 0;
@@ -487,8 +495,13 @@ struct PeerFlags {
 };
 static __global__ void k_rank_barrier(unsigned long long* flags, PeerFlags peers, int world, int rank,
                                unsigned long long epoch, unsigned long long* err, long iter,
-                               unsigned long long timeout_ns) {
+                               unsigned long long timeout_ns, const unsigned long long* cnt,
+                               unsigned long long* snap) {
     const int t = threadIdx.x;
+    // (the step's second barrier) this rank's diagnostic counters into the
+    // step-parity slot peers sum after the barrier
+    if (snap && t < CNT_N) snap[t] = cnt[t];
+    __syncwarp();
     if (t < world && t != rank) {
         __threadfence_system();
         asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(peers.p[t] + rank), "l"(epoch) : "memory");
