@@ -325,7 +325,10 @@ class Engine {
     uint8_t* d_bmask_ = nullptr;  // [slot] faces whose trigger would be a birth
     uint8_t* d_omask_ = nullptr;  // [slot] faces whose trigger is out of bounds (suppressed)
     int* d_halt_ = nullptr;       // sticky halt flag of the speculative step queue
-    int* h_flags_ = nullptr;      // pinned copies of the halt flag, one per queued step
+    int* h_flags_ = nullptr;      // pinned copies of the halt flag, one per queued step (+ birth
+                                  // count at h_flags_[8 + k]: sync_births needs no round trip
+                                  // when the retired steps had no births)
+    int births_seen_ = -1;        // birth count of the last retired queued step (-1: unknown)
     cudaEvent_t flag_ev_[8] = {};
     int spec_depth_ = 3;          // steps queued ahead (1 = a host round trip every step)
     bool in_spec_ = false;        // a speculative queue is open (profiling events stay unresolved)
@@ -557,7 +560,7 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     d_omask_ = dmalloc<uint8_t>(nslot);
     d_halt_ = dmalloc<int>(1);
     CK(cudaMemsetAsync(d_halt_, 0, sizeof(int), stream_));
-    CK(cudaMallocHost(&h_flags_, 8 * sizeof(int)));
+    CK(cudaMallocHost(&h_flags_, 16 * sizeof(int)));
     // (environment overrides first: device expansion depends on the queue depth)
     if (const char* sd = std::getenv("PLBM_SPEC_DEPTH")) spec_depth_ = std::max(1, std::min(8, std::atoi(sd)));
     if (const char* fv = std::getenv("PLBM_FACE_VARIANT")) K_.face = K_.face_v[std::atoi(fv) == 1 ? 1 : 0];
@@ -1215,8 +1218,12 @@ void Engine::sync_births() {
     for (size_t s = 0; s < h_mode_.size(); ++s)
         if (h_mode_[s] != MODE_PULL && slots_[s].birth < iteration_) h_mode_[s] = MODE_PULL;
     int nb = 0;
-    CK(cudaMemcpyAsync(&nb, d_nbirths_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
-    CK(cudaStreamSynchronize(stream_));
+    if (births_seen_ >= 0 && !in_spec_) {
+        nb = births_seen_;  // (the queue is drained: the last retired step's count is final)
+    } else {
+        CK(cudaMemcpyAsync(&nb, d_nbirths_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+    }
     if (nb <= synced_births_) return;
     std::vector<BirthRec> recs(size_t(nb - synced_births_));
     CK(cudaMemcpyAsync(recs.data(), d_births_ + synced_births_, recs.size() * sizeof(BirthRec),
@@ -1710,6 +1717,8 @@ int Engine::step_speculative(int n, plbm_error* err) {
             CK(cudaGetLastError());
             ++stats_.kernels_launched;
             CK(cudaMemcpyAsync(&h_flags_[e.flag], d_halt_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+            if (dev_expand_)
+                CK(cudaMemcpyAsync(&h_flags_[8 + e.flag], d_nbirths_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
             CK(cudaEventRecord(flag_ev_[e.flag], stream_));
             stats_.d2h_bytes += sizeof(int);
             q.push_back(e);
@@ -1718,6 +1727,7 @@ int Engine::step_speculative(int n, plbm_error* err) {
         const Queued e = q.front();
         q.pop_front();
         CK(cudaEventSynchronize(flag_ev_[e.flag]));
+        if (dev_expand_) births_seen_ = h_flags_[8 + e.flag];
         if (h_flags_[e.flag] == 0) {  // final (births, if any, done on the device)
             iteration_ = e.it;
             if (!dev_expand_) {  // else counted by k_check_expand
@@ -1888,19 +1898,21 @@ int Engine::rank_of(const int32_t* cc) const {
 
 void Engine::counters(plbm_counters* out) {
     std::memset(out, 0, sizeof *out);
-    unsigned long long c[CNT_N] = {};
+    // every device word in one round trip: this rank's counters, the
+    // job-wide diagnostics (several ranks), the device-side accumulators
+    unsigned long long c[CNT_N] = {}, g[CNT_N] = {}, acc[4] = {};
+    const bool use_g = world_ > 1 && gcnt_valid_;
     CK(cudaMemcpyAsync(c, d_cnt_, sizeof c, cudaMemcpyDeviceToHost, stream_));
+    if (use_g) CK(cudaMemcpyAsync(g, d_gcnt_, sizeof g, cudaMemcpyDeviceToHost, stream_));
+    if (dev_expand_) CK(cudaMemcpyAsync(acc, d_acc_, sizeof acc, cudaMemcpyDeviceToHost, stream_));
     CK(cudaStreamSynchronize(stream_));
-    stats_.d2h_bytes += sizeof c;
+    stats_.d2h_bytes += sizeof c + (use_g ? sizeof g : 0) + (dev_expand_ ? sizeof acc : 0);
     out->iteration = iteration_;
     out->cell_updates = cell_updates_;
     out->negative_populations = c[CNT_NEG];  // this rank's tiles (one rank: all)
     out->psi_clamps = c[CNT_CLAMP];
     out->zero_rho_forcings = c[CNT_ZERO_RHO];
-    if (world_ > 1 && gcnt_valid_) {  // job-wide sums of the last step (k_check_expand)
-        unsigned long long g[CNT_N] = {};
-        CK(cudaMemcpyAsync(g, d_gcnt_, sizeof g, cudaMemcpyDeviceToHost, stream_));
-        CK(cudaStreamSynchronize(stream_));
+    if (use_g) {  // job-wide sums of the last step (k_check_expand)
         out->negative_populations = g[CNT_NEG];
         out->psi_clamps = g[CNT_CLAMP];
         out->zero_rho_forcings = g[CNT_ZERO_RHO];
@@ -1908,16 +1920,13 @@ void Engine::counters(plbm_counters* out) {
     out->suppressed_expansions = suppressed_ + c[CNT_SUPP];  // host expand + device k_check
     for (int a = 0; a < 3; ++a) out->bytes[a] = bytes_[a];
     if (dev_expand_) {  // accumulated by k_check_expand
-        unsigned long long acc[4] = {};
-        CK(cudaMemcpyAsync(acc, d_acc_, sizeof acc, cudaMemcpyDeviceToHost, stream_));
-        CK(cudaStreamSynchronize(stream_));
         out->cell_updates += acc[0];
         for (int a = 0; a < 3; ++a) out->bytes[a] += acc[1 + a];
     }
     out->tiles = all_active_.size();
     out->active_cells = active_cells_;
-    const uint64_t g = uint64_t(E_ + 2) * (E_ + 2) * (E_ + 2);
-    out->bytes_resident = out->tiles * g * (uint64_t(C_) * (2 * Q + 8) * 8 + 1);  // tile.cpp:7-13
+    const uint64_t gc = uint64_t(E_ + 2) * (E_ + 2) * (E_ + 2);
+    out->bytes_resident = out->tiles * gc * (uint64_t(C_) * (2 * Q + 8) * 8 + 1);  // tile.cpp:7-13
 }
 
 int Engine::tiles(int32_t* coords, int32_t* owners, int64_t* births, int max) const {
