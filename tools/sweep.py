@@ -17,6 +17,13 @@
         BASELINE configs[2], the paper's comparison: the same MPMC release run
         on the progressive mesh and on the static full-domain mesh for the
         same number of steps; wall time on the device, tiles over time.
+    python tools/sweep.py ranks [--steps 30]
+        The multi-rank device protocol on ONE GPU: the C2 bench workload split
+        over 1, 2 and 4 ranks' engines in one process (one host thread per
+        rank, attached to each other's pools, stepping with plbm_gpu_step's
+        device barriers and replicated expansion); total MLUPS/comp against
+        the single engine = the protocol's own cost (the ranks share one GPU,
+        so this is not a scaling number).
     python tools/sweep.py placement [--steps 400]
         The paper's GPU-assignment study (simple vs optimized assign_device,
         PAPER.md Figures 13/16) on C4's channel network with 8 simulated
@@ -158,6 +165,41 @@ def c1(a):
                       "speedup": round(ref_s * 1e3 / ms, 1), "same_log_and_counters": same}), flush=True)
 
 
+def ranks(a):
+    from paper_1510_03560_b200 import dist
+    for world in (1, 2, 4):
+        sc = S.bench_c2()
+        sc.devices = max(sc.devices, world)
+        engs = [capi.gpu_engine(sc, rank=r, world=world) for r in range(world)]
+        if world > 1:
+            pools = [e.pool_pointers() for e in engs]
+            for r, e in enumerate(engs):
+                for q in range(world):
+                    if q != r:
+                        e.set_peer_pools(q, pools[q])
+            for e in engs:
+                e.prepare()
+        step = (lambda n: engs[0].step(n)) if world == 1 else (lambda n: dist.step_ranks_threaded(engs, n))
+        step(100 + a.warmup)
+        for e in engs:
+            e.sync()
+        c0 = engs[0].counters()["cell_updates"]
+        t0 = time.perf_counter()
+        step(a.steps)
+        for e in engs:
+            e.sync()
+        dt = time.perf_counter() - t0
+        cells = engs[0].counters()["cell_updates"] - c0
+        print(json.dumps({"sweep": "ranks", "world": world, "gpus": 1, "steps": a.steps,
+                          "tiles": engs[0].counters()["tiles"],
+                          "tiles_per_rank": [len([t for t in engs[0].tiles() if engs[0].tile_rank(t[0]) == r])
+                                             for r in range(world)],
+                          "ms_per_step": round(1e3 * dt / a.steps, 3),
+                          "mlups_per_comp": round(cells * sc.n_components / dt / 1e6, 1)}), flush=True)
+        for e in engs:
+            e.close()
+
+
 def placement(a):
     import numpy as np
     n_dev = 8
@@ -196,7 +238,7 @@ def placement(a):
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("what", choices=["c1", "c5", "c3", "c4", "placement"])
+    p.add_argument("what", choices=["c1", "c5", "c3", "c4", "placement", "ranks"])
     p.add_argument("--n", type=int, default=None)
     p.add_argument("--steps", type=int, default=None)
     p.add_argument("--warmup", type=int, default=3)
@@ -218,6 +260,9 @@ def main():
         a.steps = a.steps or 400
         a.every = 50
         c4(a)
+    elif a.what == "ranks":
+        a.steps = a.steps or 30
+        ranks(a)
     elif a.what == "placement":
         a.n = a.n or 512
         a.steps = a.steps or 400
