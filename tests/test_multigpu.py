@@ -270,3 +270,60 @@ def test_ranks_overflow_to_host_expansion(built, name, monkeypatch):
                 a = single.read_tile(coords, comp, f)
                 b = engs[r].read_tile(coords, comp, f)
                 assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), (coords, comp, f)
+
+
+class _MockEngine:
+    """Stands in for a GpuEngine on CPU: records the plumbing calls."""
+
+    def __init__(self, rank):
+        self.rank, self.opened, self.prepared, self.steps = rank, {}, False, []
+
+    def ipc_handles(self):
+        return bytes([self.rank]) * 192  # 3 x cudaIpcMemHandle_t
+
+    def open_peer(self, r, h):
+        self.opened[r] = h
+
+    def prepare(self):
+        self.prepared = True
+
+    def step(self, n):
+        self.steps.append(n)
+
+
+def _plumbing_worker(rank, world, port, q):
+    import torch.distributed as td
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    td.init_process_group("gloo", rank=rank, world_size=world)
+    eng = _MockEngine(rank)
+    stepper = dist.DistStepper(eng, td, 0)
+    stepper.step(3)
+    stepper.step(1)
+    q.put((rank, sorted(eng.opened), [eng.opened[r][0] for r in sorted(eng.opened)], eng.prepared, eng.steps))
+    td.destroy_process_group()
+
+
+def test_device_protocol_plumbing_over_gloo_world2():
+    """The N > 1 set-up of the device protocol on CPU (gloo, world size 2):
+    every rank all-gathers the IPC handles, opens exactly its peers' handles,
+    prepares, and then steps with plbm_gpu_step alone (no per-step host
+    collective)."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_plumbing_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {r: rest for r, *rest in (q.get(timeout=120) for _ in procs)}
+    for p in procs:
+        p.join(60)
+    for r in range(2):
+        peers, first_bytes, prepared, steps = res[r]
+        assert peers == [1 - r] and first_bytes == [1 - r]
+        assert prepared and steps == [3, 1]
