@@ -135,6 +135,8 @@ void* plbm_gpu_stream(void* h);
  * lowest error key of all ranks (read from the peers' sync blocks) — so the
  * map, placement and any EngineError are identical on every rank, and steps
  * are queued ahead without a host round trip (Engine::step_speculative).
+ * After an EngineError a multi-rank engine stays failed (every later step
+ * reports the same error): create the engines again to start over.
  *
  * The host-merge protocol of round 1 remains for callers that merge the
  * triggers themselves: step_main, a barrier across ranks, step_face, an

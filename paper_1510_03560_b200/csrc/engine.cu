@@ -1450,6 +1450,19 @@ void Engine::check_error(plbm_error* err, bool& failed) {
                        stream_));
     stats_.d2h_bytes += sizeof h_err;
     CK(cudaStreamSynchronize(stream_));
+    if (world_ > 1 && !in_spec_ && peers_ready()) {
+        // host-merge protocol (step_end after the trigger all-reduce: every
+        // rank's face pass of this step is complete): the lowest key of all
+        // ranks, read from the peers' sync blocks; a peer may already have
+        // recorded a key of the next step, which does not count yet
+        const unsigned long long lim = (unsigned long long)(iteration_ + 2) << 37;
+        for (int r = 0; r < world_; ++r) {
+            if (r == rank_) continue;
+            unsigned long long k = ERR_NONE_KEY;
+            CK(cudaMemcpy(&k, peer_sync_[r] + 8, sizeof k, cudaMemcpyDefault));
+            if (k < lim && k < h_err) h_err = k;
+        }
+    }
     failed = h_err != ERR_NONE_KEY;
     if (!failed) return;
     const int code = int(h_err & 0xf);
@@ -1476,7 +1489,13 @@ void Engine::check_error(plbm_error* err, bool& failed) {
         std::snprintf(err->message, sizeof err->message, "iteration %ld, tile (%d,%d,%d), phase %s: %s",
                       it, tx, ty, tz, phase, what);
     }
-    reset_err();
+    // One rank: clear the key so the engine can go on.  Several ranks: a peer
+    // may still have to read this rank's key (its device check or step_end
+    // can run after this host saw the error), so the key stays; it carries
+    // its iteration and every reader filters by iteration, and a multi-rank
+    // engine that raised an EngineError stays failed (the reference's state
+    // after an EngineError is not stepped further either).
+    if (world_ == 1) reset_err();
     CK(cudaStreamSynchronize(stream_));
 }
 

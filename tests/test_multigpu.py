@@ -327,3 +327,51 @@ def test_device_protocol_plumbing_over_gloo_world2():
         peers, first_bytes, prepared, steps = res[r]
         assert peers == [1 - r] and first_bytes == [1 - r]
         assert prepared and steps == [3, 1]
+
+
+@pytest.mark.gpu
+def test_host_merge_protocol_ranks_agree_on_engine_error(built):
+    """The host-merge protocol too: step_end merges the peers' error keys, so
+    a NaN in one rank's tile gives both ranks the single engine's error."""
+    import numpy as np
+    from paper_1510_03560_b200.scenario import EngineError
+    make, _ = scenarios.ALL["mpmc_e32"]
+    sc = make()
+    sc.devices = max(sc.devices, 2)
+    single = capi.gpu_engine(sc, capture=True)
+    engs = _attach(sc, 2)
+    single.step(3)
+    dist.step_same_process(engs, 3)
+    tiles = [t[0] for t in single.tiles()]
+    coords = tiles[len(tiles) // 2]
+    owner = engs[0].tile_rank(coords)
+    local = (16, 15, 17)
+    single.poke_f(coords, 0, 7, local, float("nan"))
+    engs[owner].poke_f(coords, 0, 7, local, float("nan"))
+    want = None
+    try:
+        single.step(3)
+    except EngineError as e:
+        want = (e.iteration, tuple(e.tile), e.phase)
+    assert want is not None
+    errs = [None, None]
+    for _ in range(3):
+        for e in engs:
+            e.step_main()
+        for e in engs:
+            e.sync()
+        for e in engs:
+            e.step_face()
+        for e in engs:
+            e.sync()
+        merged = np.zeros(engs[0].trigger_bytes(), np.uint8)
+        for e in engs:
+            merged |= e.local_triggers()
+        for k, e in enumerate(engs):
+            try:
+                e.step_end(merged)
+            except EngineError as ex:
+                errs[k] = (ex.iteration, tuple(ex.tile), ex.phase)
+        if errs[0] or errs[1]:
+            break
+    assert errs[0] == want and errs[1] == want, (errs, want)
