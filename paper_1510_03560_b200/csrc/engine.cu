@@ -1657,7 +1657,15 @@ void Engine::host_expand(const uint8_t* merged, long it) {
     for (int s : all_active_)
         for (int f = 0; f < 6; ++f)
             if (merged[s] & (1u << f)) triggers.push_back({slots_[s].c, f});
-    CK(cudaMemsetAsync(d_trig_, 0, (world_ > 1 ? 2 : 1) * trig_bytes_, stream_));
+    if (world_ > 1 && in_spec_) {
+        // device protocol, host fallback after a halt at step `it`: a slower
+        // peer's k_check_expand may still read this rank's bytes of step it,
+        // so only the next step's parity is cleared here (step it's bytes are
+        // cleared by this rank's check of step it + 1, after its barrier)
+        CK(cudaMemsetAsync(d_trig_ + size_t((it + 1) & 1) * trig_bytes_, 0, trig_bytes_, stream_));
+    } else {
+        CK(cudaMemsetAsync(d_trig_, 0, (world_ > 1 ? 2 : 1) * trig_bytes_, stream_));
+    }
     if (!triggers.empty()) {
         std::vector<int> created;
         expand(triggers, it, created);
