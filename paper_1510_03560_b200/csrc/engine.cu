@@ -97,6 +97,14 @@ T* dmalloc(size_t n) {
     return p;
 }
 
+// Test hook (ordering stress of the multi-rank protocol):
+// PLBM_TEST_RANK_DELAY_US="<rank>:<us>" makes that rank spin on the device
+// before every step's fused kernel, so it trails its peers.
+__global__ void k_spin(unsigned long long ns) {
+    const unsigned long long t0 = global_ns();
+    while (global_ns() - t0 < ns) __nanosleep(1000);
+}
+
 Kernels pick_kernels(int E, int C, bool nopsi) {
 #ifdef PLBM_ONLY_E32C2  // experiment builds link inst_e32.cu only
     if (E == 32) return pick_kernels_e32(C, nopsi);
@@ -525,7 +533,7 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     {   // this unit's kernels too (lazy loading, see dispatch.cuh preload)
         cudaFuncAttributes a;
         const void* fs[] = {(const void*)k_post_main, (const void*)k_rank_barrier, (const void*)k_check,
-                            (const void*)k_err_halt, (const void*)k_fill};
+                            (const void*)k_err_halt, (const void*)k_fill, (const void*)k_spin};
         for (const void* f : fs) CK(cudaFuncGetAttributes(&a, f));
         switch (E_) {
         case 8: CK(cudaFuncGetAttributes(&a, (const void*)k_check_expand<8>)); break;
@@ -1676,6 +1684,18 @@ void Engine::host_expand(const uint8_t* merged, long it) {
 
 // One step's launches (= step_main + step_face of a single rank).
 void Engine::enqueue_step(long it) {
+    if (world_ > 1) {
+        const std::pair<int, long> delay = [] {
+            const char* v = std::getenv("PLBM_TEST_RANK_DELAY_US");
+            if (!v) return std::pair<int, long>(-1, 0);
+            const char* c = std::strchr(v, ':');
+            return std::pair<int, long>(std::atoi(v), c ? std::atol(c + 1) : 0);
+        }();
+        if (delay.first == rank_ && delay.second > 0) {
+            k_spin<<<1, 1, 0, stream_>>>((unsigned long long)delay.second * 1000ull);
+            CK(cudaGetLastError());
+        }
+    }
     launch_main(it);
     cur_ ^= 1;
     if (dev_expand_) {

@@ -196,13 +196,16 @@ def test_two_processes_one_gpu_match_single_engine(built, name, protocol):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("slow", [None, 0, 1])
 @pytest.mark.parametrize("name", ["mpmc_progressive_e16", "mpmc_e32"])
-def test_ranks_agree_on_engine_error(built, name):
+def test_ranks_agree_on_engine_error(built, name, slow, monkeypatch):
     """EngineError on several ranks: a NaN poked into one rank's tile makes
     EVERY rank raise the same (iteration, tile, phase) as one engine — the
     device check merges the lowest error key of all ranks — with iteration and
     cell_updates not advanced anywhere."""
     from paper_1510_03560_b200.scenario import EngineError
+    if slow is not None:  # one rank trails (ordering stress of the error merge)
+        monkeypatch.setenv("PLBM_TEST_RANK_DELAY_US", f"{slow}:300")
     make, _ = scenarios.ALL[name]
     sc = make()
     sc.devices = max(sc.devices, 2)
@@ -244,8 +247,9 @@ def test_ranks_agree_on_engine_error(built, name):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("slow", [None, 0, 1])
 @pytest.mark.parametrize("name", ["mpmc_progressive_e16", "c1_progressive"])
-def test_ranks_overflow_to_host_expansion(built, name, monkeypatch):
+def test_ranks_overflow_to_host_expansion(built, name, slow, monkeypatch):
     """Several ranks, no launch headroom (PLBM_EXPAND_HEADROOM=0): every birth
     overflows the launched grid, the device check halts EVERY rank at the
     same step and each rank's host mirror expands from the merged trigger
@@ -253,6 +257,8 @@ def test_ranks_overflow_to_host_expansion(built, name, monkeypatch):
     import numpy as np
     from tests.compare import FIELDS
     monkeypatch.setenv("PLBM_EXPAND_HEADROOM", "0")
+    if slow is not None:  # one rank trails (ordering stress of the fallback)
+        monkeypatch.setenv("PLBM_TEST_RANK_DELAY_US", f"{slow}:300")
     make, steps = scenarios.ALL[name]
     sc = make()
     sc.devices = max(sc.devices, 2)
@@ -375,3 +381,33 @@ def test_host_merge_protocol_ranks_agree_on_engine_error(built):
         if errs[0] or errs[1]:
             break
     assert errs[0] == want and errs[1] == want, (errs, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("slow", [0, 1])
+@pytest.mark.parametrize("name", ["mpmc_progressive_e16", "mpmc_channel_e16", "c1_progressive"])
+def test_ranks_with_one_rank_trailing(built, name, slow, monkeypatch):
+    """Ordering stress of the device protocol: one rank spins 300 us on the
+    device before every step, so its peer runs ahead into the barriers, the
+    replicated expansion and the next step's pulls — still bit-identical."""
+    import numpy as np
+    from tests.compare import FIELDS
+    monkeypatch.setenv("PLBM_TEST_RANK_DELAY_US", f"{slow}:300")
+    make, steps = scenarios.ALL[name]
+    sc = make()
+    sc.devices = max(sc.devices, 2)
+    single = capi.gpu_engine(sc, capture=True)
+    single.step(steps)
+    engs = _two_rank_run(sc, steps, 2, "device")
+    for e in engs:
+        for k in ("iteration", "cell_updates", "suppressed_expansions", "tiles", "bytes",
+                  "negative_populations", "psi_clamps"):
+            assert e.counters()[k] == single.counters()[k], k
+        assert e.creation_log() == single.creation_log()
+    for coords, _, _ in single.tiles():
+        r = engs[0].tile_rank(coords)
+        for comp in range(sc.n_components):
+            for f in FIELDS:
+                a = single.read_tile(coords, comp, f)
+                b = engs[r].read_tile(coords, comp, f)
+                assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), (coords, comp, f)
