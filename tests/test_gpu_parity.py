@@ -255,3 +255,38 @@ def test_aa_rejects_shapes_without_one_cluster_per_tile(built):
     sc = scenarios.ALL["mpmc3_e64_solid"][0]()
     with pytest.raises(ValueError, match="A-A storage"):
         capi.gpu_engine(sc, storage="aa")
+
+
+@pytest.mark.parametrize("storage", ["ab", "aa"])
+@pytest.mark.parametrize("name", ["mpmc_progressive_e16", "mpmc_e32"])
+def test_eos_pole_matches_reference(built, name, storage):
+    """proj/src/physics.cpp:12-27: pr_pressure throws when b * rho >= 1.  A
+    rest population of 20 poked into a Peng-Robinson cell (b = 2/21, so rho
+    > 1/b) must give the reference's EngineError (iteration, tile, "P1") and
+    leave iteration / cell_updates where the reference leaves them."""
+    from tests.conftest import have_ref
+    from paper_1510_03560_b200.scenario import EngineError
+    if not have_ref():
+        pytest.skip("reference shim not built")
+    make, _ = scenarios.ALL[name]
+    sc = make()
+    ref = capi.ref_engine(sc)
+    gpu = capi.gpu_engine(sc, capture=True, storage=storage)
+    ref.step(3)
+    gpu.step(3)
+    tiles = [t[0] for t in ref.tiles()]
+    coords = tiles[len(tiles) // 2]
+    E = sc.tile_extent
+    local = (E // 2 + 1, E // 2, E // 2 - 1)
+    ref.poke_f(coords, 0, 0, local, 20.0)
+    gpu.poke_f(coords, 0, 0, local, 20.0)
+    errs = []
+    for eng in (ref, gpu):
+        try:
+            eng.step(2)
+            errs.append(None)
+        except EngineError as e:
+            errs.append((e.iteration, tuple(e.tile), e.phase, "pole" in str(e).lower()))
+    assert errs[0] is not None and errs[0] == errs[1], errs
+    for k in ("iteration", "cell_updates"):
+        assert ref.counters()[k] == gpu.counters()[k], k
