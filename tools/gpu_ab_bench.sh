@@ -1,6 +1,6 @@
 set -x
 mkdir -p gpurun_out; rm -f gpurun_out/bench_ab_*
-for lib in base nointer base nointer; do
+for lib in base ${CAND:-nointer} base ${CAND:-nointer}; do
   PLBM_GPU_LIB=build/exp/lib_$lib.so timeout 600 python bench.py --no-cpu-baseline --steps 30 ${BENCH_ARGS:-} >> gpurun_out/bench_ab_$lib.log 2>&1
 done
 python - <<'PY'
