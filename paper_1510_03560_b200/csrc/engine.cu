@@ -515,7 +515,7 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
         if (world_ == 1) lcap_ = int(n_tiles);
     }
     // f block + xcol side buffer (A-B); A-A keeps one f block and no xcol
-    per_slot_ = size_t(C_) * Q * E3_ + (aa_ ? 0 : size_t(C_) * XN * E2_);
+    per_slot_ = size_t(C_) * Q * E3_ + size_t(C_) * XN * E2_;
     nbuf_ = aa_ ? 1 : 2;
     per_pf_ = size_t(C_) * 6 * E2_;
     const int nslot = cap_ + 1;
@@ -636,7 +636,7 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
         for (int c = 0; c < C_; ++c)
             for (int i = 0; i < Q; ++i) {
                 std::fill_n(amb.begin() + (size_t(c) * Q + i) * E3_, E3_, p.comp[c].feq_amb[i]);
-                for (int cls = 0; cls < 4 && !aa_; ++cls)
+                for (int cls = 0; cls < 4; ++cls)
                     if (xslot_(cls, i) >= 0)
                         std::fill_n(amb.begin() + size_t(C_) * Q * E3_ + (size_t(c) * XN + xslot_(cls, i)) * E2_,
                                     E2_, p.comp[c].feq_amb[i]);
@@ -1396,7 +1396,8 @@ void Engine::launch_main(long iter) {
     if (aa_) fn = K_.main_aa[aa_kind(1, iter) - 1];
     face_fused_ = fusable(fn) && fuse_;
     // the pc kernels write the xcol side buffers the face pass reads
-    d_.xcol_ok = (fn == K_.main_pc || fn == K_.main_pc2 || fn == K_.main_pc_late || fn == K_.main_pc_mem) && !no_xcol_;
+    d_.xcol_ok = (fn == K_.main_pc || fn == K_.main_pc2 || fn == K_.main_pc_late || fn == K_.main_pc_mem ||
+                  (aa_ && K_.aa_xcol)) && !no_xcol_;
     d_.face_flags = face_fused_ ? (FACE_FUSED | FACE_NAN | (mode_ == PLBM_MODE_PROGRESSIVE ? FACE_CRITERION : 0))
                                 : 0;
     const int ntiles = dev_expand_ && d_.nactive ? launch_bound() : int(active_.size());

@@ -90,6 +90,7 @@ Kernels make_kernels() {
         setup(k_main_pc<E, C, 1, PNT, true, false, AA_NEIGH>, T1::SMEM, T1::CL);
         k.main_aa[0] = launch_pc<E, C, 1, PNT, true, false, AA_LOCAL>;
         k.main_aa[1] = launch_pc<E, C, 1, PNT, true, false, AA_NEIGH>;
+        k.aa_xcol = true;
 #endif
     } else if constexpr (E <= 32) {
 #ifndef PLBM_NO_AA

@@ -807,7 +807,10 @@ __device__ __forceinline__ void face_load(const RouteTab& rt, int mode, const in
     int x, y, z;
     face_xyz<E>(face, idx, x, y, z);
     if (hs && solid_at<E>(sb, x, y, z)) return;
-    if (kind != AA_OFF) {  // A-A storage: no xcol buffers, general addressing
+    // x faces from the xcol side buffers (below) whatever the storage kind:
+    // they hold f_post of the boundary columns, i.e. the values the A-B pull
+    // rule reads, which is f_in of the next step under A-A storage too
+    if (kind != AA_OFF && !(xcol && face < 2 && !hs && mode == MODE_PULL)) {  // A-A: general addressing
         if (mode != MODE_PULL) {
             double a0, a1, a2;
             gen_fin<E>(mode, c, tc, x, y, z, f, a0, a1, a2);

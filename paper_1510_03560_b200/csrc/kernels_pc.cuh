@@ -105,8 +105,7 @@ struct PcCfg {
 // MEMONLY (probe, variant 24, NOT a correct step): the same pulls, psi
 // pushes, TMEM stash, stores and xcol staging with the physics removed (psi
 // = 0, f stored unchanged) — the memory pipeline's own ceiling.
-// AA: population storage kind of this step (kernels.cuh AA_*); A-A steps
-// write no xcol side buffers (the face pass reads the SoA block).
+// AA: population storage kind of this step (kernels.cuh AA_*).
 template <int E, int C, int LAG, int NT_ = 256, bool EARLY = true, bool MEMONLY = false, int AA = AA_OFF>
 __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __restrict__ active,
                                                             int src_buf, int write_uface, long iter) {
@@ -182,7 +181,9 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
     const int y = y0 + yl;
     const int xcls = x == 0 ? 0 : x == 1 ? 1 : x == E - 2 ? 2 : x == E - 1 ? 3 : -1;  // xcol lanes
     double* const xcol = d.slot_f[src_buf ^ 1][slot] + size_t(C) * Q * E3 + size_t(c) * XN * E2;
-    const bool wx = AA == AA_OFF && d.xcol_ok != 0;
+    // xcol holds f_post of the boundary columns — the A-B pull's values — so
+    // the face pass reads it the same way whatever the storage kind
+    const bool wx = d.xcol_ok != 0;
     // xcol: the x-column lanes stage their values in shared memory during the
     // collision; after the next CTA barrier the block writes them out as
     // 8-row (64-byte) segments of xcol[c][slot][z][y]
