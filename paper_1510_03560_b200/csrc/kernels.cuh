@@ -340,18 +340,73 @@ struct StoreF {
     int c, x, y, z;
     bool hs;
     const uint32_t* sb;
+    // AA_NEIGH rows of a solid-free tile with z interior (warp-uniform): the
+    // targets (x + e_i, i) from six precomputed bases (this row / the row
+    // across the y edge, each with its x neighbours; nullptr = absent tile,
+    // dropped); every row of such a plane takes it, so no warp lags behind
+    // at the plane barrier.
+    bool fast = false;
+    double *xm = nullptr, *xp = nullptr, *yo = nullptr, *yxm = nullptr, *yxp = nullptr;
     __device__ __forceinline__ void operator()(int i, double v) const {
+        constexpr int E2 = E * E;
         constexpr int E3 = E * E * E;
         if constexpr (AA == AA_OFF) {
             own[size_t(i) * E3] = v;
         } else if constexpr (AA == AA_LOCAL) {
             own[size_t(opp_(i)) * E3] = v;
         } else {
+            if (fast) {
+                const bool cy = (ey_(i) > 0 && y == E - 1) || (ey_(i) < 0 && y == 0);
+                double* b;
+                if (ex_(i) > 0) b = cy ? yxp : (x == E - 1 ? xp : own + 1);
+                else if (ex_(i) < 0) b = cy ? yxm : (x == 0 ? xm : own - 1);
+                else b = cy ? yo : own;
+                if (b) b[i * E3 + ey_(i) * E + ez_(i) * E2] = v;
+                return;
+            }
             double* p = aa_push_addr<E>(*rw, c, hs, sb, x, y, z, i);
             if (p) *p = v;
         }
     }
 };
+
+// A-A pulls of a row of a solid-free tile with z interior (warp-uniform; any
+// y): LOCAL reads (x, i), NEIGH reads (x - e_i, opp i); a source in an absent
+// tile reads feq_amb[i] from the ambient slot.  Six bases as in
+// pull_addr_fast_yedge (this row and the row across the y edge, with their
+// x neighbours).
+template <int E, int AA, class Op>
+__device__ __forceinline__ void pull_addr_row_aa(const RouteTab& rt, int c, int x, int y, int z, Op&& op) {
+    constexpr int E2 = E * E;
+    constexpr int E3 = E * E * E;
+    const size_t cs = size_t(Q) * E3;
+    const int amb = P.amb_slot;
+    const int row = (z * E + y) * E;
+    const double* own = rt.p[13] + c * cs + row + x;
+    const double* bp = x == 0 ? rt.p[12] + c * cs + row + (E - 1) : own - 1;
+    const double* bm = x == E - 1 ? rt.p[14] + c * cs + row : own + 1;
+    const bool ap = x == 0 && rt.s[12] == amb;
+    const bool am = x == E - 1 && rt.s[14] == amb;
+    const int oy = y == 0 ? -1 : 1;      // the row across the y edge (edge rows only)
+    const int wrap = y == 0 ? E2 : -E2;
+    const double* ownY = rt.p[13 + 3 * oy] + c * cs + row + x + wrap;
+    const double* bpY = x == 0 ? rt.p[12 + 3 * oy] + c * cs + row + (E - 1) + wrap : ownY - 1;
+    const double* bmY = x == E - 1 ? rt.p[14 + 3 * oy] + c * cs + row + wrap : ownY + 1;
+    const bool aY = rt.s[13 + 3 * oy] == amb;
+    const bool apY = x == 0 ? rt.s[12 + 3 * oy] == amb : aY;
+    const bool amY = x == E - 1 ? rt.s[14 + 3 * oy] == amb : aY;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+        const bool cy = (ey_(i) > 0 && y == 0) || (ey_(i) < 0 && y == E - 1);
+        const double* b;
+        bool a;
+        if (ex_(i) > 0) { b = cy ? bpY : bp; a = cy ? apY : ap; }
+        else if (ex_(i) < 0) { b = cy ? bmY : bm; a = cy ? amY : am; }
+        else { b = cy ? ownY : own; a = cy && aY; }
+        if constexpr (AA == AA_LOCAL) op(i, (a ? b : own) + size_t(i) * E3);
+        else op(i, a ? b + size_t(i) * E3 : b + (opp_(i) * E3 - ey_(i) * E - ez_(i) * E2));
+    }
+}
 
 // Fast pull for a cell whose y and z neighbours all lie inside the tile and
 // whose tile has no solid cell (warp-uniform in callers: one warp = one x row).

@@ -306,8 +306,10 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
     auto issue_pulls = [&](int pz) {
         if (pz >= E || mode != MODE_PULL || (hs && solid_at<E>(s_solid, x, y, pz))) return;
         auto op = [&](int i, const double* p) { cp_async8(land_u32 + uint32_t(i * NT + tid) * 8u, p); };
-        if constexpr (AA != AA_OFF) pull_addr<E, AA>(rt_pull, c, hs, s_solid, x, y, pz, op);
-        else if (fast_rows && pz >= 1 && pz <= E - 2) pull_addr_fast<E>(rt_pull, c, x, y, pz, op);
+        if constexpr (AA != AA_OFF) {
+            if (mode == MODE_PULL && !hs && pz >= 1 && pz <= E - 2) pull_addr_row_aa<E, AA>(rt_pull, c, x, y, pz, op);
+            else pull_addr<E, AA>(rt_pull, c, hs, s_solid, x, y, pz, op);
+        } else if (fast_rows && pz >= 1 && pz <= E - 2) pull_addr_fast<E>(rt_pull, c, x, y, pz, op);
         else if (fast_yedge && pz >= 1 && pz <= E - 2) pull_addr_fast_yedge<E>(rt_pull, c, x, y, pz, op);
         else pull_addr<E>(rt_pull, c, hs, s_solid, x, y, pz, op);
     };
@@ -439,7 +441,24 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
                 cp[2 * E3 + cell] = u1;
                 cp[3 * E3 + cell] = u2;
             }
-            const StoreF<E, AA> st{fo + cell, &rt_w, c, x, y, z, hs, s_solid};
+            StoreF<E, AA> st{fo + cell, &rt_w, c, x, y, z, hs, s_solid};
+            if constexpr (AA == AA_NEIGH) {
+                if (mode == MODE_PULL && !hs && z >= 1 && z <= E - 2) {
+                    constexpr size_t cs = size_t(Q) * E3;
+                    const int row = (z * E + y) * E;
+                    auto nb = [&](int pat, int off) -> double* {
+                        return rt_w.s[pat] == amb ? nullptr : const_cast<double*>(rt_w.p[pat]) + c * cs + row + off;
+                    };
+                    const int oy = y == E - 1 ? 1 : -1;   // the row across the y edge (edge rows)
+                    const int wrap = y == E - 1 ? -E2 : E2;
+                    st.fast = true;
+                    st.xm = x == 0 ? nb(12, E - 1) : nullptr;
+                    st.xp = x == E - 1 ? nb(14, 0) : nullptr;
+                    st.yo = (y == 0 || y == E - 1) ? nb(13 + 3 * oy, x + wrap) : nullptr;
+                    st.yxm = x == 0 ? nb(12 + 3 * oy, E - 1 + wrap) : (st.yo ? st.yo - 1 : nullptr);
+                    st.yxp = x == E - 1 ? nb(14 + 3 * oy, wrap) : (st.yo ? st.yo + 1 : nullptr);
+                }
+            }
             collide_bgk(f, rho, u0, u1, u2, F0, F1, F2, kc.omega, st, zero_rho, suspect,
                         (xcls >= 0 && wx) ? xst + ((z & 1) * 4 + xcls) * Q * BY + yl : nullptr, BY);
         }
