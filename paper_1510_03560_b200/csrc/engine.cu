@@ -179,7 +179,11 @@ class Engine {
     int poke_f(const int32_t* coords, int comp, int i, const int32_t* local, double v);
     void set_profiling(bool on) { profiling_ = on; }
     int set_variant(int v) {
-        if (aa_) return v == 0 ? 0 : -1;  // A-A storage has one kernel pair
+        if (aa_) {  // A-A storage has one kernel pair; +200 = no xcol side buffers
+            if (v != 0 && v != 200) return -1;
+            no_xcol_ = v == 200;
+            return 0;
+        }
         const int base = v % 100;
         const bool ok = v >= 0 && v < 400 && (base == 0 || base == 1 || base == 21 || base == 22
 #ifdef PLBM_PROBES
@@ -282,6 +286,7 @@ class Engine {
     int* d_lidx_ = nullptr;
     uint32_t* d_solid_ = nullptr;
     uint8_t* d_has_solid_ = nullptr;
+    uint8_t* d_no_fluid_ = nullptr;  // [slot] the tile has no fluid cell (Dev::no_fluid)
     uint8_t* d_mode_ = nullptr;
     int* d_coords_ = nullptr;
     double* d_u_face_ = nullptr;
@@ -552,6 +557,8 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     d_lidx_ = dmalloc<int>(nslot);
     d_solid_ = dmalloc<uint32_t>(size_t(nslot) * solid_words_);
     d_has_solid_ = dmalloc<uint8_t>(nslot);
+    d_no_fluid_ = dmalloc<uint8_t>(nslot);
+    CK(cudaMemsetAsync(d_no_fluid_, 0, nslot, stream_));
     d_mode_ = dmalloc<uint8_t>(nslot);
     d_coords_ = dmalloc<int>(size_t(nslot) * 3);
     d_u_face_ = dmalloc<double>(size_t(lcap_ + 1) * C_ * 6 * 3 * E2_);
@@ -668,6 +675,7 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     d_.lidx = d_lidx_;
     d_.solid = d_solid_;
     d_.has_solid = d_has_solid_;
+    d_.no_fluid = d_no_fluid_;
     d_.mode = d_mode_;
     d_.coords = d_coords_;
     d_.u_face = d_u_face_;
@@ -803,7 +811,8 @@ void Engine::release() {
             cudaIpcCloseMemHandle(peer_sync_[r]);
         }
     void* ptrs[] = {d_pool_f_, d_pool_pf_, d_slot_f_[0], d_slot_f_[1], d_slot_pf_[0], d_slot_pf_[1],
-                    d_route_[0], d_route_[1], d_route_[2], d_lidx_, d_solid_, d_has_solid_, d_mode_, d_coords_,
+                    d_route_[0], d_route_[1], d_route_[2], d_lidx_, d_solid_, d_has_solid_, d_no_fluid_, d_mode_,
+                    d_coords_,
                     d_u_face_, d_sync_, d_gcnt_, d_capture_, d_cnt_, d_all_active_, d_nall_, d_merged_, d_active_,
                     d_scratch_slots_,
                     d_readback_, d_dep_cnt_, d_dep_need_, d_geo_, d_bmask_, d_omask_, d_halt_, d_pokes_,
@@ -1084,6 +1093,12 @@ void Engine::upload_map(const std::vector<int>& new_slots, bool initial) {
     CK(cudaMemcpyAsync(d_coords_, h_coords_.data(), nslot * 3 * sizeof(int), cudaMemcpyHostToDevice,
                        stream_));
     CK(cudaMemcpyAsync(d_has_solid_, h_has_solid_.data(), nslot, cudaMemcpyHostToDevice, stream_));
+    {   // tiles without a fluid cell (from the mirror's fluid counts)
+        std::vector<uint8_t> nf(nslot, 0);
+        for (int s : all_active_) nf[size_t(s)] = slots_[s].fluid == 0 ? 1 : 0;
+        CK(cudaMemcpyAsync(d_no_fluid_, nf.data(), nslot, cudaMemcpyHostToDevice, stream_));
+        CK(cudaStreamSynchronize(stream_));
+    }
     CK(cudaMemcpyAsync(d_mode_, h_mode_.data(), nslot, cudaMemcpyHostToDevice, stream_));
     CK(cudaMemcpyAsync(d_lidx_, h_lidx_.data(), nslot * sizeof(int), cudaMemcpyHostToDevice, stream_));
     std::vector<int> mine;
@@ -1320,6 +1335,7 @@ ExpandDev Engine::expand_dev() const {
     x.coords = d_coords_;
     x.mode = d_mode_;
     x.has_solid = d_has_solid_;
+    x.no_fluid = d_no_fluid_;
     x.solid = d_solid_;
     x.lidx = d_lidx_;
     x.route_psi = d_route_[ROUTE_PSI];

@@ -60,6 +60,7 @@ struct ExpandDev {
     int* coords;                  // [slot][3]
     uint8_t* mode;                // [slot]
     uint8_t* has_solid;           // [slot]
+    uint8_t* no_fluid;            // [slot] (Dev::no_fluid)
     uint32_t* solid;              // [slot][solid_words]
     int* lidx;                    // [slot]
     int* route_psi;               // [slot][18]
@@ -299,6 +300,7 @@ __global__ void __launch_bounds__(1024) k_check_expand(Dev d, ExpandDev x, long 
             b.fluid = tot;
             b.has_solid = s_solid_any;
             x.has_solid[slot] = uint8_t(s_solid_any);
+            x.no_fluid[slot] = uint8_t(tot == 0);
         }
         __syncthreads();
     }

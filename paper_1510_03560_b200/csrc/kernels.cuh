@@ -116,6 +116,13 @@ struct Dev {
     int screen_all;             // the ambient populations fail the screen: k_p5 checks every tile
     unsigned* susp_any;         // [2] by step parity: some tile was marked (nullptr: multi-rank)
     int neg_exact;              // always count negative populations with FP compares (see k_main_pc)
+    // [slot] 1 = the tile has no fluid cell.  Nothing ever reads such a tile:
+    // a fluid cell next to a solid one bounces back (its own populations), a
+    // solid ghost's psi is 0 from the reader's own solid mask, and a reader
+    // without solids (the only one using xcol) cannot border it.  Its
+    // fused-kernel and face-pass CTAs exit at once (state, counters and
+    // read-back are unaffected: it has no fluid cell to update or report).
+    const uint8_t* no_fluid;
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -551,6 +558,7 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
 
     if (d.nactive && d.tile_base + int(blockIdx.x / (NZC * NYC)) >= *d.nactive) return;
     const int slot = active[blockIdx.x / (NZC * NYC)];
+    if (d.no_fluid && d.no_fluid[slot]) return;  // (see Dev::no_fluid)
     const int z0 = (blockIdx.x % NZC) * BZ;
     const int y0 = ((blockIdx.x / NZC) % NYC) * YB;
     const uint8_t mode = d.mode[slot];
@@ -1058,6 +1066,7 @@ __global__ void __launch_bounds__(NT, MINB) k_face(Dev d, const int* __restrict_
     __shared__ int s_tc[3];
     if (d.nactive && d.tile_base + int(blockIdx.x / 6) >= *d.nactive) return;
     const int slot = active[blockIdx.x / 6];
+    if (d.no_fluid && d.no_fluid[slot]) return;  // (see Dev::no_fluid)
     const int face = blockIdx.x % 6;
     const uint8_t mode = d.mode[slot];
     const bool hs = d.has_solid[slot] != 0;
@@ -1095,6 +1104,7 @@ __global__ void __launch_bounds__(NT) k_p5(Dev d, const int* __restrict__ active
     __shared__ int s_tc[3];
     if (d.nactive && d.tile_base + int(blockIdx.x) >= *d.nactive) return;
     const int slot = active[blockIdx.x];
+    if (d.no_fluid && d.no_fluid[slot]) return;  // (see Dev::no_fluid)
     const bool marked = d.suspect[slot] != 0;
     if (!marked && !d.screen_all) return;
     if (d.mode[slot] != MODE_PULL) return;  // (every tile that stepped pulls by now)

@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
     const int y0 = yb * BY;
     if (d.nactive && d.tile_base + tile_i >= *d.nactive) return;  // (whole clusters: same tile)
     const int slot = active[tile_i];
+    if (d.no_fluid && d.no_fluid[slot] && !(d.face_flags & FACE_FUSED)) return;  // (whole clusters: same tile)
     const uint8_t mode = d.mode[slot];
     const bool hs = d.has_solid[slot] != 0;
     const int amb = P.amb_slot;

@@ -117,6 +117,8 @@ def c4(a):
         t0 = time.time()
         sc = S.mpmc_channel(nx=1024, ny=512, nz=512, extent=32, threshold=1e-9, mode=mode)
         eng = capi.gpu_engine(sc, storage=a.storage)
+        if a.variant:
+            eng.set_kernel_variant(a.variant)
         setup_s = time.time() - t0
         series, total_ms, cells = [], 0.0, 0
         for k0 in range(0, a.steps, a.every):
@@ -246,6 +248,7 @@ def main():
     p.add_argument("--storage", choices=["ab", "aa"], default="ab",
                    help="population storage: two buffers (ab) or one in-place A-A buffer (aa)")
     p.add_argument("--static", action="store_true", help="c4: also the static full mesh")
+    p.add_argument("--variant", type=int, default=0, help="c4: fused-kernel variant / modifiers (plbm_gpu.h)")
     p.add_argument("--extents", type=int, nargs="+", default=[16, 32, 64], help="c5: tile extents")
     p.add_argument("--comps", type=int, nargs="+", default=[1, 2, 3], help="c5: component counts")
     a = p.parse_args()
