@@ -115,6 +115,18 @@ int plbm_gpu_set_kernel_variant(void* h, int variant);
 /* The engine's CUDA stream (cudaStream_t) for callers that time with events. */
 void* plbm_gpu_stream(void* h);
 
+/* Population pool footprint: out[0] = bytes of the pool's address range
+ * (nbuf x (tile capacity + 1) x slot), out[1] = bytes physically backed,
+ * out[2] = mapping granule (0: allocated up front), out[3] = microseconds the
+ * engine's mapper thread spent mapping, out[4] = microseconds the stepping
+ * thread waited for it (out has 5 elements).
+ * One-rank engines reserve the range and map device memory in granules (about
+ * 1/64 of the pool, at most 2 GiB) only for the tiles the launches can reach (tiles + expansion headroom), so
+ * a progressive mesh occupies HBM in proportion to its active tiles
+ * (PLBM_POOL_GRANULE_MB overrides the granule; PLBM_LAZY_POOL=0: allocate the whole pool up front, as multi-rank engines
+ * do for their IPC-exported pools). */
+void plbm_gpu_memory(void* h, uint64_t* out);
+
 /* ---- multi-GPU (one process per GPU) -----------------------
  * Every rank builds the same deterministic host mirror from the same
  * descriptor; tile owner o (assign_device) lives on rank o % world.  Each

@@ -363,6 +363,15 @@ class GpuEngine(StepEngine):
     def stream(self) -> int:
         return self.lib.plbm_gpu_stream(self._h)
 
+    def memory(self) -> dict:
+        """Population pool footprint (plbm_gpu_memory): the address range and
+        the bytes physically backed."""
+        out = (C.c_uint64 * 5)()
+        self.lib.plbm_gpu_memory.argtypes = [C.c_void_p, C.c_void_p]
+        self.lib.plbm_gpu_memory(self._h, out)
+        return {"pool_reserved_bytes": out[0], "pool_mapped_bytes": out[1], "granule_bytes": out[2],
+                "map_host_ms": out[3] / 1e3, "map_wait_ms": out[4] / 1e3}
+
 
 def gpu_engine(sc: Scenario, device: int = 0, capture: bool = False, rank: int = 0,
                world: int = 1, storage: str = "ab") -> GpuEngine:

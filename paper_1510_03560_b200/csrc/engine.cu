@@ -21,6 +21,7 @@
 #include "expand.cuh"
 #include "plbm_gpu.h"
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -31,7 +32,13 @@
 #include <cstring>
 #include <memory>
 #include <stdexcept>
+#include <chrono>
+#include <atomic>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 namespace plbm {
@@ -275,6 +282,42 @@ class Engine {
     cudaStream_t stream_ = nullptr;
     Dev d_{};
     double* d_pool_f_ = nullptr;   // [2][lcap+1][per_slot]  (local index lcap = ambient)
+    // One rank: the population pool is a reserved virtual address range whose
+    // physical memory is mapped in granules only for the pool indices the
+    // launches can reach (tiles + expansion headroom) and the ambient slot,
+    // so the progressive mesh's footprint follows its active tiles (the
+    // reference allocates a tile at creation, tilemap.cpp:83-175).
+    bool vm_pool_ = false;
+    CUdeviceptr vm_base_ = 0;
+    size_t vm_size_ = 0, vm_gran_ = 0;
+    std::vector<CUmemGenericAllocationHandle> vm_handles_;  // per granule (0 = unmapped)
+    std::atomic<uint64_t> vm_mapped_{0}, vm_map_us_{0}, vm_wait_us_{0};
+    // A mapper thread backs the pool ahead of the launches (target = the
+    // slots asked for + a quarter), overlapping the driver's mapping work with
+    // the steps; the launching thread waits only when it outruns the mapper.
+    std::thread vm_thread_;
+    mutable std::mutex vm_mu_;
+    std::condition_variable vm_cv_;
+    int vm_want_ = 0, vm_ready_ = 0;  // pool indices [0, n) asked for / backed
+    bool vm_stop_ = false;
+    std::string vm_err_;
+    void vm_reserve(size_t bytes);
+    void vm_map_range(size_t off, size_t len);
+    void vm_mapper();
+    void ensure_pool(int n_slots);  // pool indices [0, n_slots) backed (waits for the mapper)
+    void vm_release();
+
+  public:
+    void memory(uint64_t* out) const {
+        const uint64_t full = uint64_t(nbuf_) * per_slot_ * uint64_t(lcap_ + 1) * sizeof(double);
+        out[0] = vm_pool_ ? vm_size_ : full;
+        out[1] = vm_pool_ ? vm_mapped_.load() : full;
+        out[2] = vm_pool_ ? vm_gran_ : 0;
+        out[3] = vm_map_us_.load();   // mapper thread, microseconds
+        out[4] = vm_wait_us_.load();  // launching thread waiting for it
+    }
+
+  private:
     double* d_pool_pf_ = nullptr;  // [2][lcap+1][per_pf]
     std::vector<double*> peer_f_, peer_pf_;  // pool bases per rank (self = own)
     std::vector<bool> peer_opened_;
@@ -547,7 +590,20 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
         default: CK(cudaFuncGetAttributes(&a, (const void*)k_check_expand<64>)); break;
         }
     }
-    d_pool_f_ = dmalloc<double>(size_t(nbuf_) * per_slot_ * size_t(lcap_ + 1));
+    {
+        const size_t bytes = size_t(nbuf_) * per_slot_ * size_t(lcap_ + 1) * sizeof(double);
+        const char* lz = std::getenv("PLBM_LAZY_POOL");
+        vm_pool_ = world_ == 1 && !(lz && lz[0] == '0');
+        if (vm_pool_) {
+            vm_reserve(bytes);
+            d_pool_f_ = reinterpret_cast<double*>(vm_base_);
+            const size_t slot_b = per_slot_ * sizeof(double);
+            for (int b = 0; b < nbuf_; ++b)  // the ambient slot of each buffer, now
+                vm_map_range((size_t(b) * (lcap_ + 1) + lcap_) * slot_b, slot_b);
+        } else {
+            d_pool_f_ = dmalloc<double>(bytes / sizeof(double));
+        }
+    }
     d_pool_pf_ = dmalloc<double>(2 * per_pf_ * size_t(lcap_ + 1));
     for (int b = 0; b < 2; ++b) {
         d_slot_f_[b] = dmalloc<double*>(nslot);
@@ -810,6 +866,8 @@ void Engine::release() {
             cudaIpcCloseMemHandle(peer_pf_[r]);
             cudaIpcCloseMemHandle(peer_sync_[r]);
         }
+    vm_release();
+    if (vm_pool_) d_pool_f_ = nullptr;
     void* ptrs[] = {d_pool_f_, d_pool_pf_, d_slot_f_[0], d_slot_f_[1], d_slot_pf_[0], d_slot_pf_[1],
                     d_route_[0], d_route_[1], d_route_[2], d_lidx_, d_solid_, d_has_solid_, d_no_fluid_, d_mode_,
                     d_coords_,
@@ -829,6 +887,158 @@ void Engine::release() {
     }
     if (stream_) cudaStreamDestroy(stream_);
     stream_ = nullptr;
+}
+
+// ---- lazily mapped population pool (one rank) ------------------------------
+// driver-API entry points through the runtime (no link-time libcuda
+// dependency: the library still loads on a host without a driver)
+struct VmApi {
+    decltype(&cuMemGetAllocationGranularity) granularity = nullptr;
+    decltype(&cuMemAddressReserve) reserve = nullptr;
+    decltype(&cuMemAddressFree) free = nullptr;
+    decltype(&cuMemCreate) create = nullptr;
+    decltype(&cuMemRelease) release = nullptr;
+    decltype(&cuMemMap) map = nullptr;
+    decltype(&cuMemUnmap) unmap = nullptr;
+    decltype(&cuMemSetAccess) access = nullptr;
+};
+static const VmApi& vm_api() {
+    static VmApi a = [] {
+        VmApi v;
+        auto get = [](const char* name, auto& fn) {
+            void* p = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            CK(cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q));
+            if (!p || q != cudaDriverEntryPointSuccess)
+                throw CudaError(std::string("driver entry point missing: ") + name);
+            fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(p);
+        };
+        get("cuMemGetAllocationGranularity", v.granularity);
+        get("cuMemAddressReserve", v.reserve);
+        get("cuMemAddressFree", v.free);
+        get("cuMemCreate", v.create);
+        get("cuMemRelease", v.release);
+        get("cuMemMap", v.map);
+        get("cuMemUnmap", v.unmap);
+        get("cuMemSetAccess", v.access);
+        return v;
+    }();
+    return a;
+}
+#define CU(x)                                                                                   \
+    do {                                                                                        \
+        CUresult r_ = (x);                                                                      \
+        if (r_ != CUDA_SUCCESS) throw CudaError(std::string(#x) + ": CUresult " + std::to_string(int(r_))); \
+    } while (0)
+
+void Engine::vm_reserve(size_t bytes) {
+    CUmemAllocationProp prop{};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = dev_;
+    CU(vm_api().granularity(&vm_gran_, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+    // A mapping costs ~0.25 ms of host time whatever its size (tools/vm_probe.py,
+    // profiles/r02q_vm_probe.jsonl), paid while the stream waits for the new
+    // tiles: the pool is cut into at most ~64 granules (<= 2 GiB each, a
+    // multiple of the device's granularity), so a run maps at most ~64 times.
+    const char* gm = std::getenv("PLBM_POOL_GRANULE_MB");
+    const size_t want = gm ? size_t(std::max(2, std::atoi(gm))) << 20
+                           : std::min<size_t>(bytes / 64, size_t(2) << 30);
+    vm_gran_ = std::max<size_t>(1, (want + vm_gran_ - 1) / vm_gran_) * vm_gran_;
+    vm_size_ = (bytes + vm_gran_ - 1) / vm_gran_ * vm_gran_;
+    CU(vm_api().reserve(&vm_base_, vm_size_, 0, 0, 0));  // device-granularity aligned
+    vm_handles_.assign(vm_size_ / vm_gran_, 0);
+}
+
+void Engine::vm_map_range(size_t off, size_t len) {
+    if (len == 0) return;
+    const auto t0 = std::chrono::steady_clock::now();
+    CUmemAllocationProp prop{};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = dev_;
+    CUmemAccessDesc acc{};
+    acc.location = prop.location;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    for (size_t g = off / vm_gran_; g <= (off + len - 1) / vm_gran_ && g < vm_handles_.size(); ++g) {
+        if (vm_handles_[g]) continue;
+        CUmemGenericAllocationHandle h;
+        CU(vm_api().create(&h, vm_gran_, &prop, 0));
+        CU(vm_api().map(vm_base_ + g * vm_gran_, vm_gran_, 0, h, 0));
+        CU(vm_api().access(vm_base_ + g * vm_gran_, vm_gran_, &acc, 1));
+        vm_handles_[g] = h;
+        vm_mapped_ += vm_gran_;
+    }
+    vm_map_us_ += uint64_t(
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+}
+
+void Engine::vm_mapper() {
+    const size_t slot_b = per_slot_ * sizeof(double);
+    const size_t buf_b = size_t(lcap_ + 1) * slot_b;
+    const int step = std::max(1, int(vm_gran_ / slot_b));
+    std::unique_lock<std::mutex> lk(vm_mu_);
+    try {
+        CK(cudaSetDevice(dev_));
+        for (;;) {
+            vm_cv_.wait(lk, [&] { return vm_stop_ || vm_want_ > vm_ready_; });
+            if (vm_stop_) return;
+            const int want = vm_want_;
+            while (vm_ready_ < want && !vm_stop_) {
+                const int s0 = vm_ready_, s1 = std::min(want, s0 + step);
+                lk.unlock();
+                for (int b = 0; b < nbuf_; ++b)
+                    vm_map_range(size_t(b) * buf_b + size_t(s0) * slot_b, size_t(s1 - s0) * slot_b);
+                lk.lock();
+                vm_ready_ = s1;
+                vm_cv_.notify_all();
+            }
+        }
+    } catch (const std::exception& e) {
+        if (!lk.owns_lock()) lk.lock();
+        vm_err_ = e.what();
+        vm_cv_.notify_all();
+    }
+}
+
+void Engine::ensure_pool(int n_slots) {
+    if (!vm_pool_) return;
+    n_slots = std::min(n_slots, lcap_);
+    const int ahead = std::max(n_slots / 4, std::max(1, int(vm_gran_ / (per_slot_ * sizeof(double)))));
+    std::unique_lock<std::mutex> lk(vm_mu_);
+    if (!vm_thread_.joinable()) vm_thread_ = std::thread([this] { vm_mapper(); });
+    const int target = std::min(lcap_, n_slots + ahead);
+    if (target > vm_want_) {
+        vm_want_ = target;
+        vm_cv_.notify_all();
+    }
+    if (vm_ready_ < n_slots && vm_err_.empty()) {
+        const auto t0 = std::chrono::steady_clock::now();
+        vm_cv_.wait(lk, [&] { return vm_ready_ >= n_slots || !vm_err_.empty(); });
+        vm_wait_us_ += uint64_t(
+            std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+    }
+    if (!vm_err_.empty()) throw CudaError("population pool mapping: " + vm_err_);
+}
+
+void Engine::vm_release() {
+    if (vm_thread_.joinable()) {
+        {
+            std::lock_guard<std::mutex> lk(vm_mu_);
+            vm_stop_ = true;
+        }
+        vm_cv_.notify_all();
+        vm_thread_.join();
+    }
+    if (!vm_base_) return;
+    for (size_t g = 0; g < vm_handles_.size(); ++g)
+        if (vm_handles_[g]) {
+            vm_api().unmap(vm_base_ + g * vm_gran_, vm_gran_);
+            vm_api().release(vm_handles_[g]);
+        }
+    vm_api().free(vm_base_, vm_size_);
+    vm_base_ = 0;
+    vm_handles_.clear();
 }
 
 // proj/src/tilemap.cpp:56-67
@@ -1087,6 +1297,8 @@ void Engine::upload_map(const std::vector<int>& new_slots, bool initial) {
             all_active_.push_back(grid_slot_[k]);
             if (slots_[grid_slot_[k]].rank == rank_) active_.push_back(grid_slot_[k]);
         }
+    ensure_pool(std::max(next_local_[size_t(rank_)],
+                         std::min(cap_, int(all_active_.size()) + expand_headroom())));
     const size_t nslot = size_t(cap_ + 1);
     CK(cudaMemcpyAsync(d_active_, active_.data(), active_.size() * sizeof(int),
                        cudaMemcpyHostToDevice, stream_));
@@ -1291,6 +1503,7 @@ void Engine::sync_births() {
     recompute_step_bytes();
     synced_births_ = nb;
     launch_tiles_ = std::min(cap_, int(all_active_.size()) + expand_headroom());
+    ensure_pool(launch_tiles_);
 }
 
 void Engine::launch_check_expand(long it) {
@@ -2410,6 +2623,8 @@ void plbm_gpu_reset_kernel_stats(void* h) {
 }
 
 void* plbm_gpu_stream(void* h) { return EG(h)->stream(); }
+
+void plbm_gpu_memory(void* h, uint64_t* out) { EG(h)->memory(out); }
 
 int plbm_gpu_set_kernel_variant(void* h, int variant) { return EG(h)->set_variant(variant); }
 

@@ -228,10 +228,12 @@ def test_aa_expansion_paths_match_oracle(built, name, mode, monkeypatch):
         assert_same_state(orc, gpu, label=f"{name}/aa/{mode}")
 
 
-def test_aa_halves_population_memory(built):
+def test_aa_halves_population_memory(built, monkeypatch):
     """The A-A engine allocates one population buffer: the device memory an
-    engine takes drops by about the size of one buffer."""
+    engine takes drops by about the size of one buffer (pools allocated up
+    front, PLBM_LAZY_POOL=0, so the whole pool is counted)."""
     import torch
+    monkeypatch.setenv("PLBM_LAZY_POOL", "0")
     sc = scenarios.ALL["mpmc_e32"][0]()
     free0 = torch.cuda.mem_get_info()[0]
     ab = capi.gpu_engine(sc)
@@ -290,3 +292,47 @@ def test_eos_pole_matches_reference(built, name, storage):
     assert errs[0] is not None and errs[0] == errs[1], errs
     for k in ("iteration", "cell_updates"):
         assert ref.counters()[k] == gpu.counters()[k], k
+
+
+@pytest.mark.parametrize("storage", ["ab", "aa"])
+def test_lazy_pool_follows_active_tiles(built, storage):
+    """One-rank pools are a reserved address range backed only for the tiles
+    the launches can reach (plus the mapper thread's look-ahead): a
+    progressive run starts with a fraction of the pool mapped, maps more as
+    the mesh grows, and stays bit-exact."""
+    from paper_1510_03560_b200 import scenario as S
+    steps = 12
+    sc = S.mpmc_channel(nx=256, ny=128, nz=128, extent=16, threshold=1e-10)  # 1024-tile capacity
+    orc = capi.oracle_engine(sc)
+    gpu = capi.gpu_engine(sc, capture=True, storage=storage)
+    m0 = gpu.memory()
+    assert 0 < m0["pool_mapped_bytes"] < m0["pool_reserved_bytes"], m0
+    orc.step(steps)
+    gpu.step(steps)
+    assert_same_state(orc, gpu, label=f"lazy/{storage}")
+    m1 = gpu.memory()
+    assert m1["pool_reserved_bytes"] == m0["pool_reserved_bytes"]
+    assert m1["pool_mapped_bytes"] >= m0["pool_mapped_bytes"]
+    # backed: the tiles (+ headroom and the ambient slot) rounded up to
+    # granules per buffer, never the whole capacity of a sparse mesh
+    nb = 1 if storage == "aa" else 2
+    tiles = len(gpu.tiles())
+    slot = m1["pool_reserved_bytes"] / nb / (sc.domain[0] * sc.domain[1] * sc.domain[2] // sc.tile_extent ** 3 + 1)
+    launch = tiles + max(64, tiles // 4)                               # launch_tiles_
+    ahead = launch + max(launch // 4, int(m1["granule_bytes"] // slot))  # the mapper's target
+    bound = nb * ((ahead + 1) * slot + 2 * m1["granule_bytes"])
+    assert m1["pool_mapped_bytes"] <= bound, (m1, tiles, slot)
+
+
+def test_eager_pool_matches_oracle(built, monkeypatch):
+    """PLBM_LAZY_POOL=0 (whole pool allocated up front) is the same engine."""
+    monkeypatch.setenv("PLBM_LAZY_POOL", "0")
+    make, steps = scenarios.ALL["mpmc_channel_e16"]
+    sc = make()
+    orc = capi.oracle_engine(sc)
+    gpu = capi.gpu_engine(sc, capture=True)
+    m = gpu.memory()
+    assert m["pool_mapped_bytes"] == m["pool_reserved_bytes"]
+    orc.step(steps)
+    gpu.step(steps)
+    assert_same_state(orc, gpu, label="eager")

@@ -99,9 +99,14 @@ def c3(a):
         for k0 in range(0, a.steps, a.every):
             ms, cells, _ = timed(eng, min(a.every, a.steps - k0), chunk=1 if mode == S.MODE_PROGRESSIVE else a.every)
             total_ms += ms
-            series.append({"step": k0 + a.every, "tiles": eng.counters()["tiles"], "ms": round(ms, 3)})
+            series.append({"step": k0 + a.every, "tiles": eng.counters()["tiles"], "ms": round(ms, 3),
+                           "pool_GB": round(eng.memory()["pool_mapped_bytes"] / 1e9, 2),
+                           "map_ms": round(eng.memory()["map_host_ms"], 1),
+                           "map_wait_ms": round(eng.memory()["map_wait_ms"], 1)})
         out[name] = {"total_ms": round(total_ms, 2), "final_tiles": eng.counters()["tiles"],
-                     "cell_updates": eng.counters()["cell_updates"], "series": series}
+                     "cell_updates": eng.counters()["cell_updates"],
+                     "pool_mapped_GB": round(eng.memory()["pool_mapped_bytes"] / 1e9, 2),
+                     "pool_reserved_GB": round(eng.memory()["pool_reserved_bytes"] / 1e9, 2), "series": series}
         eng.close()
     out["speedup_progressive_vs_static"] = round(out["static"]["total_ms"] / out["progressive"]["total_ms"], 3)
     print(json.dumps({"sweep": "c3", "domain": a.n, "steps": a.steps, **out}), flush=True)
@@ -110,7 +115,7 @@ def c3(a):
 def c4(a):
     """BASELINE configs[3] on one GPU: the 3-D channel network at full size,
     progressive mesh, and with --static the static full domain on the same
-    scenario (8192 tiles; fits one B200 only with A-A storage)."""
+    scenario (8192 tiles: 174 GB of A-B pool, 87 GB A-A)."""
     modes = [(S.MODE_PROGRESSIVE, "progressive")] + ([(S.MODE_STATIC, "static")] if a.static else [])
     out = {}
     for mode, name in modes:
@@ -127,8 +132,13 @@ def c4(a):
             total_ms += ms
             cells += c
             series.append({"step": k0 + a.every, "tiles": eng.counters()["tiles"], "ms": round(ms, 3),
-                           "mlups_per_comp": round(c * 2 / (ms / 1e3) / 1e6, 1)})
+                           "mlups_per_comp": round(c * 2 / (ms / 1e3) / 1e6, 1),
+                           "pool_GB": round(eng.memory()["pool_mapped_bytes"] / 1e9, 2),
+                           "map_ms": round(eng.memory()["map_host_ms"], 1),
+                           "map_wait_ms": round(eng.memory()["map_wait_ms"], 1)})
         out[name] = {"setup_s": round(setup_s, 2), "total_ms": round(total_ms, 2),
+                     "pool_mapped_GB": round(eng.memory()["pool_mapped_bytes"] / 1e9, 2),
+                     "pool_reserved_GB": round(eng.memory()["pool_reserved_bytes"] / 1e9, 2),
                      "final_tiles": eng.counters()["tiles"], "cell_updates": eng.counters()["cell_updates"],
                      "mlups_per_comp": round(cells * 2 / (total_ms / 1e3) / 1e6, 1), "series": series}
         fluid = round(1 - float(sc.geometry.mean()), 4)
