@@ -23,11 +23,18 @@ struct HasPc {
     static constexpr bool value = !NOPSI && (E == 16 || E == 32 || (E == 64 && C <= 2));
 };
 
-template <int E, int C, int LAG, int NT = 256, bool EARLY = true, bool MEMONLY = false, int AA = AA_OFF>
+// half-tile clusters (NH = 2) where a whole-tile cluster has more than 4 CTAs
+template <int E, int C, bool NOPSI>
+struct HasHalf {
+    static constexpr bool value = HasPc<E, C, NOPSI>::value && E >= 32;
+};
+
+template <int E, int C, int LAG, int NT = 256, bool EARLY = true, bool MEMONLY = false, int AA = AA_OFF,
+          int NH = 1>
 void launch_pc(Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
-    using T = PcCfg<E, C, LAG, NT>;
+    using T = PcCfg<E, C, LAG, NT, NH>;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ntiles * T::CL);
+    cfg.gridDim = dim3(ntiles * NH * T::CL);
     cfg.blockDim = dim3(T::NT);
     cfg.dynamicSmemBytes = T::SMEM;
     cfg.stream = s;
@@ -38,7 +45,7 @@ void launch_pc(Dev d, const int* act, int src, int wu, long it, unsigned ntiles,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_main_pc<E, C, LAG, NT, EARLY, MEMONLY, AA>, d, act, src, wu, it);
+    cudaLaunchKernelEx(&cfg, k_main_pc<E, C, LAG, NT, EARLY, MEMONLY, AA, NH>, d, act, src, wu, it);
 }
 
 template <int E, int C, bool NOPSI>
@@ -58,8 +65,9 @@ Kernels make_kernels() {
     k.main_plain = [](Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
         k_main<E, C, BZ, NT, NOPSI, YB><<<ntiles * (E / BZ) * (E / YB), NT, SMEM_PLAIN, s>>>(d, act, src, wu, it);
     };
-    k.main_pc = k.main_pc2 = k.main_pc_late = k.main_pc_mem = nullptr;
-    k.main_aa[0] = k.main_aa[1] = nullptr;
+    k.main_pc = k.main_pc2 = k.main_pc_late = k.main_pc_mem = k.main_pc_half = nullptr;
+    k.main_aa[0] = k.main_aa[1] = k.main_aa_half[0] = k.main_aa_half[1] = nullptr;
+    k.mid_faces = HasHalf<E, C, NOPSI>::value;
     // k_main_pc: 256-thread CTAs (8 warps, 2 per SM) for E = 16 / 32; for
     // E = 64 one 512-thread CTA per SM (8 rows of 64 cells, 16 warps) so that
     // a tile is 8 y-blocks x C components: a 16-CTA cluster at C = 2
@@ -84,6 +92,17 @@ Kernels make_kernels() {
             using T2 = PcCfg<E, C, 2, PNT>;
             setup(k_main_pc<E, C, 2, PNT>, T2::SMEM, T2::CL);
             k.main_pc2 = launch_pc<E, C, 2, PNT>;
+        }
+        if constexpr (HasHalf<E, C, NOPSI>::value) {
+            using TH = PcCfg<E, C, 1, PNT, 2>;
+            setup(k_main_pc<E, C, 1, PNT, true, false, AA_OFF, 2>, TH::SMEM, TH::CL);
+            k.main_pc_half = launch_pc<E, C, 1, PNT, true, false, AA_OFF, 2>;
+#ifndef PLBM_NO_AA
+            setup(k_main_pc<E, C, 1, PNT, true, false, AA_LOCAL, 2>, TH::SMEM, TH::CL);
+            setup(k_main_pc<E, C, 1, PNT, true, false, AA_NEIGH, 2>, TH::SMEM, TH::CL);
+            k.main_aa_half[0] = launch_pc<E, C, 1, PNT, true, false, AA_LOCAL, 2>;
+            k.main_aa_half[1] = launch_pc<E, C, 1, PNT, true, false, AA_NEIGH, 2>;
+#endif
         }
 #ifndef PLBM_NO_AA
         setup(k_main_pc<E, C, 1, PNT, true, false, AA_LOCAL>, T1::SMEM, T1::CL);
@@ -113,10 +132,10 @@ Kernels make_kernels() {
     // k_face at 4 CTAs/SM, one item in flight per thread (64 registers),
     // measured faster than 2 CTAs/SM with a one-item prefetch (PLBM_FACE_VARIANT=1)
     k.face_v[0] = [](Dev d, const int* act, int src, int flags, long it, unsigned ntiles, cudaStream_t s) {
-        k_face<E, C, NT, 4, false><<<ntiles * 6, NT, 0, s>>>(d, act, src, flags, it);
+        k_face<E, C, NT, 4, false><<<ntiles * (d.mid_faces ? 8 : 6), NT, 0, s>>>(d, act, src, flags, it);
     };
     k.face_v[1] = [](Dev d, const int* act, int src, int flags, long it, unsigned ntiles, cudaStream_t s) {
-        k_face<E, C, NT, 2, true><<<ntiles * 6, NT, 0, s>>>(d, act, src, flags, it);
+        k_face<E, C, NT, 2, true><<<ntiles * (d.mid_faces ? 8 : 6), NT, 0, s>>>(d, act, src, flags, it);
     };
     k.face = k.face_v[0];
     k.p5 = [](Dev d, const int* act, int src, long it, unsigned ntiles, cudaStream_t s) {
@@ -145,6 +164,12 @@ Kernels make_kernels() {
             ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_LOCAL>);
             ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_NEIGH>);
             if constexpr (C <= 2) ld((const void*)k_main_pc<E, C, 2, PN>);
+        }
+        if constexpr (HasHalf<E, C, NOPSI>::value) {
+            constexpr int PN = PcNT<E>::value;
+            ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_OFF, 2>);
+            ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_LOCAL, 2>);
+            ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_NEIGH, 2>);
         }
     };
     k.set_params = [](const Params& p, cudaStream_t s) {

@@ -106,6 +106,8 @@ struct Dev {
     const int* geo;             // [slot][18] active geometric neighbour or -1
     int face_flags;             // FACE_* bits
     int xcol_ok;                // the last fused kernel wrote the xcol side buffers
+    int mid_faces;              // the face pass also writes psi of rows E/2-1, E/2 (faces 6, 7:
+                                // the half-tile clusters' boundary rows), after the 6 faces
     const int* halt;            // speculative queue: a step kernel finding *halt != 0 does nothing
     const struct Poke* pokes;   // test hook (plbm_gpu_poke_f): overrides of f_in for the next step
     int npoke;
@@ -851,8 +853,16 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
 // it finishes the current one (two items in flight per thread, 126 registers);
 // without PF one item is in flight and occupancy supplies the parallelism (the
 // standalone k_face runs that way at 4 CTAs/SM, measured 0.216 vs 0.245 ms).
+// Faces 6 / 7 ("mid faces", Dev::mid_faces): the rows y = E/2 - 1 and E/2
+// inside the tile, in-face index x + E z like the y faces.
 template <int E>
 __device__ __forceinline__ void face_xyz(int face, int idx, int& x, int& y, int& z) {
+    if (face >= 6) {
+        x = idx % E;
+        y = E / 2 - 1 + (face - 6);
+        z = idx / E;
+        return;
+    }
     const int axis = face >> 1;
     const int fixed = (face & 1) ? E - 1 : 0;
     const int a = idx % E, b = idx / E;
@@ -902,6 +912,11 @@ __device__ __forceinline__ void face_load(const RouteTab& rt, int mode, const in
                               (size_t(c) * XN + xslot_sel(cls, i)) * E2 + (sz & (E - 1)) * E + (sy & (E - 1));
             f[i] = COH ? __ldcg(p) : __ldg(p);
         }
+        return;
+    }
+    if (mode == MODE_PULL && !hs && face >= 6 && z >= 1 && z <= E - 2) {  // mid faces: interior rows
+        if (COH) pull_addr_fast<E>(rt, c, x, y, z, [&](int i, const double* p) { f[i] = __ldcg(p); });
+        else pull_addr_fast<E>(rt, c, x, y, z, [&](int i, const double* p) { f[i] = __ldg(p); });
         return;
     }
     if (mode == MODE_PULL && !hs && (face == 2 || face == 3) && z >= 1 && z <= E - 2) {
@@ -970,7 +985,7 @@ __device__ __forceinline__ bool face_finish(const Dev& d, int mode, int c, bool 
             v = pseudo_potential(rho, press, P.comp[c], cl);
         }
     }
-    pf[(size_t(c) * 6 + face) * E2 + idx] = v;
+    pf[(face < 6 ? size_t(c) * 6 + face : size_t(P.C) * 6 + c * 2 + (face - 6)) * E2 + idx] = v;
     return fired;
 }
 
@@ -1001,8 +1016,9 @@ __device__ unsigned face_run(const Dev& d, const RouteTab& rt, int mode, const i
     auto finish = [&](int t, const double* f) {
         int face, idx, c;
         if (!item(t, face, idx, c)) return false;
-        const bool frontier = criterion && routes[face] == P.amb_slot && !(fired & (1u << face));
-        if (face_finish<E>(d, mode, c, hs, sb, face, idx, f, frontier, nan_check, li, pf, iter, tile_lin))
+        const bool frontier = criterion && face < 6 && routes[face] == P.amb_slot && !(fired & (1u << face));
+        if (face_finish<E>(d, mode, c, hs, sb, face, idx, f, frontier, nan_check && face < 6, li, pf, iter,
+                           tile_lin))
             fired |= 1u << face;
         return true;
     };
@@ -1064,10 +1080,11 @@ __global__ void __launch_bounds__(NT, MINB) k_face(Dev d, const int* __restrict_
     __shared__ RouteTab rt;
     __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
     __shared__ int s_tc[3];
-    if (d.nactive && d.tile_base + int(blockIdx.x / 6) >= *d.nactive) return;
-    const int slot = active[blockIdx.x / 6];
+    const int nf = d.mid_faces ? 8 : 6;
+    if (d.nactive && d.tile_base + int(blockIdx.x / nf) >= *d.nactive) return;
+    const int slot = active[blockIdx.x / nf];
     if (d.no_fluid && d.no_fluid[slot]) return;  // (see Dev::no_fluid)
-    const int face = blockIdx.x % 6;
+    const int face = blockIdx.x % nf;
     const uint8_t mode = d.mode[slot];
     const bool hs = d.has_solid[slot] != 0;
     // after k_main every tile pulls with the map it just stepped on (ROUTE_PSI)

@@ -69,12 +69,15 @@ __device__ __forceinline__ const double* psi_ghost_src(const RouteTab& rt, int c
 }
 
 
-template <int E, int C, int LAG = 1, int NT_ = 256>
+template <int E, int C, int LAG = 1, int NT_ = 256, int NH_ = 1>
 struct PcCfg {
     static constexpr int NT = NT_;      // 256: 8 warps, 2 CTAs/SM; 512 (E = 64): 16 warps, 1 CTA/SM
     static constexpr int BY = NT / E;   // rows per CTA
     static constexpr int NB = E / BY;   // y-blocks per tile
-    static constexpr int CL = NB * C;   // cluster size
+    static constexpr int NH = NH_;      // clusters per tile (tile halves along y)
+    static constexpr int NBC = NB / NH; // y-blocks per cluster
+    static constexpr int CL = NBC * C;  // cluster size
+    static_assert(NH == 1 || (NH == 2 && NB % 2 == 0), "whole tiles or y-halves");
     static constexpr int CB = 40;       // TMEM columns per plane slot (19 f + rho)
     static constexpr int WPQ = NT / 128;  // warps per TMEM lane quarter
     static constexpr int NCOLS = 128 * WPQ;  // 128 columns per thread
@@ -106,14 +109,20 @@ struct PcCfg {
 // pushes, TMEM stash, stores and xcol staging with the physics removed (psi
 // = 0, f stored unchanged) — the memory pipeline's own ceiling.
 // AA: population storage kind of this step (kernels.cuh AA_*).
-template <int E, int C, int LAG, int NT_ = 256, bool EARLY = true, bool MEMONLY = false, int AA = AA_OFF>
+// NH = 2: a cluster covers one y-half of the tile (half the CTAs: 4 instead of
+// 8 at E = 32, C = 2, which pack the SMs better); the psi rows across the
+// half boundary come from the mid-face buffers the previous step's face pass
+// wrote (face_xyz faces 6 / 7), as tile-edge rows come from the neighbours'
+// face buffers.
+template <int E, int C, int LAG, int NT_ = 256, bool EARLY = true, bool MEMONLY = false, int AA = AA_OFF,
+          int NH = 1>
 __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __restrict__ active,
                                                             int src_buf, int write_uface, long iter) {
     if (halted(d)) return;
     const unsigned long long t_start = d.probe ? global_ns() : 0ull;
-    using T = PcCfg<E, C, LAG, NT_>;
+    using T = PcCfg<E, C, LAG, NT_, NH>;
     constexpr int NMB = T::NMB;
-    constexpr int NT = T::NT, BY = T::BY, NB = T::NB, PW = T::PW, PH = T::PH, PP = T::PP;
+    constexpr int NT = T::NT, BY = T::BY, NBC = T::NBC, PW = T::PW, PH = T::PH, PP = T::PP;
     constexpr int R = T::RING;
     constexpr int G = E + 2;
     constexpr int E2 = E * E;
@@ -132,12 +141,13 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int rank = int(blockIdx.x % T::CL);  // = cluster CTA rank (1-D clusters)
-    const int tile_i = int(blockIdx.x / T::CL);
+    const int tile_i = int(blockIdx.x / T::CL) / NH;
     // (interleaving the components in the rank order measured no different:
     // the 8 CTAs of a cluster sit on 8 different SMs, tools/probe_cluster.py)
-    const int c = rank / NB;                   // this CTA's component
-    const int yb = rank % NB;
-    auto crank = [&](int cc, int bb) { return cc * NB + bb; };
+    const int c = rank / NBC;                  // this CTA's component
+    const int ybl = rank % NBC;                // y-block within the cluster
+    const int yb = int(blockIdx.x / T::CL) % NH * NBC + ybl;
+    auto crank = [&](int cc, int bb) { return cc * NBC + bb; };
     const int y0 = yb * BY;
     if (d.nactive && d.tile_base + tile_i >= *d.nactive) return;  // (whole clusters: same tile)
     const int slot = active[tile_i];
@@ -233,14 +243,14 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
     auto push_all = [&](int pz, double v) {
 #pragma unroll
         for (int c2 = 0; c2 < C; ++c2) {
-            if (c2 != c) push(crank(c2, yb), pz, yl, v);
-            if (yl == 0 && yb > 0) push(crank(c2, yb - 1), pz, BY, v);
-            if (yl == BY - 1 && yb < NB - 1) push(crank(c2, yb + 1), pz, -1, v);
+            if (c2 != c) push(crank(c2, ybl), pz, yl, v);
+            if (yl == 0 && ybl > 0) push(crank(c2, ybl - 1), pz, BY, v);
+            if (yl == BY - 1 && ybl < NBC - 1) push(crank(c2, ybl + 1), pz, -1, v);
         }
     };
     constexpr uint32_t PLANE_BYTES = uint32_t((C - 1) * BY * E * 8);
     const uint32_t expect_bytes =
-        PLANE_BYTES + uint32_t(((yb > 0) + (yb < NB - 1)) * C * E * 8);
+        PLANE_BYTES + uint32_t(((ybl > 0) + (ybl < NBC - 1)) * C * E * 8);
     auto expect = [&](int pz) {
         if (T::CL > 1 && tid == 0)
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
@@ -292,7 +302,21 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
                 xx = q % E;
                 yyl = (q / E) ? BY : -1;
                 const int yy = y0 + yyl;
-                if (yy >= 0 && yy < E) continue;  // pushed by the adjacent y-block
+                if (yy >= 0 && yy < E) {
+                    if (yyl < 0 ? ybl > 0 : ybl < NBC - 1) continue;  // pushed by the adjacent y-block
+                    // across the half boundary: the mid-face buffers (faces 6 / 7)
+                    const int m = yy == E / 2 ? 1 : 0;
+#pragma unroll 1
+                    for (int cc = 0; cc < C; ++cc) {
+                        const int idx = pidx(pz, cc, xx, yyl);
+                        if (hs && solid_at<E>(s_solid, xx, yy, pz)) psi[idx] = 0.0;
+                        else if (rt_psi.nb[13]) psi[idx] = P.comp[cc].psi_nb;  // newborn: ambient cells
+                        else
+                            cp_async8(smem_u32(psi + idx), rt_psi.p[13] + (size_t(C) * 6 + cc * 2 + m) * E2 +
+                                                               xx + E * pz);
+                    }
+                    continue;
+                }
             }
 #pragma unroll 1
             for (int cc = 0; cc < C; ++cc) {
@@ -576,7 +600,7 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
         d.probe[3 * blockIdx.x + 2] = global_ns();
     }
 #endif
-    if (!fused) return;
+    if (NH != 1 || !fused) return;  // (the fused face pass needs whole-tile clusters)
 
     // ---- fused face pass ---------------------------------------------------------
     // This tile is complete: count it towards itself and its active geometric
@@ -611,9 +635,9 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
             asm volatile("ld.shared::cluster.u32 %0, [%1];\n" : "=r"(ready[j]) : "r"(a0 + 4u * j) : "memory");
     }
     cluster_sync();  // rank 0 may exit once everyone has the list
-    constexpr int PER = 6 * E2 / NB;
+    const int per = (d.mid_faces ? 8 : 6) * E2 / T::NB;
     for (int j = 0; j < nready; ++j)
-        face_pass_part<E, NT>(d, ready[j], c, 1, yb * PER, (yb + 1) * PER, src_buf ^ 1, iter, rt_pull,
+        face_pass_part<E, NT>(d, ready[j], c, 1, yb * per, (yb + 1) * per, src_buf ^ 1, iter, rt_pull,
                               s_solid, s_tc);
 }
 

@@ -11,7 +11,7 @@ from tests.compare import assert_same_state
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("variant", [0, 1, 21, 22, 100, 200], ids=["default_percomp", "plain", "percomp_late_head", "percomp_lag2", "percomp_fused_face", "percomp_strided_xfaces"])
+@pytest.mark.parametrize("variant", [0, 20, 1, 21, 22, 100, 200], ids=["default_halftile", "percomp_wholetile", "plain", "percomp_late_head", "percomp_lag2", "percomp_fused_face", "percomp_strided_xfaces"])
 @pytest.mark.parametrize("name", sorted(scenarios.ALL))
 def test_gpu_matches_oracle(built, name, variant):
     make, steps = scenarios.ALL[name]
@@ -77,7 +77,7 @@ def test_poked_nan_matches_reference(built, name, variant):
 
 
 @pytest.mark.parametrize("mode", ["device", "host_overflow", "host"])
-@pytest.mark.parametrize("name", ["mpmc_progressive_e16", "c1_progressive_S0", "mpmc_channel_e16"])
+@pytest.mark.parametrize("name", ["mpmc_progressive_e16", "c1_progressive_S0", "mpmc_channel_e16", "mpmc_e32", "mpmc_e64"])
 def test_expansion_paths_match_oracle(built, name, mode, monkeypatch):
     """The device-side expansion (k_check_expand), its overflow to the host
     (births beyond the launched grid, headroom 0) and the host-only path give
@@ -195,8 +195,9 @@ def _aa_scenarios():
     return sorted(n for n, (make, _) in scenarios.ALL.items() if ok(make()))
 
 
+@pytest.mark.parametrize("variant", [0, 20], ids=["halftile", "wholetile"])
 @pytest.mark.parametrize("name", _aa_scenarios())
-def test_aa_storage_matches_oracle(built, name):
+def test_aa_storage_matches_oracle(built, name, variant):
     """A-A in-place streaming (one population buffer): the
     same bit-exact state as the oracle after the first step (an AA_LOCAL
     step), after the second (AA_NEIGH) and at the end — the read-back itself
@@ -205,6 +206,7 @@ def test_aa_storage_matches_oracle(built, name):
     sc = make()
     orc = capi.oracle_engine(sc)
     gpu = capi.gpu_engine(sc, capture=True, storage="aa")
+    gpu.set_kernel_variant(variant)
     for k in (1, 1, steps - 2):
         orc.step(k)
         gpu.step(k)
@@ -212,7 +214,7 @@ def test_aa_storage_matches_oracle(built, name):
 
 
 @pytest.mark.parametrize("mode", ["device", "host"])
-@pytest.mark.parametrize("name", ["mpmc_progressive_e16", "c1_progressive_S0", "mpmc_channel_e16"])
+@pytest.mark.parametrize("name", ["mpmc_progressive_e16", "c1_progressive_S0", "mpmc_channel_e16", "mpmc_e32"])
 def test_aa_expansion_paths_match_oracle(built, name, mode, monkeypatch):
     """A-A with births: stores into newborn tiles follow ROUTE_W, whether the
     device (k_check_expand) or the host mirror grows the map."""
