@@ -17,9 +17,9 @@ struct Kernels {
     MainFn main_pc_mem;   // variant 24 (PLBM_PROBES builds only): memory-only probe (E = 32, C = 2)
     MainFn main_pc2;    // variant 22: psi computed two planes ahead
     MainFn main_aa[2];  // A-A storage: AA_LOCAL / AA_NEIGH steps (k_main_pc, else the whole-tile plain kernel)
-    MainFn main_pc_half;     // k_main_pc with one cluster per tile y-half (E >= 32; default, variant 20 = whole tiles)
-    MainFn main_aa_half[2];  // the same for the A-A steps
-    bool mid_faces = false;  // the face pass writes the half boundary rows (Dev::mid_faces)
+    MainFn main_pc_split[2];     // k_main_pc with 2 / 4 clusters per tile (E >= 32; see Engine::set_variant)
+    MainFn main_aa_split[2][2];  // the same for the A-A steps [split][AA_LOCAL / AA_NEIGH]
+    int nhmax = 1;               // finest split: the face pass writes its boundary rows (Dev::mid_faces)
     bool aa_xcol = false;  // the A-A kernels write the xcol side buffers (k_main_pc does)
     void (*face)(Dev, const int*, int, int, long, unsigned, cudaStream_t);
     void (*face_v[2])(Dev, const int*, int, int, long, unsigned, cudaStream_t);

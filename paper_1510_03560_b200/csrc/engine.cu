@@ -186,14 +186,17 @@ class Engine {
     int poke_f(const int32_t* coords, int comp, int i, const int32_t* local, double v);
     void set_profiling(bool on) { profiling_ = on; }
     int set_variant(int v) {
-        if (aa_) {  // A-A storage: half-tile (0) or whole-tile (20) clusters; +200 = no xcol side buffers
-            if (v != 0 && v != 200 && v != 20 && v != 220) return -1;
+        if (aa_) {  // A-A storage: the cluster split (0 default, 20 / 26 / 27); +200 = no xcol side buffers
+            const int b = v % 100;
+            if (!(v >= 0 && v < 300 && v / 100 != 1 && (b == 0 || b == 20 || b == 26 || b == 27))) return -1;
+            if (b == 20 && !K_.main_aa[0]) return -1;  // no whole-tile cluster at this shape
             no_xcol_ = v >= 200;
-            variant_ = v % 100;
+            variant_ = b;
             return 0;
         }
         const int base = v % 100;
-        const bool ok = v >= 0 && v < 400 && (base == 0 || base == 1 || base == 20 || base == 21 || base == 22
+        const bool ok = v >= 0 && v < 400 && (base == 0 || base == 1 || base == 20 || base == 21 || base == 22 ||
+                                              base == 26 || base == 27
 #ifdef PLBM_PROBES
                                               || base == 24
 #endif
@@ -408,6 +411,8 @@ class Engine {
     int solid_words_ = 0;
     bool profiling_ = false;
     int variant_ = 0;
+    int mid_faces_ = 0;
+    int split_ = 1;  // clusters per tile of the default k_main_pc (PLBM_SPLIT, 1 / 2 / 4)
     bool fuse_ = false, no_xcol_ = false;
     plbm_kernel_stats stats_{};
     struct EvPair {
@@ -575,10 +580,14 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     CK(cudaSetDevice(dev_));
     CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     K_ = pick_kernels(E_, C_, nopsi_);
-    if (K_.mid_faces) per_pf_ = size_t(C_) * 8 * E2_;  // + the half boundary rows (Dev::mid_faces)
-    if (aa_ && !K_.main_aa[0])
-        throw std::invalid_argument("A-A storage needs one CTA or cluster per tile: tile_extent <= 32, "
-                                    "or 64 with at most 2 components");
+    if (const char* sp = std::getenv("PLBM_SPLIT")) split_ = std::atoi(sp);
+    else split_ = 4;
+    mid_faces_ = 2 * (K_.nhmax - 1);                   // boundary rows of split-tile clusters
+    params_.mid_sp = K_.nhmax > 1 ? E_ / K_.nhmax : 0;  // (Dev::mid_faces, face_xyz)
+    per_pf_ = size_t(C_) * (6 + mid_faces_) * E2_;
+    if (aa_ && !K_.main_aa[0] && !K_.main_aa_split[0][0])
+        throw std::invalid_argument("A-A storage needs the fused cluster kernels or one CTA per tile "
+                                    "(a psi-free scenario at tile_extent 64 has neither)");
     K_.preload();
     {   // this unit's kernels too (lazy loading, see dispatch.cuh preload)
         cudaFuncAttributes a;
@@ -730,7 +739,7 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     }
     for (int r = 0; r < 3; ++r) d_.route[r] = d_route_[r];
     d_.aa = aa_ ? 1 : 0;
-    d_.mid_faces = K_.mid_faces ? 1 : 0;
+    d_.mid_faces = mid_faces_;
     d_.lidx = d_lidx_;
     d_.solid = d_solid_;
     d_.has_solid = d_has_solid_;
@@ -1621,16 +1630,22 @@ void Engine::launch_main(long iter) {
     MainFn fn = K_.main_plain;
     // single rank: the pc kernels run the face pass themselves (no k_face)
     const auto fusable = [&](MainFn f) { return world_ == 1 && f && (f == K_.main_pc || f == K_.main_pc2 || f == K_.main_pc_late) && !dev_expand_; };
-    if (variant_ == 0 && K_.main_pc) fn = K_.main_pc_half && !fuse_ ? K_.main_pc_half : K_.main_pc;
-    if (variant_ == 20 && K_.main_pc) fn = K_.main_pc;  // whole-tile clusters
+    // clusters per tile: variant 20 = 1 (whole tiles), 26 = 2, 27 = 4, 0 = the default split_
+    const int split = variant_ == 20 ? 1 : variant_ == 26 ? 2 : variant_ == 27 ? 4 : split_;
+    const int sj = split == 2 ? 0 : split == 4 ? 1 : -1;
+    if (variant_ == 0 || variant_ == 20 || variant_ == 26 || variant_ == 27) {
+        if (sj >= 0 && K_.main_pc_split[sj] && !fuse_) fn = K_.main_pc_split[sj];
+        else if (K_.main_pc) fn = K_.main_pc;
+    }
     if (K_.main_pc_late && variant_ == 21) fn = K_.main_pc_late;
     if (K_.main_pc_mem && variant_ == 24) fn = K_.main_pc_mem;  // probe: not a correct step
     if (K_.main_pc2 && variant_ == 22) fn = K_.main_pc2;
-    if (aa_) fn = (K_.main_aa_half[0] && variant_ == 0 ? K_.main_aa_half : K_.main_aa)[aa_kind(1, iter) - 1];
+    if (aa_) fn = (sj >= 0 && K_.main_aa_split[sj][0] ? K_.main_aa_split[sj]
+                   : K_.main_aa[0] ? K_.main_aa : K_.main_aa_split[1])[aa_kind(1, iter) - 1];
     face_fused_ = fusable(fn) && fuse_;
     // the pc kernels write the xcol side buffers the face pass reads
-    d_.xcol_ok = (fn == K_.main_pc || fn == K_.main_pc_half || fn == K_.main_pc2 || fn == K_.main_pc_late ||
-                  fn == K_.main_pc_mem ||
+    d_.xcol_ok = (fn == K_.main_pc || fn == K_.main_pc_split[0] || fn == K_.main_pc_split[1] ||
+                  fn == K_.main_pc2 || fn == K_.main_pc_late || fn == K_.main_pc_mem ||
                   (aa_ && K_.aa_xcol)) && !no_xcol_;
     d_.face_flags = face_fused_ ? (FACE_FUSED | FACE_NAN | (mode_ == PLBM_MODE_PROGRESSIVE ? FACE_CRITERION : 0))
                                 : 0;

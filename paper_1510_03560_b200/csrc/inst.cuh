@@ -23,11 +23,13 @@ struct HasPc {
     static constexpr bool value = !NOPSI && (E == 16 || E == 32 || (E == 64 && C <= 2));
 };
 
-// half-tile clusters (NH = 2) where a whole-tile cluster has more than 4 CTAs
+// split-tile clusters (NH = 2 / 4 clusters per tile) for E >= 32; the face
+// pass writes the boundary rows of the finest split (NHMAX = 4)
 template <int E, int C, bool NOPSI>
 struct HasHalf {
-    static constexpr bool value = HasPc<E, C, NOPSI>::value && E >= 32;
+    static constexpr bool value = !NOPSI && (E == 32 || E == 64);
 };
+constexpr int NHMAX = 4;
 
 template <int E, int C, int LAG, int NT = 256, bool EARLY = true, bool MEMONLY = false, int AA = AA_OFF,
           int NH = 1>
@@ -65,18 +67,40 @@ Kernels make_kernels() {
     k.main_plain = [](Dev d, const int* act, int src, int wu, long it, unsigned ntiles, cudaStream_t s) {
         k_main<E, C, BZ, NT, NOPSI, YB><<<ntiles * (E / BZ) * (E / YB), NT, SMEM_PLAIN, s>>>(d, act, src, wu, it);
     };
-    k.main_pc = k.main_pc2 = k.main_pc_late = k.main_pc_mem = k.main_pc_half = nullptr;
-    k.main_aa[0] = k.main_aa[1] = k.main_aa_half[0] = k.main_aa_half[1] = nullptr;
-    k.mid_faces = HasHalf<E, C, NOPSI>::value;
+    k.main_pc = k.main_pc2 = k.main_pc_late = k.main_pc_mem = nullptr;
+    k.main_aa[0] = k.main_aa[1] = nullptr;
+    for (int j = 0; j < 2; ++j) k.main_pc_split[j] = k.main_aa_split[j][0] = k.main_aa_split[j][1] = nullptr;
+    k.nhmax = HasHalf<E, C, NOPSI>::value ? NHMAX : 1;
     // k_main_pc: 256-thread CTAs (8 warps, 2 per SM) for E = 16 / 32; for
     // E = 64 one 512-thread CTA per SM (8 rows of 64 cells, 16 warps) so that
     // a tile is 8 y-blocks x C components: a 16-CTA cluster at C = 2
     constexpr int PNT = PcNT<E>::value;
+    auto setup = [](auto fn, int smem, int cl) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (cl > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    };
+    // split-tile clusters (E = 64 at C = 3 too: 12 / 6 CTAs where a whole
+    // tile would need 24)
+    if constexpr (HasHalf<E, C, NOPSI>::value) {
+        using TH = PcCfg<E, C, 1, PNT, 2>;
+        using TQ = PcCfg<E, C, 1, PNT, 4>;
+        setup(k_main_pc<E, C, 1, PNT, true, false, AA_OFF, 2>, TH::SMEM, TH::CL);
+        setup(k_main_pc<E, C, 1, PNT, true, false, AA_OFF, 4>, TQ::SMEM, TQ::CL);
+        k.main_pc_split[0] = launch_pc<E, C, 1, PNT, true, false, AA_OFF, 2>;
+        k.main_pc_split[1] = launch_pc<E, C, 1, PNT, true, false, AA_OFF, 4>;
+#ifndef PLBM_NO_AA
+        setup(k_main_pc<E, C, 1, PNT, true, false, AA_LOCAL, 2>, TH::SMEM, TH::CL);
+        setup(k_main_pc<E, C, 1, PNT, true, false, AA_NEIGH, 2>, TH::SMEM, TH::CL);
+        setup(k_main_pc<E, C, 1, PNT, true, false, AA_LOCAL, 4>, TQ::SMEM, TQ::CL);
+        setup(k_main_pc<E, C, 1, PNT, true, false, AA_NEIGH, 4>, TQ::SMEM, TQ::CL);
+        k.main_aa_split[0][0] = launch_pc<E, C, 1, PNT, true, false, AA_LOCAL, 2>;
+        k.main_aa_split[0][1] = launch_pc<E, C, 1, PNT, true, false, AA_NEIGH, 2>;
+        k.main_aa_split[1][0] = launch_pc<E, C, 1, PNT, true, false, AA_LOCAL, 4>;
+        k.main_aa_split[1][1] = launch_pc<E, C, 1, PNT, true, false, AA_NEIGH, 4>;
+        k.aa_xcol = true;
+#endif
+    }
     if constexpr (HasPc<E, C, NOPSI>::value) {
-        auto setup = [](auto fn, int smem, int cl) {
-            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            if (cl > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        };
         using T1 = PcCfg<E, C, 1, PNT>;
         setup(k_main_pc<E, C, 1, PNT>, T1::SMEM, T1::CL);
         k.main_pc = launch_pc<E, C, 1, PNT>;
@@ -92,17 +116,6 @@ Kernels make_kernels() {
             using T2 = PcCfg<E, C, 2, PNT>;
             setup(k_main_pc<E, C, 2, PNT>, T2::SMEM, T2::CL);
             k.main_pc2 = launch_pc<E, C, 2, PNT>;
-        }
-        if constexpr (HasHalf<E, C, NOPSI>::value) {
-            using TH = PcCfg<E, C, 1, PNT, 2>;
-            setup(k_main_pc<E, C, 1, PNT, true, false, AA_OFF, 2>, TH::SMEM, TH::CL);
-            k.main_pc_half = launch_pc<E, C, 1, PNT, true, false, AA_OFF, 2>;
-#ifndef PLBM_NO_AA
-            setup(k_main_pc<E, C, 1, PNT, true, false, AA_LOCAL, 2>, TH::SMEM, TH::CL);
-            setup(k_main_pc<E, C, 1, PNT, true, false, AA_NEIGH, 2>, TH::SMEM, TH::CL);
-            k.main_aa_half[0] = launch_pc<E, C, 1, PNT, true, false, AA_LOCAL, 2>;
-            k.main_aa_half[1] = launch_pc<E, C, 1, PNT, true, false, AA_NEIGH, 2>;
-#endif
         }
 #ifndef PLBM_NO_AA
         setup(k_main_pc<E, C, 1, PNT, true, false, AA_LOCAL>, T1::SMEM, T1::CL);
@@ -132,10 +145,10 @@ Kernels make_kernels() {
     // k_face at 4 CTAs/SM, one item in flight per thread (64 registers),
     // measured faster than 2 CTAs/SM with a one-item prefetch (PLBM_FACE_VARIANT=1)
     k.face_v[0] = [](Dev d, const int* act, int src, int flags, long it, unsigned ntiles, cudaStream_t s) {
-        k_face<E, C, NT, 4, false><<<ntiles * (d.mid_faces ? 8 : 6), NT, 0, s>>>(d, act, src, flags, it);
+        k_face<E, C, NT, 4, false><<<ntiles * (6 + d.mid_faces), NT, 0, s>>>(d, act, src, flags, it);
     };
     k.face_v[1] = [](Dev d, const int* act, int src, int flags, long it, unsigned ntiles, cudaStream_t s) {
-        k_face<E, C, NT, 2, true><<<ntiles * (d.mid_faces ? 8 : 6), NT, 0, s>>>(d, act, src, flags, it);
+        k_face<E, C, NT, 2, true><<<ntiles * (6 + d.mid_faces), NT, 0, s>>>(d, act, src, flags, it);
     };
     k.face = k.face_v[0];
     k.p5 = [](Dev d, const int* act, int src, long it, unsigned ntiles, cudaStream_t s) {
@@ -170,6 +183,9 @@ Kernels make_kernels() {
             ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_OFF, 2>);
             ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_LOCAL, 2>);
             ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_NEIGH, 2>);
+            ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_OFF, 4>);
+            ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_LOCAL, 4>);
+            ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_NEIGH, 4>);
         }
     };
     k.set_params = [](const Params& p, cudaStream_t s) {

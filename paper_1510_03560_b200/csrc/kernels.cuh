@@ -78,6 +78,7 @@ struct Params {
     int amb_slot;
     int progressive;
     double s2;  // threshold^2 (tilemap.cpp:185)
+    int mid_sp; // rows between the mid-face boundaries (E / finest clusters per tile; 0: none)
     CompConst comp[MAX_COMP];
     double coupling[MAX_COMP * MAX_COMP];
     SeedConst seeds[MAX_SEEDS];
@@ -106,8 +107,9 @@ struct Dev {
     const int* geo;             // [slot][18] active geometric neighbour or -1
     int face_flags;             // FACE_* bits
     int xcol_ok;                // the last fused kernel wrote the xcol side buffers
-    int mid_faces;              // the face pass also writes psi of rows E/2-1, E/2 (faces 6, 7:
-                                // the half-tile clusters' boundary rows), after the 6 faces
+    int mid_faces;              // the face pass also writes psi of the rows on both sides of
+                                // every y = b * P.mid_sp boundary (faces 6.., the boundary rows
+                                // of clusters covering part of a tile), after the 6 faces
     const int* halt;            // speculative queue: a step kernel finding *halt != 0 does nothing
     const struct Poke* pokes;   // test hook (plbm_gpu_poke_f): overrides of f_in for the next step
     int npoke;
@@ -853,13 +855,15 @@ __global__ void __launch_bounds__(NT) k_main(Dev d, const int* __restrict__ acti
 // it finishes the current one (two items in flight per thread, 126 registers);
 // without PF one item is in flight and occupancy supplies the parallelism (the
 // standalone k_face runs that way at 4 CTAs/SM, measured 0.216 vs 0.245 ms).
-// Faces 6 / 7 ("mid faces", Dev::mid_faces): the rows y = E/2 - 1 and E/2
-// inside the tile, in-face index x + E z like the y faces.
+// Faces 6.. ("mid faces", Dev::mid_faces): face 6 + 2 (b - 1) + s is the row
+// y = b * P.mid_sp - 1 + s inside the tile (s = 0 below the boundary, 1
+// above), in-face index x + E z like the y faces.
+__device__ __forceinline__ int mid_face_row(int face) { return ((face - 6) / 2 + 1) * P.mid_sp - 1 + (face & 1); }
 template <int E>
 __device__ __forceinline__ void face_xyz(int face, int idx, int& x, int& y, int& z) {
     if (face >= 6) {
         x = idx % E;
-        y = E / 2 - 1 + (face - 6);
+        y = mid_face_row(face);
         z = idx / E;
         return;
     }
@@ -985,7 +989,7 @@ __device__ __forceinline__ bool face_finish(const Dev& d, int mode, int c, bool 
             v = pseudo_potential(rho, press, P.comp[c], cl);
         }
     }
-    pf[(face < 6 ? size_t(c) * 6 + face : size_t(P.C) * 6 + c * 2 + (face - 6)) * E2 + idx] = v;
+    pf[(face < 6 ? size_t(c) * 6 + face : size_t(P.C) * 6 + size_t(c) * d.mid_faces + (face - 6)) * E2 + idx] = v;
     return fired;
 }
 
@@ -1080,7 +1084,7 @@ __global__ void __launch_bounds__(NT, MINB) k_face(Dev d, const int* __restrict_
     __shared__ RouteTab rt;
     __shared__ uint32_t s_solid[(G * G * G + 31) / 32];
     __shared__ int s_tc[3];
-    const int nf = d.mid_faces ? 8 : 6;
+    const int nf = 6 + d.mid_faces;
     if (d.nactive && d.tile_base + int(blockIdx.x / nf) >= *d.nactive) return;
     const int slot = active[blockIdx.x / nf];
     if (d.no_fluid && d.no_fluid[slot]) return;  // (see Dev::no_fluid)

@@ -77,7 +77,7 @@ struct PcCfg {
     static constexpr int NH = NH_;      // clusters per tile (tile halves along y)
     static constexpr int NBC = NB / NH; // y-blocks per cluster
     static constexpr int CL = NBC * C;  // cluster size
-    static_assert(NH == 1 || (NH == 2 && NB % 2 == 0), "whole tiles or y-halves");
+    static_assert(NB % NH == 0, "clusters split a tile's y-blocks evenly");
     static constexpr int CB = 40;       // TMEM columns per plane slot (19 f + rho)
     static constexpr int WPQ = NT / 128;  // warps per TMEM lane quarter
     static constexpr int NCOLS = 128 * WPQ;  // 128 columns per thread
@@ -109,11 +109,11 @@ struct PcCfg {
 // pushes, TMEM stash, stores and xcol staging with the physics removed (psi
 // = 0, f stored unchanged) — the memory pipeline's own ceiling.
 // AA: population storage kind of this step (kernels.cuh AA_*).
-// NH = 2: a cluster covers one y-half of the tile (half the CTAs: 4 instead of
-// 8 at E = 32, C = 2, which pack the SMs better); the psi rows across the
-// half boundary come from the mid-face buffers the previous step's face pass
-// wrote (face_xyz faces 6 / 7), as tile-edge rows come from the neighbours'
-// face buffers.
+// NH > 1: a cluster covers 1/NH of the tile's y-blocks (fewer CTAs per
+// cluster: 2 instead of 8 at E = 32, C = 2, NH = 4, which pack the SMs
+// better); the psi rows across a cluster boundary come from the mid-face
+// buffers the previous step's face pass wrote (face_xyz faces 6..), as
+// tile-edge rows come from the neighbours' face buffers.
 template <int E, int C, int LAG, int NT_ = 256, bool EARLY = true, bool MEMONLY = false, int AA = AA_OFF,
           int NH = 1>
 __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __restrict__ active,
@@ -304,15 +304,16 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
                 const int yy = y0 + yyl;
                 if (yy >= 0 && yy < E) {
                     if (yyl < 0 ? ybl > 0 : ybl < NBC - 1) continue;  // pushed by the adjacent y-block
-                    // across the half boundary: the mid-face buffers (faces 6 / 7)
-                    const int m = yy == E / 2 ? 1 : 0;
+                    // across a cluster boundary: the mid-face buffers (face_xyz faces 6..)
+                    const int m = 2 * ((yyl < 0 ? y0 : yy) / P.mid_sp - 1) + (yyl < 0 ? 0 : 1);
 #pragma unroll 1
                     for (int cc = 0; cc < C; ++cc) {
                         const int idx = pidx(pz, cc, xx, yyl);
                         if (hs && solid_at<E>(s_solid, xx, yy, pz)) psi[idx] = 0.0;
                         else if (rt_psi.nb[13]) psi[idx] = P.comp[cc].psi_nb;  // newborn: ambient cells
                         else
-                            cp_async8(smem_u32(psi + idx), rt_psi.p[13] + (size_t(C) * 6 + cc * 2 + m) * E2 +
+                            cp_async8(smem_u32(psi + idx), rt_psi.p[13] +
+                                                               (size_t(C) * 6 + cc * d.mid_faces + m) * E2 +
                                                                xx + E * pz);
                     }
                     continue;
@@ -635,7 +636,7 @@ __global__ void __launch_bounds__(NT_, 512 / NT_) k_main_pc(Dev d, const int* __
             asm volatile("ld.shared::cluster.u32 %0, [%1];\n" : "=r"(ready[j]) : "r"(a0 + 4u * j) : "memory");
     }
     cluster_sync();  // rank 0 may exit once everyone has the list
-    const int per = (d.mid_faces ? 8 : 6) * E2 / T::NB;
+    const int per = (6 + d.mid_faces) * E2 / T::NB;
     for (int j = 0; j < nready; ++j)
         face_pass_part<E, NT>(d, ready[j], c, 1, yb * per, (yb + 1) * per, src_buf ^ 1, iter, rt_pull,
                               s_solid, s_tc);

@@ -11,7 +11,7 @@ from tests.compare import assert_same_state
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("variant", [0, 20, 1, 21, 22, 100, 200], ids=["default_halftile", "percomp_wholetile", "plain", "percomp_late_head", "percomp_lag2", "percomp_fused_face", "percomp_strided_xfaces"])
+@pytest.mark.parametrize("variant", [0, 20, 26, 27, 1, 21, 22, 100, 200], ids=["default", "percomp_wholetile", "percomp_halftile", "percomp_quartertile", "plain", "percomp_late_head", "percomp_lag2", "percomp_fused_face", "percomp_strided_xfaces"])
 @pytest.mark.parametrize("name", sorted(scenarios.ALL))
 def test_gpu_matches_oracle(built, name, variant):
     make, steps = scenarios.ALL[name]
@@ -189,13 +189,12 @@ def test_p5_screen_has_no_false_alarm(built, name):
 
 
 def _aa_scenarios():
-    # A-A needs one CTA (or cluster) per tile: E <= 32, or E = 64 with C <= 2
-    def ok(sc):
-        return sc.tile_extent <= 32 or sc.n_components <= 2
-    return sorted(n for n, (make, _) in scenarios.ALL.items() if ok(make()))
+    # A-A runs on the fused cluster kernels (whole or split tiles) or on one
+    # CTA per tile (E <= 32): every parity scenario
+    return sorted(scenarios.ALL)
 
 
-@pytest.mark.parametrize("variant", [0, 20], ids=["halftile", "wholetile"])
+@pytest.mark.parametrize("variant", [20, 26, 27], ids=["wholetile", "halftile", "quartertile"])
 @pytest.mark.parametrize("name", _aa_scenarios())
 def test_aa_storage_matches_oracle(built, name, variant):
     """A-A in-place streaming (one population buffer): the
@@ -206,6 +205,10 @@ def test_aa_storage_matches_oracle(built, name, variant):
     sc = make()
     orc = capi.oracle_engine(sc)
     gpu = capi.gpu_engine(sc, capture=True, storage="aa")
+    if variant == 20 and sc.tile_extent == 64 and sc.n_components == 3:
+        with pytest.raises(ValueError):  # no whole-tile cluster (24 CTAs) at this shape
+            gpu.set_kernel_variant(variant)
+        return
     gpu.set_kernel_variant(variant)
     for k in (1, 1, steps - 2):
         orc.step(k)
@@ -253,12 +256,21 @@ def test_aa_halves_population_memory(built, monkeypatch):
     assert used_ab - used_aa >= 0.9 * one_buffer, (used_ab, used_aa, one_buffer)
 
 
-def test_aa_rejects_shapes_without_one_cluster_per_tile(built):
-    """A-A needs one CTA or cluster per tile: E = 64 with three components
-    (a 24-CTA cluster) is refused at creation, with the reason."""
-    sc = scenarios.ALL["mpmc3_e64_solid"][0]()
-    with pytest.raises(ValueError, match="A-A storage"):
-        capi.gpu_engine(sc, storage="aa")
+def test_e64_three_components_run_on_split_clusters(built):
+    """E = 64 with three components: a whole-tile cluster would need 24 CTAs,
+    so k_main_pc runs with 2 or 4 clusters per tile (12 / 6 CTAs) — A-B and
+    A-A, bit-exact against the oracle — and the whole-tile variant falls back
+    to the plain kernel (A-B) or is refused (A-A)."""
+    make, steps = scenarios.ALL["mpmc3_e64_solid"]
+    for storage in ("ab", "aa"):
+        for v in (26, 27):
+            sc = make()
+            orc = capi.oracle_engine(sc)
+            gpu = capi.gpu_engine(sc, capture=True, storage=storage)
+            gpu.set_kernel_variant(v)
+            orc.step(steps)
+            gpu.step(steps)
+            assert_same_state(orc, gpu, label=f"e64c3/{storage}/{v}")
 
 
 @pytest.mark.parametrize("storage", ["ab", "aa"])

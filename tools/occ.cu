@@ -33,6 +33,10 @@ void report(const char* name, K kern, int nt, int smem, int cl) {
 }
 
 int main() {
+    {   // the half-tile kernel at cluster sizes 2 / 4 / 8 (what quarter / half / whole tiles would pack)
+        auto kh = k_main_pc<32, 2, 1, 256, true, false, AA_OFF, 2>;
+        for (int cl : {1, 2, 4, 8}) report("k_main_pc<32,2,NH=2> as", kh, 256, PcCfg<32, 2, 1, 256, 2>::SMEM, cl);
+    }
     report("k_main_pc<32,2,1>", k_main_pc<32, 2, 1, 256>, 256, PcCfg<32, 2, 1>::SMEM, PcCfg<32, 2, 1>::CL);
     report("k_main_pc<32,1,1>", k_main_pc<32, 1, 1, 256>, 256, PcCfg<32, 1, 1>::SMEM, PcCfg<32, 1, 1>::CL);
     report("k_main_pc<32,3,1>", k_main_pc<32, 3, 1, 256>, 256, PcCfg<32, 3, 1>::SMEM, PcCfg<32, 3, 1>::CL);
