@@ -30,6 +30,13 @@ struct HasHalf {
     static constexpr bool value = !NOPSI && (E == 32 || E == 64);
 };
 constexpr int NHMAX = 4;
+// experiment builds (build.py --exp): the split kernel's pipeline shape
+#ifndef PLBM_SPLIT_LAG
+#define PLBM_SPLIT_LAG 1
+#endif
+#ifndef PLBM_SPLIT_EARLY
+#define PLBM_SPLIT_EARLY true
+#endif
 
 template <int E, int C, int LAG, int NT = 256, bool EARLY = true, bool MEMONLY = false, int AA = AA_OFF,
           int NH = 1>
@@ -84,10 +91,11 @@ Kernels make_kernels() {
     if constexpr (HasHalf<E, C, NOPSI>::value) {
         using TH = PcCfg<E, C, 1, PNT, 2>;
         using TQ = PcCfg<E, C, 1, PNT, 4>;
+        using TX = PcCfg<E, C, PLBM_SPLIT_LAG, PNT, 4>;
         setup(k_main_pc<E, C, 1, PNT, true, false, AA_OFF, 2>, TH::SMEM, TH::CL);
-        setup(k_main_pc<E, C, 1, PNT, true, false, AA_OFF, 4>, TQ::SMEM, TQ::CL);
+        setup(k_main_pc<E, C, PLBM_SPLIT_LAG, PNT, PLBM_SPLIT_EARLY, false, AA_OFF, 4>, TX::SMEM, TX::CL);
         k.main_pc_split[0] = launch_pc<E, C, 1, PNT, true, false, AA_OFF, 2>;
-        k.main_pc_split[1] = launch_pc<E, C, 1, PNT, true, false, AA_OFF, 4>;
+        k.main_pc_split[1] = launch_pc<E, C, PLBM_SPLIT_LAG, PNT, PLBM_SPLIT_EARLY, false, AA_OFF, 4>;
 #ifndef PLBM_NO_AA
         setup(k_main_pc<E, C, 1, PNT, true, false, AA_LOCAL, 2>, TH::SMEM, TH::CL);
         setup(k_main_pc<E, C, 1, PNT, true, false, AA_NEIGH, 2>, TH::SMEM, TH::CL);
@@ -183,7 +191,7 @@ Kernels make_kernels() {
             ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_OFF, 2>);
             ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_LOCAL, 2>);
             ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_NEIGH, 2>);
-            ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_OFF, 4>);
+            ld((const void*)k_main_pc<E, C, PLBM_SPLIT_LAG, PN, PLBM_SPLIT_EARLY, false, AA_OFF, 4>);
             ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_LOCAL, 4>);
             ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_NEIGH, 4>);
         }
