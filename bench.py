@@ -48,7 +48,7 @@ FALLBACK_HBM_GBS = 6650.0         # /opt/skills/guides/B200_PROFILING.md
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=30)
+    p.add_argument("--steps", type=int, default=100)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", choices=["c2", "c2_static", "c1", "c3", "c3_static", "c4", "c5"], default="c2")
