@@ -19,8 +19,11 @@
 // components) through distributed shared memory with st.async, completing
 // transactions on the receiver's per-plane mbarrier.
 //
-// Cluster = NB y-blocks x C components of one tile (E = 32: 4 x 2 = 8 CTAs;
-// 4 x 3 = 12 at C = 3, a non-portable cluster size B200 supports).
+// Cluster = NB / NH y-blocks x C components of one tile: NH = 1 is the whole
+// tile (E = 32: 4 x 2 = 8 CTAs; 12 at C = 3, a non-portable size B200
+// supports), NH = 2 / 4 split it (the default NH = 4: 2-CTA clusters at
+// E = 32, C = 2, which fill every SM slot; psi across the split boundaries
+// from the face pass's mid faces, see k_main_pc).
 // Per plane z:  wait landing(z+1) | psi pass z+1 -> TMEM, push psi | issue
 //               pulls(z+2) | CTA barrier | issue ghosts(z+2) | wait pushes(z+1)
 //               | collide z from TMEM.
