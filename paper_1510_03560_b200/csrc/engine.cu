@@ -385,6 +385,7 @@ class Engine {
     uint8_t* d_bmask_ = nullptr;  // [slot] faces whose trigger would be a birth
     uint8_t* d_omask_ = nullptr;  // [slot] faces whose trigger is out of bounds (suppressed)
     int* d_halt_ = nullptr;       // sticky halt flag of the speculative step queue
+    unsigned long long* h_cnt_ = nullptr;  // pinned landing area of counters(): CNT_N x 2 + 4
     int* h_flags_ = nullptr;      // pinned copies of the halt flag, one per queued step (+ birth
                                   // count at h_flags_[8 + k]: sync_births needs no round trip
                                   // when the retired steps had no births)
@@ -643,6 +644,7 @@ void Engine::init(const plbm_scenario_desc& d, int device, int rank, int world) 
     d_halt_ = dmalloc<int>(1);
     CK(cudaMemsetAsync(d_halt_, 0, sizeof(int), stream_));
     CK(cudaMallocHost(&h_flags_, 16 * sizeof(int)));
+    CK(cudaMallocHost(&h_cnt_, (2 * CNT_N + 4) * sizeof(unsigned long long)));
     // (environment overrides first: device expansion depends on the queue depth)
     if (const char* sd = std::getenv("PLBM_SPEC_DEPTH")) spec_depth_ = std::max(1, std::min(8, std::atoi(sd)));
     if (const char* fv = std::getenv("PLBM_FACE_VARIANT")) K_.face = K_.face_v[std::atoi(fv) == 1 ? 1 : 0];
@@ -891,6 +893,7 @@ void Engine::release() {
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (h_flags_) cudaFreeHost(h_flags_);
+    if (h_cnt_) cudaFreeHost(h_cnt_);
     for (auto& e : flag_ev_)
         if (e) cudaEventDestroy(e);
     for (auto& e : ev_pool_) {
@@ -2197,13 +2200,17 @@ void Engine::counters(plbm_counters* out) {
     std::memset(out, 0, sizeof *out);
     // every device word in one round trip: this rank's counters, the
     // job-wide diagnostics (several ranks), the device-side accumulators
-    unsigned long long c[CNT_N] = {}, g[CNT_N] = {}, acc[4] = {};
+    // (into pinned memory: true async copies, one synchronisation)
+    unsigned long long* c = h_cnt_;
+    unsigned long long* g = h_cnt_ + CNT_N;
+    unsigned long long* acc = h_cnt_ + 2 * CNT_N;
+    std::memset(h_cnt_, 0, (2 * CNT_N + 4) * sizeof(unsigned long long));
     const bool use_g = world_ > 1 && gcnt_valid_;
-    CK(cudaMemcpyAsync(c, d_cnt_, sizeof c, cudaMemcpyDeviceToHost, stream_));
-    if (use_g) CK(cudaMemcpyAsync(g, d_gcnt_, sizeof g, cudaMemcpyDeviceToHost, stream_));
-    if (dev_expand_) CK(cudaMemcpyAsync(acc, d_acc_, sizeof acc, cudaMemcpyDeviceToHost, stream_));
+    CK(cudaMemcpyAsync(c, d_cnt_, CNT_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream_));
+    if (use_g) CK(cudaMemcpyAsync(g, d_gcnt_, CNT_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream_));
+    if (dev_expand_) CK(cudaMemcpyAsync(acc, d_acc_, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream_));
     CK(cudaStreamSynchronize(stream_));
-    stats_.d2h_bytes += sizeof c + (use_g ? sizeof g : 0) + (dev_expand_ ? sizeof acc : 0);
+    stats_.d2h_bytes += (CNT_N + (use_g ? CNT_N : 0) + (dev_expand_ ? 4 : 0)) * sizeof(unsigned long long);
     out->iteration = iteration_;
     out->cell_updates = cell_updates_;
     out->negative_populations = c[CNT_NEG];  // this rank's tiles (one rank: all)
