@@ -424,7 +424,10 @@ def main():
                 "d2h_bytes_per_step": int(e_ks["d2h_bytes"] / max(a.steps, 1)),
                 "loop": "plbm_gpu_step(h, 1) + plbm_gpu_counters per iteration" +
                         (f", rho snapshot of every component to a host grid every {a.snapshot_every} steps"
-                         if a.snapshot_every else " (snapshot_interval 0, the reference driver's default)")},
+                         if a.snapshot_every else " (snapshot_interval 0, the reference driver's default)"),
+                "copies": "a step has no host input (the lattice state is resident, as in the reference's "
+                          "run loop); its result read each step is the report counters (D2H, counted); "
+                          "--snapshot-every N adds the field read-backs the reference's snapshots do"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
                      "peak": peak, "unit": "GB/s",
