@@ -104,8 +104,8 @@ void plbm_gpu_reset_kernel_stats(void* h);
  *   21 = k_main_pc with the collision head (TMEM load, u) after the cluster
  *        wait (the default runs it before the wait)
  *   22 = k_main_pc with psi computed two planes ahead (three TMEM slots)
- *   20 / 26 / 27 = k_main_pc with 1 / 2 / 4 clusters per tile (E >= 32: a
- *        cluster covers all / half / a quarter of the tile's y-blocks; the
+ *   20 / 26 / 27 = k_main_pc with 1 / 2 / E/8 clusters per tile (E >= 32: a
+ *        cluster covers all / half / one of the tile's 8-row y-blocks; the
  *        psi rows across a cluster boundary come from the face pass's
  *        mid-face buffers).  Variant 0 uses the measured default split
  *        (PLBM_SPLIT overrides it).  A-A storage accepts 0, 20, 26, 27.

@@ -1633,7 +1633,7 @@ void Engine::launch_main(long iter) {
     MainFn fn = K_.main_plain;
     // single rank: the pc kernels run the face pass themselves (no k_face)
     const auto fusable = [&](MainFn f) { return world_ == 1 && f && (f == K_.main_pc || f == K_.main_pc2 || f == K_.main_pc_late) && !dev_expand_; };
-    // clusters per tile: variant 20 = 1 (whole tiles), 26 = 2, 27 = 4, 0 = the default split_
+    // clusters per tile: variant 20 = 1 (whole tiles), 26 = 2, 27 = the finest (E / 8), 0 = the default split_
     const int split = variant_ == 20 ? 1 : variant_ == 26 ? 2 : variant_ == 27 ? 4 : split_;
     const int sj = split == 2 ? 0 : split == 4 ? 1 : -1;
     if (variant_ == 0 || variant_ == 20 || variant_ == 26 || variant_ == 27) {

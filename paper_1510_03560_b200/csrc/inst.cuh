@@ -23,13 +23,18 @@ struct HasPc {
     static constexpr bool value = !NOPSI && (E == 16 || E == 32 || (E == 64 && C <= 2));
 };
 
-// split-tile clusters (NH = 2 / 4 clusters per tile) for E >= 32; the face
-// pass writes the boundary rows of the finest split (NHMAX = 4)
+// split-tile clusters (NH = 2 and the finest split, nh_fine: 4 clusters per
+// tile at E = 32, 8 at E = 64 — one y-block x C components each) for
+// E >= 32; the face pass writes the boundary rows of the finest split
 template <int E, int C, bool NOPSI>
 struct HasHalf {
     static constexpr bool value = !NOPSI && (E == 32 || E == 64);
 };
-constexpr int NHMAX = 4;
+#ifndef PLBM_E64_NH
+#define PLBM_E64_NH 8  // the finest split at E = 64: one y-block per cluster (4: two, measured slower at C >= 2)
+#endif
+template <int E>
+constexpr int nh_fine() { return E == 64 ? PLBM_E64_NH : 4; }
 // experiment builds (build.py --exp): the split kernel's pipeline shape
 #ifndef PLBM_SPLIT_LAG
 #define PLBM_SPLIT_LAG 1
@@ -77,7 +82,7 @@ Kernels make_kernels() {
     k.main_pc = k.main_pc2 = k.main_pc_late = k.main_pc_mem = nullptr;
     k.main_aa[0] = k.main_aa[1] = nullptr;
     for (int j = 0; j < 2; ++j) k.main_pc_split[j] = k.main_aa_split[j][0] = k.main_aa_split[j][1] = nullptr;
-    k.nhmax = HasHalf<E, C, NOPSI>::value ? NHMAX : 1;
+    k.nhmax = HasHalf<E, C, NOPSI>::value ? nh_fine<E>() : 1;
     // k_main_pc: 256-thread CTAs (8 warps, 2 per SM) for E = 16 / 32; for
     // E = 64 one 512-thread CTA per SM (8 rows of 64 cells, 16 warps) so that
     // a tile is 8 y-blocks x C components: a 16-CTA cluster at C = 2
@@ -90,21 +95,21 @@ Kernels make_kernels() {
     // tile would need 24)
     if constexpr (HasHalf<E, C, NOPSI>::value) {
         using TH = PcCfg<E, C, 1, PNT, 2>;
-        using TQ = PcCfg<E, C, 1, PNT, 4>;
-        using TX = PcCfg<E, C, PLBM_SPLIT_LAG, PNT, 4>;
+        using TQ = PcCfg<E, C, 1, PNT, nh_fine<E>()>;
+        using TX = PcCfg<E, C, PLBM_SPLIT_LAG, PNT, nh_fine<E>()>;
         setup(k_main_pc<E, C, 1, PNT, true, false, AA_OFF, 2>, TH::SMEM, TH::CL);
-        setup(k_main_pc<E, C, PLBM_SPLIT_LAG, PNT, PLBM_SPLIT_EARLY, false, AA_OFF, 4>, TX::SMEM, TX::CL);
+        setup(k_main_pc<E, C, PLBM_SPLIT_LAG, PNT, PLBM_SPLIT_EARLY, false, AA_OFF, nh_fine<E>()>, TX::SMEM, TX::CL);
         k.main_pc_split[0] = launch_pc<E, C, 1, PNT, true, false, AA_OFF, 2>;
-        k.main_pc_split[1] = launch_pc<E, C, PLBM_SPLIT_LAG, PNT, PLBM_SPLIT_EARLY, false, AA_OFF, 4>;
+        k.main_pc_split[1] = launch_pc<E, C, PLBM_SPLIT_LAG, PNT, PLBM_SPLIT_EARLY, false, AA_OFF, nh_fine<E>()>;
 #ifndef PLBM_NO_AA
         setup(k_main_pc<E, C, 1, PNT, true, false, AA_LOCAL, 2>, TH::SMEM, TH::CL);
         setup(k_main_pc<E, C, 1, PNT, true, false, AA_NEIGH, 2>, TH::SMEM, TH::CL);
-        setup(k_main_pc<E, C, 1, PNT, true, false, AA_LOCAL, 4>, TQ::SMEM, TQ::CL);
-        setup(k_main_pc<E, C, 1, PNT, true, false, AA_NEIGH, 4>, TQ::SMEM, TQ::CL);
+        setup(k_main_pc<E, C, 1, PNT, true, false, AA_LOCAL, nh_fine<E>()>, TQ::SMEM, TQ::CL);
+        setup(k_main_pc<E, C, 1, PNT, true, false, AA_NEIGH, nh_fine<E>()>, TQ::SMEM, TQ::CL);
         k.main_aa_split[0][0] = launch_pc<E, C, 1, PNT, true, false, AA_LOCAL, 2>;
         k.main_aa_split[0][1] = launch_pc<E, C, 1, PNT, true, false, AA_NEIGH, 2>;
-        k.main_aa_split[1][0] = launch_pc<E, C, 1, PNT, true, false, AA_LOCAL, 4>;
-        k.main_aa_split[1][1] = launch_pc<E, C, 1, PNT, true, false, AA_NEIGH, 4>;
+        k.main_aa_split[1][0] = launch_pc<E, C, 1, PNT, true, false, AA_LOCAL, nh_fine<E>()>;
+        k.main_aa_split[1][1] = launch_pc<E, C, 1, PNT, true, false, AA_NEIGH, nh_fine<E>()>;
         k.aa_xcol = true;
 #endif
     }
@@ -191,9 +196,9 @@ Kernels make_kernels() {
             ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_OFF, 2>);
             ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_LOCAL, 2>);
             ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_NEIGH, 2>);
-            ld((const void*)k_main_pc<E, C, PLBM_SPLIT_LAG, PN, PLBM_SPLIT_EARLY, false, AA_OFF, 4>);
-            ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_LOCAL, 4>);
-            ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_NEIGH, 4>);
+            ld((const void*)k_main_pc<E, C, PLBM_SPLIT_LAG, PN, PLBM_SPLIT_EARLY, false, AA_OFF, nh_fine<E>()>);
+            ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_LOCAL, nh_fine<E>()>);
+            ld((const void*)k_main_pc<E, C, 1, PN, true, false, AA_NEIGH, nh_fine<E>()>);
         }
     };
     k.set_params = [](const Params& p, cudaStream_t s) {
